@@ -1,0 +1,118 @@
+/*
+ * hyperball_b200.h -- C-ABI of the B200 HyperBall hot path (libhyperball_b200.so).
+ *
+ * Plain pointers and sizes only; every pointer argument documented as "device" must be
+ * a CUDA device pointer (the host side allocates with torch, the library allocates
+ * nothing).  `stream` is a cudaStream_t passed as void*.  Every entry point returns 0
+ * on success and a nonzero code otherwise; hb_last_error() describes the last failure
+ * of the calling thread.  All launches are asynchronous on `stream`.
+ *
+ * Reference interfaces each entry point replaces (paths relative to
+ * /root/reference/pkg/src/hyperball):
+ *
+ *   hb_seed           engine.py:153-162 _ProbabilisticBackend.seed
+ *                     (-> hll.py:79-88 hash_items, hll.py:147-158 register_values,
+ *                         _kernels.py:43-51 scatter_max, _kernels.py:37-40
+ *                         estimate_register_rows)
+ *   hb_estimate_rows  _kernels.py:37-40 estimate_register_rows (+ 15-34 per row)
+ *   hb_union_step     engine.py:164-169 _ProbabilisticBackend.union_range
+ *                     (-> _kernels.py:67-114 hll_union_range) fused with
+ *                     centrality.py:132-150 CentralityAccumulator.on_step/accumulate
+ *   hb_relabel_csr    graph.py:145-155 transpose's output consumed in schedule order
+ *                     (internal relabelling; no reference counterpart)
+ *   hb_hash_items     hll.py:79-88 hash_items (device twin, used by tests)
+ *
+ * Layout:
+ *   regs / cur / nxt   uint8  [n, p] row-major, p = 2^b, row stride p bytes
+ *                      (the reference's dense working registers, engine.py:147-148)
+ *   offsets            int64  [n+1]   CSR of the transpose graph, internal ids
+ *   succ               int32  [m]     in-neighbour ids (internal ids)
+ *   chg_prev, chg_now  uint32 [ceil(n/32)] change bitmaps, bit (v & 31) of word v >> 5
+ *   est                fp64   [n]     cached estimates, updated in place
+ *   sum_dist,sum_recip fp64   [n]     CentralityAccumulator sums (either may be NULL)
+ *   lc_table           fp64   [p+1]   lc_table[V] = p * log(p / V) built on the host with
+ *                                     math.log (bit-identical to numba's np.log)
+ */
+#ifndef HYPERBALL_B200_H
+#define HYPERBALL_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Library version string and the last error message of the calling thread. */
+const char *hb_version(void);
+const char *hb_last_error(void);
+
+/* Minimum / maximum supported log2m (b).  The reference accepts any b >= 4
+ * (hll.py:117-122); this build instantiates kernels for HB_MIN_LOG2M..HB_MAX_LOG2M. */
+int hb_min_log2m(void);
+int hb_max_log2m(void);
+
+/* Seed one counter per node (engine.py:153-162).  regs: device uint8 [n, 2^b] (fully
+ * overwritten); est: device fp64 [n].  perm: device int32 [n] mapping internal id ->
+ * original node id (the id that is hashed), or NULL for the identity.  weights: device
+ * int64 [n] indexed by ORIGINAL id, or NULL for one item (v, replica=1) per node
+ * (engine.py:100-119).  seed is the CounterParams.seed reduced mod 2^64. */
+int hb_seed(uint8_t *regs, double *est, int64_t n, int b, int register_width, uint64_t seed,
+            const int32_t *perm, const int64_t *weights, const double *lc_table,
+            double alpha_p2, double lc_cut, void *stream);
+
+/* out[v] = estimate(regs[v]) for v in [lo, hi) (_kernels.py:15-40). */
+int hb_estimate_rows(const uint8_t *regs, int64_t lo, int64_t hi, int b,
+                     const double *lc_table, double alpha_p2, double lc_cut, double *out,
+                     void *stream);
+
+/* One ball-growth step over internal ids [lo, hi) (_kernels.py:67-114), fused with the
+ * accumulator fold (centrality.py:132-150):
+ *   nxt[v] = cur[v] max (max over succ w of v with chg_prev[w] (or every w when dense))
+ *   chg_now[v] = nxt[v] != cur[v];  est[v] = estimate(nxt[v]) where changed;
+ *   sum_dist[v] += t * max(new - old, 0);  sum_recip[v] += max(new - old, 0) / t.
+ * nxt rows are written only when chg_prev[v] or chg_now[v] (the other rows of the
+ * recycled buffer already hold the right value).
+ * The schedule splits [lo, hi) into:
+ *   light nodes: in-degree <= light_max_deg, one lane group per node, every id in
+ *                [lo, hi) visited (heavier ids are skipped);
+ *   heavy nodes: heavy_nodes[0..n_heavy) (device int32), each split into work items
+ *                item_first[j]..item_first[j+1] (device int32 [n_heavy+1]); item i covers
+ *                arcs [item_beg[i], min(item_beg[i] + item_arcs, offsets[v+1])) of node
+ *                item_node[i] (device int32 / int64 [n_items]) and leaves a partial row
+ *                in partial (device uint8 [n_items, p]).
+ * chg_now words covering [lo, hi) must be zero on entry (hb_union_step clears the whole
+ * bitmap when clear_chg_now != 0).  *nch_out (device uint64) receives the changed count
+ * (zeroed by the call); *merged_out (device uint64, may be NULL) receives the number of
+ * arcs whose source row was actually merged (source-skip aware).  dense != 0 treats
+ * every source as changed (first iteration and
+ * skip_stable_nodes=False; results are identical). */
+int hb_union_step(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets,
+                  const int32_t *succ, const uint8_t *cur, uint8_t *nxt,
+                  const uint32_t *chg_prev, uint32_t *chg_now, int clear_chg_now,
+                  double *est, double *sum_dist, double *sum_recip, int64_t t,
+                  const double *lc_table, double alpha_p2, double lc_cut, int b, int dense,
+                  int64_t light_max_deg, const int32_t *heavy_nodes, const int32_t *item_first,
+                  int64_t n_heavy, const int32_t *item_node, const int64_t *item_beg,
+                  int64_t n_items, int64_t item_arcs, uint8_t *partial, uint64_t *nch_out,
+                  uint64_t *merged_out, void *stream);
+
+/* Relabel a CSR into schedule order: new row i is old row perm[i] with every id mapped
+ * through rank (rank[perm[i]] == i).  new_offsets (device int64 [n+1]) must already hold
+ * the prefix sums of the permuted degrees. */
+int hb_relabel_csr(int64_t n, const int64_t *old_offsets, const int32_t *old_succ,
+                   const int32_t *perm, const int32_t *rank, const int64_t *new_offsets,
+                   int32_t *new_succ, void *stream);
+
+/* out[i] = hash_items(items[i], replicas[i], seed) (hll.py:79-88), device arrays. */
+int hb_hash_items(int64_t n, const uint64_t *items, const uint64_t *replicas, uint64_t seed,
+                  uint64_t *out, void *stream);
+
+/* Number of work items / recommended item size for heavy-node splitting at log2m b. */
+int64_t hb_item_arcs(int b);
+int64_t hb_light_max_deg(int b);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HYPERBALL_B200_H */

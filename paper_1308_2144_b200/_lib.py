@@ -1,0 +1,106 @@
+"""Loader for the in-tree native libraries.
+
+* ``libhyperball_b200.so`` -- the sm_100a kernels behind the C-ABI declared in
+  ``include/hyperball_b200.h``.  There is no CPU fallback: every device entry point
+  raises ``RuntimeError`` when the library is missing or a call fails.
+* ``libhbgraph.so`` -- host C builders for the synthetic benchmark graphs.
+
+Both are built in place by ``__graft_entry__.build()`` (``make -C
+paper_1308_2144_b200/csrc``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+HB_LIB_PATH = os.path.join(_HERE, "libhyperball_b200.so")
+GRAPH_LIB_PATH = os.path.join(_HERE, "libhbgraph.so")
+HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "hyperball_b200.h")
+
+_lock = threading.Lock()
+_hb = None
+_graph = None
+
+_i64 = ctypes.c_int64
+_u64 = ctypes.c_uint64
+_int = ctypes.c_int
+_dbl = ctypes.c_double
+_vp = ctypes.c_void_p
+
+# name -> (restype, argtypes), in header order
+HB_SIGNATURES = {
+    "hb_version": (ctypes.c_char_p, []),
+    "hb_last_error": (ctypes.c_char_p, []),
+    "hb_min_log2m": (_int, []),
+    "hb_max_log2m": (_int, []),
+    "hb_seed": (_int, [_vp, _vp, _i64, _int, _int, _u64, _vp, _vp, _vp, _dbl, _dbl, _vp]),
+    "hb_estimate_rows": (_int, [_vp, _i64, _i64, _int, _vp, _dbl, _dbl, _vp, _vp]),
+    "hb_union_step": (_int, [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _int, _vp, _vp,
+                             _vp, _i64, _vp, _dbl, _dbl, _int, _int, _i64, _vp, _vp, _i64,
+                             _vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp]),
+    "hb_relabel_csr": (_int, [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "hb_hash_items": (_int, [_i64, _vp, _vp, _u64, _vp, _vp]),
+    "hb_item_arcs": (_i64, [_int]),
+    "hb_light_max_deg": (_i64, [_int]),
+}
+
+GRAPH_SIGNATURES = {
+    "hbg_er": (_vp, [_i64, _dbl, _u64, _int]),
+    "hbg_rmat": (_vp, [_int, _i64, _dbl, _dbl, _dbl, _u64, _int]),
+    "hbg_disconnected": (_vp, [_i64, _i64, _dbl, _dbl, _u64, _int]),
+    "hbg_weblike": (_vp, [_i64, _dbl, _i64, _i64, _dbl, _i64, _u64, _int]),
+    "hbg_from_arcs": (_vp, [_i64, _i64, _vp, _vp, _int]),
+    "hbg_n": (_i64, [_vp]),
+    "hbg_m": (_i64, [_vp]),
+    "hbg_copy": (None, [_vp, _vp, _vp]),
+    "hbg_free": (None, [_vp]),
+}
+
+
+def build_native() -> None:
+    """Compile both libraries in place (nvcc for sm_100a + gcc)."""
+    subprocess.run(["make", "-s", "-C", os.path.join(_HERE, "csrc")], check=True)
+
+
+def _bind(path: str, sigs: dict):
+    L = ctypes.CDLL(path)
+    for name, (res, args) in sigs.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    return L
+
+
+def hb():
+    """The CUDA kernel library; raises if it was not built."""
+    global _hb
+    if _hb is None:
+        with _lock:
+            if _hb is None:
+                if not os.path.exists(HB_LIB_PATH):
+                    raise RuntimeError(
+                        f"{HB_LIB_PATH} is missing: build it with __graft_entry__.build() "
+                        "(there is no CPU fallback for the HyperBall hot path)")
+                _hb = _bind(HB_LIB_PATH, HB_SIGNATURES)
+    return _hb
+
+
+def graphlib():
+    global _graph
+    if _graph is None:
+        with _lock:
+            if _graph is None:
+                if not os.path.exists(GRAPH_LIB_PATH):
+                    raise RuntimeError(f"{GRAPH_LIB_PATH} is missing: run __graft_entry__.build()")
+                _graph = _bind(GRAPH_LIB_PATH, GRAPH_SIGNATURES)
+    return _graph
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        msg = hb().hb_last_error().decode(errors="replace")
+        raise RuntimeError(f"{what} failed (code {rc}): {msg}")

@@ -1,0 +1,674 @@
+// hyperball.cu -- sm_100a kernels of the HyperBall hot path and their C-ABI
+// (include/hyperball_b200.h).
+//
+// Reference algorithm: /root/reference/pkg/src/hyperball/_kernels.py:15-114 (estimate,
+// scatter_max, hll_union_range), hll.py:70-158 (hash, register values),
+// centrality.py:132-150 (accumulate).  DESIGN.md explains the data layout, the work
+// decomposition and the roofline of each kernel.
+//
+// Bit-exactness rules:
+//   * sum_j 2^-M[j] is computed as the exact integer sum_j 2^(31-M[j]) times 2^-31 when
+//     every register is <= 31 (always true at register_width 5); otherwise by the
+//     reference's own ascending-j fp64 sum.  Both equal the reference's sequential sum.
+//   * the linear-counting value comes from a host-built table (math.log).
+//   * the accumulate uses explicitly rounded fp64 ops (__dmul_rn/__ddiv_rn/__dadd_rn);
+//     the translation unit is also built with -fmad=false.
+//   * registers are < 128 (rho_max = 65 - b <= 61), so the 7-bit-safe SIMD byte max below
+//     is exact.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "../../include/hyperball_b200.h"
+
+#define HB_MIN_B 4
+#define HB_MAX_B 12
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+int set_err(const char *what, cudaError_t e) {
+  snprintf(g_err, sizeof(g_err), "%s: %s", what, cudaGetErrorString(e));
+  return (int)e;
+}
+int set_err_msg(const char *msg) {
+  snprintf(g_err, sizeof(g_err), "%s", msg);
+  return -1;
+}
+int check_launch(const char *what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_err(what, e);
+  return 0;
+}
+
+// ------------------------------------------------------------------ row geometry
+template <int LOGP>
+struct Geo {
+  static constexpr int P = 1 << LOGP;
+  static constexpr int CH = P / 16;               // 16-byte chunks per row
+  static constexpr int G = CH < 32 ? CH : 32;     // lanes cooperating on one row
+  static constexpr int CPL = CH / G;              // chunks per lane (> 1 only for p > 512)
+  static constexpr int NPW = 32 / G;              // rows handled side by side per warp
+};
+
+// Work-item size for heavy nodes: 16 row loads per lane (16 * NPW arcs), at least 64.
+__host__ __device__ constexpr int64_t item_arcs_for(int b) {
+  return (16 * (32 / ((1 << b) / 16 < 32 ? (1 << b) / 16 : 32))) > 64
+             ? (16 * (32 / ((1 << b) / 16 < 32 ? (1 << b) / 16 : 32)))
+             : 64;
+}
+constexpr int64_t kLightMaxDeg = 64;
+
+// ------------------------------------------------------------------ small helpers
+__device__ __forceinline__ uint32_t prmt_sign(uint32_t d) {
+  uint32_t m;
+  // byte i of m = 0xFF if bit 7 of byte i of d is set, else 0x00 (prmt sign-replicate)
+  asm("prmt.b32 %0, %1, 0, 0xba98;" : "=r"(m) : "r"(d));
+  return m;
+}
+// Per-byte unsigned max of a and b, exact when every byte is < 128.
+__device__ __forceinline__ uint32_t bmax(uint32_t a, uint32_t b) {
+  uint32_t d = (a | 0x80808080u) - b;  // bit 7 of byte i set  <=>  a_i >= b_i
+  uint32_t m = prmt_sign(d);
+  return (a & m) | (b & ~m);
+}
+__device__ __forceinline__ uint4 bmax4(uint4 a, uint4 b) {
+  return make_uint4(bmax(a.x, b.x), bmax(a.y, b.y), bmax(a.z, b.z), bmax(a.w, b.w));
+}
+__device__ __forceinline__ uint4 ldg4(const uint8_t *p) {
+  return __ldg(reinterpret_cast<const uint4 *>(p));
+}
+__device__ __forceinline__ bool test_bit(const uint32_t *bm, int64_t v) {
+  return (__ldg(bm + (v >> 5)) >> (v & 31)) & 1u;
+}
+__device__ __forceinline__ uint4 shfl_xor4(uint4 a, int off) {
+  a.x = __shfl_xor_sync(0xffffffffu, a.x, off);
+  a.y = __shfl_xor_sync(0xffffffffu, a.y, off);
+  a.z = __shfl_xor_sync(0xffffffffu, a.z, off);
+  a.w = __shfl_xor_sync(0xffffffffu, a.w, off);
+  return a;
+}
+__device__ __forceinline__ bool neq4(uint4 a, uint4 b) {
+  return ((a.x ^ b.x) | (a.y ^ b.y) | (a.z ^ b.z) | (a.w ^ b.w)) != 0u;
+}
+__device__ __forceinline__ bool nz4(uint4 a) { return (a.x | a.y | a.z | a.w) != 0u; }
+
+// splitmix64 finaliser (hll.py:70-76)
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+// hll.py:79-88
+__device__ __forceinline__ uint64_t hash_item(uint64_t item, uint64_t replica, uint64_t seed) {
+  uint64_t key = mix64(replica + mix64(seed));
+  return mix64(item + key);
+}
+// 2^-r as an exact double (POW2NEG, hll.py:33), r <= 255
+__device__ __forceinline__ double pow2neg(uint32_t r) {
+  return __hiloint2double((int)((1023u - r) << 20), 0);
+}
+
+// Per-word contribution to the exact register sum: sum over bytes of 2^(31-M) (M <= 31),
+// zero count, running max.
+__device__ __forceinline__ void acc_word(uint32_t w, uint64_t &S, int &zeros, uint32_t &mx) {
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    uint32_t m = (w >> (8 * i)) & 0xffu;
+    zeros += (m == 0u);
+    mx = m > mx ? m : mx;
+    S += (m <= 31u) ? (uint64_t)(1u << (31u - m)) : 0ull;
+  }
+}
+
+struct EstConst {
+  double alpha_p2, lc_cut;
+  const double *lc;  // lc_table[0..p]
+};
+
+// Raw estimate from the (exact) register sum, with the linear-counting switch
+// (_kernels.py:31-33).
+__device__ __forceinline__ double finish_estimate(double s, int zeros, const EstConst &ec) {
+  double e = __ddiv_rn(ec.alpha_p2, s);
+  if (e <= ec.lc_cut && zeros > 0) e = __ldg(ec.lc + zeros);
+  return e;
+}
+
+// Whole-row estimate by one thread (seed / estimate_rows kernels).
+template <int P>
+__device__ double estimate_row_thread(const uint8_t *row, const EstConst &ec) {
+  uint64_t S = 0;
+  int zeros = 0;
+  uint32_t mx = 0;
+  for (int c = 0; c < P / 16; c++) {
+    uint4 q = *reinterpret_cast<const uint4 *>(row + 16 * c);
+    acc_word(q.x, S, zeros, mx);
+    acc_word(q.y, S, zeros, mx);
+    acc_word(q.z, S, zeros, mx);
+    acc_word(q.w, S, zeros, mx);
+  }
+  double s;
+  if (mx <= 31u) {
+    s = (double)S * 0x1p-31;
+  } else {  // reference order: ascending-j fp64 sum (_kernels.py:25-30)
+    s = 0.0;
+    for (int j = 0; j < P; j++) s = __dadd_rn(s, pow2neg(row[j]));
+  }
+  return finish_estimate(s, zeros, ec);
+}
+
+// numpy.maximum(x, 0.0) (centrality.py:134)
+__device__ __forceinline__ double np_max0(double x) { return (x >= 0.0 || x != x) ? x : 0.0; }
+
+// ------------------------------------------------------------------ shared epilogue
+// Group of G lanes finishing node v: merge own row, change test, lazy write, estimate,
+// accumulate.  acc holds the max over merged sources.  Returns the (group-uniform)
+// changed flag.  All lanes of gmask must call it together.
+template <int LOGP>
+__device__ __forceinline__ bool finish_node(int64_t v, const uint4 (&acc)[Geo<LOGP>::CPL],
+                                            bool self_chg, unsigned gmask, int gl,
+                                            const uint8_t *__restrict__ cur,
+                                            uint8_t *__restrict__ nxt, double *__restrict__ est,
+                                            double *__restrict__ sum_dist,
+                                            double *__restrict__ sum_recip, const EstConst &ec,
+                                            double tf) {
+  using Gm = Geo<LOGP>;
+  const uint8_t *crow = cur + (size_t)v * Gm::P;
+  uint8_t *nrow = nxt + (size_t)v * Gm::P;
+  uint4 nw[Gm::CPL];
+  bool diff = false;
+#pragma unroll
+  for (int c = 0; c < Gm::CPL; c++) {
+    uint4 self = ldg4(crow + 16 * (c * Gm::G + gl));
+    nw[c] = bmax4(acc[c], self);
+    diff |= neq4(nw[c], self);
+  }
+  const bool changed = __any_sync(gmask, diff);
+  if (changed || self_chg) {
+#pragma unroll
+    for (int c = 0; c < Gm::CPL; c++)
+      *reinterpret_cast<uint4 *>(nrow + 16 * (c * Gm::G + gl)) = nw[c];
+  }
+  if (changed) {
+    uint64_t S = 0;
+    int zeros = 0;
+    uint32_t mx = 0;
+#pragma unroll
+    for (int c = 0; c < Gm::CPL; c++) {
+      acc_word(nw[c].x, S, zeros, mx);
+      acc_word(nw[c].y, S, zeros, mx);
+      acc_word(nw[c].z, S, zeros, mx);
+      acc_word(nw[c].w, S, zeros, mx);
+    }
+#pragma unroll
+    for (int off = 1; off < Gm::G; off <<= 1) {
+      S += __shfl_xor_sync(gmask, S, off);
+      zeros += __shfl_xor_sync(gmask, zeros, off);
+      uint32_t o = __shfl_xor_sync(gmask, mx, off);
+      mx = o > mx ? o : mx;
+    }
+    if (mx > 31u) __syncwarp(gmask);  // the row was stored above; make it visible
+    if (gl == 0) {
+      double s;
+      if (mx <= 31u) {
+        s = (double)S * 0x1p-31;
+      } else {
+        s = 0.0;
+        for (int j = 0; j < Gm::P; j++) s = __dadd_rn(s, pow2neg(nrow[j]));
+      }
+      const double e = finish_estimate(s, zeros, ec);
+      const double old = est[v];
+      est[v] = e;
+      const double d = np_max0(__dsub_rn(e, old));
+      if (sum_dist) sum_dist[v] = __dadd_rn(sum_dist[v], __dmul_rn(tf, d));
+      if (sum_recip) sum_recip[v] = __dadd_rn(sum_recip[v], __ddiv_rn(d, tf));
+    }
+  }
+  return changed;
+}
+
+// Block-wide sum of two per-thread counters, one atomicAdd per block and counter.
+__device__ __forceinline__ void block_add2(uint32_t a, uint32_t b, unsigned long long *out_a,
+                                           unsigned long long *out_b) {
+  __shared__ uint32_t red[2][32];
+  uint32_t wa = __reduce_add_sync(0xffffffffu, a);
+  uint32_t wb = __reduce_add_sync(0xffffffffu, b);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) { red[0][wid] = wa; red[1][wid] = wb; }
+  __syncthreads();
+  if (wid == 0) {
+    const bool in = lane < (int)(blockDim.x >> 5);
+    uint32_t x = __reduce_add_sync(0xffffffffu, in ? red[0][lane] : 0u);
+    uint32_t y = __reduce_add_sync(0xffffffffu, in ? red[1][lane] : 0u);
+    if (lane == 0) {
+      if (x && out_a) atomicAdd(out_a, (unsigned long long)x);
+      if (y && out_b) atomicAdd(out_b, (unsigned long long)y);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ kernels
+constexpr int kThreads = 256;
+constexpr int kUnroll = 4;
+
+// Light nodes: one group of G lanes per node, NPW nodes per warp side by side.
+// _kernels.py:67-114 restated with the source-skip rule.
+template <int LOGP>
+__global__ void __launch_bounds__(kThreads)
+k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
+        const uint8_t *__restrict__ cur, uint8_t *__restrict__ nxt,
+        const uint32_t *__restrict__ chg_prev, uint32_t *__restrict__ chg_now,
+        double *__restrict__ est, double *__restrict__ sum_dist, double *__restrict__ sum_recip,
+        EstConst ec, int64_t lo, int64_t hi, int64_t max_deg, int dense, double tf,
+        unsigned long long *__restrict__ nch_out, unsigned long long *__restrict__ merged_out) {
+  using Gm = Geo<LOGP>;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane % Gm::G;
+  const int grp = lane / Gm::G;
+  uint32_t my_merged = 0;
+  const unsigned gmask =
+      Gm::G == 32 ? 0xffffffffu : (((1u << (Gm::G & 31)) - 1u) << (grp * Gm::G));
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  uint32_t my_nch = 0;
+  const int64_t start = (lo / Gm::NPW) * Gm::NPW;
+  for (int64_t base = start + warp * Gm::NPW; base < hi; base += nwarps * Gm::NPW) {
+    const int64_t v = base + grp;
+    bool valid = (v >= lo) && (v < hi);
+    int64_t beg = 0, end = 0;
+    if (valid) {
+      beg = __ldg(offsets + v);
+      end = __ldg(offsets + v + 1);
+      if (end - beg > max_deg) valid = false;  // heavy: handled by the item path
+    }
+    const bool self_chg = valid && test_bit(chg_prev, v);
+    uint4 acc[Gm::CPL];
+#pragma unroll
+    for (int c = 0; c < Gm::CPL; c++) acc[c] = make_uint4(0, 0, 0, 0);
+    bool any = false;
+    if (valid) {
+      for (int64_t k = beg; k < end; k += kUnroll) {
+        int32_t w[kUnroll];
+        bool act[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; u++) {
+          act[u] = (k + u) < end;
+          w[u] = act[u] ? __ldg(succ + k + u) : 0;
+        }
+        if (!dense) {
+#pragma unroll
+          for (int u = 0; u < kUnroll; u++) act[u] = act[u] && test_bit(chg_prev, w[u]);
+        }
+        uint4 r[kUnroll][Gm::CPL];
+#pragma unroll
+        for (int u = 0; u < kUnroll; u++)
+#pragma unroll
+          for (int c = 0; c < Gm::CPL; c++)
+            r[u][c] = act[u] ? ldg4(cur + (size_t)w[u] * Gm::P + 16 * (c * Gm::G + gl))
+                             : make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int u = 0; u < kUnroll; u++) {
+          any |= act[u];
+          my_merged += (act[u] && gl == 0);
+#pragma unroll
+          for (int c = 0; c < Gm::CPL; c++) acc[c] = bmax4(acc[c], r[u][c]);
+        }
+      }
+    }
+    bool changed = false;
+    if (valid && (any || self_chg))
+      changed = finish_node<LOGP>(v, acc, self_chg, gmask, gl, cur, nxt, est, sum_dist,
+                                  sum_recip, ec, tf);
+    // Warp-level aggregation of the NPW change bits (they share one bitmap word).
+    const unsigned b = __ballot_sync(0xffffffffu, changed && gl == 0);
+    if (lane == 0 && b) {
+      uint32_t m = 0;
+#pragma unroll
+      for (int g = 0; g < Gm::NPW; g++) m |= ((b >> (g * Gm::G)) & 1u) << g;
+      atomicOr(chg_now + (base >> 5), m << (base & 31));
+      my_nch += __popc(m);
+    }
+  }
+  block_add2(my_nch, my_merged, nch_out, merged_out);
+}
+
+// Heavy nodes, phase 1: one warp per work item (a slice of one node's arcs).  The warp
+// is NPW arc slots of G lanes; slots stride over the slice, then a shuffle tree merges
+// the slots and slot 0 writes the partial row.
+template <int LOGP>
+__global__ void __launch_bounds__(kThreads)
+k_heavy_partial(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
+                const uint8_t *__restrict__ cur, const uint32_t *__restrict__ chg_prev,
+                const int32_t *__restrict__ item_node, const int64_t *__restrict__ item_beg,
+                int64_t n_items, int64_t item_arcs, int dense, uint8_t *__restrict__ partial,
+                unsigned long long *__restrict__ merged_out) {
+  using Gm = Geo<LOGP>;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane % Gm::G;
+  const int slot = lane / Gm::G;
+  uint32_t my_merged = 0;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < n_items; i += nwarps) {
+    const int64_t v = __ldg(item_node + i);
+    const int64_t beg = __ldg(item_beg + i);
+    int64_t end = __ldg(offsets + v + 1);
+    if (end > beg + item_arcs) end = beg + item_arcs;
+    uint4 acc[Gm::CPL];
+#pragma unroll
+    for (int c = 0; c < Gm::CPL; c++) acc[c] = make_uint4(0, 0, 0, 0);
+    for (int64_t k = beg + slot; k < end; k += (int64_t)Gm::NPW * kUnroll) {
+      int32_t w[kUnroll];
+      bool act[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; u++) {
+        const int64_t kk = k + (int64_t)u * Gm::NPW;
+        act[u] = kk < end;
+        w[u] = act[u] ? __ldg(succ + kk) : 0;
+      }
+      if (!dense) {
+#pragma unroll
+        for (int u = 0; u < kUnroll; u++) act[u] = act[u] && test_bit(chg_prev, w[u]);
+      }
+      uint4 r[kUnroll][Gm::CPL];
+#pragma unroll
+      for (int u = 0; u < kUnroll; u++)
+#pragma unroll
+        for (int c = 0; c < Gm::CPL; c++)
+          r[u][c] = act[u] ? ldg4(cur + (size_t)w[u] * Gm::P + 16 * (c * Gm::G + gl))
+                           : make_uint4(0, 0, 0, 0);
+#pragma unroll
+      for (int u = 0; u < kUnroll; u++) {
+        my_merged += (act[u] && gl == 0);
+#pragma unroll
+        for (int c = 0; c < Gm::CPL; c++) acc[c] = bmax4(acc[c], r[u][c]);
+      }
+    }
+#pragma unroll
+    for (int off = Gm::G; off < 32; off <<= 1)
+#pragma unroll
+      for (int c = 0; c < Gm::CPL; c++) acc[c] = bmax4(acc[c], shfl_xor4(acc[c], off));
+    if (slot == 0) {
+#pragma unroll
+      for (int c = 0; c < Gm::CPL; c++)
+        *reinterpret_cast<uint4 *>(partial + (size_t)i * Gm::P + 16 * (c * Gm::G + gl)) = acc[c];
+    }
+  }
+  block_add2(my_merged, 0u, merged_out, nullptr);
+}
+
+// Heavy nodes, phase 2: one group per heavy node merges its partial rows and runs the
+// shared epilogue.
+template <int LOGP>
+__global__ void __launch_bounds__(kThreads)
+k_heavy_finish(const int32_t *__restrict__ heavy_nodes, const int32_t *__restrict__ item_first,
+               int64_t n_heavy, const uint8_t *__restrict__ partial,
+               const uint8_t *__restrict__ cur, uint8_t *__restrict__ nxt,
+               const uint32_t *__restrict__ chg_prev, uint32_t *__restrict__ chg_now,
+               double *__restrict__ est, double *__restrict__ sum_dist,
+               double *__restrict__ sum_recip, EstConst ec, double tf,
+               unsigned long long *__restrict__ nch_out) {
+  using Gm = Geo<LOGP>;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane % Gm::G;
+  const int grp = lane / Gm::G;
+  const unsigned gmask =
+      Gm::G == 32 ? 0xffffffffu : (((1u << (Gm::G & 31)) - 1u) << (grp * Gm::G));
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  uint32_t my_nch = 0;
+  for (int64_t base = warp * Gm::NPW; base < n_heavy; base += nwarps * Gm::NPW) {
+    const int64_t j = base + grp;
+    if (j < n_heavy) {
+      const int64_t v = __ldg(heavy_nodes + j);
+      const int i0 = __ldg(item_first + j), i1 = __ldg(item_first + j + 1);
+      uint4 acc[Gm::CPL];
+#pragma unroll
+      for (int c = 0; c < Gm::CPL; c++) acc[c] = make_uint4(0, 0, 0, 0);
+      for (int i = i0; i < i1; i++)
+#pragma unroll
+        for (int c = 0; c < Gm::CPL; c++)
+          acc[c] = bmax4(acc[c], ldg4(partial + (size_t)i * Gm::P + 16 * (c * Gm::G + gl)));
+      bool any = false;
+#pragma unroll
+      for (int c = 0; c < Gm::CPL; c++) any |= nz4(acc[c]);
+      any = __any_sync(gmask, any);
+      const bool self_chg = test_bit(chg_prev, v);
+      if (any || self_chg) {
+        const bool changed = finish_node<LOGP>(v, acc, self_chg, gmask, gl, cur, nxt, est,
+                                               sum_dist, sum_recip, ec, tf);
+        if (changed && gl == 0) {
+          atomicOr(chg_now + (v >> 5), 1u << (v & 31));
+          my_nch++;
+        }
+      }
+    }
+  }
+  block_add2(my_nch, 0u, nch_out, nullptr);
+}
+
+// Seed (engine.py:153-162): zero the row, scatter-max every replica item, estimate.
+template <int LOGP>
+__global__ void __launch_bounds__(kThreads)
+k_seed(uint8_t *__restrict__ regs, double *__restrict__ est, int64_t n,
+       const int32_t *__restrict__ perm, const int64_t *__restrict__ weights, int width,
+       uint64_t seed, EstConst ec) {
+  using Gm = Geo<LOGP>;
+  const int b = LOGP;
+  const int sat = (1 << width) - 1;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t orig = perm ? (uint64_t)__ldg(perm + i) : (uint64_t)i;
+    uint8_t *row = regs + (size_t)i * Gm::P;
+    for (int c = 0; c < Gm::CH; c++)
+      reinterpret_cast<uint4 *>(row)[c] = make_uint4(0, 0, 0, 0);
+    const int64_t w = weights ? __ldg(weights + orig) : 1;
+    for (int64_t r = 1; r <= w; r++) {
+      const uint64_t h = hash_item(orig, (uint64_t)r, seed);
+      const uint32_t idx = (uint32_t)(h & (uint64_t)(Gm::P - 1));
+      const uint64_t rest = h >> b;
+      const int bitlen = rest ? 64 - __clzll((long long)rest) : 0;
+      int rho = (64 - b + 1) - bitlen;  // hll.py:138-141,156
+      if (rho > sat) rho = sat;
+      if ((uint8_t)rho > row[idx]) row[idx] = (uint8_t)rho;
+    }
+    est[i] = estimate_row_thread<Gm::P>(row, ec);
+  }
+}
+
+template <int LOGP>
+__global__ void __launch_bounds__(kThreads)
+k_estimate_rows(const uint8_t *__restrict__ regs, int64_t lo, int64_t hi, EstConst ec,
+                double *__restrict__ out) {
+  using Gm = Geo<LOGP>;
+  for (int64_t v = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < hi;
+       v += (int64_t)gridDim.x * blockDim.x)
+    out[v] = estimate_row_thread<Gm::P>(regs + (size_t)v * Gm::P, ec);
+}
+
+__global__ void k_relabel(int64_t n, const int64_t *__restrict__ old_off,
+                          const int32_t *__restrict__ old_succ, const int32_t *__restrict__ perm,
+                          const int32_t *__restrict__ rank, const int64_t *__restrict__ new_off,
+                          int32_t *__restrict__ new_succ) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < n; i += nwarps) {
+    const int64_t o = __ldg(perm + i);
+    const int64_t b0 = __ldg(old_off + o), len = __ldg(old_off + o + 1) - b0;
+    const int64_t d0 = __ldg(new_off + i);
+    for (int64_t k = lane; k < len; k += 32) new_succ[d0 + k] = __ldg(rank + __ldg(old_succ + b0 + k));
+  }
+}
+
+__global__ void k_hash(int64_t n, const uint64_t *__restrict__ items,
+                       const uint64_t *__restrict__ replicas, uint64_t seed,
+                       uint64_t *__restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = hash_item(items[i], replicas[i], seed);
+}
+
+// ------------------------------------------------------------------ launch helpers
+int g_num_sms = 0;
+int num_sms() {
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+        g_num_sms <= 0)
+      g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+// Grid for `work_warps` warps of work: enough CTAs to fill every SM several times over,
+// capped by the work; kernels grid-stride over the rest.
+unsigned grid_for_warps(int64_t work_warps) {
+  const int64_t per_cta = kThreads / 32;
+  int64_t ctas = (work_warps + per_cta - 1) / per_cta;
+  const int64_t cap = (int64_t)num_sms() * 8;  // 8 resident 256-thread CTAs per SM
+  if (ctas > cap) ctas = cap;
+  if (ctas < 1) ctas = 1;
+  return (unsigned)ctas;
+}
+unsigned grid_for_threads(int64_t work) { return grid_for_warps((work + 31) / 32); }
+
+template <int LOGP>
+int union_step_impl(int64_t lo, int64_t hi, const int64_t *offsets, const int32_t *succ,
+                    const uint8_t *cur, uint8_t *nxt, const uint32_t *chg_prev,
+                    uint32_t *chg_now, double *est, double *sum_dist, double *sum_recip,
+                    double tf, EstConst ec, int dense, int64_t light_max_deg,
+                    const int32_t *heavy_nodes, const int32_t *item_first, int64_t n_heavy,
+                    const int32_t *item_node, const int64_t *item_beg, int64_t n_items,
+                    int64_t item_arcs, uint8_t *partial, unsigned long long *nch,
+                    unsigned long long *merged, cudaStream_t s) {
+  using Gm = Geo<LOGP>;
+  if (n_items > 0) {
+    k_heavy_partial<LOGP><<<grid_for_warps(n_items), kThreads, 0, s>>>(
+        offsets, succ, cur, chg_prev, item_node, item_beg, n_items, item_arcs, dense, partial,
+        merged);
+    if (int e = check_launch("k_heavy_partial")) return e;
+  }
+  if (hi > lo) {
+    const int64_t warps = (hi - lo + Gm::NPW - 1) / Gm::NPW + 1;
+    k_light<LOGP><<<grid_for_warps(warps), kThreads, 0, s>>>(
+        offsets, succ, cur, nxt, chg_prev, chg_now, est, sum_dist, sum_recip, ec, lo, hi,
+        light_max_deg, dense, tf, nch, merged);
+    if (int e = check_launch("k_light")) return e;
+  }
+  if (n_heavy > 0) {
+    k_heavy_finish<LOGP><<<grid_for_warps((n_heavy + Gm::NPW - 1) / Gm::NPW), kThreads, 0, s>>>(
+        heavy_nodes, item_first, n_heavy, partial, cur, nxt, chg_prev, chg_now, est, sum_dist,
+        sum_recip, ec, tf, nch);
+    if (int e = check_launch("k_heavy_finish")) return e;
+  }
+  return 0;
+}
+
+#define HB_DISPATCH(B, CALL)                 \
+  switch (B) {                               \
+    case 4: { constexpr int LB = 4; CALL; } break;   \
+    case 5: { constexpr int LB = 5; CALL; } break;   \
+    case 6: { constexpr int LB = 6; CALL; } break;   \
+    case 7: { constexpr int LB = 7; CALL; } break;   \
+    case 8: { constexpr int LB = 8; CALL; } break;   \
+    case 9: { constexpr int LB = 9; CALL; } break;   \
+    case 10: { constexpr int LB = 10; CALL; } break; \
+    case 11: { constexpr int LB = 11; CALL; } break; \
+    case 12: { constexpr int LB = 12; CALL; } break; \
+    default: return set_err_msg("unsupported log2m (b) for this build");  \
+  }
+
+}  // namespace
+
+// ------------------------------------------------------------------ C-ABI
+extern "C" {
+
+const char *hb_version(void) { return "hyperball_b200 0.1 (sm_100a)"; }
+const char *hb_last_error(void) { return g_err; }
+int hb_min_log2m(void) { return HB_MIN_B; }
+int hb_max_log2m(void) { return HB_MAX_B; }
+int64_t hb_item_arcs(int b) { return item_arcs_for(b); }
+int64_t hb_light_max_deg(int b) { (void)b; return kLightMaxDeg; }
+
+int hb_seed(uint8_t *regs, double *est, int64_t n, int b, int register_width, uint64_t seed,
+            const int32_t *perm, const int64_t *weights, const double *lc_table,
+            double alpha_p2, double lc_cut, void *stream) {
+  if (n < 0 || !regs || !est || !lc_table) return set_err_msg("hb_seed: bad arguments");
+  if (register_width < 1 || register_width > 8) return set_err_msg("hb_seed: bad register_width");
+  if (n == 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  EstConst ec{alpha_p2, lc_cut, lc_table};
+  HB_DISPATCH(b, (k_seed<LB><<<grid_for_threads(n), kThreads, 0, s>>>(
+                     regs, est, n, perm, weights, register_width, seed, ec)));
+  return check_launch("k_seed");
+}
+
+int hb_estimate_rows(const uint8_t *regs, int64_t lo, int64_t hi, int b,
+                     const double *lc_table, double alpha_p2, double lc_cut, double *out,
+                     void *stream) {
+  if (hi <= lo) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  EstConst ec{alpha_p2, lc_cut, lc_table};
+  HB_DISPATCH(b, (k_estimate_rows<LB><<<grid_for_threads(hi - lo), kThreads, 0, s>>>(
+                     regs, lo, hi, ec, out)));
+  return check_launch("k_estimate_rows");
+}
+
+int hb_union_step(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets,
+                  const int32_t *succ, const uint8_t *cur, uint8_t *nxt,
+                  const uint32_t *chg_prev, uint32_t *chg_now, int clear_chg_now,
+                  double *est, double *sum_dist, double *sum_recip, int64_t t,
+                  const double *lc_table, double alpha_p2, double lc_cut, int b, int dense,
+                  int64_t light_max_deg, const int32_t *heavy_nodes, const int32_t *item_first,
+                  int64_t n_heavy, const int32_t *item_node, const int64_t *item_beg,
+                  int64_t n_items, int64_t item_arcs, uint8_t *partial, uint64_t *nch_out,
+                  uint64_t *merged_out, void *stream) {
+  if (n < 0 || lo < 0 || hi > n || lo > hi || t < 1 || !nch_out)
+    return set_err_msg("hb_union_step: bad range / t / nch_out");
+  if ((n_items > 0 && (!item_node || !item_beg || !partial)) ||
+      (n_heavy > 0 && (!heavy_nodes || !item_first || !partial)))
+    return set_err_msg("hb_union_step: heavy schedule arrays missing");
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(nch_out, 0, sizeof(uint64_t), s)) != cudaSuccess)
+    return set_err("hb_union_step memset nch", e);
+  if (merged_out && (e = cudaMemsetAsync(merged_out, 0, sizeof(uint64_t), s)) != cudaSuccess)
+    return set_err("hb_union_step memset merged", e);
+  if (clear_chg_now && n > 0) {
+    if ((e = cudaMemsetAsync(chg_now, 0, sizeof(uint32_t) * (size_t)((n + 31) / 32), s)) !=
+        cudaSuccess)
+      return set_err("hb_union_step memset chg_now", e);
+  }
+  if (n == 0) return 0;
+  EstConst ec{alpha_p2, lc_cut, lc_table};
+  const double tf = (double)t;
+  HB_DISPATCH(b, return union_step_impl<LB>(
+                     lo, hi, offsets, succ, cur, nxt, chg_prev, chg_now, est, sum_dist,
+                     sum_recip, tf, ec, dense, light_max_deg, heavy_nodes, item_first, n_heavy,
+                     item_node, item_beg, n_items, item_arcs, partial,
+                     reinterpret_cast<unsigned long long *>(nch_out),
+                     reinterpret_cast<unsigned long long *>(merged_out), s));
+  return 0;
+}
+
+int hb_relabel_csr(int64_t n, const int64_t *old_offsets, const int32_t *old_succ,
+                   const int32_t *perm, const int32_t *rank, const int64_t *new_offsets,
+                   int32_t *new_succ, void *stream) {
+  if (n <= 0) return 0;
+  k_relabel<<<grid_for_warps(n), kThreads, 0, (cudaStream_t)stream>>>(
+      n, old_offsets, old_succ, perm, rank, new_offsets, new_succ);
+  return check_launch("k_relabel");
+}
+
+int hb_hash_items(int64_t n, const uint64_t *items, const uint64_t *replicas, uint64_t seed,
+                  uint64_t *out, void *stream) {
+  if (n <= 0) return 0;
+  k_hash<<<grid_for_threads(n), kThreads, 0, (cudaStream_t)stream>>>(n, items, replicas, seed,
+                                                                      out);
+  return check_launch("k_hash");
+}
+
+}  // extern "C"

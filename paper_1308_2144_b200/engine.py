@@ -1,0 +1,561 @@
+"""Ball-growth engine on the B200: the reference's public API (engine.py:52-435) over
+device-resident state and the sm_100a kernels of ``libhyperball_b200.so``.
+
+Drop-in surface (same names, argument meanings, errors and result layout as
+/root/reference/pkg/src/hyperball/engine.py):
+
+* ``HyperBallConfig``  engine.py:82-97, plus ``device`` and ``schedule`` (B200 fields)
+* ``HyperBallState``   engine.py:216-280 (``t``, ``num_changed``, ``est``,
+  ``changed_prev``, ``estimates()``, ``register_matrix()``, ``counters()``, ``save``)
+* ``initialize`` / ``iterate`` / ``run`` / ``resume`` / ``load_state``
+  engine.py:283-435, ``ConvergenceError`` engine.py:52-60, ``BallObserver`` 63-79.
+
+What runs where: the graph (CSR of G^T), both register buffers, the change bitmaps, the
+estimates and the fused accumulator sums live in HBM for the whole run.  One iteration is
+one ``hb_union_step`` call (heavy-item pass, light pass, heavy finish) plus a
+single 8-byte read-back of the changed count, which is the loop's termination test
+exactly as in engine.py:390,426-427.  Host copies are made only when a caller asks for
+them (``state.est``, ``register_matrix()``, a non-fused observer).  There is no CPU
+fallback: without a CUDA device or the built library every entry point raises.
+"""
+
+from __future__ import annotations
+
+import io
+import math
+import struct
+import time
+from dataclasses import dataclass, field
+from typing import IO, Iterable
+
+import numpy as np
+import torch
+
+from . import _lib
+from .centrality import BallObserver, CentralityAccumulator, fusable
+from .hll import CounterArray, CounterParams, estimator_constants, lc_table
+from .schedule import Schedule, build_schedule
+
+CHECKPOINT_MAGIC = b"HBCK"
+CHECKPOINT_VERSION = 1
+
+BACKEND_PROBABILISTIC = "probabilistic"
+BACKEND_EXACT = "exact"
+_BACKEND_ALIASES = {"hll": BACKEND_PROBABILISTIC}
+
+
+class ConvergenceError(RuntimeError):
+    """Safety-cap overrun; reports the iteration and open counter count."""
+
+    def __init__(self, t: int, num_changed: int):
+        super().__init__(f"max_iterations reached at t={t} with {num_changed} counters "
+                         f"still changing")
+        self.t = t
+        self.num_changed = num_changed
+
+
+@dataclass
+class HyperBallConfig:
+    params: CounterParams = field(default_factory=lambda: CounterParams(b=6))
+    weights: object | None = None
+    backend: str = BACKEND_PROBABILISTIC
+    workers: int = 1
+    max_iterations: int | None = None
+    skip_stable_nodes: bool = True
+    progress: IO[str] | None = None
+    device: object | None = None        # B200: CUDA device (index, "cuda:k" or None = current)
+    schedule: str = "auto"              # B200: "auto" | "identity" | "degree" (schedule.py)
+
+    def __post_init__(self) -> None:
+        self.backend = _BACKEND_ALIASES.get(self.backend, self.backend)
+        if self.backend not in (BACKEND_PROBABILISTIC, BACKEND_EXACT):
+            raise ValueError(f"unknown counter backend {self.backend!r}")
+        if self.workers < 1:
+            raise ValueError("workers must be >= 1")
+        if self.schedule not in ("auto", "identity", "degree"):
+            raise ValueError(f"unknown schedule {self.schedule!r}")
+
+
+# ---------------------------------------------------------------------------- helpers
+
+def _weights_array(weights, n: int):
+    if weights is None:
+        return None
+    vals = np.asarray(getattr(weights, "values", weights), dtype=np.int64)
+    if vals.shape[0] != n:
+        raise ValueError(f"weights length {vals.shape[0]} != node count {n}")
+    if n and vals.min() < 1:
+        raise ValueError("node weights must be >= 1")
+    return vals
+
+
+def _check_weighted_width(params: CounterParams, vals: np.ndarray) -> None:
+    """Registers must be able to reach log2(total weight) (engine.py:122-135)."""
+    total = max(int(vals.sum()), 2)
+    needed = math.log2(total)
+    if params.saturation < math.ceil(needed):
+        raise ValueError(
+            f"register_width={params.register_width} saturates at {params.saturation}, "
+            f"below log2(total weight) = {needed:.1f}; register_width 6 (or wider) is "
+            f"required for this weighting")
+
+
+def _resolve_device(dev) -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1308_2144_b200 needs a CUDA device (no CPU fallback)")
+    if dev is None:
+        return torch.device("cuda", torch.cuda.current_device())
+    if isinstance(dev, int):
+        return torch.device("cuda", dev)
+    d = torch.device(dev)
+    if d.type != "cuda":
+        raise ValueError(f"device must be a CUDA device, got {dev!r}")
+    return d if d.index is not None else torch.device("cuda", torch.cuda.current_device())
+
+
+def pack_bits(flags: torch.Tensor) -> torch.Tensor:
+    """bool [n] -> int32 bitmap [ceil(n/32)], bit v & 31 of word v >> 5."""
+    n = flags.numel()
+    words = (n + 31) // 32
+    padded = torch.zeros(words * 32, dtype=torch.int64, device=flags.device)
+    padded[:n] = flags.to(torch.int64)
+    shifts = torch.arange(32, dtype=torch.int64, device=flags.device)
+    w = (padded.view(words, 32) << shifts).sum(dim=1)
+    return torch.where(w >= 2**31, w - 2**32, w).to(torch.int32)
+
+
+def unpack_bits(words: torch.Tensor, n: int) -> torch.Tensor:
+    shifts = torch.arange(32, dtype=torch.int64, device=words.device)
+    bits = (words.to(torch.int64).unsqueeze(1) >> shifts) & 1
+    return bits.view(-1)[:n].to(torch.bool)
+
+
+def _graph_arrays(g):
+    return g.offsets, g.successors
+
+
+def _graph_key(g):
+    off, suc = _graph_arrays(g)
+    return (id(off), id(suc), int(np.asarray(off).shape[0]) - 1 if not isinstance(off, torch.Tensor)
+            else off.numel() - 1)
+
+
+class _DeviceSums:
+    """Device-resident CentralityAccumulator sums (internal node order)."""
+
+    def __init__(self, dev: "_Device", acc):
+        self.dev = dev
+        self.acc = acc
+        self.foreign = not isinstance(acc, CentralityAccumulator)
+        if self.foreign:
+            sd, sr = acc.sum_dist, acc.sum_recip
+        else:
+            sd, sr = acc._sum_dist, acc._sum_recip
+        self.host_ids = (id(sd), id(sr))
+        self.sum_dist = dev.to_internal(np.asarray(sd, dtype=np.float64))
+        self.sum_recip = dev.to_internal(np.asarray(sr, dtype=np.float64))
+        self.dirty = False
+        self.stale = False
+
+    def pull_into(self, acc) -> None:
+        sd = self.dev.to_host(self.sum_dist)
+        sr = self.dev.to_host(self.sum_recip)
+        self.dirty = False
+        if self.foreign:
+            acc.sum_dist, acc.sum_recip = sd, sr
+            self.host_ids = (id(acc.sum_dist), id(acc.sum_recip))
+        else:
+            acc._sum_dist, acc._sum_recip = sd, sr
+
+    def invalidate(self) -> None:
+        self.stale = True
+
+    def still_valid(self) -> bool:
+        if self.stale:
+            return False
+        if self.foreign:
+            return self.host_ids == (id(self.acc.sum_dist), id(self.acc.sum_recip))
+        return True
+
+
+class _Device:
+    """Per-run device resources; all per-node arrays are in internal (schedule) order."""
+
+    def __init__(self, g, config: HyperBallConfig, world: int = 1, rank_id: int = 0):
+        self.params = config.params
+        self.b = config.params.b
+        self.p = config.params.p
+        L = _lib.hb()
+        if not (L.hb_min_log2m() <= self.b <= L.hb_max_log2m()):
+            raise ValueError(f"log2m b={self.b} outside the built range "
+                             f"[{L.hb_min_log2m()}, {L.hb_max_log2m()}]")
+        self.device = _resolve_device(config.device)
+        self.stream = torch.cuda.current_stream(self.device)
+        self.order = config.schedule
+        self.world, self.rank_id = world, rank_id
+        self._build_graph(g)
+        n, p = self.n, self.p
+        words = max((n + 31) // 32, 1)
+        dv = self.device
+        self.cur = torch.empty((n, p), dtype=torch.uint8, device=dv)
+        self.nxt = torch.empty((n, p), dtype=torch.uint8, device=dv)
+        self.chg_prev = torch.full((words,), -1, dtype=torch.int32, device=dv)
+        self.chg_now = torch.zeros((words,), dtype=torch.int32, device=dv)
+        self.est = torch.zeros(n, dtype=torch.float64, device=dv)
+        self.lc = torch.from_numpy(lc_table(p)).to(dv)
+        self.alpha_p2, self.lc_cut, _ = estimator_constants(p)
+        self.counts = torch.zeros(2, dtype=torch.int64, device=dv)   # [changed, merged arcs]
+        self.merged_total = 0         # arcs whose source row was merged, all iterations
+        self.prev_all = True          # chg_prev is all-ones (first iteration)
+        self.full_pass = True         # zero in-degree nodes may still need their copy
+        self.launches = 0             # kernels launched by hb_union_step calls
+
+    # -- graph ---------------------------------------------------------------
+    def _build_graph(self, g) -> None:
+        off, suc = _graph_arrays(g)
+        with torch.cuda.device(self.device):
+            self.sched: Schedule = build_schedule(off, suc, self.b, self.device, self.order,
+                                                  self.world, self.rank_id, self.stream)
+        self.n = self.sched.n
+        self.graph_key = _graph_key(g)
+
+    def bind_graph(self, g) -> None:
+        if _graph_key(g) == self.graph_key:
+            return
+        off, _ = _graph_arrays(g)
+        n_new = (off.numel() if isinstance(off, torch.Tensor) else np.asarray(off).shape[0]) - 1
+        if n_new != self.n:
+            raise ValueError(f"graph has {n_new} nodes, state has {self.n}")
+        # different graph object: carry the state over in original order
+        snap = self.snapshot_original()
+        self._build_graph(g)
+        self.restore_original(*snap)
+
+    # -- order conversion ----------------------------------------------------
+    def to_internal(self, host_or_dev) -> torch.Tensor:
+        x = host_or_dev
+        if not isinstance(x, torch.Tensor):
+            x = torch.from_numpy(np.ascontiguousarray(x))
+        return self.sched.to_internal(x.to(self.device)).contiguous()
+
+    def to_host(self, x: torch.Tensor) -> np.ndarray:
+        return self.sched.to_original(x).cpu().numpy()
+
+    def snapshot_original(self):
+        s = self.sched
+        cur = s.to_original(self.cur)
+        nxt = s.to_original(self.nxt)
+        est = s.to_original(self.est)
+        prev = s.to_original(unpack_bits(self.chg_prev, self.n))
+        return cur, nxt, est, prev
+
+    def restore_original(self, cur, nxt, est, prev) -> None:
+        s = self.sched
+        self.cur = s.to_internal(cur).contiguous()
+        self.nxt = s.to_internal(nxt).contiguous()
+        self.est = s.to_internal(est).contiguous()
+        self.chg_prev = pack_bits(s.to_internal(prev))
+
+    # -- kernels -------------------------------------------------------------
+    def seed(self, weights: np.ndarray | None) -> None:
+        w = None
+        if weights is not None:
+            w = torch.from_numpy(np.ascontiguousarray(weights, dtype=np.int64)).to(self.device)
+        perm = self.sched.perm
+        _lib.check(_lib.hb().hb_seed(
+            self.cur.data_ptr(), self.est.data_ptr(), self.n, self.b,
+            self.params.register_width, self.params.seed & ((1 << 64) - 1),
+            perm.data_ptr() if perm is not None else None,
+            w.data_ptr() if w is not None else None, self.lc.data_ptr(), self.alpha_p2,
+            self.lc_cut, self.stream.cuda_stream), "hb_seed")
+        self.launches += 1 if self.n else 0
+        self._seed_weights = w
+
+    def union_step(self, t: int, dense: bool, sums: _DeviceSums | None) -> int:
+        s = self.sched
+        light_hi = s.light_hi if self.full_pass else s.light_hi_steady
+        sd = sums.sum_dist.data_ptr() if sums is not None else None
+        sr = sums.sum_recip.data_ptr() if sums is not None else None
+        _lib.check(_lib.hb().hb_union_step(
+            self.n, s.light_lo, light_hi, s.offsets.data_ptr(), s.succ.data_ptr(),
+            self.cur.data_ptr(), self.nxt.data_ptr(), self.chg_prev.data_ptr(),
+            self.chg_now.data_ptr(), 1, self.est.data_ptr(), sd, sr, t, self.lc.data_ptr(),
+            self.alpha_p2, self.lc_cut, self.b, int(dense), s.light_max_deg,
+            s.heavy_nodes.data_ptr(), s.item_first.data_ptr(), s.n_heavy,
+            s.item_node.data_ptr(), s.item_beg.data_ptr(), s.n_items, s.item_arcs,
+            s.partial.data_ptr(), self.counts.data_ptr(), self.counts.data_ptr() + 8,
+            self.stream.cuda_stream), "hb_union_step")
+        self.launches += (light_hi > s.light_lo) + (s.n_items > 0) + (s.n_heavy > 0)
+        nch, merged = (int(x) for x in self.counts.cpu())
+        self.last_merged = merged
+        self.merged_total += merged
+        return nch
+
+    def swap(self) -> None:
+        self.cur, self.nxt = self.nxt, self.cur
+        self.chg_prev, self.chg_now = self.chg_now, self.chg_prev
+        self.prev_all = False
+        self.full_pass = False
+
+
+class HyperBallState:
+    """Engine state resident on the device; host views are copies in original node order.
+
+    At the end of iteration t, counter v holds the radius-t ball around v, ``est[v]`` its
+    size estimate and ``changed_prev[v]`` whether v's counter moved in iteration t.
+    """
+
+    def __init__(self, config: HyperBallConfig, n: int, dev: _Device | None):
+        self.config = config
+        self.n = n
+        self.t = 0
+        self.num_changed = n
+        self._dev = dev
+        self._sums: _DeviceSums | None = None
+
+    # host views -------------------------------------------------------------
+    @property
+    def est(self) -> np.ndarray:
+        if self._dev is None:
+            return np.zeros(0, dtype=np.float64)
+        return self._dev.to_host(self._dev.est)
+
+    def estimates(self) -> np.ndarray:
+        """Current per-node ball-size estimates (a copy)."""
+        return self.est
+
+    @property
+    def changed_prev(self) -> np.ndarray:
+        if self._dev is None:
+            return np.zeros(0, dtype=np.bool_)
+        d = self._dev
+        return d.to_host(unpack_bits(d.chg_prev, d.n))
+
+    def register_matrix(self) -> np.ndarray:
+        """Host copy of the working counter rows, uint8 [n, p], original order, read-only."""
+        if self._dev is None:
+            m = np.zeros((0, self.config.params.p), dtype=np.uint8)
+        else:
+            m = self._dev.to_host(self._dev.cur)
+        m.setflags(write=False)
+        return m
+
+    def counters(self) -> CounterArray:
+        """Bit-packed snapshot of the current counters."""
+        return CounterArray.from_dense(self.register_matrix(), self.config.params)
+
+    @property
+    def kernel_launches(self) -> int:
+        return 0 if self._dev is None else self._dev.launches
+
+    # checkpointing (engine.py:254-280, HBCK v1, probabilistic kind) -------------
+    def save(self, path) -> None:
+        pr = self.config.params
+        blob_cur = CounterArray.from_dense(self.register_matrix(), pr).to_blob()
+        blob_nxt = CounterArray(self.n, pr).to_blob()
+        buf = io.BytesIO()
+        buf.write(CHECKPOINT_MAGIC)
+        buf.write(struct.pack("<HBQQQ", CHECKPOINT_VERSION, 0, self.n, self.t,
+                              self.num_changed))
+        buf.write(struct.pack("<BBQ", pr.b, pr.register_width, pr.seed & ((1 << 64) - 1)))
+        for blob in (blob_cur, blob_nxt):
+            buf.write(struct.pack("<Q", len(blob)))
+            buf.write(blob)
+        buf.write(self.changed_prev.astype(np.bool_).tobytes())
+        buf.write(self.est.astype(np.float64).tobytes())
+        with open(path, "wb") as fh:
+            fh.write(buf.getvalue())
+
+
+# ---------------------------------------------------------------------------- API
+
+def initialize(g, config: HyperBallConfig) -> HyperBallState:
+    """Seed one counter per node with item (v, 1) (or its weight replicas) on the device."""
+    off = g.offsets
+    n = (off.numel() if isinstance(off, torch.Tensor) else np.asarray(off).shape[0]) - 1
+    if config.backend != BACKEND_PROBABILISTIC:
+        raise ValueError("the B200 engine implements the probabilistic (HyperLogLog) backend "
+                         "only; the exact bitset backend is a CPU validation tool")
+    w = _weights_array(config.weights, n)
+    if w is not None:
+        _check_weighted_width(config.params, w)
+    dev = _Device(g, config)
+    state = HyperBallState(config, n, dev)
+    dev.seed(w)
+    return state
+
+
+def _split_observers(state: HyperBallState, observers):
+    fused, generic = None, []
+    for obs in observers:
+        if fused is None and fusable(obs, state.n):
+            fused = obs
+        else:
+            generic.append(obs)
+    return fused, generic
+
+
+def _bind_sums(state: HyperBallState, acc) -> _DeviceSums | None:
+    dev = state._dev
+    if acc is None:
+        return None
+    cur = state._sums
+    if cur is not None and cur.acc is acc and cur.dev is dev and cur.still_valid():
+        return cur
+    if cur is not None and cur.dirty and cur.acc is not acc:
+        cur.pull_into(cur.acc)
+    if isinstance(acc, CentralityAccumulator) and acc._binding is not None:
+        if acc._binding.dirty and not acc._binding.stale:
+            acc._binding.pull_into(acc)
+        acc._binding = None
+    sums = _DeviceSums(dev, acc)
+    if isinstance(acc, CentralityAccumulator):
+        acc._binding = sums
+    state._sums = sums
+    return sums
+
+
+def iterate(g, state: HyperBallState, observers: Iterable = ()) -> int:
+    """One synchronous ball-growth step on the device; returns how many counters changed."""
+    if isinstance(state, _PendingState):
+        state._attach(g)
+    dev = state._dev
+    t_next = state.t + 1
+    observers = list(observers)
+    if state.n == 0 or dev is None:
+        for obs in observers:
+            obs.on_step(t_next, np.zeros(0), np.zeros(0))
+        state.t = t_next
+        state.num_changed = 0
+        return 0
+    dev.bind_graph(g)
+    fused, generic = _split_observers(state, observers)
+    sums = _bind_sums(state, fused)
+    old = dev.est.clone() if generic else None
+    dense = dev.prev_all or not state.config.skip_stable_nodes
+    nch = dev.union_step(t_next, dense, sums)
+    if generic:
+        old_h, new_h = dev.to_host(old), dev.to_host(dev.est)
+        old_h.setflags(write=False)
+        new_h.setflags(write=False)
+        for obs in generic:
+            obs.on_step(t_next, old_h, new_h)
+    dev.swap()
+    if sums is not None:
+        sums.dirty = True
+        if sums.foreign:
+            sums.pull_into(sums.acc)
+    state.t = t_next
+    state.num_changed = nch
+    return nch
+
+
+def run(g, config: HyperBallConfig, observers: Iterable = ()) -> HyperBallState:
+    """Initialize and iterate until no counter changes (engine.py:402-410)."""
+    state = initialize(g, config)
+    return resume(g, state, observers)
+
+
+def resume(g, state: HyperBallState, observers: Iterable = ()) -> HyperBallState:
+    """Continue a (possibly checkpointed) run to convergence (engine.py:413-435)."""
+    cfg = state.config
+    observers = list(observers)
+    if state.n > 0:
+        while True:
+            started = time.perf_counter()
+            nch = iterate(g, state, observers)
+            if cfg.progress is not None:
+                elapsed_ms = (time.perf_counter() - started) * 1000.0
+                cfg.progress.write(f"t={state.t} changed={nch} elapsed_ms={elapsed_ms:.0f}\n")
+            if nch == 0:
+                break
+            if cfg.max_iterations is not None and state.t >= cfg.max_iterations:
+                raise ConvergenceError(state.t, nch)
+    else:
+        state.num_changed = 0
+    final = state.est
+    final.setflags(write=False)
+    for obs in observers:
+        obs.on_converged(final)
+    return state
+
+
+def load_state(path, config: HyperBallConfig | None = None, graph=None) -> HyperBallState:
+    """Rebuild a saved HBCK v1 state (engine.py:283-327).  The device half is attached on
+    the first ``iterate``/``resume`` with the graph (or immediately when `graph` is given)."""
+    with open(path, "rb") as fh:
+        data = fh.read()
+    if data[:4] != CHECKPOINT_MAGIC:
+        raise ValueError("bad checkpoint magic")
+    version, kind, n, t, num_changed = struct.unpack("<HBQQQ", data[4:31])
+    if version != CHECKPOINT_VERSION:
+        raise ValueError(f"unsupported checkpoint version {version}")
+    if kind != 0:
+        raise ValueError("only probabilistic checkpoints can be resumed on the B200 engine")
+    b, width, seed = struct.unpack("<BBQ", data[31:41])
+    params = CounterParams(b=b, register_width=width, seed=seed)
+    pos = 41
+    blobs = []
+    for _ in range(2):
+        (length,) = struct.unpack("<Q", data[pos:pos + 8])
+        pos += 8
+        blobs.append(data[pos:pos + length])
+        pos += length
+    changed_prev = np.frombuffer(data, dtype=np.bool_, count=n, offset=pos).copy()
+    pos += n
+    est = np.frombuffer(data, dtype=np.float64, count=n, offset=pos).copy()
+    dense = CounterArray.from_blob(blobs[0]).to_dense() if n else np.zeros((0, params.p),
+                                                                           np.uint8)
+    if config is None:
+        config = HyperBallConfig(params=params)
+    state = _PendingState(config, n, (dense, changed_prev, est))
+    state.t = t
+    state.num_changed = num_changed
+    if graph is not None:
+        state._attach(graph)
+    return state
+
+
+class _PendingState(HyperBallState):
+    """A loaded state whose device half is created once the graph is known."""
+
+    def __init__(self, config, n, host):
+        super().__init__(config, n, None)
+        self._host = host
+
+    def _attach(self, g) -> None:
+        if self._dev is not None:
+            return
+        dense, changed_prev, est = self._host
+        dev = _Device(g, self.config)
+        if dev.n != self.n:
+            raise ValueError(f"graph has {dev.n} nodes, checkpoint has {self.n}")
+        cur = torch.from_numpy(dense).to(dev.device)
+        dev.restore_original(cur, cur.clone(), torch.from_numpy(est).to(dev.device),
+                             torch.from_numpy(changed_prev).to(dev.device))
+        # the recycled buffer must hold the current rows (lazy double-buffer invariant)
+        dev.nxt.copy_(dev.cur)
+        dev.prev_all = bool(changed_prev.all()) if self.n else False
+        dev.full_pass = True
+        self._dev = dev
+        self._host = None
+
+    @property
+    def est(self):
+        if self._dev is None:
+            return self._host[2].copy()
+        return super().est
+
+    @property
+    def changed_prev(self):
+        if self._dev is None:
+            return self._host[1].copy()
+        return super().changed_prev
+
+    def register_matrix(self):
+        if self._dev is None:
+            m = self._host[0].copy()
+            m.setflags(write=False)
+            return m
+        return super().register_matrix()
+

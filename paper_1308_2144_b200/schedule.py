@@ -1,0 +1,156 @@
+"""Device-resident graph in schedule order, plus the heavy-node work split.
+
+The reference walks nodes in id order with one CPU thread per arc-balanced range
+(engine.py:351-390).  On the B200 the union kernel assigns lane groups to nodes, so the
+schedule decides:
+
+* ``order``: ``identity`` keeps node ids (best when in-degrees are flat and ids carry
+  locality, e.g. config 4's +-1024 window); ``degree`` relabels nodes by descending
+  in-degree (stable), so every warp sees neighbours of equal degree, hubs sit first and
+  their hot register rows share cache lines, and zero in-degree nodes trail.  The
+  relabelling is internal: hashes use original ids and every host-visible array is
+  returned in original order, so registers stay bit-identical.
+* ``heavy`` nodes (in-degree above ``light_max_deg``) are cut into work items of
+  ``item_arcs`` arcs; one warp merges an item into a partial row, a second pass merges
+  the partial rows of a node and runs the epilogue.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+
+
+@dataclass
+class Schedule:
+    n: int
+    m: int
+    b: int
+    order: str
+    perm: torch.Tensor | None      # int32 [n]: internal id -> original id
+    rank: torch.Tensor | None      # int32 [n]: original id -> internal id
+    offsets: torch.Tensor          # int64 [n+1], internal ids
+    succ: torch.Tensor             # int32 [m], internal ids
+    lo: int
+    hi: int
+    light_lo: int
+    light_hi: int
+    light_hi_steady: int           # light_hi once zero in-degree nodes can no longer change
+    light_max_deg: int
+    item_arcs: int
+    heavy_nodes: torch.Tensor
+    item_first: torch.Tensor
+    item_node: torch.Tensor
+    item_beg: torch.Tensor
+    partial: torch.Tensor
+    max_deg: int
+
+    @property
+    def n_heavy(self) -> int:
+        return int(self.heavy_nodes.numel())
+
+    @property
+    def n_items(self) -> int:
+        return int(self.item_node.numel())
+
+    def to_internal(self, x: torch.Tensor) -> torch.Tensor:
+        """Reorder a per-node array from original to internal order."""
+        return x if self.perm is None else x.index_select(0, self.perm.long())
+
+    def to_original(self, x: torch.Tensor) -> torch.Tensor:
+        return x if self.rank is None else x.index_select(0, self.rank.long())
+
+
+def _as_device(a, dtype, device) -> torch.Tensor:
+    if isinstance(a, torch.Tensor):
+        return a.to(device=device, dtype=dtype, non_blocking=True)
+    arr = np.asarray(a)
+    t = torch.from_numpy(np.ascontiguousarray(arr))
+    return t.to(device=device, non_blocking=True).to(dtype)
+
+
+def choose_order(max_deg: int, light_max_deg: int) -> str:
+    """auto: relabel by degree when any node needs the heavy path (skewed in-degree)."""
+    return "degree" if max_deg > light_max_deg else "identity"
+
+
+def partition_bounds(n: int, world: int):
+    """Internal-id ranges [bounds[r], bounds[r+1]) owned by each rank (equal node counts;
+    in degree order every rank's slice is a round-robin deal of the degree ranking, so
+    node and arc counts are balanced together -- SURVEY.md section 8(e))."""
+    sizes = [(n - r + world - 1) // world for r in range(world)]   # = len(range(r, n, world))
+    bounds = [0]
+    for sz in sizes:
+        bounds.append(bounds[-1] + sz)
+    return bounds
+
+
+def build_schedule(offsets, successors, b: int, device, order: str = "auto", world: int = 1,
+                   rank_id: int = 0, stream=None) -> Schedule:
+    """Upload the CSR of G^T, relabel it into schedule order and split the heavy nodes of
+    this rank's internal-id range [lo, hi) into work items."""
+    L = _lib.hb()
+    off = _as_device(offsets, torch.int64, device)
+    succ = _as_device(successors, torch.int32, device)
+    n = off.numel() - 1
+    m = succ.numel()
+    bounds = partition_bounds(n, world)
+    lo, hi = bounds[rank_id], bounds[rank_id + 1]
+    light_max_deg = int(L.hb_light_max_deg(b))
+    item_arcs = int(L.hb_item_arcs(b))
+    deg = off[1:] - off[:-1]
+    max_deg = int(deg.max().item()) if n else 0
+    if order == "auto":
+        order = choose_order(max_deg, light_max_deg)
+    if order not in ("identity", "degree"):
+        raise ValueError(f"unknown schedule order {order!r}")
+    perm = rank = None
+    if order == "degree" and n > 0:
+        srt = torch.sort(deg, descending=True, stable=True).indices
+        if world > 1:
+            # deal the degree ranking round-robin: rank r gets ranks r, r+W, r+2W, ...
+            # (bounds[r+1]-bounds[r] of them), each slice still in descending degree.
+            srt = torch.cat([srt[r::world] for r in range(world)])
+        perm = srt.to(torch.int32)
+        rank = torch.empty_like(perm)
+        rank[srt] = torch.arange(n, dtype=torch.int32, device=device)
+        new_deg = deg[srt]
+        new_off = torch.zeros(n + 1, dtype=torch.int64, device=device)
+        torch.cumsum(new_deg, 0, out=new_off[1:])
+        new_succ = torch.empty(m, dtype=torch.int32, device=device)
+        s = stream if stream is not None else torch.cuda.current_stream(device)
+        _lib.check(L.hb_relabel_csr(n, off.data_ptr(), succ.data_ptr(), perm.data_ptr(),
+                                    rank.data_ptr(), new_off.data_ptr(), new_succ.data_ptr(),
+                                    s.cuda_stream), "hb_relabel_csr")
+        off, succ, deg = new_off, new_succ, new_deg
+        del srt
+    dloc = deg[lo:hi]
+    heavy = torch.nonzero(dloc > light_max_deg).squeeze(1) + lo
+    cnt = (deg[heavy] + item_arcs - 1) // item_arcs
+    item_first = torch.zeros(heavy.numel() + 1, dtype=torch.int64, device=device)
+    if heavy.numel():
+        torch.cumsum(cnt, 0, out=item_first[1:])
+    n_items = int(item_first[-1].item())
+    owner = torch.repeat_interleave(torch.arange(heavy.numel(), device=device), cnt)
+    item_node = heavy[owner]
+    item_beg = off[item_node] + (torch.arange(n_items, device=device) - item_first[owner]) * item_arcs
+    p = 1 << b
+    partial = torch.empty((max(n_items, 1), p), dtype=torch.uint8, device=device)
+    if order == "degree":
+        # this rank's slice is in descending degree: heavy first, zero in-degree last
+        n_heavy = int(heavy.numel())
+        n_nonzero = int((dloc > 0).sum().item())
+        light_lo, light_hi = lo + n_heavy, hi
+        steady = lo + max(n_nonzero, n_heavy)
+    else:
+        light_lo, light_hi, steady = lo, hi, hi
+    return Schedule(n=n, m=m, b=b, order=order, perm=perm, rank=rank, offsets=off, succ=succ,
+                    lo=lo, hi=hi, light_lo=light_lo, light_hi=light_hi,
+                    light_hi_steady=steady, light_max_deg=light_max_deg, item_arcs=item_arcs,
+                    heavy_nodes=heavy.to(torch.int32), item_first=item_first.to(torch.int32),
+                    item_node=item_node.to(torch.int32), item_beg=item_beg.contiguous(),
+                    partial=partial, max_deg=max_deg)

@@ -1,0 +1,174 @@
+"""Parity of the CUDA path (through the C-ABI) with the reference, on the GPU.
+
+Golden cases: per-iteration register / estimate digests, changed counts, iteration count
+and final centralities must equal the reference's bit for bit (tests/golden/, produced by
+running the reference).  Larger seeded graphs: compared with the CPU oracle iteration by
+iteration.  Tolerance for the fp64 centralities: exact (0 ulp) -- stronger than the 1e-9
+relative bound BASELINE.json allows.
+"""
+
+import hashlib
+import io
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as orc
+from conftest import golden, golden_cases, golden_graph
+
+pytestmark = pytest.mark.gpu
+
+hb = pytest.importorskip("paper_1308_2144_b200")
+from paper_1308_2144_b200 import generators as gen  # noqa: E402
+
+CASES = golden_cases()
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def bits_equal(a, b):
+    a = np.ascontiguousarray(a, np.float64)
+    b = np.ascontiguousarray(b, np.float64)
+    return a.shape == b.shape and np.array_equal(a.view(np.uint64), b.view(np.uint64))
+
+
+def drive(off, suc, b, seed, width=5, schedule="auto", skip=True):
+    g = hb.CsrGraph(off, suc)
+    cfg = hb.HyperBallConfig(params=hb.CounterParams(b=b, register_width=width, seed=seed),
+                             schedule=schedule, skip_stable_nodes=skip)
+    acc = hb.CentralityAccumulator(g.n)
+    st = hb.initialize(g, cfg)
+    regs, ests, nchs = [sha(st.register_matrix())], [sha(st.est)], []
+    if g.n:
+        while True:
+            nch = hb.iterate(g, st, [acc])
+            regs.append(sha(st.register_matrix()))
+            ests.append(sha(st.est))
+            nchs.append(nch)
+            if nch == 0:
+                break
+    acc.on_converged(st.est)
+    return st, acc, regs, ests, nchs
+
+
+@pytest.mark.parametrize("schedule", ["auto", "identity", "degree"])
+@pytest.mark.parametrize("case", CASES, ids=[c["key"] for c in CASES])
+def test_golden_case(case, schedule):
+    off, suc = golden_graph(case)
+    st, acc, regs, ests, nchs = drive(off, suc, case["b"], int(case["seed"]), case["width"],
+                                      schedule)
+    assert st.t == case["t"]
+    assert nchs == case["nch"]
+    assert regs == case["reg_digests"]
+    assert ests == case["est_digests"]
+    _, arrays = golden()
+    key = case["key"]
+    fin = dict(sum_dist=acc.sum_dist, sum_recip=acc.sum_recip, coreach=acc.coreach,
+               closeness=hb.finalize_closeness(acc), harmonic=hb.finalize_harmonic(acc),
+               lin=hb.finalize_lin(acc))
+    for name, got in fin.items():
+        assert bits_equal(got, arrays[f"{key}/{name}"]), name
+
+
+def test_run_api_matches_golden_config1():
+    case = next(c for c in CASES if c["key"] == "config1_b6_s42_w5")
+    off, suc = golden_graph(case)
+    g = hb.CsrGraph(off, suc)
+    acc = hb.CentralityAccumulator(g.n)
+    prog = io.StringIO()
+    st = hb.run(g, hb.HyperBallConfig(params=hb.CounterParams(b=6, seed=42), progress=prog),
+                [acc])
+    _, arrays = golden()
+    assert st.t == case["t"]
+    assert bits_equal(hb.finalize_harmonic(acc), arrays["config1_b6_s42_w5/harmonic"])
+    assert bits_equal(hb.finalize_lin(acc), arrays["config1_b6_s42_w5/lin"])
+    lines = prog.getvalue().strip().splitlines()
+    assert len(lines) == case["t"] and lines[-1].startswith(f"t={case['t']} changed=0")
+
+
+def test_skip_equals_naive_on_gpu():
+    case = next(c for c in CASES if c["key"].startswith("disc14_b4"))
+    off, suc = golden_graph(case)
+    a = drive(off, suc, 4, 42, skip=True)
+    b = drive(off, suc, 4, 42, skip=False)
+    assert a[2] == b[2] and a[3] == b[3]
+
+
+def _oracle_compare(gT, b, seed, schedule="auto", max_iters=None):
+    off = np.asarray(gT.offsets, np.int64)
+    suc = np.asarray(gT.successors, np.int64)
+    ref = orc.run_oracle(off, suc, b, seed, workers=8, record=True)
+    st, acc, regs, ests, nchs = drive(off, suc, b, seed, schedule=schedule)
+    assert nchs == ref.nch
+    assert regs == ref.reg_digests
+    assert ests == ref.est_digests
+    assert bits_equal(acc.sum_dist, ref.sum_dist)
+    assert bits_equal(acc.sum_recip, ref.sum_recip)
+    assert bits_equal(hb.finalize_lin(acc), ref.lin)
+
+
+@pytest.mark.parametrize("b", [4, 5, 7, 8, 9, 10, 12])
+def test_rmat_heavy_split_vs_oracle(b):
+    """R-MAT scale 14 has in-degrees in the thousands: exercises heavy items."""
+    g = gen.rmat_t(14, 16 << 14, seed=21)
+    _oracle_compare(g, b, 42)
+
+
+@pytest.mark.parametrize("schedule", ["identity", "degree"])
+def test_rmat16_both_schedules(schedule):
+    g = gen.rmat_t(16, 16 << 16, seed=22)
+    _oracle_compare(g, 4, 7, schedule)
+
+
+def test_estimate_rows_pins(pins):
+    from paper_1308_2144_b200 import _lib
+    from paper_1308_2144_b200.hll import estimator_constants, lc_table
+    p_, arrays = pins
+    for bs in p_["estimate_rows"]:
+        b = int(bs)
+        rows = torch.from_numpy(arrays[f"est_rows/{b}/rows"]).cuda()
+        want = arrays[f"est_rows/{b}/est"]
+        out = torch.zeros(rows.shape[0], dtype=torch.float64, device="cuda")
+        lc = torch.from_numpy(lc_table(1 << b)).cuda()
+        a2, cut, _ = estimator_constants(1 << b)
+        _lib.check(_lib.hb().hb_estimate_rows(rows.data_ptr(), 0, rows.shape[0], b, lc.data_ptr(),
+                                              a2, cut, out.data_ptr(),
+                                              torch.cuda.current_stream().cuda_stream), "est")
+        assert bits_equal(out.cpu().numpy(), want), b
+
+
+def test_device_hash_pins(pins):
+    from paper_1308_2144_b200 import _lib
+    p_, _ = pins
+    items = np.array([int(x) for x in p_["hash_items"]["items"]], dtype=np.uint64)
+    for key, vals in p_["hash_items"]["values"].items():
+        seed, replica = (int(x) for x in key.split(":"))
+        it = torch.from_numpy(items.view(np.int64)).cuda()
+        rp = torch.full_like(it, replica if replica < 2**63 else replica - 2**64)
+        out = torch.empty_like(it)
+        _lib.check(_lib.hb().hb_hash_items(it.numel(), it.data_ptr(), rp.data_ptr(), seed,
+                                           out.data_ptr(), torch.cuda.current_stream().cuda_stream),
+                   "hash")
+        assert [str(int(h)) for h in out.cpu().numpy().view(np.uint64)] == vals
+
+
+def test_checkpoint_bytes_match_reference(pins, tmp_path):
+    p_, arrays = pins
+    case = next(c for c in CASES if c["key"] == "random300_b6_s42_w5")
+    off, suc = golden_graph(case)
+    g = hb.CsrGraph(off, suc)
+    st = hb.initialize(g, hb.HyperBallConfig(params=hb.CounterParams(b=6, seed=42)))
+    hb.iterate(g, st)
+    hb.iterate(g, st)
+    path = tmp_path / "ck.bin"
+    st.save(path)
+    assert hashlib.sha256(path.read_bytes()).hexdigest() == p_["hbck_random300_b6_t2"]
+    # resume from the checkpoint reaches the golden end state
+    st2 = hb.load_state(path)
+    hb.resume(g, st2)
+    assert st2.t == case["t"]
+    assert sha(st2.register_matrix()) == case["reg_digests"][-1]
+    assert sha(st2.est) == case["est_digests"][-1]

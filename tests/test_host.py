@@ -1,0 +1,150 @@
+"""CPU-only tests: host logic, API validation, formats, and that the C-ABI library loads
+and exports every symbol include/hyperball_b200.h declares (no compute without a GPU)."""
+
+import ctypes
+import hashlib
+import io
+import re
+
+import numpy as np
+import pytest
+
+import paper_1308_2144_b200 as hb
+from paper_1308_2144_b200 import _lib, generators as gen
+from paper_1308_2144_b200.hll import (CounterArray, CounterParams, alpha, estimator_constants,
+                                      hash_items, lc_table, register_values)
+from paper_1308_2144_b200.schedule import partition_bounds
+
+
+def header_symbols():
+    text = open(_lib.HEADER_PATH).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(hb_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_header_symbol():
+    L = ctypes.CDLL(_lib.HB_LIB_PATH)
+    syms = header_symbols()
+    assert len(syms) >= 10
+    for name in syms:
+        assert hasattr(L, name), name
+    assert set(syms) == set(_lib.HB_SIGNATURES), "ctypes table out of sync with header"
+
+
+def test_library_metadata_calls():
+    L = _lib.hb()
+    assert b"sm_100a" in L.hb_version()
+    assert L.hb_min_log2m() == 4 and L.hb_max_log2m() >= 12
+    assert L.hb_item_arcs(4) == 512 and L.hb_item_arcs(8) == 64
+
+
+def test_hash_and_register_pins(pins):
+    p, _ = pins
+    items = np.array([int(x) for x in p["hash_items"]["items"]], dtype=np.uint64)
+    for key, vals in p["hash_items"]["values"].items():
+        seed, replica = (int(x) for x in key.split(":"))
+        got = hash_items(items, np.full(items.shape, replica, np.uint64), seed)
+        assert [str(int(h)) for h in got] == vals
+    hs = np.array([int(x) for x in p["register_values"]["hashes"]], dtype=np.uint64)
+    for key, (idx, rho) in p["register_values"]["values"].items():
+        b, w = (int(x) for x in key.split(":"))
+        gi, gr = register_values(hs, CounterParams(b=b, register_width=w))
+        assert gi.tolist() == idx and gr.tolist() == rho, key
+
+
+def test_alpha_and_constants(pins):
+    p, _ = pins
+    for ps, a in p["alpha"].items():
+        assert alpha(int(ps)) == a
+    for ps, a2 in p["alpha_p2"].items():
+        assert estimator_constants(int(ps))[0] == a2
+
+
+def test_lc_table_matches_libm():
+    import math
+    for b in (4, 6, 8, 12):
+        p = 1 << b
+        t = lc_table(p)
+        assert t[p] == 0.0 and t[p - 1] == float(p) * math.log(float(p) / (p - 1))
+
+
+def test_hlla_blob_pins(pins):
+    p, arrays = pins
+    dense = arrays["hlla/dense"]
+    for w, key in ((5, "hlla_blob_w5"), (6, "hlla_blob_w6")):
+        blob = CounterArray.from_dense(dense, CounterParams(b=6, register_width=w, seed=9)).to_blob()
+        assert hashlib.sha256(blob).hexdigest() == p[key]
+        back = CounterArray.from_blob(blob)
+        assert np.array_equal(back.to_dense(), dense)
+
+
+@pytest.mark.parametrize("kw,exc", [(dict(b=3), ValueError), (dict(b=6, register_width=0), ValueError),
+                                    (dict(b=6, register_width=9), ValueError)])
+def test_counter_params_validation(kw, exc):
+    with pytest.raises(exc):
+        CounterParams(**kw)
+
+
+def test_config_validation():
+    with pytest.raises(ValueError):
+        hb.HyperBallConfig(backend="nope")
+    with pytest.raises(ValueError):
+        hb.HyperBallConfig(workers=0)
+    with pytest.raises(ValueError):
+        hb.HyperBallConfig(schedule="random")
+    assert hb.HyperBallConfig(backend="hll").backend == "probabilistic"
+
+
+def test_engine_fails_loudly_without_cuda():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    g = hb.CsrGraph([0, 1, 1], [1])
+    with pytest.raises(RuntimeError, match="CUDA"):
+        hb.run(g, hb.HyperBallConfig(params=CounterParams(b=4)))
+
+
+def test_exact_backend_rejected():
+    g = hb.CsrGraph([0, 1, 1], [1])
+    with pytest.raises(ValueError):
+        hb.initialize(g, hb.HyperBallConfig(backend="exact"))
+
+
+def test_graph_roundtrip_and_transpose():
+    rng = np.random.default_rng(1)
+    s, d = rng.integers(0, 50, 300), rng.integers(0, 50, 300)
+    g = hb.CsrGraph.from_edges(s, d, n=50)
+    assert all((np.diff(g.successors_of(v)) > 0).all() for v in range(50))
+    gt = hb.transpose(g)
+    assert hb.transpose(gt) == g
+    buf = io.BytesIO()
+    hb.write_binary(g, buf)
+    assert len(buf.getvalue()) == 20 + 8 * 51 + 8 * g.m
+    buf.seek(0)
+    assert hb.read_binary(buf) == g
+
+
+def test_generator_matches_reference_normalisation():
+    """G^T from the C builder equals transpose(from_edges(arcs)) minus self-loops."""
+    rng = np.random.default_rng(2)
+    n = 300
+    s = rng.integers(0, n, 3000).astype(np.uint32)
+    d = rng.integers(0, n, 3000).astype(np.uint32)
+    gt = gen.from_arcs_t(n, s, d, threads=3)
+    keep = s != d
+    want = hb.transpose(hb.CsrGraph.from_edges(s[keep], d[keep], n=n))
+    assert gt == want
+
+
+def test_generator_deterministic_across_threads():
+    a = gen.rmat_t(11, 8 << 11, seed=5, threads=1)
+    b = gen.rmat_t(11, 8 << 11, seed=5, threads=7)
+    assert gen.graph_digest(a) == gen.graph_digest(b)
+
+
+@pytest.mark.parametrize("n,w", [(10, 4), (7, 8), (1000, 3), (0, 2)])
+def test_partition_bounds_cover(n, w):
+    b = partition_bounds(n, w)
+    assert b[0] == 0 and b[-1] == n and all(b[i] <= b[i + 1] for i in range(w))
+    # round-robin deal sizes
+    assert [b[r + 1] - b[r] for r in range(w)] == [len(range(r, n, w)) for r in range(w)]
