@@ -596,9 +596,9 @@ int64_t hb_light_max_deg(int b) { (void)b; return kLightMaxDeg; }
 int hb_seed(uint8_t *regs, double *est, int64_t n, int b, int register_width, uint64_t seed,
             const int32_t *perm, const int64_t *weights, const double *lc_table,
             double alpha_p2, double lc_cut, void *stream) {
-  if (n < 0 || !regs || !est || !lc_table) return set_err_msg("hb_seed: bad arguments");
   if (register_width < 1 || register_width > 8) return set_err_msg("hb_seed: bad register_width");
   if (n == 0) return 0;
+  if (n < 0 || !regs || !est || !lc_table) return set_err_msg("hb_seed: bad arguments");
   cudaStream_t s = (cudaStream_t)stream;
   EstConst ec{alpha_p2, lc_cut, lc_table};
   HB_DISPATCH(b, (k_seed<LB><<<grid_for_threads(n), kThreads, 0, s>>>(

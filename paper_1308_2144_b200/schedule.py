@@ -17,6 +17,7 @@ schedule decides:
 
 from __future__ import annotations
 
+import warnings
 from dataclasses import dataclass
 
 import numpy as np
@@ -68,8 +69,10 @@ class Schedule:
 def _as_device(a, dtype, device) -> torch.Tensor:
     if isinstance(a, torch.Tensor):
         return a.to(device=device, dtype=dtype, non_blocking=True)
-    arr = np.asarray(a)
-    t = torch.from_numpy(np.ascontiguousarray(arr))
+    arr = np.ascontiguousarray(a)
+    with warnings.catch_warnings():   # read-only host arrays are only copied to the device
+        warnings.simplefilter("ignore", UserWarning)
+        t = torch.from_numpy(arr)
     return t.to(device=device, non_blocking=True).to(dtype)
 
 
