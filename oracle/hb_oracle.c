@@ -86,13 +86,19 @@ void orc_constants(int b, double *alpha_p2, double *lc_cut, double *p_float) {
     *p_float = (double)p;
 }
 
-/* hll.py:33: POW2NEG[r] = 2.0 ** -r (exact powers of two) */
-static double pow2neg(int r) { return ldexp(1.0, -r); }
+/* hll.py:33: POW2NEG[r] = 2.0 ** -r (exact powers of two), tabulated once */
+static double POW2NEG_TAB[256];
+static pthread_once_t pow2neg_once = PTHREAD_ONCE_INIT;
+static void pow2neg_init(void) {
+    for (int r = 0; r < 256; r++) POW2NEG_TAB[r] = ldexp(1.0, -r);
+}
+static inline double pow2neg(int r) { return POW2NEG_TAB[r]; }
 
 /* _kernels.py:15-34: ascending-index fp64 sum of 2^-M[j]; raw harmonic-mean estimate;
  * linear counting p*ln(p/V) when raw <= 2.5p and V > 0. */
 double orc_estimate_row(const uint8_t *row, int64_t p, double alpha_p2, double lc_cut,
                         double p_float) {
+    pthread_once(&pow2neg_once, pow2neg_init);
     double s = 0.0;
     int64_t zeros = 0;
     for (int64_t j = 0; j < p; j++) {
@@ -135,6 +141,15 @@ void orc_seed(int64_t n, int b, int width, uint64_t seed, const int64_t *weights
  * successors changed in the previous step (82-87); stable nodes copy their row and
  * reuse the cached estimate (88-93); otherwise byte-wise max over successor rows
  * (94-101), change test (102-106), estimate of changed rows (107-113). */
+/* dst[j] = max(dst[j], src[j]); restrict-qualified so the loop vectorises */
+static inline void max_into(uint8_t *restrict dst, const uint8_t *restrict src, int64_t p) {
+    for (int64_t j = 0; j < p; j++) dst[j] = src[j] > dst[j] ? src[j] : dst[j];
+}
+
+/* target_clones: the reference's numba kernels are JIT-compiled for the host CPU, so the
+ * port dispatches at load time to an AVX2 build where the CPU has it (same results: the
+ * byte max is exact in any width). */
+__attribute__((target_clones("avx2", "default")))
 int64_t orc_union_range(int64_t lo, int64_t hi, const int64_t *offsets, const int64_t *succ,
                         const uint8_t *cur, uint8_t *nxt, const uint8_t *changed_prev,
                         uint8_t *changed_now, const double *est, double *new_est, int b,
@@ -160,9 +175,7 @@ int64_t orc_union_range(int64_t lo, int64_t hi, const int64_t *offsets, const in
         }
         memcpy(nv, cv, (size_t)p);
         for (int64_t k = offsets[v]; k < offsets[v + 1]; k++) {
-            const uint8_t *cw = cur + succ[k] * p;
-            for (int64_t j = 0; j < p; j++)
-                if (cw[j] > nv[j]) nv[j] = cw[j];
+            max_into(nv, cur + succ[k] * p, p);
         }
         int changed = memcmp(nv, cv, (size_t)p) != 0;
         changed_now[v] = (uint8_t)changed;
@@ -217,25 +230,31 @@ static void *orc_job_run(void *arg) {
     return NULL;
 }
 
-/* engine.py:362-390: one union pass over [0, n) split over `workers` threads; returns the
- * total changed count (the `sum(f.result() ...)` barrier). */
-int64_t orc_iterate_mt(int64_t n, const int64_t *offsets, const int64_t *succ,
-                       const uint8_t *cur, uint8_t *nxt, const uint8_t *chg_prev,
-                       uint8_t *chg_now, const double *est, double *new_est, int b, int skip,
-                       int workers) {
-    if (n == 0) return 0;
+/* engine.py:362-390: one union pass over nodes [lo, hi) split into arc-balanced ranges
+ * over `workers` threads; returns the total changed count (the `sum(f.result() ...)`
+ * barrier).  All arrays are full-size (indexed by global node id). */
+int64_t orc_iterate_range_mt(int64_t lo, int64_t hi, const int64_t *offsets,
+                             const int64_t *succ, const uint8_t *cur, uint8_t *nxt,
+                             const uint8_t *chg_prev, uint8_t *chg_now, const double *est,
+                             double *new_est, int b, int skip, int workers) {
+    int64_t n = hi - lo;
+    if (n <= 0) return 0;
     if (workers < 1) workers = 1;
     if (workers > n) workers = (int)n;
     if (workers == 1)
-        return orc_union_range(0, n, offsets, succ, cur, nxt, chg_prev, chg_now, est, new_est,
-                               b, skip);
+        return orc_union_range(lo, hi, offsets, succ, cur, nxt, chg_prev, chg_now, est,
+                               new_est, b, skip);
     int64_t *bounds = (int64_t *)malloc(sizeof(int64_t) * (size_t)(workers + 1));
     orc_job *jobs = (orc_job *)calloc((size_t)workers, sizeof(orc_job));
     pthread_t *th = (pthread_t *)calloc((size_t)workers, sizeof(pthread_t));
-    worker_bounds(offsets, n, workers, bounds);
+    /* bounds over the sub-range: shift offsets so the range starts at arc 0 */
+    int64_t *sub = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n + 1));
+    for (int64_t i = 0; i <= n; i++) sub[i] = offsets[lo + i] - offsets[lo];
+    worker_bounds(sub, n, workers, bounds);
+    free(sub);
     for (int w = 0; w < workers; w++) {
         orc_job *j = &jobs[w];
-        j->lo = bounds[w]; j->hi = bounds[w + 1];
+        j->lo = lo + bounds[w]; j->hi = lo + bounds[w + 1];
         j->offsets = offsets; j->succ = succ; j->cur = cur; j->nxt = nxt;
         j->chg_prev = chg_prev; j->chg_now = chg_now; j->est = est; j->new_est = new_est;
         j->b = b; j->skip = skip; j->nch = 0;
@@ -247,6 +266,14 @@ int64_t orc_iterate_mt(int64_t n, const int64_t *offsets, const int64_t *succ,
     }
     free(bounds); free(jobs); free(th);
     return nch;
+}
+
+int64_t orc_iterate_mt(int64_t n, const int64_t *offsets, const int64_t *succ,
+                       const uint8_t *cur, uint8_t *nxt, const uint8_t *chg_prev,
+                       uint8_t *chg_now, const double *est, double *new_est, int b, int skip,
+                       int workers) {
+    return orc_iterate_range_mt(0, n, offsets, succ, cur, nxt, chg_prev, chg_now, est, new_est,
+                                b, skip, workers);
 }
 
 /* numpy.maximum(x, 0.0): returns x when x >= 0 or x is NaN, else 0.0 */

@@ -65,6 +65,9 @@ def lib():
         L.orc_iterate_mt.restype = _i64
         L.orc_iterate_mt.argtypes = [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _int,
                                      _int, _int]
+        L.orc_iterate_range_mt.restype = _i64
+        L.orc_iterate_range_mt.argtypes = [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                           _int, _int, _int]
         L.orc_accumulate.restype = None
         L.orc_accumulate.argtypes = [_i64, _i64, _vp, _vp, _vp, _vp]
         L.orc_finalize.restype = None
