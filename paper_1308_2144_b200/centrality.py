@@ -101,23 +101,24 @@ class CentralityAccumulator(BallObserver):
 
 
 def fusable(obs, n: int) -> bool:
-    """An accumulator whose per-iteration fold the union kernel can do (no discounts)."""
+    """An accumulator whose per-iteration fold the union kernel can do (no discounts).
+    Never touches the lazily-refreshed sums (that would force a device read-back)."""
+    if isinstance(obs, CentralityAccumulator):
+        return not obs.discounts and obs.n == n
     if type(obs).__name__ != "CentralityAccumulator":
         return False
-    if not all(hasattr(obs, a) for a in ("sum_dist", "sum_recip", "coreach")):
+    attrs = vars(obs) if hasattr(obs, "__dict__") else {}
+    if not all(a in attrs for a in ("sum_dist", "sum_recip", "coreach")):
         return False
-    if getattr(obs, "discounts", None):
+    if attrs.get("discounts"):
         return False
-    return int(getattr(obs, "n", n)) == n
+    return int(attrs.get("n", n)) == n
 
 
 def finalize_closeness(acc) -> np.ndarray:
     """1 / distance sum where positive, 0 for nodes nothing else coreaches."""
     s = np.asarray(acc.sum_dist, dtype=np.float64)
-    out = np.zeros_like(s)
-    pos = s > 0
-    out[pos] = 1.0 / s[pos]
-    return out
+    return np.divide(1.0, s, out=np.zeros_like(s), where=s > 0)
 
 
 def finalize_harmonic(acc) -> np.ndarray:
@@ -129,7 +130,4 @@ def finalize_lin(acc) -> np.ndarray:
     """coreach^2 / distance sum where positive, 1 otherwise."""
     s = np.asarray(acc.sum_dist, dtype=np.float64)
     c = np.asarray(acc.coreach, dtype=np.float64)
-    out = np.ones_like(s)
-    pos = s > 0
-    out[pos] = (c * c)[pos] / s[pos]
-    return out
+    return np.divide(c * c, s, out=np.ones_like(s), where=s > 0)

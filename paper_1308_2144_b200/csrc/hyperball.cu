@@ -168,12 +168,13 @@ __device__ __forceinline__ double np_max0(double x) { return (x >= 0.0 || x != x
 // changed flag.  All lanes of gmask must call it together.
 template <int LOGP>
 __device__ __forceinline__ bool finish_node(int64_t v, const uint4 (&acc)[Geo<LOGP>::CPL],
+                                            const uint4 (&pre)[Geo<LOGP>::CPL], bool have_pre,
                                             bool self_chg, unsigned gmask, int gl,
                                             const uint8_t *__restrict__ cur,
                                             uint8_t *__restrict__ nxt, double *__restrict__ est,
                                             double *__restrict__ sum_dist,
                                             double *__restrict__ sum_recip, const EstConst &ec,
-                                            double tf) {
+                                            double tf, const double *pre_vals = nullptr) {
   using Gm = Geo<LOGP>;
   const uint8_t *crow = cur + (size_t)v * Gm::P;
   uint8_t *nrow = nxt + (size_t)v * Gm::P;
@@ -181,7 +182,7 @@ __device__ __forceinline__ bool finish_node(int64_t v, const uint4 (&acc)[Geo<LO
   bool diff = false;
 #pragma unroll
   for (int c = 0; c < Gm::CPL; c++) {
-    uint4 self = ldg4(crow + 16 * (c * Gm::G + gl));
+    const uint4 self = have_pre ? pre[c] : ldg4(crow + 16 * (c * Gm::G + gl));
     nw[c] = bmax4(acc[c], self);
     diff |= neq4(nw[c], self);
   }
@@ -219,11 +220,13 @@ __device__ __forceinline__ bool finish_node(int64_t v, const uint4 (&acc)[Geo<LO
         for (int j = 0; j < Gm::P; j++) s = __dadd_rn(s, pow2neg(nrow[j]));
       }
       const double e = finish_estimate(s, zeros, ec);
-      const double old = est[v];
+      const double old = pre_vals ? pre_vals[0] : est[v];
       est[v] = e;
       const double d = np_max0(__dsub_rn(e, old));
-      if (sum_dist) sum_dist[v] = __dadd_rn(sum_dist[v], __dmul_rn(tf, d));
-      if (sum_recip) sum_recip[v] = __dadd_rn(sum_recip[v], __ddiv_rn(d, tf));
+      if (sum_dist)
+        sum_dist[v] = __dadd_rn(pre_vals ? pre_vals[1] : sum_dist[v], __dmul_rn(tf, d));
+      if (sum_recip)
+        sum_recip[v] = __dadd_rn(pre_vals ? pre_vals[2] : sum_recip[v], __ddiv_rn(d, tf));
     }
   }
   return changed;
@@ -251,12 +254,72 @@ __device__ __forceinline__ void block_add2(uint32_t a, uint32_t b, unsigned long
 
 // ------------------------------------------------------------------ kernels
 constexpr int kThreads = 256;
-constexpr int kUnroll = 4;
 
-// Light nodes: one group of G lanes per node, NPW nodes per warp side by side.
+// Batch geometry of the union kernels.
+//   light: a group of G lanes owns one node; per batch it loads NB = max(G, 8) successor
+//          ids (J per lane, coalesced within the group), compacts the ids whose source
+//          changed into shared memory, then every lane issues U independent 16-byte row
+//          loads (its chunk of U different source rows) before merging -- while the next
+//          batch's ids are already in flight.
+//   heavy: the whole warp loads 32*J ids of one work item per batch, compacts them, and
+//          its NPW slots of G lanes take every NPW-th compacted id, U rows in flight each.
+template <int LOGP>
+struct Batch {
+  using Gm = Geo<LOGP>;
+  static constexpr int U = Gm::CPL >= 8 ? 1 : 8 / Gm::CPL;   // row loads in flight per lane
+  static constexpr int NB = Gm::G > 8 ? Gm::G : 8;            // light: ids per group batch
+  static constexpr int J = NB / Gm::G;                        // light: ids loaded per lane
+  static constexpr int WARP_IDS = Gm::NPW * NB;               // light: smem ids per warp
+  static constexpr int HJ = (U * Gm::NPW) / 32 > 0 ? (U * Gm::NPW) / 32 : 1;  // heavy: ids/lane
+  static constexpr int HEAVY_IDS = 32 * HJ;                   // heavy: smem ids per warp
+};
+
+// L2 prefetch of [p, p + bytes) with the async bulk-copy unit (no registers, no wait).
+// Rounded out to 16-byte granules; every buffer here is a torch allocation (>= 512-byte
+// aligned and padded), so the rounded range stays inside the allocation.
+__device__ __forceinline__ void l2_prefetch(const void *p, int64_t bytes) {
+  if (bytes <= 0) return;
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)15;
+  const uintptr_t a1 = (reinterpret_cast<uintptr_t>(p) + (uintptr_t)bytes + 15) & ~(uintptr_t)15;
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0))
+               : "memory");
+}
+
+// Smallest v in [lo, hi] with off[v] + v >= target (f(hi) >= target), by a warp-wide
+// 32-ary search: every lane probes one point per round.
+__device__ __forceinline__ int64_t warp_lower_bound(const int64_t *__restrict__ off, int64_t lo,
+                                                    int64_t hi, int64_t target, int lane) {
+  int64_t L = lo, R = hi;
+  while (R > L) {
+    const int64_t step = (R - L + 31) / 32;
+    const int64_t probe = L + (int64_t)lane * step;
+    const bool ge = probe >= R || (__ldg(off + probe) + probe >= target);
+    const unsigned b = __ballot_sync(0xffffffffu, ge);
+    if (b == 0) {
+      L = L + 31 * step + 1;
+    } else {
+      const int f = __ffs(b) - 1;
+      if (f == 0) {
+        R = L;
+      } else {
+        R = L + (int64_t)f * step;
+        L = L + (int64_t)(f - 1) * step + 1;
+      }
+    }
+  }
+  return L;
+}
+
+constexpr int kLookRounds = 4;   // L2 prefetch distance of the light kernel, in warp rounds
+
+// Light nodes (in-degree <= max_deg): one group of G lanes per node, NPW nodes per warp
+// round.  Each warp owns one contiguous node range, balanced over the grid by arcs +
+// nodes, so its offsets, ids, own rows and estimates are sequential streams: one lane
+// prefetches them into L2 kLookRounds rounds ahead, leaving the random source-row
+// gather as the only exposed memory latency of a round.
 // _kernels.py:67-114 restated with the source-skip rule.
 template <int LOGP>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, (LOGP >= 10 ? 2 : 4))
 k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
         const uint8_t *__restrict__ cur, uint8_t *__restrict__ nxt,
         const uint32_t *__restrict__ chg_prev, uint32_t *__restrict__ chg_now,
@@ -264,19 +327,75 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
         EstConst ec, int64_t lo, int64_t hi, int64_t max_deg, int dense, double tf,
         unsigned long long *__restrict__ nch_out, unsigned long long *__restrict__ merged_out) {
   using Gm = Geo<LOGP>;
+  using B = Batch<LOGP>;
+  __shared__ int32_t sids[kThreads / 32][B::WARP_IDS];
   const int lane = threadIdx.x & 31;
   const int gl = lane % Gm::G;
   const int grp = lane / Gm::G;
-  uint32_t my_merged = 0;
-  const unsigned gmask =
-      Gm::G == 32 ? 0xffffffffu : (((1u << (Gm::G & 31)) - 1u) << (grp * Gm::G));
+  const unsigned lowmask = Gm::G == 32 ? 0xffffffffu : ((1u << (Gm::G & 31)) - 1u);
+  const unsigned gmask = lowmask << (grp * Gm::G);
+  const unsigned below = (1u << gl) - 1u;
+  int32_t *my_ids = &sids[threadIdx.x >> 5][grp * B::NB];
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  uint32_t my_nch = 0;
-  const int64_t start = (lo / Gm::NPW) * Gm::NPW;
-  for (int64_t base = start + warp * Gm::NPW; base < hi; base += nwarps * Gm::NPW) {
+  uint32_t my_nch = 0, my_merged = 0;
+
+  // this warp's node range [vb, ve), rounds of NPW nodes (NPW-aligned so a round's change
+  // bits share one bitmap word)
+  const int64_t lo_al = (lo / Gm::NPW) * Gm::NPW;
+  const int64_t f0 = __ldg(offsets + lo_al) + lo_al, f1 = __ldg(offsets + hi) + hi;
+  const int64_t span = f1 - f0;
+  int64_t vb = lo_al, ve = hi;
+  if (warp > 0) {
+    const int64_t t = f0 + (int64_t)(((__int128)span * warp) / nwarps);
+    vb = (warp_lower_bound(offsets, lo_al, hi, t, lane) / Gm::NPW) * Gm::NPW;
+  }
+  if (warp + 1 < nwarps) {
+    const int64_t t = f0 + (int64_t)(((__int128)span * (warp + 1)) / nwarps);
+    ve = (warp_lower_bound(offsets, lo_al, hi, t, lane) / Gm::NPW) * Gm::NPW;
+  }
+  if (vb < lo_al) vb = lo_al;
+
+  // prefetch pipeline (lane 0): offsets 2*kLook rounds ahead; own rows, estimates, sums
+  // and successor ids kLook rounds ahead, using offsets read one round earlier.
+  int64_t pf_a0 = -1, pf_a1 = -1;
+  if (lane == 0) {
+    for (int r = 0; r < kLookRounds && vb + (int64_t)r * Gm::NPW < ve; r++) {
+      const int64_t pb = vb + (int64_t)r * Gm::NPW;
+      const int64_t pe = pb + Gm::NPW < ve ? pb + Gm::NPW : ve;
+      l2_prefetch(cur + (size_t)pb * Gm::P, (pe - pb) * Gm::P);
+      l2_prefetch(est + pb, (pe - pb) * 8);
+      if (sum_dist) l2_prefetch(sum_dist + pb, (pe - pb) * 8);
+      if (sum_recip) l2_prefetch(sum_recip + pb, (pe - pb) * 8);
+      const int64_t a0 = __ldg(offsets + pb), a1 = __ldg(offsets + pe);
+      l2_prefetch(succ + a0, (a1 - a0) * 4);
+    }
+    l2_prefetch(offsets + vb, (ve - vb + 1 < 8 * kLookRounds * Gm::NPW
+                                   ? ve - vb + 1 : 8 * kLookRounds * Gm::NPW) * 8);
+  }
+
+  for (int64_t base = vb; base < ve; base += Gm::NPW) {
+    if (lane == 0) {
+      const int64_t pb = base + (int64_t)kLookRounds * Gm::NPW;
+      if (pf_a0 >= 0) {          // ids of round pb - NPW (offsets loaded last round)
+        l2_prefetch(succ + pf_a0, (pf_a1 - pf_a0) * 4);
+        pf_a0 = -1;
+      }
+      if (pb < ve) {
+        const int64_t pe = pb + Gm::NPW < ve ? pb + Gm::NPW : ve;
+        l2_prefetch(cur + (size_t)pb * Gm::P, (pe - pb) * Gm::P);
+        l2_prefetch(est + pb, (pe - pb) * 8);
+        if (sum_dist) l2_prefetch(sum_dist + pb, (pe - pb) * 8);
+        if (sum_recip) l2_prefetch(sum_recip + pb, (pe - pb) * 8);
+        pf_a0 = __ldg(offsets + pb);         // consumed next round
+        pf_a1 = __ldg(offsets + pe);
+        const int64_t ob = pb + (int64_t)kLookRounds * Gm::NPW;
+        if (ob < ve && ((ob * 8) & 127) < Gm::NPW * 8)   // one offsets line ahead
+          l2_prefetch(offsets + ob, 128);
+      }
+    }
     const int64_t v = base + grp;
-    bool valid = (v >= lo) && (v < hi);
+    bool valid = (v >= lo) && (v < ve);
     int64_t beg = 0, end = 0;
     if (valid) {
       beg = __ldg(offsets + v);
@@ -284,49 +403,71 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
       if (end - beg > max_deg) valid = false;  // heavy: handled by the item path
     }
     const bool self_chg = valid && test_bit(chg_prev, v);
-    uint4 acc[Gm::CPL];
+    const bool pre = valid && (dense || self_chg);   // own row certainly needed: load early
+    uint4 self[Gm::CPL], acc[Gm::CPL];
 #pragma unroll
-    for (int c = 0; c < Gm::CPL; c++) acc[c] = make_uint4(0, 0, 0, 0);
-    bool any = false;
-    if (valid) {
-      for (int64_t k = beg; k < end; k += kUnroll) {
-        int32_t w[kUnroll];
-        bool act[kUnroll];
+    for (int c = 0; c < Gm::CPL; c++) {
+      acc[c] = make_uint4(0, 0, 0, 0);
+      self[c] = pre ? ldg4(cur + (size_t)v * Gm::P + 16 * (c * Gm::G + gl)) : acc[c];
+    }
+    double vals[3] = {0.0, 0.0, 0.0};
+    if (pre && gl == 0) {
+      vals[0] = est[v];
+      if (sum_dist) vals[1] = sum_dist[v];
+      if (sum_recip) vals[2] = sum_recip[v];
+    }
+    int32_t idr[B::J];
 #pragma unroll
-        for (int u = 0; u < kUnroll; u++) {
-          act[u] = (k + u) < end;
-          w[u] = act[u] ? __ldg(succ + k + u) : 0;
-        }
-        if (!dense) {
+    for (int j = 0; j < B::J; j++) {
+      const int64_t k = beg + j * Gm::G + gl;
+      idr[j] = (k < end) ? __ldg(succ + k) : -1;
+    }
+    int total = 0;
+    for (int64_t kb = beg; kb < end; kb += B::NB) {   // group-uniform trip count
+      int cnt = 0;
 #pragma unroll
-          for (int u = 0; u < kUnroll; u++) act[u] = act[u] && test_bit(chg_prev, w[u]);
-        }
-        uint4 r[kUnroll][Gm::CPL];
+      for (int j = 0; j < B::J; j++) {
+        const bool act = idr[j] >= 0 && (dense || test_bit(chg_prev, idr[j]));
+        const unsigned bal = (__ballot_sync(gmask, act) >> (grp * Gm::G)) & lowmask;
+        if (act) my_ids[cnt + __popc(bal & below)] = idr[j];
+        cnt += __popc(bal);
+      }
 #pragma unroll
-        for (int u = 0; u < kUnroll; u++)
+      for (int j = 0; j < B::J; j++) {                // next batch's ids, in flight meanwhile
+        const int64_t k = kb + B::NB + j * Gm::G + gl;
+        idr[j] = (k < end) ? __ldg(succ + k) : -1;
+      }
+      __syncwarp(gmask);
+      for (int i = 0; i < cnt; i += B::U) {
+        uint4 r[B::U][Gm::CPL];
+#pragma unroll
+        for (int u = 0; u < B::U; u++) {
+          const bool ok = i + u < cnt;
+          const int32_t w = ok ? my_ids[i + u] : 0;
 #pragma unroll
           for (int c = 0; c < Gm::CPL; c++)
-            r[u][c] = act[u] ? ldg4(cur + (size_t)w[u] * Gm::P + 16 * (c * Gm::G + gl))
-                             : make_uint4(0, 0, 0, 0);
+            r[u][c] = ok ? ldg4(cur + (size_t)w * Gm::P + 16 * (c * Gm::G + gl))
+                         : make_uint4(0, 0, 0, 0);
+        }
 #pragma unroll
-        for (int u = 0; u < kUnroll; u++) {
-          any |= act[u];
-          my_merged += (act[u] && gl == 0);
+        for (int u = 0; u < B::U; u++)
 #pragma unroll
           for (int c = 0; c < Gm::CPL; c++) acc[c] = bmax4(acc[c], r[u][c]);
-        }
       }
+      total += cnt;
+      __syncwarp(gmask);
     }
+    my_merged += (gl == 0) ? (uint32_t)total : 0u;
     bool changed = false;
-    if (valid && (any || self_chg))
-      changed = finish_node<LOGP>(v, acc, self_chg, gmask, gl, cur, nxt, est, sum_dist,
-                                  sum_recip, ec, tf);
+    if (valid && (total > 0 || self_chg))
+      changed = finish_node<LOGP>(v, acc, self, pre, self_chg, gmask, gl, cur, nxt, est,
+                                  sum_dist, sum_recip, ec, tf, pre ? vals : nullptr);
     // Warp-level aggregation of the NPW change bits (they share one bitmap word).
-    const unsigned b = __ballot_sync(0xffffffffu, changed && gl == 0);
-    if (lane == 0 && b) {
+    const unsigned bb = __ballot_sync(0xffffffffu, changed && gl == 0);
+    if (lane == 0 && bb) {
       uint32_t m = 0;
 #pragma unroll
-      for (int g = 0; g < Gm::NPW; g++) m |= ((b >> (g * Gm::G)) & 1u) << g;
+      for (int g = 0; g < Gm::NPW; g++) m |= ((bb >> (g * Gm::G)) & 1u) << g;
       atomicOr(chg_now + (base >> 5), m << (base & 31));
       my_nch += __popc(m);
     }
@@ -334,57 +475,74 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
   block_add2(my_nch, my_merged, nch_out, merged_out);
 }
 
-// Heavy nodes, phase 1: one warp per work item (a slice of one node's arcs).  The warp
-// is NPW arc slots of G lanes; slots stride over the slice, then a shuffle tree merges
-// the slots and slot 0 writes the partial row.
+// Heavy nodes, phase 1: one warp per work item (a slice of one node's arcs) leaves the
+// max over the slice's changed sources as a partial row.
 template <int LOGP>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, (LOGP >= 10 ? 2 : 4))
 k_heavy_partial(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
                 const uint8_t *__restrict__ cur, const uint32_t *__restrict__ chg_prev,
                 const int32_t *__restrict__ item_node, const int64_t *__restrict__ item_beg,
                 int64_t n_items, int64_t item_arcs, int dense, uint8_t *__restrict__ partial,
                 unsigned long long *__restrict__ merged_out) {
   using Gm = Geo<LOGP>;
+  using B = Batch<LOGP>;
+  __shared__ int32_t sids[kThreads / 32][B::HEAVY_IDS];
   const int lane = threadIdx.x & 31;
   const int gl = lane % Gm::G;
   const int slot = lane / Gm::G;
-  uint32_t my_merged = 0;
+  const unsigned below = (1u << lane) - 1u;
+  int32_t *wids = sids[threadIdx.x >> 5];
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t i = warp; i < n_items; i += nwarps) {
-    const int64_t v = __ldg(item_node + i);
-    const int64_t beg = __ldg(item_beg + i);
+  uint32_t my_merged = 0;
+  for (int64_t it = warp; it < n_items; it += nwarps) {
+    const int64_t v = __ldg(item_node + it);
+    const int64_t beg = __ldg(item_beg + it);
     int64_t end = __ldg(offsets + v + 1);
     if (end > beg + item_arcs) end = beg + item_arcs;
     uint4 acc[Gm::CPL];
 #pragma unroll
     for (int c = 0; c < Gm::CPL; c++) acc[c] = make_uint4(0, 0, 0, 0);
-    for (int64_t k = beg + slot; k < end; k += (int64_t)Gm::NPW * kUnroll) {
-      int32_t w[kUnroll];
-      bool act[kUnroll];
+    int32_t idr[B::HJ];
 #pragma unroll
-      for (int u = 0; u < kUnroll; u++) {
-        const int64_t kk = k + (int64_t)u * Gm::NPW;
-        act[u] = kk < end;
-        w[u] = act[u] ? __ldg(succ + kk) : 0;
+    for (int j = 0; j < B::HJ; j++) {
+      const int64_t k = beg + j * 32 + lane;
+      idr[j] = (k < end) ? __ldg(succ + k) : -1;
+    }
+    for (int64_t kb = beg; kb < end; kb += B::HEAVY_IDS) {
+      int cnt = 0;
+#pragma unroll
+      for (int j = 0; j < B::HJ; j++) {
+        const bool act = idr[j] >= 0 && (dense || test_bit(chg_prev, idr[j]));
+        const unsigned bal = __ballot_sync(0xffffffffu, act);
+        if (act) wids[cnt + __popc(bal & below)] = idr[j];
+        cnt += __popc(bal);
       }
-      if (!dense) {
 #pragma unroll
-        for (int u = 0; u < kUnroll; u++) act[u] = act[u] && test_bit(chg_prev, w[u]);
+      for (int j = 0; j < B::HJ; j++) {
+        const int64_t k = kb + B::HEAVY_IDS + j * 32 + lane;
+        idr[j] = (k < end) ? __ldg(succ + k) : -1;
       }
-      uint4 r[kUnroll][Gm::CPL];
+      __syncwarp();
+      for (int i = slot; i < cnt; i += Gm::NPW * B::U) {
+        uint4 r[B::U][Gm::CPL];
 #pragma unroll
-      for (int u = 0; u < kUnroll; u++)
+        for (int u = 0; u < B::U; u++) {
+          const int e = i + u * Gm::NPW;
+          const bool ok = e < cnt;
+          const int32_t w = ok ? wids[e] : 0;
 #pragma unroll
-        for (int c = 0; c < Gm::CPL; c++)
-          r[u][c] = act[u] ? ldg4(cur + (size_t)w[u] * Gm::P + 16 * (c * Gm::G + gl))
-                           : make_uint4(0, 0, 0, 0);
+          for (int c = 0; c < Gm::CPL; c++)
+            r[u][c] = ok ? ldg4(cur + (size_t)w * Gm::P + 16 * (c * Gm::G + gl))
+                         : make_uint4(0, 0, 0, 0);
+        }
 #pragma unroll
-      for (int u = 0; u < kUnroll; u++) {
-        my_merged += (act[u] && gl == 0);
+        for (int u = 0; u < B::U; u++)
 #pragma unroll
-        for (int c = 0; c < Gm::CPL; c++) acc[c] = bmax4(acc[c], r[u][c]);
+          for (int c = 0; c < Gm::CPL; c++) acc[c] = bmax4(acc[c], r[u][c]);
       }
+      my_merged += (lane == 0) ? (uint32_t)cnt : 0u;
+      __syncwarp();
     }
 #pragma unroll
     for (int off = Gm::G; off < 32; off <<= 1)
@@ -393,7 +551,7 @@ k_heavy_partial(const int64_t *__restrict__ offsets, const int32_t *__restrict__
     if (slot == 0) {
 #pragma unroll
       for (int c = 0; c < Gm::CPL; c++)
-        *reinterpret_cast<uint4 *>(partial + (size_t)i * Gm::P + 16 * (c * Gm::G + gl)) = acc[c];
+        *reinterpret_cast<uint4 *>(partial + (size_t)it * Gm::P + 16 * (c * Gm::G + gl)) = acc[c];
     }
   }
   block_add2(my_merged, 0u, merged_out, nullptr);
@@ -437,8 +595,8 @@ k_heavy_finish(const int32_t *__restrict__ heavy_nodes, const int32_t *__restric
       any = __any_sync(gmask, any);
       const bool self_chg = test_bit(chg_prev, v);
       if (any || self_chg) {
-        const bool changed = finish_node<LOGP>(v, acc, self_chg, gmask, gl, cur, nxt, est,
-                                               sum_dist, sum_recip, ec, tf);
+        const bool changed = finish_node<LOGP>(v, acc, acc, false, self_chg, gmask, gl, cur,
+                                               nxt, est, sum_dist, sum_recip, ec, tf);
         if (changed && gl == 0) {
           atomicOr(chg_now + (v >> 5), 1u << (v & 31));
           my_nch++;
@@ -552,7 +710,7 @@ int union_step_impl(int64_t lo, int64_t hi, const int64_t *offsets, const int32_
     if (int e = check_launch("k_heavy_partial")) return e;
   }
   if (hi > lo) {
-    const int64_t warps = (hi - lo + Gm::NPW - 1) / Gm::NPW + 1;
+    const int64_t warps = (hi - lo + Gm::NPW - 1) / Gm::NPW + 1;   // capped at the resident set
     k_light<LOGP><<<grid_for_warps(warps), kThreads, 0, s>>>(
         offsets, succ, cur, nxt, chg_prev, chg_now, est, sum_dist, sum_recip, ec, lo, hi,
         light_max_deg, dense, tf, nch, merged);
