@@ -97,6 +97,8 @@ BUILDERS = {
     "config3": lambda th=None: disconnected_t(1 << 22, 1 << 21, 0.1, 6.0, seed=2, threads=th),
     "config4": lambda th=None: weblike_t(1 << 24, seed=3, threads=th),
     "config5": lambda th=None: rmat_t(28, 1 << 32, seed=4, threads=th),
+    # config 5 at 1/16 scale (same law, same parameters): for iteration on smaller boxes
+    "config5s": lambda th=None: rmat_t(24, 1 << 28, seed=4, threads=th),
 }
 
 CONFIGS = {
@@ -110,6 +112,8 @@ CONFIGS = {
                            "web-like n=2^24, Zipf(2.1) on {3..10^4}, 80% within +-1024, seed 3, log2m 8"),
     "config5": BenchConfig("config5", 4, 42, ("harmonic",),
                            "R-MAT scale 28, 2^32 arcs, seed 4, log2m 4"),
+    "config5s": BenchConfig("config5s", 4, 42, ("harmonic",),
+                            "R-MAT scale 24, 2^28 arcs (config 5 at 1/16 scale), seed 4, log2m 4"),
 }
 
 
