@@ -310,7 +310,8 @@ __device__ __forceinline__ int64_t warp_lower_bound(const int64_t *__restrict__ 
   return L;
 }
 
-constexpr int kLookRounds = 4;   // L2 prefetch distance of the light kernel, in warp rounds
+constexpr int kLookRounds = 4;    // L2 prefetch distance of the light kernel, in warp rounds
+constexpr int kChunkRounds = 16;  // warp rounds per grid-stride chunk of the light kernel
 
 // Light nodes (in-degree <= max_deg): one group of G lanes per node, NPW nodes per warp
 // round.  Each warp owns one contiguous node range, balanced over the grid by arcs +
@@ -340,24 +341,19 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   uint32_t my_nch = 0, my_merged = 0;
 
-  // this warp's node range [vb, ve), rounds of NPW nodes (NPW-aligned so a round's change
-  // bits share one bitmap word)
+  // Node chunks of kChunkRounds warp rounds, dealt to warps grid-stride: at any moment the
+  // resident warps sweep one contiguous window of the id space (L2 reuse of shared
+  // sources, e.g. config 4's +-1024 locality), while inside a chunk the offsets, ids,
+  // own rows and estimates are sequential streams that lane 0 prefetches into L2
+  // kLookRounds rounds ahead -- leaving the random source-row gather as the only exposed
+  // memory latency of a round.  Rounds are NPW-aligned so a round's change bits share one
+  // bitmap word.
   const int64_t lo_al = (lo / Gm::NPW) * Gm::NPW;
-  const int64_t f0 = __ldg(offsets + lo_al) + lo_al, f1 = __ldg(offsets + hi) + hi;
-  const int64_t span = f1 - f0;
-  int64_t vb = lo_al, ve = hi;
-  if (warp > 0) {
-    const int64_t t = f0 + (int64_t)(((__int128)span * warp) / nwarps);
-    vb = (warp_lower_bound(offsets, lo_al, hi, t, lane) / Gm::NPW) * Gm::NPW;
-  }
-  if (warp + 1 < nwarps) {
-    const int64_t t = f0 + (int64_t)(((__int128)span * (warp + 1)) / nwarps);
-    ve = (warp_lower_bound(offsets, lo_al, hi, t, lane) / Gm::NPW) * Gm::NPW;
-  }
-  if (vb < lo_al) vb = lo_al;
-
-  // prefetch pipeline (lane 0): offsets 2*kLook rounds ahead; own rows, estimates, sums
-  // and successor ids kLook rounds ahead, using offsets read one round earlier.
+  constexpr int64_t CN = (int64_t)kChunkRounds * Gm::NPW;
+  const int64_t nchunks = (hi - lo_al + CN - 1) / CN;
+  for (int64_t chunk = warp; chunk < nchunks; chunk += nwarps) {
+  const int64_t vb = lo_al + chunk * CN;
+  const int64_t ve = vb + CN < hi ? vb + CN : hi;
   int64_t pf_a0 = -1, pf_a1 = -1;
   if (lane == 0) {
     for (int r = 0; r < kLookRounds && vb + (int64_t)r * Gm::NPW < ve; r++) {
@@ -370,10 +366,8 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
       const int64_t a0 = __ldg(offsets + pb), a1 = __ldg(offsets + pe);
       l2_prefetch(succ + a0, (a1 - a0) * 4);
     }
-    l2_prefetch(offsets + vb, (ve - vb + 1 < 8 * kLookRounds * Gm::NPW
-                                   ? ve - vb + 1 : 8 * kLookRounds * Gm::NPW) * 8);
+    l2_prefetch(offsets + vb, (ve - vb + 1) * 8);
   }
-
   for (int64_t base = vb; base < ve; base += Gm::NPW) {
     if (lane == 0) {
       const int64_t pb = base + (int64_t)kLookRounds * Gm::NPW;
@@ -389,9 +383,6 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
         if (sum_recip) l2_prefetch(sum_recip + pb, (pe - pb) * 8);
         pf_a0 = __ldg(offsets + pb);         // consumed next round
         pf_a1 = __ldg(offsets + pe);
-        const int64_t ob = pb + (int64_t)kLookRounds * Gm::NPW;
-        if (ob < ve && ((ob * 8) & 127) < Gm::NPW * 8)   // one offsets line ahead
-          l2_prefetch(offsets + ob, 128);
       }
     }
     const int64_t v = base + grp;
@@ -472,6 +463,7 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
       my_nch += __popc(m);
     }
   }
+  }  // chunk
   block_add2(my_nch, my_merged, nch_out, merged_out);
 }
 
