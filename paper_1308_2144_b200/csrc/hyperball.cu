@@ -48,16 +48,28 @@ template <int LOGP>
 struct Geo {
   static constexpr int P = 1 << LOGP;
   static constexpr int CH = P / 16;               // 16-byte chunks per row
-  static constexpr int G = CH < 32 ? CH : 32;     // lanes cooperating on one row
-  static constexpr int CPL = CH / G;              // chunks per lane (> 1 only for p > 512)
+  // lanes cooperating on one row: one 16-byte chunk per lane up to p = 128, then two
+  // (p = 256 -> 8 lanes: four nodes per warp round amortise the per-node epilogue),
+  // at most 32
+  static constexpr int G = CH <= 8 ? CH : (CH / 2 < 32 ? CH / 2 : 32);
+  static constexpr int CPL = CH / G;              // chunks per lane
   static constexpr int NPW = 32 / G;              // rows handled side by side per warp
 };
 
 // Work-item size for heavy nodes: 16 row loads per lane (16 * NPW arcs), at least 64.
-__host__ __device__ constexpr int64_t item_arcs_for(int b) {
-  return (16 * (32 / ((1 << b) / 16 < 32 ? (1 << b) / 16 : 32))) > 64
-             ? (16 * (32 / ((1 << b) / 16 < 32 ? (1 << b) / 16 : 32)))
-             : 64;
+template <int LOGP>
+constexpr int64_t item_arcs_t() {
+  return 16 * Geo<LOGP>::NPW > 64 ? 16 * Geo<LOGP>::NPW : 64;
+}
+int64_t item_arcs_for(int b) {
+  switch (b) {
+    case 4: return item_arcs_t<4>();   case 5: return item_arcs_t<5>();
+    case 6: return item_arcs_t<6>();   case 7: return item_arcs_t<7>();
+    case 8: return item_arcs_t<8>();   case 9: return item_arcs_t<9>();
+    case 10: return item_arcs_t<10>(); case 11: return item_arcs_t<11>();
+    case 12: return item_arcs_t<12>();
+  }
+  return 64;
 }
 constexpr int64_t kLightMaxDeg = 64;
 
@@ -193,33 +205,38 @@ __device__ __forceinline__ bool finish_node(int64_t v, const uint4 (&acc)[Geo<LO
       *reinterpret_cast<uint4 *>(nrow + 16 * (c * Gm::G + gl)) = nw[c];
   }
   if (changed) {
-    uint64_t S = 0;
-    int zeros = 0;
-    uint32_t mx = 0;
+    // sum_j 2^-M[j] as exact fp64 partial sums (every M <= 31 here: at most 36 significant
+    // bits, so any summation order gives the reference's sequential result), zero count by
+    // SWAR, and an OR of all bytes to detect registers > 31 (sequential fallback).
+    double s = 0.0;
+    uint32_t zeros = 0, big = 0;
 #pragma unroll
     for (int c = 0; c < Gm::CPL; c++) {
-      acc_word(nw[c].x, S, zeros, mx);
-      acc_word(nw[c].y, S, zeros, mx);
-      acc_word(nw[c].z, S, zeros, mx);
-      acc_word(nw[c].w, S, zeros, mx);
-    }
+      const uint32_t ws[4] = {nw[c].x, nw[c].y, nw[c].z, nw[c].w};
 #pragma unroll
-    for (int off = 1; off < Gm::G; off <<= 1) {
-      S += __shfl_xor_sync(gmask, S, off);
-      zeros += __shfl_xor_sync(gmask, zeros, off);
-      uint32_t o = __shfl_xor_sync(gmask, mx, off);
-      mx = o > mx ? o : mx;
+      for (int q = 0; q < 4; q++) {
+        const uint32_t w = ws[q];
+        zeros += __popc(~(((w & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | w) & 0x80808080u);
+        big |= w;
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+          const uint32_t m = (w >> (8 * i)) & 0xffu;
+          s = __dadd_rn(s, __hiloint2double((int)(0x3FF00000u - (m << 20)), 0));
+        }
+      }
     }
-    if (mx > 31u) __syncwarp(gmask);  // the row was stored above; make it visible
+    zeros = __reduce_add_sync(gmask, zeros);
+    big = __reduce_or_sync(gmask, big);
+#pragma unroll
+    for (int off = 1; off < Gm::G; off <<= 1) s = __dadd_rn(s, __shfl_xor_sync(gmask, s, off));
+    const bool seq = (big & 0xE0E0E0E0u) != 0u;   // some register > 31
+    if (seq) __syncwarp(gmask);  // the row was stored above; make it visible
     if (gl == 0) {
-      double s;
-      if (mx <= 31u) {
-        s = (double)S * 0x1p-31;
-      } else {
+      if (seq) {  // reference order: ascending-j fp64 sum (_kernels.py:25-30)
         s = 0.0;
         for (int j = 0; j < Gm::P; j++) s = __dadd_rn(s, pow2neg(nrow[j]));
       }
-      const double e = finish_estimate(s, zeros, ec);
+      const double e = finish_estimate(s, (int)zeros, ec);
       const double old = pre_vals ? pre_vals[0] : est[v];
       est[v] = e;
       const double d = np_max0(__dsub_rn(e, old));
@@ -354,34 +371,36 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
   for (int64_t chunk = warp; chunk < nchunks; chunk += nwarps) {
   const int64_t vb = lo_al + chunk * CN;
   const int64_t ve = vb + CN < hi ? vb + CN : hi;
+  // prefetch of the per-round streams, kLookRounds rounds per batch: own rows, estimates,
+  // sums and successor ids of rounds [pb, pe).  Ids need offsets, which lane 0 loads one
+  // round before issuing their prefetch (offsets of the chunk are prefetched first).
+  auto stream_prefetch = [&](int64_t pb, int64_t pe) {
+    l2_prefetch(cur + (size_t)pb * Gm::P, (pe - pb) * Gm::P);
+    l2_prefetch(est + pb, (pe - pb) * 8);
+    if (sum_dist) l2_prefetch(sum_dist + pb, (pe - pb) * 8);
+    if (sum_recip) l2_prefetch(sum_recip + pb, (pe - pb) * 8);
+  };
   int64_t pf_a0 = -1, pf_a1 = -1;
   if (lane == 0) {
-    for (int r = 0; r < kLookRounds && vb + (int64_t)r * Gm::NPW < ve; r++) {
-      const int64_t pb = vb + (int64_t)r * Gm::NPW;
-      const int64_t pe = pb + Gm::NPW < ve ? pb + Gm::NPW : ve;
-      l2_prefetch(cur + (size_t)pb * Gm::P, (pe - pb) * Gm::P);
-      l2_prefetch(est + pb, (pe - pb) * 8);
-      if (sum_dist) l2_prefetch(sum_dist + pb, (pe - pb) * 8);
-      if (sum_recip) l2_prefetch(sum_recip + pb, (pe - pb) * 8);
-      const int64_t a0 = __ldg(offsets + pb), a1 = __ldg(offsets + pe);
-      l2_prefetch(succ + a0, (a1 - a0) * 4);
-    }
     l2_prefetch(offsets + vb, (ve - vb + 1) * 8);
+    const int64_t pe = vb + (int64_t)kLookRounds * Gm::NPW < ve ? vb + (int64_t)kLookRounds * Gm::NPW : ve;
+    stream_prefetch(vb, pe);
+    const int64_t a0 = __ldg(offsets + vb), a1 = __ldg(offsets + pe);
+    l2_prefetch(succ + a0, (a1 - a0) * 4);
   }
   for (int64_t base = vb; base < ve; base += Gm::NPW) {
     if (lane == 0) {
-      const int64_t pb = base + (int64_t)kLookRounds * Gm::NPW;
-      if (pf_a0 >= 0) {          // ids of round pb - NPW (offsets loaded last round)
+      if (pf_a0 >= 0) {                        // ids of the batch announced last round
         l2_prefetch(succ + pf_a0, (pf_a1 - pf_a0) * 4);
         pf_a0 = -1;
       }
-      if (pb < ve) {
-        const int64_t pe = pb + Gm::NPW < ve ? pb + Gm::NPW : ve;
-        l2_prefetch(cur + (size_t)pb * Gm::P, (pe - pb) * Gm::P);
-        l2_prefetch(est + pb, (pe - pb) * 8);
-        if (sum_dist) l2_prefetch(sum_dist + pb, (pe - pb) * 8);
-        if (sum_recip) l2_prefetch(sum_recip + pb, (pe - pb) * 8);
-        pf_a0 = __ldg(offsets + pb);         // consumed next round
+      const int64_t rnd = (base - vb) / Gm::NPW;
+      const int64_t pb = base + (int64_t)kLookRounds * Gm::NPW;
+      if (rnd % kLookRounds == 0 && pb < ve) {
+        const int64_t pe = pb + (int64_t)kLookRounds * Gm::NPW < ve
+                               ? pb + (int64_t)kLookRounds * Gm::NPW : ve;
+        stream_prefetch(pb, pe);
+        pf_a0 = __ldg(offsets + pb);           // consumed next round
         pf_a1 = __ldg(offsets + pe);
       }
     }
@@ -394,7 +413,9 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
       if (end - beg > max_deg) valid = false;  // heavy: handled by the item path
     }
     const bool self_chg = valid && test_bit(chg_prev, v);
-    const bool pre = valid && (dense || self_chg);   // own row certainly needed: load early
+    bool pre;                                   // own row certainly needed: load early
+    if (dense) pre = valid;                     // (no wait on the bitmap word)
+    else pre = self_chg;
     uint4 self[Gm::CPL], acc[Gm::CPL];
 #pragma unroll
     for (int c = 0; c < Gm::CPL; c++) {
