@@ -18,6 +18,8 @@
  *   hb_union_step     engine.py:164-169 _ProbabilisticBackend.union_range
  *                     (-> _kernels.py:67-114 hll_union_range) fused with
  *                     centrality.py:132-150 CentralityAccumulator.on_step/accumulate
+ *   hb_finalize       centrality.py:153-171 finalize_closeness / finalize_harmonic /
+ *                     finalize_lin (on the device-resident sums)
  *   hb_relabel_csr    graph.py:145-155 transpose's output consumed in schedule order
  *                     (internal relabelling; no reference counterpart)
  *   hb_hash_items     hll.py:79-88 hash_items (device twin, used by tests)
@@ -95,6 +97,16 @@ int hb_union_step(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets,
                   int64_t n_heavy, const int32_t *item_node, const int64_t *item_beg,
                   int64_t n_items, int64_t item_arcs, uint8_t *partial, uint64_t *nch_out,
                   uint64_t *merged_out, void *stream);
+
+/* Finalizers (centrality.py:153-171) over device sums in internal order, written in
+ * original order: out[o] uses internal row rank[o] (rank NULL = identity).
+ *   closeness[o] = 1 / sum_dist where sum_dist > 0, else 0
+ *   harmonic[o]  = sum_recip
+ *   lin[o]       = coreach^2 / sum_dist where sum_dist > 0, else 1
+ * Any output pointer may be NULL (not computed). */
+int hb_finalize(int64_t n, const int32_t *rank, const double *sum_dist, const double *sum_recip,
+                const double *coreach, double *closeness, double *harmonic, double *lin,
+                void *stream);
 
 /* Relabel a CSR into schedule order: new row i is old row perm[i] with every id mapped
  * through rank (rank[perm[i]] == i).  new_offsets (device int64 [n+1]) must already hold

@@ -46,6 +46,7 @@ class CentralityAccumulator(BallObserver):
         self.coreach = np.zeros(n, dtype=np.float64)
         self.converged = False
         self._binding = None   # engine-side DeviceSums when fused
+        self._fresh = True     # sums never touched: the device copy can start from zeros
 
     # lazily refreshed host views of the device sums
     def _pull(self) -> None:
@@ -61,6 +62,7 @@ class CentralityAccumulator(BallObserver):
     def sum_dist(self, value) -> None:
         self._pull()
         self._sum_dist = np.asarray(value, dtype=np.float64)
+        self._fresh = False
         if self._binding is not None:
             self._binding.invalidate()
 
@@ -73,6 +75,7 @@ class CentralityAccumulator(BallObserver):
     def sum_recip(self, value) -> None:
         self._pull()
         self._sum_recip = np.asarray(value, dtype=np.float64)
+        self._fresh = False
         if self._binding is not None:
             self._binding.invalidate()
 
@@ -83,8 +86,11 @@ class CentralityAccumulator(BallObserver):
         self.accumulate(t, np.maximum(diff, 0.0))
 
     def on_converged(self, final_estimates: np.ndarray) -> None:
-        self._pull()
-        self.coreach = np.array(final_estimates, dtype=np.float64, copy=True)
+        final = np.asarray(final_estimates, dtype=np.float64)
+        # the engine hands every observer a fresh read-only host copy: keep it as is
+        self.coreach = final if not final.flags.writeable else final.copy()
+        if self._binding is not None and not self._binding.stale:
+            self._binding.capture_coreach(self.coreach)
         self.converged = True
 
     def accumulate(self, t: int, delta: np.ndarray) -> None:
@@ -92,6 +98,7 @@ class CentralityAccumulator(BallObserver):
         if t <= 0:
             raise ValueError(f"distance t must be >= 1, got {t}")
         self._pull()
+        self._fresh = False
         if self._binding is not None:
             self._binding.invalidate()
         self._sum_dist += t * delta
@@ -115,19 +122,39 @@ def fusable(obs, n: int) -> bool:
     return int(attrs.get("n", n)) == n
 
 
+def _on_device(acc, which: str):
+    """Finalize on the device when the accumulator's sums (and, for Lin, its coreach) are
+    the live device copies; None otherwise (host path)."""
+    b = getattr(acc, "_binding", None)
+    if b is None or b.stale:
+        return None
+    if which == "lin" and (b.coreach_dev is None or b.coreach_host_id != id(acc.coreach)):
+        return None
+    return b.finalize(which)
+
+
 def finalize_closeness(acc) -> np.ndarray:
     """1 / distance sum where positive, 0 for nodes nothing else coreaches."""
+    out = _on_device(acc, "closeness")
+    if out is not None:
+        return out
     s = np.asarray(acc.sum_dist, dtype=np.float64)
     return np.divide(1.0, s, out=np.zeros_like(s), where=s > 0)
 
 
 def finalize_harmonic(acc) -> np.ndarray:
     """Sum of reciprocal distances (unreachable pairs contribute 0)."""
+    out = _on_device(acc, "harmonic")
+    if out is not None:
+        return out
     return np.array(acc.sum_recip, dtype=np.float64, copy=True)
 
 
 def finalize_lin(acc) -> np.ndarray:
     """coreach^2 / distance sum where positive, 1 otherwise."""
+    out = _on_device(acc, "lin")
+    if out is not None:
+        return out
     s = np.asarray(acc.sum_dist, dtype=np.float64)
     c = np.asarray(acc.coreach, dtype=np.float64)
     return np.divide(c * c, s, out=np.ones_like(s), where=s > 0)

@@ -659,6 +659,28 @@ k_estimate_rows(const uint8_t *__restrict__ regs, int64_t lo, int64_t hi, EstCon
     out[v] = estimate_row_thread<Gm::P>(regs + (size_t)v * Gm::P, ec);
 }
 
+// Finalizers (centrality.py:153-171), optionally gathering from internal order:
+// out[o] for original id o reads internal row rank[o].  Explicitly rounded fp64 ops.
+__global__ void k_finalize(int64_t n, const int32_t *__restrict__ rank,
+                           const double *__restrict__ sum_dist,
+                           const double *__restrict__ sum_recip,
+                           const double *__restrict__ coreach, double *__restrict__ closeness,
+                           double *__restrict__ harmonic, double *__restrict__ lin) {
+  for (int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; o < n;
+       o += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = rank ? (int64_t)__ldg(rank + o) : o;
+    if (harmonic) harmonic[o] = __ldg(sum_recip + v);
+    if (closeness || lin) {
+      const double s = __ldg(sum_dist + v);
+      if (closeness) closeness[o] = s > 0.0 ? __ddiv_rn(1.0, s) : 0.0;
+      if (lin) {
+        const double c = __ldg(coreach + v);
+        lin[o] = s > 0.0 ? __ddiv_rn(__dmul_rn(c, c), s) : 1.0;
+      }
+    }
+  }
+}
+
 __global__ void k_relabel(int64_t n, const int64_t *__restrict__ old_off,
                           const int32_t *__restrict__ old_succ, const int32_t *__restrict__ perm,
                           const int32_t *__restrict__ rank, const int64_t *__restrict__ new_off,
@@ -823,6 +845,18 @@ int hb_union_step(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets,
                      reinterpret_cast<unsigned long long *>(nch_out),
                      reinterpret_cast<unsigned long long *>(merged_out), s));
   return 0;
+}
+
+int hb_finalize(int64_t n, const int32_t *rank, const double *sum_dist, const double *sum_recip,
+                const double *coreach, double *closeness, double *harmonic, double *lin,
+                void *stream) {
+  if (n <= 0) return 0;
+  if ((closeness || lin) && !sum_dist) return set_err_msg("hb_finalize: sum_dist required");
+  if (harmonic && !sum_recip) return set_err_msg("hb_finalize: sum_recip required");
+  if (lin && !coreach) return set_err_msg("hb_finalize: coreach required");
+  k_finalize<<<grid_for_threads(n), kThreads, 0, (cudaStream_t)stream>>>(
+      n, rank, sum_dist, sum_recip, coreach, closeness, harmonic, lin);
+  return check_launch("k_finalize");
 }
 
 int hb_relabel_csr(int64_t n, const int64_t *old_offsets, const int32_t *old_succ,

@@ -152,10 +152,39 @@ class _DeviceSums:
         else:
             sd, sr = acc._sum_dist, acc._sum_recip
         self.host_ids = (id(sd), id(sr))
-        self.sum_dist = dev.to_internal(np.asarray(sd, dtype=np.float64))
-        self.sum_recip = dev.to_internal(np.asarray(sr, dtype=np.float64))
+        if not self.foreign and acc._fresh:       # nothing accumulated yet: no upload
+            self.sum_dist = torch.zeros(dev.n, dtype=torch.float64, device=dev.device)
+            self.sum_recip = torch.zeros(dev.n, dtype=torch.float64, device=dev.device)
+        else:
+            self.sum_dist = dev.to_internal(np.asarray(sd, dtype=np.float64))
+            self.sum_recip = dev.to_internal(np.asarray(sr, dtype=np.float64))
         self.dirty = False
         self.stale = False
+
+    coreach_dev = None
+    coreach_host_id = None
+
+    def capture_coreach(self, host_final) -> None:
+        """on_converged: keep the final estimates on the device for finalize_lin."""
+        self.coreach_dev = self.dev.est.clone()
+        self.coreach_host_id = id(host_final)
+
+    def finalize(self, which: str) -> np.ndarray:
+        """closeness / harmonic / lin computed on the device (hb_finalize), original order."""
+        dev = self.dev
+        n = dev.n
+        out = torch.empty(n, dtype=torch.float64, device=dev.device)
+        ptrs = {"closeness": None, "harmonic": None, "lin": None}
+        ptrs[which] = out.data_ptr()
+        rank = dev.sched.rank
+        _lib.check(_lib.hb().hb_finalize(
+            n, rank.data_ptr() if rank is not None else None, self.sum_dist.data_ptr(),
+            self.sum_recip.data_ptr(),
+            self.coreach_dev.data_ptr() if self.coreach_dev is not None else None,
+            ptrs["closeness"], ptrs["harmonic"], ptrs["lin"], dev.stream.cuda_stream),
+            "hb_finalize")
+        dev.launches += 1
+        return dev.to_host_raw(out)
 
     def pull_into(self, acc) -> None:
         sd = self.dev.to_host(self.sum_dist)
@@ -166,6 +195,7 @@ class _DeviceSums:
             self.host_ids = (id(acc.sum_dist), id(acc.sum_recip))
         else:
             acc._sum_dist, acc._sum_recip = sd, sr
+            acc._fresh = False
 
     def invalidate(self) -> None:
         self.stale = True
@@ -239,7 +269,14 @@ class _Device:
         return self.sched.to_internal(x.to(self.device)).contiguous()
 
     def to_host(self, x: torch.Tensor) -> np.ndarray:
-        return self.sched.to_original(x).cpu().numpy()
+        """Original-order host copy (through pinned memory: full PCIe rate)."""
+        return self.to_host_raw(self.sched.to_original(x))
+
+    def to_host_raw(self, x: torch.Tensor) -> np.ndarray:
+        buf = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
+        buf.copy_(x, non_blocking=True)
+        self.stream.synchronize()
+        return buf.numpy()
 
     def snapshot_original(self):
         s = self.sched
