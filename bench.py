@@ -334,7 +334,6 @@ def run_b200(args):
             merged_total = st2._dev.merged_total
             iters = st2.t
             del st2, acc2, har, clo, lin
-            torch.cuda.empty_cache()
             if i >= args.e2e_warmup:
                 runs.append((dt, merged_total, iters))
         dt = max(r[0] for r in runs) if runs else float("nan")
