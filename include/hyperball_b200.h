@@ -20,6 +20,10 @@
  *                     centrality.py:132-150 CentralityAccumulator.on_step/accumulate
  *   hb_finalize       centrality.py:153-171 finalize_closeness / finalize_harmonic /
  *                     finalize_lin (on the device-resident sums)
+ *   hb_gather_changed / hb_scatter_rows / hb_refresh_rows
+ *                     multi-GPU exchange of changed counter rows (no reference
+ *                     counterpart: the reference shares `cur` between threads,
+ *                     engine.py:377-390)
  *   hb_relabel_csr    graph.py:145-155 transpose's output consumed in schedule order
  *                     (internal relabelling; no reference counterpart)
  *   hb_hash_items     hll.py:79-88 hash_items (device twin, used by tests)
@@ -107,6 +111,22 @@ int hb_union_step(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets,
 int hb_finalize(int64_t n, const int32_t *rank, const double *sum_dist, const double *sum_recip,
                 const double *coreach, double *closeness, double *harmonic, double *lin,
                 void *stream);
+
+/* Multi-GPU exchange.
+ * hb_gather_changed: for every v in [lo, hi) with chg_bits bit v set, append v to ids_out
+ *   and rows[v] (p = 2^b bytes) to rows_out; *count_out (device uint64, zeroed by the
+ *   call) receives the number appended.  Order is unspecified.
+ * hb_scatter_rows: dst[ids[i]] = rows[i] for i < k and set bit ids[i] of chg_bits
+ *   (chg_bits may be NULL).
+ * hb_refresh_rows: dst[v] = src[v] for every v in [0, n) outside [lo, hi) whose bit is
+ *   set in bits (keeps the lazy double buffer of rows owned by other ranks). */
+int hb_gather_changed(int64_t lo, int64_t hi, const uint32_t *chg_bits, const uint8_t *rows,
+                      int b, int32_t *ids_out, uint8_t *rows_out, uint64_t *count_out,
+                      void *stream);
+int hb_scatter_rows(int64_t k, const int32_t *ids, const uint8_t *rows, int b, uint8_t *dst,
+                    uint32_t *chg_bits, void *stream);
+int hb_refresh_rows(int64_t n, int64_t lo, int64_t hi, const uint32_t *bits, const uint8_t *src,
+                    uint8_t *dst, int b, void *stream);
 
 /* Relabel a CSR into schedule order: new row i is old row perm[i] with every id mapped
  * through rank (rank[perm[i]] == i).  new_offsets (device int64 [n+1]) must already hold

@@ -43,6 +43,9 @@ HB_SIGNATURES = {
                              _vp, _i64, _vp, _dbl, _dbl, _int, _int, _i64, _vp, _vp, _i64,
                              _vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp]),
     "hb_finalize": (_int, [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "hb_gather_changed": (_int, [_i64, _i64, _vp, _vp, _int, _vp, _vp, _vp, _vp]),
+    "hb_scatter_rows": (_int, [_i64, _vp, _vp, _int, _vp, _vp, _vp]),
+    "hb_refresh_rows": (_int, [_i64, _i64, _i64, _vp, _vp, _vp, _int, _vp]),
     "hb_relabel_csr": (_int, [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "hb_hash_items": (_int, [_i64, _vp, _vp, _u64, _vp, _vp]),
     "hb_item_arcs": (_i64, [_int]),

@@ -659,6 +659,82 @@ k_estimate_rows(const uint8_t *__restrict__ regs, int64_t lo, int64_t hi, EstCon
     out[v] = estimate_row_thread<Gm::P>(regs + (size_t)v * Gm::P, ec);
 }
 
+// ---- multi-GPU exchange --------------------------------------
+// Pack the rows of [lo, hi) whose chg_now bit is set: ids_out[k] = v, rows_out[k] = nxt[v].
+// One warp per bitmap word; positions by one atomicAdd per word (order is irrelevant:
+// receivers scatter by id).
+__global__ void k_gather_changed(int64_t lo, int64_t hi, const uint32_t *__restrict__ bits,
+                                 const uint8_t *__restrict__ src, int p,
+                                 int32_t *__restrict__ ids_out, uint8_t *__restrict__ rows_out,
+                                 unsigned long long *__restrict__ count) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t w0 = lo >> 5, w1 = (hi + 31) >> 5;
+  for (int64_t w = w0 + warp; w < w1; w += nwarps) {
+    uint32_t m = __ldg(bits + w);
+    const int64_t v0 = w << 5;
+    if (v0 < lo) m &= ~0u << (lo - v0);
+    if (v0 + 32 > hi) m &= (hi - v0 >= 32) ? ~0u : ((1u << (hi - v0)) - 1u);
+    const int c = __popc(m);
+    if (c == 0) continue;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(count, (unsigned long long)c);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (lane < c) {
+      const int bit = __fns(m, 0, lane + 1);
+      const int64_t v = v0 + bit;
+      ids_out[base + lane] = (int32_t)v;
+      const uint4 *s4 = reinterpret_cast<const uint4 *>(src + (size_t)v * p);
+      uint4 *d4 = reinterpret_cast<uint4 *>(rows_out + (size_t)(base + lane) * p);
+      for (int q = 0; q < p / 16; q++) d4[q] = __ldg(s4 + q);
+    }
+  }
+}
+
+// Apply received rows: dst[ids[k]] = rows[k] and set their change bits.
+__global__ void k_scatter_rows(int64_t k, const int32_t *__restrict__ ids,
+                               const uint8_t *__restrict__ rows, int p,
+                               uint8_t *__restrict__ dst, uint32_t *__restrict__ bits) {
+  const int64_t chunks = p / 16;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < k * chunks;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t / chunks, q = t % chunks;
+    const int64_t v = __ldg(ids + r);
+    reinterpret_cast<uint4 *>(dst + (size_t)v * p)[q] =
+        __ldg(reinterpret_cast<const uint4 *>(rows + (size_t)r * p) + q);
+    if (q == 0 && bits) atomicOr(bits + (v >> 5), 1u << (v & 31));
+  }
+}
+
+// Lazy double buffer for rows this rank does not own: dst[v] = src[v] for every v outside
+// [lo, hi) whose bit is set in `bits` (rows that changed last iteration).
+__global__ void k_refresh_rows(int64_t n, int64_t lo, int64_t hi,
+                               const uint32_t *__restrict__ bits,
+                               const uint8_t *__restrict__ src, uint8_t *__restrict__ dst,
+                               int p) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t words = (n + 31) >> 5;
+  const int chunks = p / 16;
+  for (int64_t w = warp; w < words; w += nwarps) {
+    const int64_t v0 = w << 5;
+    if (v0 >= lo && v0 + 32 <= hi) continue;          // fully owned
+    uint32_t m = __ldg(bits + w);
+    if (v0 + 32 > n) m &= (n - v0 >= 32) ? ~0u : ((1u << (n - v0)) - 1u);
+    while (m) {
+      const int bit = __ffs(m) - 1;
+      m &= m - 1;
+      const int64_t v = v0 + bit;
+      if (v >= lo && v < hi) continue;
+      for (int q = lane; q < chunks; q += 32)
+        reinterpret_cast<uint4 *>(dst + (size_t)v * p)[q] =
+            __ldg(reinterpret_cast<const uint4 *>(src + (size_t)v * p) + q);
+    }
+  }
+}
+
 // Finalizers (centrality.py:153-171), optionally gathering from internal order:
 // out[o] for original id o reads internal row rank[o].  Explicitly rounded fp64 ops.
 __global__ void k_finalize(int64_t n, const int32_t *__restrict__ rank,
@@ -857,6 +933,35 @@ int hb_finalize(int64_t n, const int32_t *rank, const double *sum_dist, const do
   k_finalize<<<grid_for_threads(n), kThreads, 0, (cudaStream_t)stream>>>(
       n, rank, sum_dist, sum_recip, coreach, closeness, harmonic, lin);
   return check_launch("k_finalize");
+}
+
+int hb_gather_changed(int64_t lo, int64_t hi, const uint32_t *chg_bits, const uint8_t *rows,
+                      int b, int32_t *ids_out, uint8_t *rows_out, uint64_t *count_out,
+                      void *stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(count_out, 0, sizeof(uint64_t), s);
+  if (e != cudaSuccess) return set_err("hb_gather_changed memset", e);
+  if (hi <= lo) return 0;
+  k_gather_changed<<<grid_for_warps(((hi + 31) >> 5) - (lo >> 5)), kThreads, 0, s>>>(
+      lo, hi, chg_bits, rows, 1 << b, ids_out, rows_out,
+      reinterpret_cast<unsigned long long *>(count_out));
+  return check_launch("k_gather_changed");
+}
+
+int hb_scatter_rows(int64_t k, const int32_t *ids, const uint8_t *rows, int b, uint8_t *dst,
+                    uint32_t *chg_bits, void *stream) {
+  if (k <= 0) return 0;
+  k_scatter_rows<<<grid_for_threads(k * ((1 << b) / 16)), kThreads, 0, (cudaStream_t)stream>>>(
+      k, ids, rows, 1 << b, dst, chg_bits);
+  return check_launch("k_scatter_rows");
+}
+
+int hb_refresh_rows(int64_t n, int64_t lo, int64_t hi, const uint32_t *bits, const uint8_t *src,
+                    uint8_t *dst, int b, void *stream) {
+  if (n <= 0) return 0;
+  k_refresh_rows<<<grid_for_warps((n + 31) >> 5), kThreads, 0, (cudaStream_t)stream>>>(
+      n, lo, hi, bits, src, dst, 1 << b);
+  return check_launch("k_refresh_rows");
 }
 
 int hb_relabel_csr(int64_t n, const int64_t *old_offsets, const int32_t *old_succ,

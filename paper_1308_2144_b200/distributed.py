@@ -1,0 +1,289 @@
+"""Multi-GPU HyperBall: node-range partition + changed-row exchange.
+
+Within an iteration every counter row depends only on the previous iteration's rows
+(Jacobi double buffer, engine.py:393), so the node set is partitioned into contiguous
+internal-id ranges, one per rank (schedule.partition_bounds; in degree order a
+round-robin deal of the degree ranking).  Every rank keeps a full replica of the
+register rows.  One iteration on rank r:
+
+1. ``hb_union_step`` over its own range: owned rows of ``nxt``, owned change bits,
+   estimates and fused accumulator sums.
+2. ``hb_refresh_rows``: rows owned elsewhere that changed in the previous iteration are
+   copied ``cur -> nxt`` (keeps the lazy double buffer valid for remote rows).
+3. ``hb_gather_changed``: pack (id, row) of the owned rows that changed.
+4. exchange: all-gather of the per-rank changed counts -- whose sum is the global
+   termination count, i.e. the reference's ``nch = sum(f.result() ...)`` barrier
+   (engine.py:390) as one collective -- then all-gather of the packed rows (padded to the
+   largest count).
+5. ``hb_scatter_rows``: write every other rank's rows into ``nxt`` and set their change
+   bits, so the next iteration's source-skip bitmap is global.
+
+The protocol is written once (``iterate_rank``) over a small rank-state interface, so the
+same driver runs with NCCL on GPUs (``CudaRankState``), in one process over several
+simulated ranks on one GPU (``run_simulated``, which exercises every exchange kernel),
+and -- in the CPU test suite -- with gloo over an oracle-backed rank state.
+"""
+
+from __future__ import annotations
+
+import time
+from typing import Iterable
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from .centrality import CentralityAccumulator, fusable
+from .engine import (ConvergenceError, HyperBallConfig, _Device, _weights_array,
+                     _check_weighted_width)
+
+
+class TorchComm:
+    """Collectives of one rank over torch.distributed (NCCL on GPUs, gloo on CPU)."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+
+    def exchange(self, ids: torch.Tensor, rows: torch.Tensor, k: int):
+        """All-gather the packed changed rows.  Returns (total changed, [(ids_q, rows_q)]
+        for every other rank q)."""
+        dev = ids.device
+        cnt = torch.tensor([k], dtype=torch.int64, device=dev)
+        counts = [torch.zeros_like(cnt) for _ in range(self.world)]
+        dist.all_gather(counts, cnt, group=self.group)
+        counts = [int(c.item()) for c in counts]
+        total = sum(counts)
+        kmax = max(counts)
+        if kmax == 0:
+            return total, []
+        p = rows.shape[1]
+        send_ids = ids[:kmax] if ids.shape[0] >= kmax else torch.cat(
+            [ids, ids.new_zeros(kmax - ids.shape[0])])
+        send_rows = rows[:kmax] if rows.shape[0] >= kmax else torch.cat(
+            [rows, rows.new_zeros((kmax - rows.shape[0], p))])
+        all_ids = [torch.empty_like(send_ids) for _ in range(self.world)]
+        all_rows = [torch.empty_like(send_rows) for _ in range(self.world)]
+        dist.all_gather(all_ids, send_ids.contiguous(), group=self.group)
+        dist.all_gather(all_rows, send_rows.contiguous(), group=self.group)
+        parts = []
+        for q in range(self.world):
+            if q == self.rank or counts[q] == 0:
+                continue
+            parts.append((all_ids[q][:counts[q]], all_rows[q][:counts[q]]))
+        return total, parts
+
+    def all_gather_slices(self, x: torch.Tensor, lo: int, hi: int, n: int) -> torch.Tensor:
+        """Every rank's [lo, hi) slice of a per-node array, assembled (internal order)."""
+        dev = x.device
+        bounds = torch.tensor([lo, hi], dtype=torch.int64, device=dev)
+        allb = [torch.zeros_like(bounds) for _ in range(self.world)]
+        dist.all_gather(allb, bounds, group=self.group)
+        allb = [tuple(int(v) for v in b.tolist()) for b in allb]
+        width = max(h - l for l, h in allb)
+        send = torch.zeros((width,) + tuple(x.shape[1:]), dtype=x.dtype, device=dev)
+        send[:hi - lo] = x[lo:hi]
+        out = [torch.empty_like(send) for _ in range(self.world)]
+        dist.all_gather(out, send, group=self.group)
+        full = torch.empty((n,) + tuple(x.shape[1:]), dtype=x.dtype, device=dev)
+        for (l, h), part in zip(allb, out):
+            full[l:h] = part[:h - l]
+        return full
+
+
+class CudaRankState:
+    """One rank's device state: full register replica, owned range [lo, hi)."""
+
+    def __init__(self, g, config: HyperBallConfig, world: int, rank: int):
+        n = (g.offsets.numel() if isinstance(g.offsets, torch.Tensor)
+             else np.asarray(g.offsets).shape[0]) - 1
+        w = _weights_array(config.weights, n)
+        if w is not None:
+            _check_weighted_width(config.params, w)
+        self.dev = _Device(g, config, world=world, rank_id=rank)
+        self.dev.seed(w)
+        self.n, self.b, self.p = self.dev.n, self.dev.b, self.dev.p
+        self.lo, self.hi = self.dev.sched.lo, self.dev.sched.hi
+        cap = max(self.hi - self.lo, 1)
+        dv = self.dev.device
+        self.ids_buf = torch.empty(cap, dtype=torch.int32, device=dv)
+        self.rows_buf = torch.empty((cap, self.p), dtype=torch.uint8, device=dv)
+        self.count = torch.zeros(1, dtype=torch.int64, device=dv)
+        self.sums = None
+
+    def bind_sums(self, zeros: bool = True):
+        class _Sums:
+            pass
+        s = _Sums()
+        s.sum_dist = torch.zeros(self.n, dtype=torch.float64, device=self.dev.device)
+        s.sum_recip = torch.zeros(self.n, dtype=torch.float64, device=self.dev.device)
+        self.sums = s
+        return s
+
+    def local_step(self, t: int, dense: bool) -> int:
+        return self.dev.union_step(t, dense, self.sums)
+
+    def refresh_unowned(self) -> None:
+        d = self.dev
+        _lib.check(_lib.hb().hb_refresh_rows(self.n, self.lo, self.hi, d.chg_prev.data_ptr(),
+                                             d.cur.data_ptr(), d.nxt.data_ptr(), self.b,
+                                             d.stream.cuda_stream), "hb_refresh_rows")
+        d.launches += 1
+
+    def gather_changed(self):
+        d = self.dev
+        _lib.check(_lib.hb().hb_gather_changed(self.lo, self.hi, d.chg_now.data_ptr(),
+                                               d.nxt.data_ptr(), self.b,
+                                               self.ids_buf.data_ptr(),
+                                               self.rows_buf.data_ptr(),
+                                               self.count.data_ptr(), d.stream.cuda_stream),
+                   "hb_gather_changed")
+        d.launches += 1
+        k = int(self.count.item())
+        return self.ids_buf[:k], self.rows_buf[:k], k
+
+    def apply_remote(self, ids: torch.Tensor, rows: torch.Tensor) -> None:
+        d = self.dev
+        k = ids.shape[0]
+        if k == 0:
+            return
+        _lib.check(_lib.hb().hb_scatter_rows(k, ids.data_ptr(), rows.contiguous().data_ptr(),
+                                             self.b, d.nxt.data_ptr(), d.chg_now.data_ptr(),
+                                             d.stream.cuda_stream), "hb_scatter_rows")
+        d.launches += 1
+
+    def swap(self) -> None:
+        self.dev.swap()
+
+    # per-node arrays in internal order for the final gather
+    def per_node(self):
+        out = {"est": self.dev.est}
+        if self.sums is not None:
+            out["sum_dist"] = self.sums.sum_dist
+            out["sum_recip"] = self.sums.sum_recip
+        return out
+
+    def to_original(self, x: torch.Tensor) -> np.ndarray:
+        return self.dev.to_host(x)
+
+
+def iterate_rank(state, comm, t: int, dense: bool) -> int:
+    """One distributed iteration on one rank; returns the GLOBAL changed count."""
+    state.local_step(t, dense)
+    state.refresh_unowned()
+    ids, rows, k = state.gather_changed()
+    total, parts = comm.exchange(ids, rows, k)
+    for ids_q, rows_q in parts:
+        state.apply_remote(ids_q, rows_q)
+    state.swap()
+    return total
+
+
+class DistributedResult:
+    """What ``run_distributed`` returns on every rank (host arrays, original order)."""
+
+    def __init__(self, t, num_changed, est, sum_dist=None, sum_recip=None, launches=0):
+        self.t, self.num_changed, self.est = t, num_changed, est
+        self.sum_dist, self.sum_recip = sum_dist, sum_recip
+        self.kernel_launches = launches
+
+    def estimates(self):
+        return self.est.copy()
+
+
+def run_distributed(g, config: HyperBallConfig, observers: Iterable = (), group=None,
+                    state_factory=None) -> DistributedResult:
+    """``run`` (engine.py:402-435) over every rank of `group`; call it on every rank with
+    the same graph.  Fused ``CentralityAccumulator`` observers are supported (filled on
+    every rank after convergence); other observers get ``on_converged`` only."""
+    comm = TorchComm(group)
+    factory = state_factory or (lambda: CudaRankState(g, config, comm.world, comm.rank))
+    st = factory()
+    observers = list(observers)
+    accs = [o for o in observers if fusable(o, st.n)]
+    if accs:
+        st.bind_sums()
+    t = 0
+    nch = st.n
+    if st.n > 0:
+        while True:
+            started = time.perf_counter()
+            nch = iterate_rank(st, comm, t + 1, dense=(t == 0 or not config.skip_stable_nodes))
+            t += 1
+            if config.progress is not None and comm.rank == 0:
+                config.progress.write(f"t={t} changed={nch} elapsed_ms="
+                                      f"{(time.perf_counter() - started) * 1000.0:.0f}\n")
+            if nch == 0:
+                break
+            if config.max_iterations is not None and t >= config.max_iterations:
+                raise ConvergenceError(t, nch)
+    else:
+        nch = 0
+    arrays = {k: comm.all_gather_slices(v, st.lo, st.hi, st.n) for k, v in st.per_node().items()}
+    host = {k: st.to_original(v) for k, v in arrays.items()}
+    res = DistributedResult(t, nch, host["est"], host.get("sum_dist"), host.get("sum_recip"),
+                            getattr(getattr(st, "dev", None), "launches", 0))
+    final = host["est"]
+    final.setflags(write=False)
+    for acc in accs:
+        if isinstance(acc, CentralityAccumulator):
+            acc._sum_dist, acc._sum_recip = host["sum_dist"].copy(), host["sum_recip"].copy()
+            acc._fresh = False
+        else:
+            acc.sum_dist, acc.sum_recip = host["sum_dist"].copy(), host["sum_recip"].copy()
+    for obs in observers:
+        obs.on_converged(final)
+    return res
+
+
+def run_simulated(g, config: HyperBallConfig, world: int, observers: Iterable = ()):
+    """All `world` ranks in one process on one GPU, phase by phase (no kernel waits on
+    another rank).  Exercises the partition and every exchange kernel; results must be
+    bit-identical to the single-GPU run."""
+    states = [CudaRankState(g, config, world, r) for r in range(world)]
+    observers = list(observers)
+    accs = [o for o in observers if fusable(o, states[0].n)]
+    if accs:
+        for s in states:
+            s.bind_sums()
+    t = 0
+    nch = states[0].n
+    if nch > 0:
+        while True:
+            dense = t == 0 or not config.skip_stable_nodes
+            for s in states:
+                s.local_step(t + 1, dense)
+                s.refresh_unowned()
+            packed = [s.gather_changed() for s in states]
+            nch = sum(k for _, _, k in packed)
+            for r, s in enumerate(states):
+                for q, (ids, rows, k) in enumerate(packed):
+                    if q != r and k:
+                        s.apply_remote(ids, rows)
+            for s in states:
+                s.swap()
+            t += 1
+            if nch == 0:
+                break
+            if config.max_iterations is not None and t >= config.max_iterations:
+                raise ConvergenceError(t, nch)
+    n = states[0].n
+    full = {}
+    for key in states[0].per_node():
+        x = torch.empty_like(states[0].per_node()[key])
+        for s in states:
+            x[s.lo:s.hi] = s.per_node()[key][s.lo:s.hi]
+        full[key] = states[0].to_original(x)
+    res = DistributedResult(t, nch, full["est"], full.get("sum_dist"), full.get("sum_recip"),
+                            sum(s.dev.launches for s in states))
+    res.registers = [s.to_original(s.dev.cur) for s in states]
+    final = full["est"]
+    for acc in accs:
+        if isinstance(acc, CentralityAccumulator):
+            acc._sum_dist, acc._sum_recip = full["sum_dist"].copy(), full["sum_recip"].copy()
+            acc._fresh = False
+    for obs in observers:
+        obs.on_converged(final)
+    return res

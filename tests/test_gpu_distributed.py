@@ -1,0 +1,58 @@
+"""Multi-rank path on one GPU: every rank simulated in one process, phase by phase
+(local union step, refresh of remote rows, hb_gather_changed, exchange, hb_scatter_rows).
+Registers, estimates, iteration count and centralities must be bit-identical to the
+reference (golden) for every world size -- the worker-count invariance of
+test_engine.py:231-239 lifted to GPUs."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import golden, golden_cases, golden_graph
+
+pytestmark = pytest.mark.gpu
+
+hb = pytest.importorskip("paper_1308_2144_b200")
+from paper_1308_2144_b200 import generators as gen  # noqa: E402
+from paper_1308_2144_b200.distributed import run_simulated  # noqa: E402
+
+CASES = {c["key"]: c for c in golden_cases()}
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+@pytest.mark.parametrize("schedule", ["identity", "degree"])
+@pytest.mark.parametrize("key", ["random300_b6_s42_w5", "disc14_b4_s42_w5", "rmat12_b7_s42_w5",
+                                 "config1_b6_s42_w5", "sparse2000_b4_s42_w5"])
+def test_simulated_ranks_match_reference(key, world, schedule):
+    case = CASES[key]
+    off, suc = golden_graph(case)
+    g = hb.CsrGraph(off, suc)
+    acc = hb.CentralityAccumulator(g.n)
+    cfg = hb.HyperBallConfig(params=hb.CounterParams(b=case["b"], seed=int(case["seed"])),
+                             schedule=schedule)
+    res = run_simulated(g, cfg, world, [acc])
+    assert res.t == case["t"]
+    for regs in res.registers:        # every replica holds the final registers
+        assert sha(regs) == case["reg_digests"][-1]
+    assert sha(res.est) == case["est_digests"][-1]
+    _, arrays = golden()
+    for name, got in (("harmonic", hb.finalize_harmonic(acc)), ("lin", hb.finalize_lin(acc)),
+                      ("closeness", hb.finalize_closeness(acc))):
+        assert np.array_equal(got.view(np.uint64), arrays[f"{key}/{name}"].view(np.uint64))
+
+
+def test_simulated_heavy_rmat_matches_single_gpu():
+    g = gen.rmat_t(15, 16 << 15, seed=31)
+    cfg = hb.HyperBallConfig(params=hb.CounterParams(b=5, seed=3))
+    a1 = hb.CentralityAccumulator(g.n)
+    st = hb.run(g, cfg, [a1])
+    a4 = hb.CentralityAccumulator(g.n)
+    res = run_simulated(g, cfg, 4, [a4])
+    assert res.t == st.t
+    assert sha(res.registers[0]) == sha(st.register_matrix())
+    assert np.array_equal(a1.sum_recip.view(np.uint64), a4.sum_recip.view(np.uint64))
