@@ -238,15 +238,24 @@ def run_b200(args):
     # ---------------------------------------------------------------- device-resident step
     cfg = hb.HyperBallConfig(params=params, device=local)
     acc = hb.CentralityAccumulator(n)
-    st = hb.initialize(g, cfg)
-    dev = st._dev
-    from paper_1308_2144_b200.engine import _bind_sums
-    sums = _bind_sums(st, acc)
+    rs = comm = st = None
+    if world > 1:
+        from paper_1308_2144_b200.distributed import CudaRankState, TorchComm
+        comm = TorchComm()
+        rs = CudaRankState(g, cfg, world, rank)
+        sums = rs.bind_sums()
+        dev = rs.dev
+    else:
+        from paper_1308_2144_b200.engine import _bind_sums
+        st = hb.initialize(g, cfg)
+        dev = st._dev
+        sums = _bind_sums(st, acc)
     s = dev.sched
     stream = dev.stream
     L = _lib.hb()
 
     def step(ev0=None, ev1=None):
+        """One dense iteration: union kernels (+ exchange of changed rows when N > 1)."""
         if ev0 is not None:
             ev0.record(stream)
         _lib.check(L.hb_union_step(
@@ -260,9 +269,18 @@ def run_b200(args):
             stream.cuda_stream), "hb_union_step")
         if ev1 is not None:
             ev1.record(stream)
-        return [int(x) for x in dev.counts.cpu()]     # the per-iteration termination read
+        nch, merged = (int(x) for x in dev.counts.cpu())   # the per-iteration termination read
+        if rs is not None:
+            rs.refresh_unowned()
+            ids, rows, k = rs.gather_changed()
+            _, parts = comm.exchange(ids, rows, k)
+            for ids_q, rows_q in parts:
+                rs.apply_remote(ids_q, rows_q)
+        return nch, merged
 
     launches_per_step = (s.light_hi > s.light_lo) + (s.n_items > 0) + (s.n_heavy > 0)
+    if world > 1:
+        launches_per_step += 2 + (world - 1)   # refresh, gather, one scatter per peer
     for _ in range(args.warmup):
         step()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -292,11 +310,15 @@ def run_b200(args):
         ksum = sum(kernel_ms)
     ms_per_step = total_ms / args.steps
     k_ms = ksum / args.steps
+    if world > 1:
+        mt = torch.tensor([merged_check], dtype=torch.int64, device="cuda")
+        dist.all_reduce(mt)
+        merged_check = int(mt.item())
     assert merged_check == m, (merged_check, m)   # dense step merges every arc
     value = m * p / (ms_per_step / 1000.0)
     peak, peak_src = measured_peak()
     B = alg_bytes(n, m, p)
-    achieved = B / (k_ms / 1000.0) / 1e9
+    achieved = B / world / (k_ms / 1000.0) / 1e9    # per GPU: its share of B / its kernel time
     traffic = None
     tpath = os.path.join(REPO, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
@@ -316,7 +338,7 @@ def run_b200(args):
         off_pin.numpy()[:] = g.offsets
         suc_pin.numpy()[:] = g.successors
         gp = hb.CsrGraph(off_pin.numpy(), suc_pin.numpy())
-        del st, dev, sums, acc
+        del st, rs, dev, sums, acc
         torch.cuda.empty_cache()
         runs = []
         for i in range(args.e2e_warmup + args.e2e_steps):
@@ -325,13 +347,18 @@ def run_b200(args):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             acc2 = hb.CentralityAccumulator(n)
-            st2 = hb.run(gp, hb.HyperBallConfig(params=params, device=local), [acc2])
+            cfg2 = hb.HyperBallConfig(params=params, device=local)
+            if world > 1:
+                from paper_1308_2144_b200.distributed import run_distributed
+                st2 = run_distributed(gp, cfg2, [acc2])
+            else:
+                st2 = hb.run(gp, cfg2, [acc2])
             har = hb.finalize_harmonic(acc2)
             clo = hb.finalize_closeness(acc2)
             lin = hb.finalize_lin(acc2)
             torch.cuda.synchronize()
             dt = time.perf_counter() - t0
-            merged_total = st2._dev.merged_total
+            merged_total = (st2._dev.merged_total if world == 1 else st2.merged_total)
             iters = st2.t
             del st2, acc2, har, clo, lin
             if i >= args.e2e_warmup:

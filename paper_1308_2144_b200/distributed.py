@@ -222,9 +222,14 @@ def run_distributed(g, config: HyperBallConfig, observers: Iterable = (), group=
     else:
         nch = 0
     arrays = {k: comm.all_gather_slices(v, st.lo, st.hi, st.n) for k, v in st.per_node().items()}
+    dev_ = getattr(st, "dev", None)
+    mt = torch.tensor([getattr(dev_, "merged_total", 0)], dtype=torch.int64,
+                      device=arrays["est"].device)
+    dist.all_reduce(mt, group=group)
     host = {k: st.to_original(v) for k, v in arrays.items()}
     res = DistributedResult(t, nch, host["est"], host.get("sum_dist"), host.get("sum_recip"),
-                            getattr(getattr(st, "dev", None), "launches", 0))
+                            getattr(dev_, "launches", 0))
+    res.merged_total = int(mt.item())
     final = host["est"]
     final.setflags(write=False)
     for acc in accs:
