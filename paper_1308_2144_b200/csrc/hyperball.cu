@@ -176,35 +176,41 @@ __device__ __forceinline__ double np_max0(double x) { return (x >= 0.0 || x != x
 
 // ------------------------------------------------------------------ shared epilogue
 // Group of G lanes finishing node v: merge own row, change test, lazy write, estimate,
-// accumulate.  acc holds the max over merged sources.  Returns the (group-uniform)
-// changed flag.  All lanes of gmask must call it together.
+// accumulate.  acc holds the max over merged sources.  Warp-uniform: EVERY lane of the
+// warp calls it (groups with nothing to do pass doit = false), so all collectives use the
+// full mask and no group's divergence serialises the others.  Returns the group's changed
+// flag.
 template <int LOGP>
-__device__ __forceinline__ bool finish_node(int64_t v, const uint4 (&acc)[Geo<LOGP>::CPL],
+__device__ __forceinline__ bool finish_node(bool doit, int64_t v,
+                                            const uint4 (&acc)[Geo<LOGP>::CPL],
                                             const uint4 (&pre)[Geo<LOGP>::CPL], bool have_pre,
-                                            bool self_chg, unsigned gmask, int gl,
+                                            bool self_chg, int grp, int gl,
                                             const uint8_t *__restrict__ cur,
                                             uint8_t *__restrict__ nxt, double *__restrict__ est,
                                             double *__restrict__ sum_dist,
                                             double *__restrict__ sum_recip, const EstConst &ec,
                                             double tf, const double *pre_vals = nullptr) {
   using Gm = Geo<LOGP>;
+  constexpr unsigned kLow = Gm::G == 32 ? 0xffffffffu : ((1u << (Gm::G & 31)) - 1u);
   const uint8_t *crow = cur + (size_t)v * Gm::P;
   uint8_t *nrow = nxt + (size_t)v * Gm::P;
   uint4 nw[Gm::CPL];
   bool diff = false;
 #pragma unroll
   for (int c = 0; c < Gm::CPL; c++) {
-    const uint4 self = have_pre ? pre[c] : ldg4(crow + 16 * (c * Gm::G + gl));
+    uint4 self = pre[c];
+    if (doit && !have_pre) self = ldg4(crow + 16 * (c * Gm::G + gl));
     nw[c] = bmax4(acc[c], self);
     diff |= neq4(nw[c], self);
   }
-  const bool changed = __any_sync(gmask, diff);
-  if (changed || self_chg) {
+  const unsigned bal = __ballot_sync(0xffffffffu, doit && diff);
+  const bool changed = ((bal >> (grp * Gm::G)) & kLow) != 0u;
+  if (doit && (changed || self_chg)) {
 #pragma unroll
     for (int c = 0; c < Gm::CPL; c++)
       *reinterpret_cast<uint4 *>(nrow + 16 * (c * Gm::G + gl)) = nw[c];
   }
-  if (changed) {
+  if (bal != 0u) {   // warp-uniform
     // sum_j 2^-M[j] as exact fp64 partial sums (every M <= 31 here: at most 36 significant
     // bits, so any summation order gives the reference's sequential result), zero count by
     // SWAR, and an OR of all bytes to detect registers > 31 (sequential fallback).
@@ -225,13 +231,15 @@ __device__ __forceinline__ bool finish_node(int64_t v, const uint4 (&acc)[Geo<LO
         }
       }
     }
-    zeros = __reduce_add_sync(gmask, zeros);
-    big = __reduce_or_sync(gmask, big);
 #pragma unroll
-    for (int off = 1; off < Gm::G; off <<= 1) s = __dadd_rn(s, __shfl_xor_sync(gmask, s, off));
+    for (int off = 1; off < Gm::G; off <<= 1) {   // xor partners stay inside the group
+      s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, off));
+      zeros += __shfl_xor_sync(0xffffffffu, zeros, off);
+      big |= __shfl_xor_sync(0xffffffffu, big, off);
+    }
     const bool seq = (big & 0xE0E0E0E0u) != 0u;   // some register > 31
-    if (seq) __syncwarp(gmask);  // the row was stored above; make it visible
-    if (gl == 0) {
+    if (__any_sync(0xffffffffu, changed && seq)) __syncwarp();  // stored rows visible
+    if (changed && gl == 0) {
       if (seq) {  // reference order: ascending-j fp64 sum (_kernels.py:25-30)
         s = 0.0;
         for (int j = 0; j < Gm::P; j++) s = __dadd_rn(s, pow2neg(nrow[j]));
@@ -434,13 +442,18 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
       const int64_t k = beg + j * Gm::G + gl;
       idr[j] = (k < end) ? __ldg(succ + k) : -1;
     }
+    // batches of NB ids per group; the loop runs the warp's longest node so that every
+    // ballot / shuffle below is full-warp (no per-group serialisation)
+    const int trips = (int)((end - beg + B::NB - 1) / B::NB);
+    const int wtrips = __reduce_max_sync(0xffffffffu, (unsigned)trips);
     int total = 0;
-    for (int64_t kb = beg; kb < end; kb += B::NB) {   // group-uniform trip count
+    for (int it = 0; it < wtrips; it++) {
+      const int64_t kb = beg + (int64_t)it * B::NB;
       int cnt = 0;
 #pragma unroll
       for (int j = 0; j < B::J; j++) {
         const bool act = idr[j] >= 0 && (dense || test_bit(chg_prev, idr[j]));
-        const unsigned bal = (__ballot_sync(gmask, act) >> (grp * Gm::G)) & lowmask;
+        const unsigned bal = (__ballot_sync(0xffffffffu, act) >> (grp * Gm::G)) & lowmask;
         if (act) my_ids[cnt + __popc(bal & below)] = idr[j];
         cnt += __popc(bal);
       }
@@ -449,8 +462,9 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
         const int64_t k = kb + B::NB + j * Gm::G + gl;
         idr[j] = (k < end) ? __ldg(succ + k) : -1;
       }
-      __syncwarp(gmask);
-      for (int i = 0; i < cnt; i += B::U) {
+      __syncwarp();
+      const int cmax = __reduce_max_sync(0xffffffffu, (unsigned)cnt);
+      for (int i = 0; i < cmax; i += B::U) {
         uint4 r[B::U][Gm::CPL];
 #pragma unroll
         for (int u = 0; u < B::U; u++) {
@@ -467,13 +481,12 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
           for (int c = 0; c < Gm::CPL; c++) acc[c] = bmax4(acc[c], r[u][c]);
       }
       total += cnt;
-      __syncwarp(gmask);
+      __syncwarp();
     }
     my_merged += (gl == 0) ? (uint32_t)total : 0u;
-    bool changed = false;
-    if (valid && (total > 0 || self_chg))
-      changed = finish_node<LOGP>(v, acc, self, pre, self_chg, gmask, gl, cur, nxt, est,
-                                  sum_dist, sum_recip, ec, tf, pre ? vals : nullptr);
+    const bool changed = finish_node<LOGP>(valid && (total > 0 || self_chg), v, acc, self, pre,
+                                           self_chg, grp, gl, cur, nxt, est, sum_dist,
+                                           sum_recip, ec, tf, pre ? vals : nullptr);
     // Warp-level aggregation of the NPW change bits (they share one bitmap word).
     const unsigned bb = __ballot_sync(0xffffffffu, changed && gl == 0);
     if (lane == 0 && bb) {
@@ -585,36 +598,33 @@ k_heavy_finish(const int32_t *__restrict__ heavy_nodes, const int32_t *__restric
   const int lane = threadIdx.x & 31;
   const int gl = lane % Gm::G;
   const int grp = lane / Gm::G;
-  const unsigned gmask =
-      Gm::G == 32 ? 0xffffffffu : (((1u << (Gm::G & 31)) - 1u) << (grp * Gm::G));
+  const unsigned lowmask = Gm::G == 32 ? 0xffffffffu : ((1u << (Gm::G & 31)) - 1u);
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   uint32_t my_nch = 0;
   for (int64_t base = warp * Gm::NPW; base < n_heavy; base += nwarps * Gm::NPW) {
     const int64_t j = base + grp;
-    if (j < n_heavy) {
-      const int64_t v = __ldg(heavy_nodes + j);
-      const int i0 = __ldg(item_first + j), i1 = __ldg(item_first + j + 1);
-      uint4 acc[Gm::CPL];
+    const bool valid = j < n_heavy;
+    const int64_t v = valid ? __ldg(heavy_nodes + j) : 0;
+    const int i0 = valid ? __ldg(item_first + j) : 0, i1 = valid ? __ldg(item_first + j + 1) : 0;
+    uint4 acc[Gm::CPL];
 #pragma unroll
-      for (int c = 0; c < Gm::CPL; c++) acc[c] = make_uint4(0, 0, 0, 0);
-      for (int i = i0; i < i1; i++)
+    for (int c = 0; c < Gm::CPL; c++) acc[c] = make_uint4(0, 0, 0, 0);
+    for (int i = i0; i < i1; i++)
 #pragma unroll
-        for (int c = 0; c < Gm::CPL; c++)
-          acc[c] = bmax4(acc[c], ldg4(partial + (size_t)i * Gm::P + 16 * (c * Gm::G + gl)));
-      bool any = false;
+      for (int c = 0; c < Gm::CPL; c++)
+        acc[c] = bmax4(acc[c], ldg4(partial + (size_t)i * Gm::P + 16 * (c * Gm::G + gl)));
+    bool any = false;
 #pragma unroll
-      for (int c = 0; c < Gm::CPL; c++) any |= nz4(acc[c]);
-      any = __any_sync(gmask, any);
-      const bool self_chg = test_bit(chg_prev, v);
-      if (any || self_chg) {
-        const bool changed = finish_node<LOGP>(v, acc, acc, false, self_chg, gmask, gl, cur,
-                                               nxt, est, sum_dist, sum_recip, ec, tf);
-        if (changed && gl == 0) {
-          atomicOr(chg_now + (v >> 5), 1u << (v & 31));
-          my_nch++;
-        }
-      }
+    for (int c = 0; c < Gm::CPL; c++) any |= nz4(acc[c]);
+    any = ((__ballot_sync(0xffffffffu, any) >> (grp * Gm::G)) & lowmask) != 0u;
+    const bool self_chg = valid && test_bit(chg_prev, v);
+    const bool changed = finish_node<LOGP>(valid && (any || self_chg), v, acc, acc, false,
+                                           self_chg, grp, gl, cur, nxt, est, sum_dist,
+                                           sum_recip, ec, tf);
+    if (changed && gl == 0) {
+      atomicOr(chg_now + (v >> 5), 1u << (v & 31));
+      my_nch++;
     }
   }
   block_add2(my_nch, 0u, nch_out, nullptr);
