@@ -264,7 +264,7 @@ def run_b200(args):
             dev.chg_now.data_ptr(), 1, dev.est.data_ptr(), sums.sum_dist.data_ptr(),
             sums.sum_recip.data_ptr(), 1, dev.lc.data_ptr(), dev.alpha_p2, dev.lc_cut, b, 1,
             s.light_max_deg, s.heavy_nodes.data_ptr(), s.item_first.data_ptr(), s.n_heavy,
-            s.item_node.data_ptr(), s.item_beg.data_ptr(), s.n_items, s.item_arcs,
+            s.finish_order.data_ptr(), s.n_mega, s.item_node.data_ptr(), s.item_beg.data_ptr(), s.n_items, s.item_arcs,
             s.partial.data_ptr(), dev.counts.data_ptr(), dev.counts.data_ptr() + 8,
             stream.cuda_stream), "hb_union_step")
         if ev1 is not None:

@@ -85,7 +85,10 @@ int hb_estimate_rows(const uint8_t *regs, int64_t lo, int64_t hi, int b,
  *                item_first[j]..item_first[j+1] (device int32 [n_heavy+1]); item i covers
  *                arcs [item_beg[i], min(item_beg[i] + item_arcs, offsets[v+1])) of node
  *                item_node[i] (device int32 / int64 [n_items]) and leaves a partial row
- *                in partial (device uint8 [n_items, p]).
+ *                in partial (device uint8 [n_items, p]).  finish_order (device int32
+ *                [n_heavy]) is a permutation of 0..n_heavy-1 whose first n_mega entries are
+ *                the heavy nodes with many items (merged one warp per node), the rest one
+ *                lane group per node.
  * chg_now words covering [lo, hi) must be zero on entry (hb_union_step clears the whole
  * bitmap when clear_chg_now != 0).  *nch_out (device uint64) receives the changed count
  * (zeroed by the call); *merged_out (device uint64, may be NULL) receives the number of
@@ -98,7 +101,8 @@ int hb_union_step(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets,
                   double *est, double *sum_dist, double *sum_recip, int64_t t,
                   const double *lc_table, double alpha_p2, double lc_cut, int b, int dense,
                   int64_t light_max_deg, const int32_t *heavy_nodes, const int32_t *item_first,
-                  int64_t n_heavy, const int32_t *item_node, const int64_t *item_beg,
+                  int64_t n_heavy, const int32_t *finish_order, int64_t n_mega,
+                  const int32_t *item_node, const int64_t *item_beg,
                   int64_t n_items, int64_t item_arcs, uint8_t *partial, uint64_t *nch_out,
                   uint64_t *merged_out, void *stream);
 

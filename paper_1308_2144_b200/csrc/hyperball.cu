@@ -583,43 +583,68 @@ k_heavy_partial(const int64_t *__restrict__ offsets, const int32_t *__restrict__
   block_add2(my_merged, 0u, merged_out, nullptr);
 }
 
-// Heavy nodes, phase 2: one group per heavy node merges its partial rows and runs the
-// shared epilogue.
+// Heavy nodes, phase 2: merge each heavy node's partial rows and run the shared epilogue.
+// order[o0, o1) lists heavy indices j.  mega == 0: one lane group per node (nodes with few
+// items); mega != 0: one warp per node, its NPW slots striding over the items (hubs with
+// hundreds of items), merged by a shuffle tree.  Partial loads are unrolled 4-deep.
 template <int LOGP>
 __global__ void __launch_bounds__(kThreads)
 k_heavy_finish(const int32_t *__restrict__ heavy_nodes, const int32_t *__restrict__ item_first,
-               int64_t n_heavy, const uint8_t *__restrict__ partial,
+               const int32_t *__restrict__ order, int64_t o0, int64_t o1, int mega,
+               const uint8_t *__restrict__ partial,
                const uint8_t *__restrict__ cur, uint8_t *__restrict__ nxt,
                const uint32_t *__restrict__ chg_prev, uint32_t *__restrict__ chg_now,
                double *__restrict__ est, double *__restrict__ sum_dist,
                double *__restrict__ sum_recip, EstConst ec, double tf,
                unsigned long long *__restrict__ nch_out) {
   using Gm = Geo<LOGP>;
+  constexpr int UF = 4;
   const int lane = threadIdx.x & 31;
   const int gl = lane % Gm::G;
   const int grp = lane / Gm::G;
   const unsigned lowmask = Gm::G == 32 ? 0xffffffffu : ((1u << (Gm::G & 31)) - 1u);
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int per_warp = mega ? 1 : Gm::NPW;
   uint32_t my_nch = 0;
-  for (int64_t base = warp * Gm::NPW; base < n_heavy; base += nwarps * Gm::NPW) {
-    const int64_t j = base + grp;
-    const bool valid = j < n_heavy;
+  for (int64_t base = o0 + warp * per_warp; base < o1; base += nwarps * per_warp) {
+    const int64_t e = mega ? base : base + grp;
+    const bool valid = e < o1;
+    const int64_t j = valid ? __ldg(order + e) : 0;
     const int64_t v = valid ? __ldg(heavy_nodes + j) : 0;
     const int i0 = valid ? __ldg(item_first + j) : 0, i1 = valid ? __ldg(item_first + j + 1) : 0;
+    const int first = mega ? i0 + grp : i0, stride = mega ? Gm::NPW : 1;
     uint4 acc[Gm::CPL];
 #pragma unroll
     for (int c = 0; c < Gm::CPL; c++) acc[c] = make_uint4(0, 0, 0, 0);
-    for (int i = i0; i < i1; i++)
+    for (int i = first; i < i1; i += stride * UF) {
+      uint4 r[UF][Gm::CPL];
 #pragma unroll
-      for (int c = 0; c < Gm::CPL; c++)
-        acc[c] = bmax4(acc[c], ldg4(partial + (size_t)i * Gm::P + 16 * (c * Gm::G + gl)));
+      for (int u = 0; u < UF; u++) {
+        const int ii = i + u * stride;
+#pragma unroll
+        for (int c = 0; c < Gm::CPL; c++)
+          r[u][c] = ii < i1 ? ldg4(partial + (size_t)ii * Gm::P + 16 * (c * Gm::G + gl))
+                            : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < UF; u++)
+#pragma unroll
+        for (int c = 0; c < Gm::CPL; c++) acc[c] = bmax4(acc[c], r[u][c]);
+    }
+    if (mega) {
+#pragma unroll
+      for (int off = Gm::G; off < 32; off <<= 1)
+#pragma unroll
+        for (int c = 0; c < Gm::CPL; c++) acc[c] = bmax4(acc[c], shfl_xor4(acc[c], off));
+    }
+    const bool owner = valid && (!mega || grp == 0);
     bool any = false;
 #pragma unroll
     for (int c = 0; c < Gm::CPL; c++) any |= nz4(acc[c]);
     any = ((__ballot_sync(0xffffffffu, any) >> (grp * Gm::G)) & lowmask) != 0u;
-    const bool self_chg = valid && test_bit(chg_prev, v);
-    const bool changed = finish_node<LOGP>(valid && (any || self_chg), v, acc, acc, false,
+    const bool self_chg = owner && test_bit(chg_prev, v);
+    const bool changed = finish_node<LOGP>(owner && (any || self_chg), v, acc, acc, false,
                                            self_chg, grp, gl, cur, nxt, est, sum_dist,
                                            sum_recip, ec, tf);
     if (changed && gl == 0) {
@@ -820,6 +845,7 @@ int union_step_impl(int64_t lo, int64_t hi, const int64_t *offsets, const int32_
                     uint32_t *chg_now, double *est, double *sum_dist, double *sum_recip,
                     double tf, EstConst ec, int dense, int64_t light_max_deg,
                     const int32_t *heavy_nodes, const int32_t *item_first, int64_t n_heavy,
+                    const int32_t *finish_order, int64_t n_mega,
                     const int32_t *item_node, const int64_t *item_beg, int64_t n_items,
                     int64_t item_arcs, uint8_t *partial, unsigned long long *nch,
                     unsigned long long *merged, cudaStream_t s) {
@@ -838,9 +864,17 @@ int union_step_impl(int64_t lo, int64_t hi, const int64_t *offsets, const int32_
     if (int e = check_launch("k_light")) return e;
   }
   if (n_heavy > 0) {
-    k_heavy_finish<LOGP><<<grid_for_warps((n_heavy + Gm::NPW - 1) / Gm::NPW), kThreads, 0, s>>>(
-        heavy_nodes, item_first, n_heavy, partial, cur, nxt, chg_prev, chg_now, est, sum_dist,
-        sum_recip, ec, tf, nch);
+    if (n_mega > 0) {
+      k_heavy_finish<LOGP><<<grid_for_warps(n_mega), kThreads, 0, s>>>(
+          heavy_nodes, item_first, finish_order, 0, n_mega, 1, partial, cur, nxt, chg_prev,
+          chg_now, est, sum_dist, sum_recip, ec, tf, nch);
+      if (int e = check_launch("k_heavy_finish(mega)")) return e;
+    }
+    if (n_heavy > n_mega)
+      k_heavy_finish<LOGP><<<grid_for_warps((n_heavy - n_mega + Gm::NPW - 1) / Gm::NPW), kThreads,
+                             0, s>>>(heavy_nodes, item_first, finish_order, n_mega, n_heavy, 0,
+                                     partial, cur, nxt, chg_prev, chg_now, est, sum_dist,
+                                     sum_recip, ec, tf, nch);
     if (int e = check_launch("k_heavy_finish")) return e;
   }
   return 0;
@@ -902,13 +936,15 @@ int hb_union_step(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets,
                   double *est, double *sum_dist, double *sum_recip, int64_t t,
                   const double *lc_table, double alpha_p2, double lc_cut, int b, int dense,
                   int64_t light_max_deg, const int32_t *heavy_nodes, const int32_t *item_first,
-                  int64_t n_heavy, const int32_t *item_node, const int64_t *item_beg,
+                  int64_t n_heavy, const int32_t *finish_order, int64_t n_mega,
+                  const int32_t *item_node, const int64_t *item_beg,
                   int64_t n_items, int64_t item_arcs, uint8_t *partial, uint64_t *nch_out,
                   uint64_t *merged_out, void *stream) {
   if (n < 0 || lo < 0 || hi > n || lo > hi || t < 1 || !nch_out)
     return set_err_msg("hb_union_step: bad range / t / nch_out");
   if ((n_items > 0 && (!item_node || !item_beg || !partial)) ||
-      (n_heavy > 0 && (!heavy_nodes || !item_first || !partial)))
+      (n_heavy > 0 && (!heavy_nodes || !item_first || !finish_order || !partial)) ||
+      n_mega < 0 || n_mega > n_heavy)
     return set_err_msg("hb_union_step: heavy schedule arrays missing");
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e;
@@ -927,7 +963,7 @@ int hb_union_step(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets,
   HB_DISPATCH(b, return union_step_impl<LB>(
                      lo, hi, offsets, succ, cur, nxt, chg_prev, chg_now, est, sum_dist,
                      sum_recip, tf, ec, dense, light_max_deg, heavy_nodes, item_first, n_heavy,
-                     item_node, item_beg, n_items, item_arcs, partial,
+                     finish_order, n_mega, item_node, item_beg, n_items, item_arcs, partial,
                      reinterpret_cast<unsigned long long *>(nch_out),
                      reinterpret_cast<unsigned long long *>(merged_out), s));
   return 0;

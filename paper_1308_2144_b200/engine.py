@@ -319,7 +319,7 @@ class _Device:
             self.chg_now.data_ptr(), 1, self.est.data_ptr(), sd, sr, t, self.lc.data_ptr(),
             self.alpha_p2, self.lc_cut, self.b, int(dense), s.light_max_deg,
             s.heavy_nodes.data_ptr(), s.item_first.data_ptr(), s.n_heavy,
-            s.item_node.data_ptr(), s.item_beg.data_ptr(), s.n_items, s.item_arcs,
+            s.finish_order.data_ptr(), s.n_mega, s.item_node.data_ptr(), s.item_beg.data_ptr(), s.n_items, s.item_arcs,
             s.partial.data_ptr(), self.counts.data_ptr(), self.counts.data_ptr() + 8,
             self.stream.cuda_stream), "hb_union_step")
         self.launches += (light_hi > s.light_lo) + (s.n_items > 0) + (s.n_heavy > 0)

@@ -45,6 +45,8 @@ class Schedule:
     item_arcs: int
     heavy_nodes: torch.Tensor
     item_first: torch.Tensor
+    finish_order: torch.Tensor     # int32 [n_heavy]: heavy indices, mega nodes first
+    n_mega: int                    # heavy nodes merged one warp per node
     item_node: torch.Tensor
     item_beg: torch.Tensor
     partial: torch.Tensor
@@ -64,6 +66,9 @@ class Schedule:
 
     def to_original(self, x: torch.Tensor) -> torch.Tensor:
         return x if self.rank is None else x.index_select(0, self.rank.long())
+
+
+MEGA_ITEMS = 16   # heavy nodes with more work items than this are finished one warp each
 
 
 def _as_device(a, dtype, device) -> torch.Tensor:
@@ -143,6 +148,10 @@ def build_schedule(offsets, successors, b: int, device, order: str = "auto", wor
     item_beg = off[item_node] + (torch.arange(n_items, device=device) - item_first[owner]) * item_arcs
     p = 1 << b
     partial = torch.empty((max(n_items, 1), p), dtype=torch.uint8, device=device)
+    mega = cnt > MEGA_ITEMS
+    finish_order = torch.cat([torch.nonzero(mega).squeeze(1),
+                              torch.nonzero(~mega).squeeze(1)]).to(torch.int32)
+    n_mega = int(mega.sum().item())
     if order == "degree":
         # this rank's slice is in descending degree: heavy first, zero in-degree last
         n_heavy = int(heavy.numel())
@@ -155,5 +164,6 @@ def build_schedule(offsets, successors, b: int, device, order: str = "auto", wor
                     lo=lo, hi=hi, light_lo=light_lo, light_hi=light_hi,
                     light_hi_steady=steady, light_max_deg=light_max_deg, item_arcs=item_arcs,
                     heavy_nodes=heavy.to(torch.int32), item_first=item_first.to(torch.int32),
+                    finish_order=finish_order, n_mega=n_mega,
                     item_node=item_node.to(torch.int32), item_beg=item_beg.contiguous(),
                     partial=partial, max_deg=max_deg)
