@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import io
 import math
+import weakref
 import struct
 import time
 from dataclasses import dataclass, field
@@ -130,6 +131,39 @@ def unpack_bits(words: torch.Tensor, n: int) -> torch.Tensor:
     return bits.view(-1)[:n].to(torch.bool)
 
 
+class _PinnedPool:
+    """Page-locked host blocks for device->host copies, recycled when the numpy array
+    handed to the caller is garbage-collected (page-locking 100+ MB costs tens of ms, a
+    recycled block costs nothing; the copy itself then runs at full PCIe rate)."""
+
+    def __init__(self):
+        import threading
+        self._free: dict = {}
+        self._lock = threading.Lock()
+
+    def array(self, shape, dtype: torch.dtype):
+        """(numpy array, the pinned torch tensor viewing the same memory)."""
+        import weakref
+        numel = int(np.prod(shape)) if len(shape) else 1
+        key = (numel, dtype)
+        with self._lock:
+            lst = self._free.get(key)
+            t = lst.pop() if lst else None
+        if t is None:
+            t = torch.empty(numel, dtype=dtype, pin_memory=True)
+        tv = t.view(shape)
+        arr = tv.numpy()
+        weakref.finalize(arr, self._give_back, key, t)
+        return arr, tv
+
+    def _give_back(self, key, t) -> None:
+        with self._lock:
+            self._free.setdefault(key, []).append(t)
+
+
+_PINNED = _PinnedPool()
+
+
 def _graph_arrays(g):
     return g.offsets, g.successors
 
@@ -143,9 +177,13 @@ def _graph_key(g):
 class _DeviceSums:
     """Device-resident CentralityAccumulator sums (internal node order)."""
 
+    @property
+    def acc(self):
+        return self._acc()
+
     def __init__(self, dev: "_Device", acc):
         self.dev = dev
-        self.acc = acc
+        self._acc = weakref.ref(acc)   # no acc <-> binding cycle: results free promptly
         self.foreign = not isinstance(acc, CentralityAccumulator)
         if self.foreign:
             sd, sr = acc.sum_dist, acc.sum_recip
@@ -169,22 +207,35 @@ class _DeviceSums:
         self.coreach_dev = self.dev.est.clone()
         self.coreach_host_id = id(host_final)
 
+    _fin_cache = None   # (key, {name: host array}, {name: handed out once})
+
     def finalize(self, which: str) -> np.ndarray:
-        """closeness / harmonic / lin computed on the device (hb_finalize), original order."""
+        """closeness / harmonic / lin on the device (one hb_finalize for all three, one
+        pinned device->host copy), original order; later calls reuse the copy."""
         dev = self.dev
-        n = dev.n
-        out = torch.empty(n, dtype=torch.float64, device=dev.device)
-        ptrs = {"closeness": None, "harmonic": None, "lin": None}
-        ptrs[which] = out.data_ptr()
-        rank = dev.sched.rank
-        _lib.check(_lib.hb().hb_finalize(
-            n, rank.data_ptr() if rank is not None else None, self.sum_dist.data_ptr(),
-            self.sum_recip.data_ptr(),
-            self.coreach_dev.data_ptr() if self.coreach_dev is not None else None,
-            ptrs["closeness"], ptrs["harmonic"], ptrs["lin"], dev.stream.cuda_stream),
-            "hb_finalize")
-        dev.launches += 1
-        return dev.to_host_raw(out)
+        key = (dev.launches_at_last_step, self.coreach_host_id)
+        if self._fin_cache is None or self._fin_cache[0] != key:
+            n = dev.n
+            with_lin = self.coreach_dev is not None
+            out = torch.empty((3 if with_lin else 2, n), dtype=torch.float64, device=dev.device)
+            rank = dev.sched.rank
+            _lib.check(_lib.hb().hb_finalize(
+                n, rank.data_ptr() if rank is not None else None, self.sum_dist.data_ptr(),
+                self.sum_recip.data_ptr(),
+                self.coreach_dev.data_ptr() if with_lin else None, out[0].data_ptr(),
+                out[1].data_ptr(), out[2].data_ptr() if with_lin else None,
+                dev.stream.cuda_stream), "hb_finalize")
+            dev.launches += 1
+            host = dev.to_host_raw(out)
+            names = ["closeness", "harmonic", "lin"][:host.shape[0]]
+            self._fin_cache = (key, {nm: host[i] for i, nm in enumerate(names)}, set())
+        _, arrays, given = self._fin_cache
+        if which not in arrays:
+            return None
+        if which in given:                 # the reference returns a fresh array per call
+            return arrays[which].copy()
+        given.add(which)
+        return arrays[which]
 
     def pull_into(self, acc) -> None:
         sd = self.dev.to_host(self.sum_dist)
@@ -239,6 +290,7 @@ class _Device:
         self.prev_all = True          # chg_prev is all-ones (first iteration)
         self.full_pass = True         # zero in-degree nodes may still need their copy
         self.launches = 0             # kernels launched by hb_union_step calls
+        self.launches_at_last_step = 0
 
     # -- graph ---------------------------------------------------------------
     def _build_graph(self, g) -> None:
@@ -273,10 +325,10 @@ class _Device:
         return self.to_host_raw(self.sched.to_original(x))
 
     def to_host_raw(self, x: torch.Tensor) -> np.ndarray:
-        buf = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
-        buf.copy_(x, non_blocking=True)
+        arr, tv = _PINNED.array(tuple(x.shape), x.dtype)
+        tv.copy_(x, non_blocking=True)
         self.stream.synchronize()
-        return buf.numpy()
+        return arr
 
     def snapshot_original(self):
         s = self.sched
@@ -323,6 +375,7 @@ class _Device:
             s.partial.data_ptr(), self.counts.data_ptr(), self.counts.data_ptr() + 8,
             self.stream.cuda_stream), "hb_union_step")
         self.launches += (light_hi > s.light_lo) + (s.n_items > 0) + (s.n_heavy > 0)
+        self.launches_at_last_step = self.launches
         nch, merged = (int(x) for x in self.counts.cpu())
         self.last_merged = merged
         self.merged_total += merged
@@ -439,7 +492,7 @@ def _bind_sums(state: HyperBallState, acc) -> _DeviceSums | None:
     cur = state._sums
     if cur is not None and cur.acc is acc and cur.dev is dev and cur.still_valid():
         return cur
-    if cur is not None and cur.dirty and cur.acc is not acc:
+    if cur is not None and cur.dirty and cur.acc is not acc and cur.acc is not None:
         cur.pull_into(cur.acc)
     if isinstance(acc, CentralityAccumulator) and acc._binding is not None:
         if acc._binding.dirty and not acc._binding.stale:
