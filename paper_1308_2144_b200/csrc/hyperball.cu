@@ -336,7 +336,10 @@ __device__ __forceinline__ int64_t warp_lower_bound(const int64_t *__restrict__ 
 }
 
 constexpr int kLookRounds = 4;    // L2 prefetch distance of the light kernel, in warp rounds
-constexpr int kChunkRounds = 16;  // warp rounds per grid-stride chunk of the light kernel
+// warp rounds per grid-stride chunk of the light kernel (resident warps x chunk nodes is
+// the id window the GPU sweeps): 16 for p >= 256, 4 below (measured on configs 3-5)
+template <int LOGP>
+__host__ __device__ constexpr int chunk_rounds() { return LOGP >= 8 ? 16 : 4; }
 
 // Light nodes (in-degree <= max_deg): one group of G lanes per node, NPW nodes per warp
 // round.  Each warp owns one contiguous node range, balanced over the grid by arcs +
@@ -374,7 +377,7 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
   // memory latency of a round.  Rounds are NPW-aligned so a round's change bits share one
   // bitmap word.
   const int64_t lo_al = (lo / Gm::NPW) * Gm::NPW;
-  constexpr int64_t CN = (int64_t)kChunkRounds * Gm::NPW;
+  constexpr int64_t CN = (int64_t)chunk_rounds<LOGP>() * Gm::NPW;
   const int64_t nchunks = (hi - lo_al + CN - 1) / CN;
   for (int64_t chunk = warp; chunk < nchunks; chunk += nwarps) {
   const int64_t vb = lo_al + chunk * CN;
