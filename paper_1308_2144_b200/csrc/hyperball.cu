@@ -48,10 +48,10 @@ template <int LOGP>
 struct Geo {
   static constexpr int P = 1 << LOGP;
   static constexpr int CH = P / 16;               // 16-byte chunks per row
-  // lanes cooperating on one row: one 16-byte chunk per lane up to p = 128, then two
-  // (p = 256 -> 8 lanes: four nodes per warp round amortise the per-node epilogue),
-  // at most 32
-  static constexpr int G = CH <= 8 ? CH : (CH / 2 < 32 ? CH / 2 : 32);
+  // lanes cooperating on one row: one 16-byte chunk per lane for p <= 32, two above
+  // (p = 64 / 128 / 256 -> 2 / 4 / 8 lanes: more nodes per warp round amortise the
+  // per-round work; measured on configs 2-4), at most 32
+  static constexpr int G = CH <= 2 ? CH : (CH / 2 < 32 ? CH / 2 : 32);
   static constexpr int CPL = CH / G;              // chunks per lane
   static constexpr int NPW = 32 / G;              // rows handled side by side per warp
 };
