@@ -26,6 +26,8 @@
  *                     engine.py:377-390)
  *   hb_relabel_csr    graph.py:145-155 transpose's output consumed in schedule order
  *                     (internal relabelling; no reference counterpart)
+ *   hb_sort_rows      graph.py:52-80 keeps successor lists sorted; this restores that
+ *                     order after the internal relabelling
  *   hb_hash_items     hll.py:79-88 hash_items (device twin, used by tests)
  *
  * Layout:
@@ -138,6 +140,15 @@ int hb_refresh_rows(int64_t n, int64_t lo, int64_t hi, const uint32_t *bits, con
 int hb_relabel_csr(int64_t n, const int64_t *old_offsets, const int32_t *old_succ,
                    const int32_t *perm, const int32_t *rank, const int64_t *new_offsets,
                    int32_t *new_succ, void *stream);
+
+/* Sort the ids of every CSR row ascending (schedule setup, after hb_relabel_csr): offsets
+ * (device int64 [n+1]) and host_offsets (HOST copy of the same array) describe the rows of
+ * ids (device int32 [m]); alt (device int32 [m]) is scratch of the same size.  Call with
+ * temp == NULL to get the scratch size in *temp_bytes, then again with that buffer.  The
+ * sorted ids end in `ids` (*result_in_alt, if given, is set to 0). */
+int hb_sort_rows(int64_t n, const int64_t *offsets, const int64_t *host_offsets, int32_t *ids,
+                 int32_t *alt, void *temp, uint64_t *temp_bytes, int *result_in_alt,
+                 void *stream);
 
 /* out[i] = hash_items(items[i], replicas[i], seed) (hll.py:79-88), device arrays. */
 int hb_hash_items(int64_t n, const uint64_t *items, const uint64_t *replicas, uint64_t seed,

@@ -47,6 +47,7 @@ HB_SIGNATURES = {
     "hb_scatter_rows": (_int, [_i64, _vp, _vp, _int, _vp, _vp, _vp]),
     "hb_refresh_rows": (_int, [_i64, _i64, _i64, _vp, _vp, _vp, _int, _vp]),
     "hb_relabel_csr": (_int, [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "hb_sort_rows": (_int, [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "hb_hash_items": (_int, [_i64, _vp, _vp, _u64, _vp, _vp]),
     "hb_item_arcs": (_i64, [_int]),
     "hb_light_max_deg": (_i64, [_int]),

@@ -16,6 +16,8 @@
 //   * registers are < 128 (rho_max = 65 - b <= 61), so the 7-bit-safe SIMD byte max below
 //     is exact.
 #include <cuda_runtime.h>
+#include <cub/device/device_segmented_sort.cuh>
+#include <cub/iterator/transform_input_iterator.cuh>
 #include <stdint.h>
 #include <stdio.h>
 #include <string.h>
@@ -899,6 +901,29 @@ int union_step_impl(int64_t lo, int64_t hi, const int64_t *offsets, const int32_
 
 }  // namespace
 
+// Row sort (schedule setup): ascending source ids inside every CSR row after relabelling,
+// so consecutive arcs of a hub read neighbouring register rows (shared 128-byte lines at
+// small p).  cub::DeviceSegmentedSort over row batches of < 2^31 arcs, ping-ponging
+// between the two id buffers.
+struct ShiftOff {
+  int64_t base;
+  __host__ __device__ __forceinline__ int operator()(const int64_t &x) const {
+    return (int)(x - base);
+  }
+};
+using OffIt = cub::TransformInputIterator<int, ShiftOff, const int64_t *>;
+
+int64_t row_batch_end(const int64_t *h_off, int64_t n, int64_t r0) {
+  // largest r1 <= n with h_off[r1] - h_off[r0] < 2^31 (at least r0 + 1)
+  const int64_t lim = h_off[r0] + ((int64_t)1 << 31) - 1;
+  int64_t lo = r0 + 1, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi + 1) / 2;
+    if (h_off[mid] <= lim) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
 // ------------------------------------------------------------------ C-ABI
 extern "C" {
 
@@ -1011,6 +1036,49 @@ int hb_refresh_rows(int64_t n, int64_t lo, int64_t hi, const uint32_t *bits, con
   k_refresh_rows<<<grid_for_warps((n + 31) >> 5), kThreads, 0, (cudaStream_t)stream>>>(
       n, lo, hi, bits, src, dst, 1 << b);
   return check_launch("k_refresh_rows");
+}
+
+int hb_sort_rows(int64_t n, const int64_t *offsets, const int64_t *host_offsets, int32_t *ids,
+                 int32_t *alt, void *temp, uint64_t *temp_bytes, int *result_in_alt,
+                 void *stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!host_offsets || !temp_bytes) return set_err_msg("hb_sort_rows: host_offsets/temp_bytes");
+  size_t need = 0;
+  for (int64_t r0 = 0; r0 < n;) {                  // temp size: max over batches
+    const int64_t r1 = row_batch_end(host_offsets, n, r0);
+    const int64_t a0 = host_offsets[r0], items = host_offsets[r1] - a0;
+    cub::DoubleBuffer<int32_t> keys(ids + a0, alt + a0);
+    OffIt beg(offsets + r0, ShiftOff{a0}), end(offsets + r0 + 1, ShiftOff{a0});
+    size_t bytes = 0;
+    cudaError_t e = cub::DeviceSegmentedSort::SortKeys(nullptr, bytes, keys, (int)items,
+                                                       (int)(r1 - r0), beg, end, s);
+    if (e != cudaSuccess) return set_err("hb_sort_rows (size)", e);
+    need = bytes > need ? bytes : need;
+    r0 = r1;
+  }
+  if (!temp) {                                     // size query
+    *temp_bytes = need;
+    return 0;
+  }
+  if (*temp_bytes < need) return set_err_msg("hb_sort_rows: temp buffer too small");
+  for (int64_t r0 = 0; r0 < n;) {
+    const int64_t r1 = row_batch_end(host_offsets, n, r0);
+    const int64_t a0 = host_offsets[r0], items = host_offsets[r1] - a0;
+    cub::DoubleBuffer<int32_t> keys(ids + a0, alt + a0);
+    OffIt beg(offsets + r0, ShiftOff{a0}), end(offsets + r0 + 1, ShiftOff{a0});
+    size_t bytes = need;
+    cudaError_t e = cub::DeviceSegmentedSort::SortKeys(temp, bytes, keys, (int)items,
+                                                       (int)(r1 - r0), beg, end, s);
+    if (e != cudaSuccess) return set_err("hb_sort_rows", e);
+    if (keys.Current() != ids + a0) {              // keep the result in `ids`
+      e = cudaMemcpyAsync(ids + a0, alt + a0, sizeof(int32_t) * (size_t)items,
+                          cudaMemcpyDeviceToDevice, s);
+      if (e != cudaSuccess) return set_err("hb_sort_rows copy", e);
+    }
+    r0 = r1;
+  }
+  if (result_in_alt) *result_in_alt = 0;
+  return check_launch("hb_sort_rows");
 }
 
 int hb_relabel_csr(int64_t n, const int64_t *old_offsets, const int32_t *old_succ,

@@ -134,6 +134,22 @@ def build_schedule(offsets, successors, b: int, device, order: str = "auto", wor
         _lib.check(L.hb_relabel_csr(n, off.data_ptr(), succ.data_ptr(), perm.data_ptr(),
                                     rank.data_ptr(), new_off.data_ptr(), new_succ.data_ptr(),
                                     s.cuda_stream), "hb_relabel_csr")
+        # restore ascending ids inside every row (graph.py's normalisation), now in
+        # internal ids: a hub's consecutive arcs then read neighbouring register rows
+        host_off = new_off.cpu().numpy()
+        if isinstance(successors, torch.Tensor) and successors.data_ptr() == succ.data_ptr():
+            succ = torch.empty_like(succ)       # never scribble on the caller's tensor
+        import ctypes
+        tb = ctypes.c_uint64(0)
+        hp = host_off.ctypes.data_as(ctypes.c_void_p)
+        _lib.check(L.hb_sort_rows(n, new_off.data_ptr(), hp, new_succ.data_ptr(),
+                                  succ.data_ptr(), None, ctypes.byref(tb), None,
+                                  s.cuda_stream), "hb_sort_rows(size)")
+        temp = torch.empty(max(int(tb.value), 1), dtype=torch.uint8, device=device)
+        _lib.check(L.hb_sort_rows(n, new_off.data_ptr(), hp, new_succ.data_ptr(),
+                                  succ.data_ptr(), temp.data_ptr(), ctypes.byref(tb), None,
+                                  s.cuda_stream), "hb_sort_rows")
+        del temp
         off, succ, deg = new_off, new_succ, new_deg
         del srt
     dloc = deg[lo:hi]
