@@ -28,6 +28,9 @@
  *                     (internal relabelling; no reference counterpart)
  *   hb_sort_rows      graph.py:52-80 keeps successor lists sorted; this restores that
  *                     order after the internal relabelling
+ *   hb_gen_rmat_keys / hb_keys_to_csr
+ *                     graph.py:52-80 (from_edges: sort, dedup, CSR) + 145-155 (transpose),
+ *                     for the synthetic R-MAT configs, on the device
  *   hb_hash_items     hll.py:79-88 hash_items (device twin, used by tests)
  *
  * Layout:
@@ -149,6 +152,22 @@ int hb_relabel_csr(int64_t n, const int64_t *old_offsets, const int32_t *old_suc
 int hb_sort_rows(int64_t n, const int64_t *offsets, const int64_t *host_offsets, int32_t *ids,
                  int32_t *alt, void *temp, uint64_t *temp_bytes, int *result_in_alt,
                  void *stream);
+
+/* GPU graph build.
+ * hb_gen_rmat_keys: m R-MAT arcs (scale levels, 32-bit quadrant thresholds thr_a <= thr_ab
+ *   <= thr_abc, counter-based splitmix RNG keyed by seed -- bit-identical to
+ *   libhbgraph.so's hbg_rmat) as device uint64 keys (dst << 32 | src) of the transpose;
+ *   self-loops are written as ~0.
+ * hb_keys_to_csr: sort + deduplicate the keys (keys and alt: device uint64 [m], both
+ *   clobbered), drop the self-loop sentinel, and write the CSR of the transpose:
+ *   offsets (device int64 [n+1]) and succ (device int32 [>= unique arcs]); *m_out (HOST)
+ *   receives the number of arcs.  temp == NULL queries *temp_bytes.  Synchronises
+ *   `stream` once (to size the output). */
+int hb_gen_rmat_keys(int scale, int64_t m, uint64_t thr_a, uint64_t thr_ab, uint64_t thr_abc,
+                     uint64_t seed, uint64_t *keys, void *stream);
+int hb_keys_to_csr(int64_t n, int64_t m, uint64_t *keys, uint64_t *alt, void *temp,
+                   uint64_t *temp_bytes, int64_t *m_out, int64_t *offsets, int32_t *succ,
+                   void *stream);
 
 /* out[i] = hash_items(items[i], replicas[i], seed) (hll.py:79-88), device arrays. */
 int hb_hash_items(int64_t n, const uint64_t *items, const uint64_t *replicas, uint64_t seed,

@@ -48,6 +48,8 @@ HB_SIGNATURES = {
     "hb_refresh_rows": (_int, [_i64, _i64, _i64, _vp, _vp, _vp, _int, _vp]),
     "hb_relabel_csr": (_int, [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "hb_sort_rows": (_int, [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "hb_gen_rmat_keys": (_int, [_int, _i64, _u64, _u64, _u64, _u64, _vp, _vp]),
+    "hb_keys_to_csr": (_int, [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "hb_hash_items": (_int, [_i64, _vp, _vp, _u64, _vp, _vp]),
     "hb_item_arcs": (_i64, [_int]),
     "hb_light_max_deg": (_i64, [_int]),

@@ -16,7 +16,9 @@
 //   * registers are < 128 (rho_max = 65 - b <= 61), so the 7-bit-safe SIMD byte max below
 //     is exact.
 #include <cuda_runtime.h>
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_segmented_sort.cuh>
+#include <cub/device/device_select.cuh>
 #include <cub/iterator/transform_input_iterator.cuh>
 #include <stdint.h>
 #include <stdio.h>
@@ -775,6 +777,57 @@ __global__ void k_refresh_rows(int64_t n, int64_t lo, int64_t hi,
   }
 }
 
+// ---- GPU graph build ---------------------------------------------
+// Counter-based R-MAT arcs, bit-identical to graphgen.c's rmat_fn (same splitmix chain,
+// same 32-bit quadrant thresholds), packed as (dst << 32 | src) keys of the TRANSPOSE;
+// self-loops become the sentinel ~0 and are dropped after the sort.
+__device__ __forceinline__ uint64_t gg_rng3(uint64_t seed, uint64_t stream, uint64_t a,
+                                            uint64_t b) {
+  return mix64(mix64(mix64(seed * 0x9E3779B97F4A7C15ull + stream) + a) + b);
+}
+
+__global__ void k_gen_rmat(int scale, int64_t m, uint64_t A, uint64_t AB, uint64_t ABC,
+                           uint64_t seed, uint64_t *__restrict__ keys) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t s = 0, d = 0, r = 0;
+    for (int l = 0; l < scale; l++) {
+      uint64_t x;
+      if ((l & 1) == 0) {
+        r = gg_rng3(seed, 4, (uint64_t)k, (uint64_t)(l >> 1));
+        x = r & 0xffffffffull;
+      } else {
+        x = r >> 32;
+      }
+      const int q = x < A ? 0 : (x < AB ? 1 : (x < ABC ? 2 : 3));
+      s = (s << 1) | (uint64_t)(q >> 1);
+      d = (d << 1) | (uint64_t)(q & 1);
+    }
+    keys[k] = (s == d) ? ~0ull : ((d << 32) | s);
+  }
+}
+
+// CSR of the sorted unique keys [0, mu): thread per key position k in [0, mu]; the rows
+// from the previous key's dst + 1 up to this key's dst all start at k (empty rows
+// included); position mu closes every remaining row.  succ[k] = src of key k.
+__global__ void k_keys_to_csr(int64_t n, int64_t mu, const uint64_t *__restrict__ keys,
+                              int64_t *__restrict__ offsets, int32_t *__restrict__ succ) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k <= mu;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t d = k < mu ? (int64_t)(__ldg(keys + k) >> 32) : n;
+    const int64_t prev = k > 0 ? (int64_t)(__ldg(keys + k - 1) >> 32) : -1;
+    for (int64_t v = prev + 1; v <= d; v++) offsets[v] = k;
+    if (k < mu) succ[k] = (int32_t)(__ldg(keys + k) & 0xffffffffull);
+  }
+}
+
+__global__ void k_count_valid(const uint64_t *__restrict__ keys, const int64_t *num,
+                              int64_t *__restrict__ out) {
+  // keys sorted and unique: the sentinel, if present, is the last one
+  const int64_t u = *num;
+  *out = (u > 0 && keys[u - 1] == ~0ull) ? u - 1 : u;
+}
+
 // Finalizers (centrality.py:153-171), optionally gathering from internal order:
 // out[o] for original id o reads internal row rank[o].  Explicitly rounded fp64 ops.
 __global__ void k_finalize(int64_t n, const int32_t *__restrict__ rank,
@@ -1079,6 +1132,52 @@ int hb_sort_rows(int64_t n, const int64_t *offsets, const int64_t *host_offsets,
   }
   if (result_in_alt) *result_in_alt = 0;
   return check_launch("hb_sort_rows");
+}
+
+int hb_gen_rmat_keys(int scale, int64_t m, uint64_t thr_a, uint64_t thr_ab, uint64_t thr_abc,
+                     uint64_t seed, uint64_t *keys, void *stream) {
+  if (scale < 1 || scale > 31 || m < 0) return set_err_msg("hb_gen_rmat_keys: bad scale / m");
+  if (m == 0) return 0;
+  k_gen_rmat<<<grid_for_threads(m), kThreads, 0, (cudaStream_t)stream>>>(scale, m, thr_a, thr_ab,
+                                                                          thr_abc, seed, keys);
+  return check_launch("k_gen_rmat");
+}
+
+int hb_keys_to_csr(int64_t n, int64_t m, uint64_t *keys, uint64_t *alt, void *temp,
+                   uint64_t *temp_bytes, int64_t *m_out, int64_t *offsets, int32_t *succ,
+                   void *stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!temp_bytes) return set_err_msg("hb_keys_to_csr: temp_bytes");
+  cub::DoubleBuffer<uint64_t> db(keys, alt);
+  size_t b_sort = 0, b_uniq = 0;
+  cudaError_t e = cub::DeviceRadixSort::SortKeys(nullptr, b_sort, db, m, 0, 64, s);
+  if (e != cudaSuccess) return set_err("hb_keys_to_csr sort size", e);
+  e = cub::DeviceSelect::Unique(nullptr, b_uniq, keys, alt, m_out, m, s);
+  if (e != cudaSuccess) return set_err("hb_keys_to_csr unique size", e);
+  const size_t need = (b_sort > b_uniq ? b_sort : b_uniq) + 64;
+  if (!temp) {
+    *temp_bytes = need;
+    return 0;
+  }
+  if (*temp_bytes < need) return set_err_msg("hb_keys_to_csr: temp buffer too small");
+  // temp layout: [int64 counters (64 B)] [cub scratch]
+  int64_t *cnt = reinterpret_cast<int64_t *>(temp);
+  void *scratch = reinterpret_cast<char *>(temp) + 64;
+  size_t bytes = need - 64;
+  e = cub::DeviceRadixSort::SortKeys(scratch, bytes, db, m, 0, 64, s);
+  if (e != cudaSuccess) return set_err("hb_keys_to_csr sort", e);
+  uint64_t *sorted = db.Current(), *other = db.Alternate();
+  bytes = need - 64;
+  e = cub::DeviceSelect::Unique(scratch, bytes, sorted, other, cnt, m, s);
+  if (e != cudaSuccess) return set_err("hb_keys_to_csr unique", e);
+  k_count_valid<<<1, 1, 0, s>>>(other, cnt, cnt + 1);
+  int64_t mu = 0;
+  e = cudaMemcpyAsync(&mu, cnt + 1, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return set_err("hb_keys_to_csr count", e);
+  k_keys_to_csr<<<grid_for_threads(mu + 1), kThreads, 0, s>>>(n, mu, other, offsets, succ);
+  *m_out = mu;
+  return check_launch("k_keys_to_csr");
 }
 
 int hb_relabel_csr(int64_t n, const int64_t *old_offsets, const int32_t *old_succ,

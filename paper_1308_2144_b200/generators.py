@@ -54,6 +54,42 @@ def rmat_t(scale: int, arcs: int, seed: int, abc=RMAT_ABC, threads: int | None =
     return _collect(graphlib().hbg_rmat(scale, arcs, a, b, c, seed, _threads(threads)))
 
 
+def rmat_t_device(scale: int, arcs: int, seed: int, abc=RMAT_ABC, device=None):
+    """rmat_t built on the GPU (hb_gen_rmat_keys + hb_keys_to_csr): the same bytes as the
+    host builder (tests pin the digest), as a DeviceCsrGraph.  Peak device memory is about
+    20 bytes per generated arc."""
+    import torch
+
+    from ._lib import check, hb
+    from .graph import DeviceCsrGraph
+
+    dev = torch.device(device) if device is not None else torch.device(
+        "cuda", torch.cuda.current_device())
+    a, b, c = abc
+    thr = [int(a * 4294967296.0), int((a + b) * 4294967296.0), int((a + b + c) * 4294967296.0)]
+    n = 1 << scale
+    L = hb()
+    stream = torch.cuda.current_stream(dev)
+    with torch.cuda.device(dev):
+        keys = torch.empty(arcs, dtype=torch.int64, device=dev)
+        alt = torch.empty(arcs, dtype=torch.int64, device=dev)
+        check(L.hb_gen_rmat_keys(scale, arcs, thr[0], thr[1], thr[2], seed, keys.data_ptr(),
+                                 stream.cuda_stream), "hb_gen_rmat_keys")
+        tb = ctypes.c_uint64(0)
+        mo = ctypes.c_int64(0)
+        check(L.hb_keys_to_csr(n, arcs, keys.data_ptr(), alt.data_ptr(), None, ctypes.byref(tb),
+                               ctypes.byref(mo), None, None, stream.cuda_stream), "size")
+        temp = torch.empty(int(tb.value), dtype=torch.uint8, device=dev)
+        offsets = torch.empty(n + 1, dtype=torch.int64, device=dev)
+        succ = torch.empty(arcs, dtype=torch.int32, device=dev)
+        check(L.hb_keys_to_csr(n, arcs, keys.data_ptr(), alt.data_ptr(), temp.data_ptr(),
+                               ctypes.byref(tb), ctypes.byref(mo), offsets.data_ptr(),
+                               succ.data_ptr(), stream.cuda_stream), "hb_keys_to_csr")
+        del keys, alt, temp
+        succ = succ[:mo.value].clone()
+    return DeviceCsrGraph(offsets, succ)
+
+
 def disconnected_t(n: int, giant: int, geo_p: float, mean_degree: float, seed: int,
                    threads: int | None = None) -> CsrGraph:
     """Giant block [0, giant) plus consecutive Geometric(geo_p)-sized blocks; each node
@@ -90,6 +126,13 @@ class BenchConfig:
     def build(self, threads: int | None = None) -> CsrGraph:
         return BUILDERS[self.name](threads)
 
+    def build_device(self, device=None):
+        """GPU-built graph where a device builder exists (R-MAT configs), else the host
+        graph (the engine uploads it)."""
+        if self.name in DEVICE_BUILDERS:
+            return DEVICE_BUILDERS[self.name](device)
+        return self.build()
+
 
 BUILDERS = {
     "config1": lambda th=None: erdos_renyi_t(10_000, 8.0, seed=0, threads=th),
@@ -99,6 +142,12 @@ BUILDERS = {
     "config5": lambda th=None: rmat_t(28, 1 << 32, seed=4, threads=th),
     # config 5 at 1/16 scale (same law, same parameters): for iteration on smaller boxes
     "config5s": lambda th=None: rmat_t(24, 1 << 28, seed=4, threads=th),
+}
+
+DEVICE_BUILDERS = {
+    "config2": lambda dev=None: rmat_t_device(20, 16 << 20, seed=1, device=dev),
+    "config5": lambda dev=None: rmat_t_device(28, 1 << 32, seed=4, device=dev),
+    "config5s": lambda dev=None: rmat_t_device(24, 1 << 28, seed=4, device=dev),
 }
 
 CONFIGS = {

@@ -93,6 +93,24 @@ class CsrGraph:
         return f"CsrGraph(n={self.n}, m={self.m})"
 
 
+class DeviceCsrGraph:
+    """A CSR already resident on a CUDA device (offsets int64 [n+1], successors int32 [m]
+    torch tensors), e.g. from the GPU graph builders; accepted wherever a CsrGraph is."""
+
+    __slots__ = ("n", "m", "offsets", "successors", "__weakref__")
+
+    def __init__(self, offsets, successors):
+        self.offsets, self.successors = offsets, successors
+        self.n = int(offsets.numel()) - 1
+        self.m = int(successors.numel())
+
+    def to_host(self) -> CsrGraph:
+        return CsrGraph(self.offsets.cpu().numpy(), self.successors.cpu().numpy())
+
+    def __repr__(self) -> str:
+        return f"DeviceCsrGraph(n={self.n}, m={self.m}, device={self.offsets.device})"
+
+
 def transpose(g) -> CsrGraph:
     """Reverse every arc; the result is normalised (sorted rows)."""
     n = int(np.asarray(g.offsets).size - 1)

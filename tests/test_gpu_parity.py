@@ -172,3 +172,22 @@ def test_checkpoint_bytes_match_reference(pins, tmp_path):
     assert st2.t == case["t"]
     assert sha(st2.register_matrix()) == case["reg_digests"][-1]
     assert sha(st2.est) == case["est_digests"][-1]
+
+
+@pytest.mark.parametrize("scale,factor,seed", [(10, 8, 3), (14, 16, 21), (16, 16, 22)])
+def test_device_rmat_builder_matches_host(scale, factor, seed):
+    """GPU graph build (hb_gen_rmat_keys + hb_keys_to_csr) == host C builder, byte for byte."""
+    host = gen.rmat_t(scale, factor << scale, seed=seed)
+    dev = gen.rmat_t_device(scale, factor << scale, seed=seed)
+    assert dev.n == host.n and dev.m == host.m
+    assert np.array_equal(dev.offsets.cpu().numpy(), host.offsets)
+    assert np.array_equal(dev.successors.cpu().numpy(), host.successors)
+
+
+def test_engine_on_device_graph():
+    g = gen.rmat_t_device(12, 16 << 12, seed=11)
+    case = next(c for c in CASES if c["key"] == "rmat12_b7_s42_w5")
+    acc = hb.CentralityAccumulator(g.n)
+    st = hb.run(g, hb.HyperBallConfig(params=hb.CounterParams(b=7, seed=42)), [acc])
+    assert st.t == case["t"]
+    assert sha(st.register_matrix()) == case["reg_digests"][-1]
