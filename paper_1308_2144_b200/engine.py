@@ -373,7 +373,7 @@ class _Device:
             s.heavy_nodes.data_ptr(), s.item_first.data_ptr(), s.n_heavy,
             s.finish_order.data_ptr(), s.n_mega, s.item_node.data_ptr(), s.item_beg.data_ptr(), s.n_items, s.item_arcs,
             s.partial.data_ptr(), self.counts.data_ptr(), self.counts.data_ptr() + 8,
-            self.stream.cuda_stream), "hb_union_step")
+            s.hot_rows, self.stream.cuda_stream), "hb_union_step")
         self.launches += (light_hi > s.light_lo) + (s.n_items > 0) + (s.n_heavy > 0)
         self.launches_at_last_step = self.launches
         nch, merged = (int(x) for x in self.counts.cpu())

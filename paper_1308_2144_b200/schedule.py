@@ -51,6 +51,7 @@ class Schedule:
     item_beg: torch.Tensor
     partial: torch.Tensor
     max_deg: int
+    hot_rows: int = 0              # degree order: head of the rows kept persisting in L2
 
     @property
     def n_heavy(self) -> int:
@@ -182,4 +183,5 @@ def build_schedule(offsets, successors, b: int, device, order: str = "auto", wor
                     heavy_nodes=heavy.to(torch.int32), item_first=item_first.to(torch.int32),
                     finish_order=finish_order, n_mega=n_mega,
                     item_node=item_node.to(torch.int32), item_beg=item_beg.contiguous(),
-                    partial=partial, max_deg=max_deg)
+                    partial=partial, max_deg=max_deg,
+                    hot_rows=n if order == "degree" else 0)
