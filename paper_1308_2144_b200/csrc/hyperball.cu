@@ -308,7 +308,11 @@ constexpr int kThreads = 256;
 template <int LOGP>
 struct Batch {
   using Gm = Geo<LOGP>;
-  static constexpr int U = Gm::CPL >= 8 ? 1 : 8 / Gm::CPL;   // row loads in flight per lane
+  // 16-byte row loads in flight per lane and resident CTAs per SM of the light kernel,
+  // per p (swept on configs 3, 4, 5s: more registers per thread pay at p = 64 / 256)
+  static constexpr int LOADS = LOGP == 8 ? 16 : 8;
+  static constexpr int MINB = LOGP >= 10 ? 2 : (LOGP == 8 ? 2 : (LOGP >= 6 ? 3 : 4));
+  static constexpr int U = Gm::CPL >= LOADS ? 1 : LOADS / Gm::CPL;  // rows in flight per lane
   static constexpr int NB = Gm::G > 8 ? Gm::G : 8;            // light: ids per group batch
   static constexpr int J = NB / Gm::G;                        // light: ids loaded per lane
   static constexpr int WARP_IDS = Gm::NPW * NB;               // light: smem ids per warp
@@ -365,7 +369,7 @@ __host__ __device__ constexpr int chunk_rounds() { return LOGP >= 8 ? 16 : 4; }
 // gather as the only exposed memory latency of a round.
 // _kernels.py:67-114 restated with the source-skip rule.
 template <int LOGP>
-__global__ void __launch_bounds__(kThreads, (LOGP >= 10 ? 2 : 4))
+__global__ void __launch_bounds__(kThreads, Batch<LOGP>::MINB)
 k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
         const uint8_t *__restrict__ cur, uint8_t *__restrict__ nxt,
         const uint32_t *__restrict__ chg_prev, uint32_t *__restrict__ chg_now,
