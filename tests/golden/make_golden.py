@@ -126,9 +126,16 @@ WIDTH_CASES = [  # register width variations (saturation at 2^w - 1)
 ]
 
 
-def drive(gT, b, seed, width=5):
+WEIGHTED_CASES = [  # NodeWeights replicas (engine.py:100-119)
+    ("random300", lambda: random_graph(7, 300, 3.0), 6, 42, 5, 1),
+    ("islands400", lambda: islands(9, 400, 1.5), 8, 3, 5, 2),
+    ("dag300", lambda: random_dag(8, 300, 2.0), 4, 42, 6, 3),
+]
+
+
+def drive(gT, b, seed, width=5, weights=None):
     cfg = ref.HyperBallConfig(params=ref.CounterParams(b=b, register_width=width, seed=seed),
-                              workers=1)
+                              workers=1, weights=weights)
     acc = ref.CentralityAccumulator(gT.n)
     state = ref.initialize(gT, cfg)
     regs, ests, nchs, clamps = [sha(state.register_matrix())], [sha(state.est)], [], 0
@@ -154,11 +161,15 @@ def drive(gT, b, seed, width=5):
 def main():
     cases, arrays = [], {}
 
-    def add(name, gT, b, seed, width, stored, digest=None):
-        meta, final, state = drive(gT, b, seed, width)
-        key = f"{name}_b{b}_s{seed % 1000}_w{width}"
+    def add(name, gT, b, seed, width, stored, digest=None, weights=None, wseed=None):
+        meta, final, state = drive(gT, b, seed, width,
+                                   None if weights is None else ref.NodeWeights.from_values(weights))
+        key = f"{name}_b{b}_s{seed % 1000}_w{width}" + ("" if wseed is None else f"_nw{wseed}")
         meta.update(key=key, graph=name, n=int(gT.n), m=int(gT.m), b=b, seed=str(seed),
-                    width=width, graph_stored=stored, graph_digest=digest)
+                    width=width, graph_stored=stored, graph_digest=digest,
+                    weights_seed=wseed)
+        if weights is not None:
+            arrays[f"{key}/weights"] = np.asarray(weights, np.int64)
         for k, v in final.items():
             arrays[f"{key}/{k}"] = v
         cases.append(meta)
@@ -177,6 +188,10 @@ def main():
         gT = ref.transpose(build())
         gname = name.split("_")[0]
         add(gname, gT, b, s, w, True)
+    for name, build, b, s, w, wseed in WEIGHTED_CASES:
+        gT = ref.transpose(build())
+        wts = np.random.default_rng(wseed).integers(1, 6, gT.n)
+        add(name, gT, b, s, w, True, weights=wts, wseed=wseed)
     for name, build, bs, seeds in GEN:
         g = build()
         digest = gen.graph_digest(g)

@@ -35,10 +35,10 @@ def bits_equal(a, b):
     return a.shape == b.shape and np.array_equal(a.view(np.uint64), b.view(np.uint64))
 
 
-def drive(off, suc, b, seed, width=5, schedule="auto", skip=True):
+def drive(off, suc, b, seed, width=5, schedule="auto", skip=True, weights=None):
     g = hb.CsrGraph(off, suc)
     cfg = hb.HyperBallConfig(params=hb.CounterParams(b=b, register_width=width, seed=seed),
-                             schedule=schedule, skip_stable_nodes=skip)
+                             schedule=schedule, skip_stable_nodes=skip, weights=weights)
     acc = hb.CentralityAccumulator(g.n)
     st = hb.initialize(g, cfg)
     regs, ests, nchs = [sha(st.register_matrix())], [sha(st.est)], []
@@ -58,8 +58,10 @@ def drive(off, suc, b, seed, width=5, schedule="auto", skip=True):
 @pytest.mark.parametrize("case", CASES, ids=[c["key"] for c in CASES])
 def test_golden_case(case, schedule):
     off, suc = golden_graph(case)
+    _, arrays = golden()
+    w = arrays[f"{case['key']}/weights"] if case.get("weights_seed") is not None else None
     st, acc, regs, ests, nchs = drive(off, suc, case["b"], int(case["seed"]), case["width"],
-                                      schedule)
+                                      schedule, weights=w)
     assert st.t == case["t"]
     assert nchs == case["nch"]
     assert regs == case["reg_digests"]

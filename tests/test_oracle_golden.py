@@ -19,7 +19,10 @@ CASES = golden_cases()
 @pytest.mark.parametrize("case", CASES, ids=[c["key"] for c in CASES])
 def test_oracle_matches_reference(case):
     off, suc = golden_graph(case)
-    res = orc.run_oracle(off, suc, case["b"], int(case["seed"]), case["width"], workers=2)
+    _, arrays = golden()
+    w = arrays[f"{case['key']}/weights"] if case.get("weights_seed") is not None else None
+    res = orc.run_oracle(off, suc, case["b"], int(case["seed"]), case["width"], workers=2,
+                         weights=w)
     assert res.t == case["t"]
     assert res.nch == case["nch"]
     assert res.reg_digests == case["reg_digests"]
