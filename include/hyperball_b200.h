@@ -101,7 +101,10 @@ int hb_estimate_rows(const uint8_t *regs, int64_t lo, int64_t hi, int b,
  * every source as changed (first iteration and
  * skip_stable_nodes=False; results are identical).  hot_rows > 0 marks rows
  * [0, hot_rows) of cur as persisting in L2 for the duration of the call (degree order:
- * the most-read rows); 0 leaves the cache policy alone. */
+ * the most-read rows); 0 leaves the cache policy alone.  Discounted-gain sums
+ * (centrality.py:26-101,149-150), at most 8: disc (device fp64 [n_disc, disc_stride])
+ * gets disc[k][v] += (bit k of disc_div) ? delta / t : disc_scale[k] * delta for every
+ * changed v (n_disc <= 8); disc_scale is a HOST array of the n_disc factors f_k(t) for this step. */
 int hb_union_step(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets,
                   const int32_t *succ, const uint8_t *cur, uint8_t *nxt,
                   const uint32_t *chg_prev, uint32_t *chg_now, int clear_chg_now,
@@ -111,7 +114,8 @@ int hb_union_step(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets,
                   int64_t n_heavy, const int32_t *finish_order, int64_t n_mega,
                   const int32_t *item_node, const int64_t *item_beg,
                   int64_t n_items, int64_t item_arcs, uint8_t *partial, uint64_t *nch_out,
-                  uint64_t *merged_out, int64_t hot_rows, void *stream);
+                  uint64_t *merged_out, int64_t hot_rows, double *disc, int64_t disc_stride,
+                  int n_disc, const double *disc_scale, int disc_div, void *stream);
 
 /* Finalizers (centrality.py:153-171) over device sums in internal order, written in
  * original order: out[o] uses internal row rank[o] (rank NULL = identity).

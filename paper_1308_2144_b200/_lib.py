@@ -41,7 +41,8 @@ HB_SIGNATURES = {
     "hb_estimate_rows": (_int, [_vp, _i64, _i64, _int, _vp, _dbl, _dbl, _vp, _vp]),
     "hb_union_step": (_int, [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _int, _vp, _vp,
                              _vp, _i64, _vp, _dbl, _dbl, _int, _int, _i64, _vp, _vp, _i64,
-                             _vp, _i64, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _i64, _vp]),
+                             _vp, _i64, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _i64,
+                             _vp, _i64, _int, _vp, _int, _vp]),
     "hb_finalize": (_int, [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "hb_gather_changed": (_int, [_i64, _i64, _vp, _vp, _int, _vp, _vp, _vp, _vp]),
     "hb_scatter_rows": (_int, [_i64, _vp, _vp, _int, _vp, _vp, _vp]),

@@ -16,9 +16,81 @@ The finalizers apply the same conventions as centrality.py:153-171.
 
 from __future__ import annotations
 
+from dataclasses import dataclass
 from typing import Sequence
 
 import numpy as np
+
+PRESET_DISCOUNTS = ("harmonic", "logarithmic", "quadratic", "constant")
+_ALIASES = {"log": "logarithmic", "quad": "quadratic", "const": "constant"}
+
+
+@dataclass(frozen=True)
+class DiscountSpec:
+    """A non-increasing, non-negative discount f(t) over distances t >= 1
+    (centrality.py:26-101): presets harmonic 1/t, logarithmic 1/log2(t+1), quadratic 1/t^2,
+    constant 1, or an explicit table f(1), f(2), ... with a mandatory tail value."""
+
+    kind: str
+    name: str = ""
+    table: tuple | None = None
+    tail: float | None = None
+
+    def __post_init__(self) -> None:
+        if self.kind not in PRESET_DISCOUNTS and self.kind != "table":
+            raise ValueError(f"unknown discount kind {self.kind!r}")
+        if not self.name:
+            object.__setattr__(self, "name", self.kind)
+        if self.kind != "table":
+            return
+        if not self.table:
+            raise ValueError("table discount needs at least one value")
+        if self.tail is None:
+            raise ValueError("table discount needs an explicit tail value for distances "
+                             "beyond the table")
+        vals = list(self.table) + [self.tail]
+        if min(vals) < 0:
+            raise ValueError("discount values must be non-negative")
+        if any(later > earlier for earlier, later in zip(vals, vals[1:])):
+            raise ValueError("discount values must be non-increasing")
+
+    @classmethod
+    def preset(cls, name: str) -> "DiscountSpec":
+        kind = _ALIASES.get(name, name)
+        if kind not in PRESET_DISCOUNTS:
+            raise ValueError(f"unknown discount preset {name!r}")
+        return cls(kind=kind, name=name)
+
+    @classmethod
+    def from_table(cls, values, tail: float, name: str = "table") -> "DiscountSpec":
+        return cls(kind="table", name=name, table=tuple(float(v) for v in values),
+                   tail=float(tail))
+
+    def value(self, t: int) -> float:
+        if t < 1:
+            raise ValueError("discounts are defined for distances t >= 1")
+        k = self.kind
+        if k == "harmonic":
+            return 1.0 / t
+        if k == "logarithmic":
+            return 1.0 / np.log2(t + 1.0)
+        if k == "quadratic":
+            return 1.0 / (float(t) * float(t))
+        if k == "constant":
+            return 1.0
+        return self.table[t - 1] if t <= len(self.table) else self.tail
+
+    def contribution(self, t: int, count):
+        """f(t) * count; the harmonic preset divides (bit-identical to the reciprocal sum)."""
+        if t < 1:
+            raise ValueError("discounts are defined for distances t >= 1")
+        return count / t if self.kind == "harmonic" else self.value(t) * count
+
+    def device_factor(self, t: int):
+        """(divide_by_t, factor) for the fused device accumulation at distance t."""
+        if self.kind == "harmonic":
+            return True, 0.0
+        return False, float(self.value(t))
 
 
 class BallObserver:
@@ -42,7 +114,7 @@ class CentralityAccumulator(BallObserver):
         names = [d.name for d in self.discounts]
         if len(names) != len(set(names)):
             raise ValueError(f"duplicate discount names: {names}")
-        self.discounted = {d.name: np.zeros(n, dtype=np.float64) for d in self.discounts}
+        self._discounted = {d.name: np.zeros(n, dtype=np.float64) for d in self.discounts}
         self.coreach = np.zeros(n, dtype=np.float64)
         self.converged = False
         self._binding = None   # engine-side DeviceSums when fused
@@ -52,6 +124,15 @@ class CentralityAccumulator(BallObserver):
     def _pull(self) -> None:
         if self._binding is not None and self._binding.dirty:
             self._binding.pull_into(self)
+
+    @property
+    def discounted(self) -> dict:
+        self._pull()
+        return self._discounted
+
+    @discounted.setter
+    def discounted(self, value) -> None:
+        self._discounted = value
 
     @property
     def sum_dist(self) -> np.ndarray:
@@ -104,14 +185,18 @@ class CentralityAccumulator(BallObserver):
         self._sum_dist += t * delta
         self._sum_recip += delta / t
         for spec in self.discounts:
-            self.discounted[spec.name] += spec.contribution(t, delta)
+            self._discounted[spec.name] += spec.contribution(t, delta)
+
+
+MAX_FUSED_DISCOUNTS = 8   # kMaxDisc in hyperball.cu
 
 
 def fusable(obs, n: int) -> bool:
     """An accumulator whose per-iteration fold the union kernel can do (no discounts).
     Never touches the lazily-refreshed sums (that would force a device read-back)."""
     if isinstance(obs, CentralityAccumulator):
-        return not obs.discounts and obs.n == n
+        return (len(obs.discounts) <= MAX_FUSED_DISCOUNTS and obs.n == n
+                and all(hasattr(d, "device_factor") for d in obs.discounts))
     if type(obs).__name__ != "CentralityAccumulator":
         return False
     attrs = vars(obs) if hasattr(obs, "__dict__") else {}
@@ -158,3 +243,8 @@ def finalize_lin(acc) -> np.ndarray:
     s = np.asarray(acc.sum_dist, dtype=np.float64)
     c = np.asarray(acc.coreach, dtype=np.float64)
     return np.divide(c * c, s, out=np.ones_like(s), where=s > 0)
+
+
+def finalize_discounted(acc, name: str) -> np.ndarray:
+    """The accumulated discounted-gain sum for one discount spec (centrality.py:174-176)."""
+    return np.array(acc.discounted[name], dtype=np.float64, copy=True)

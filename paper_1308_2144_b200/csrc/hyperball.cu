@@ -152,9 +152,17 @@ __device__ __forceinline__ void acc_word(uint32_t w, uint64_t &S, int &zeros, ui
   }
 }
 
+// Fused discounted-gain sums (centrality.py:26-101,149-150): up to kMaxDisc arrays
+// disc[k * disc_stride + v] += (bit k of disc_div) ? delta / t : disc_scale[k] * delta.
+constexpr int kMaxDisc = 8;
+
 struct EstConst {
   double alpha_p2, lc_cut;
   const double *lc;  // lc_table[0..p]
+  double *disc;      // [n_disc, disc_stride] or nullptr
+  int64_t disc_stride;
+  int n_disc, disc_div;
+  double disc_scale[kMaxDisc];
 };
 
 // Raw estimate from the (exact) register sum, with the linear-counting switch
@@ -269,6 +277,11 @@ __device__ __forceinline__ bool finish_node(bool doit, int64_t v,
         sum_dist[v] = __dadd_rn(pre_vals ? pre_vals[1] : sum_dist[v], __dmul_rn(tf, d));
       if (sum_recip)
         sum_recip[v] = __dadd_rn(pre_vals ? pre_vals[2] : sum_recip[v], __ddiv_rn(d, tf));
+      for (int k = 0; k < ec.n_disc; k++) {
+        double *q = ec.disc + k * ec.disc_stride + v;
+        const double c = ((ec.disc_div >> k) & 1) ? __ddiv_rn(d, tf) : __dmul_rn(ec.disc_scale[k], d);
+        *q = __dadd_rn(*q, c);
+      }
     }
   }
   return changed;
@@ -1055,7 +1068,7 @@ int hb_seed(uint8_t *regs, double *est, int64_t n, int b, int register_width, ui
   if (n == 0) return 0;
   if (n < 0 || !regs || !est || !lc_table) return set_err_msg("hb_seed: bad arguments");
   cudaStream_t s = (cudaStream_t)stream;
-  EstConst ec{alpha_p2, lc_cut, lc_table};
+  EstConst ec{alpha_p2, lc_cut, lc_table, nullptr, 0, 0, 0, {0, 0, 0, 0, 0, 0, 0, 0}};
   HB_DISPATCH(b, (k_seed<LB><<<grid_for_threads(n), kThreads, 0, s>>>(
                      regs, est, n, perm, weights, register_width, seed, ec)));
   return check_launch("k_seed");
@@ -1066,7 +1079,7 @@ int hb_estimate_rows(const uint8_t *regs, int64_t lo, int64_t hi, int b,
                      void *stream) {
   if (hi <= lo) return 0;
   cudaStream_t s = (cudaStream_t)stream;
-  EstConst ec{alpha_p2, lc_cut, lc_table};
+  EstConst ec{alpha_p2, lc_cut, lc_table, nullptr, 0, 0, 0, {0, 0, 0, 0, 0, 0, 0, 0}};
   HB_DISPATCH(b, (k_estimate_rows<LB><<<grid_for_threads(hi - lo), kThreads, 0, s>>>(
                      regs, lo, hi, ec, out)));
   return check_launch("k_estimate_rows");
@@ -1081,7 +1094,10 @@ int hb_union_step(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets,
                   int64_t n_heavy, const int32_t *finish_order, int64_t n_mega,
                   const int32_t *item_node, const int64_t *item_beg,
                   int64_t n_items, int64_t item_arcs, uint8_t *partial, uint64_t *nch_out,
-                  uint64_t *merged_out, int64_t hot_rows, void *stream) {
+                  uint64_t *merged_out, int64_t hot_rows, double *disc, int64_t disc_stride,
+                  int n_disc, const double *disc_scale, int disc_div, void *stream) {
+  if (n_disc < 0 || n_disc > kMaxDisc || (n_disc > 0 && (!disc || !disc_scale)))
+    return set_err_msg("hb_union_step: bad discount arguments (at most 8 fused)");
   if (n < 0 || lo < 0 || hi > n || lo > hi || t < 1 || !nch_out)
     return set_err_msg("hb_union_step: bad range / t / nch_out");
   if ((n_items > 0 && (!item_node || !item_beg || !partial)) ||
@@ -1100,7 +1116,8 @@ int hb_union_step(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets,
       return set_err("hb_union_step memset chg_now", e);
   }
   if (n == 0) return 0;
-  EstConst ec{alpha_p2, lc_cut, lc_table};
+  EstConst ec{alpha_p2, lc_cut, lc_table, disc, disc_stride, n_disc, disc_div, {0, 0, 0, 0, 0, 0, 0, 0}};
+  for (int k = 0; k < n_disc; k++) ec.disc_scale[k] = disc_scale[k];
   const double tf = (double)t;
   HB_DISPATCH(b, return union_step_impl<LB>(
                      lo, hi, offsets, succ, cur, nxt, chg_prev, chg_now, est, sum_dist,

@@ -190,14 +190,36 @@ class _DeviceSums:
         else:
             sd, sr = acc._sum_dist, acc._sum_recip
         self.host_ids = (id(sd), id(sr))
+        self.specs = [] if self.foreign else list(acc.discounts)
+        k = len(self.specs)
         if not self.foreign and acc._fresh:       # nothing accumulated yet: no upload
             self.sum_dist = torch.zeros(dev.n, dtype=torch.float64, device=dev.device)
             self.sum_recip = torch.zeros(dev.n, dtype=torch.float64, device=dev.device)
+            self.disc = torch.zeros((k, dev.n), dtype=torch.float64, device=dev.device)
         else:
             self.sum_dist = dev.to_internal(np.asarray(sd, dtype=np.float64))
             self.sum_recip = dev.to_internal(np.asarray(sr, dtype=np.float64))
+            self.disc = torch.zeros((k, dev.n), dtype=torch.float64, device=dev.device)
+            for i, spec in enumerate(self.specs):
+                self.disc[i] = dev.to_internal(np.asarray(acc._discounted[spec.name],
+                                                          dtype=np.float64))
         self.dirty = False
         self.stale = False
+
+    def disc_args(self, t: int):
+        """(base ptr, stride, count, host scale array, divide mask) for hb_union_step."""
+        import ctypes
+        k = len(self.specs)
+        if k == 0:
+            return None, 0, 0, None, 0
+        scale = (ctypes.c_double * k)()
+        div = 0
+        for i, spec in enumerate(self.specs):
+            d, f = spec.device_factor(t)
+            scale[i] = f
+            div |= int(d) << i
+        self._scale_keepalive = scale
+        return self.disc.data_ptr(), self.dev.n, k, ctypes.cast(scale, ctypes.c_void_p), div
 
     coreach_dev = None
     coreach_host_id = None
@@ -246,6 +268,8 @@ class _DeviceSums:
             self.host_ids = (id(acc.sum_dist), id(acc.sum_recip))
         else:
             acc._sum_dist, acc._sum_recip = sd, sr
+            acc._discounted = {spec.name: self.dev.to_host(self.disc[i])
+                               for i, spec in enumerate(self.specs)}
             acc._fresh = False
 
     def invalidate(self) -> None:
@@ -365,6 +389,7 @@ class _Device:
         light_hi = s.light_hi if self.full_pass else s.light_hi_steady
         sd = sums.sum_dist.data_ptr() if sums is not None else None
         sr = sums.sum_recip.data_ptr() if sums is not None else None
+        dargs = sums.disc_args(t) if hasattr(sums, "disc_args") else (None, 0, 0, None, 0)
         _lib.check(_lib.hb().hb_union_step(
             self.n, s.light_lo, light_hi, s.offsets.data_ptr(), s.succ.data_ptr(),
             self.cur.data_ptr(), self.nxt.data_ptr(), self.chg_prev.data_ptr(),
@@ -373,7 +398,7 @@ class _Device:
             s.heavy_nodes.data_ptr(), s.item_first.data_ptr(), s.n_heavy,
             s.finish_order.data_ptr(), s.n_mega, s.item_node.data_ptr(), s.item_beg.data_ptr(), s.n_items, s.item_arcs,
             s.partial.data_ptr(), self.counts.data_ptr(), self.counts.data_ptr() + 8,
-            s.hot_rows, self.stream.cuda_stream), "hb_union_step")
+            s.hot_rows, *dargs, self.stream.cuda_stream), "hb_union_step")
         self.launches += (light_hi > s.light_lo) + (s.n_items > 0) + (s.n_heavy > 0)
         self.launches_at_last_step = self.launches
         nch, merged = (int(x) for x in self.counts.cpu())

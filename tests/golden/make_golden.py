@@ -133,10 +133,28 @@ WEIGHTED_CASES = [  # NodeWeights replicas (engine.py:100-119)
 ]
 
 
-def drive(gT, b, seed, width=5, weights=None):
+DISCOUNT_SPECS = [("harmonic", None), ("log", None), ("quad", None), ("const", None),
+                  ("table", ((1.0, 0.5, 0.25), 0.125))]
+DISCOUNT_CASES = [  # fused discounted-gain sums (centrality.py:26-101,149-150)
+    ("random300", lambda: random_graph(7, 300, 3.0), 6, 42),
+    ("sparse2000", lambda: random_graph(10, 2000, 1.1), 4, 42),
+]
+
+
+def ref_discounts():
+    out = []
+    for name, tab in DISCOUNT_SPECS:
+        if tab is None:
+            out.append(ref.DiscountSpec.preset(name))
+        else:
+            out.append(ref.DiscountSpec.from_table(tab[0], tab[1], name="table"))
+    return out
+
+
+def drive(gT, b, seed, width=5, weights=None, discounts=()):
     cfg = ref.HyperBallConfig(params=ref.CounterParams(b=b, register_width=width, seed=seed),
                               workers=1, weights=weights)
-    acc = ref.CentralityAccumulator(gT.n)
+    acc = ref.CentralityAccumulator(gT.n, discounts)
     state = ref.initialize(gT, cfg)
     regs, ests, nchs, clamps = [sha(state.register_matrix())], [sha(state.est)], [], 0
     if gT.n > 0:
@@ -154,6 +172,8 @@ def drive(gT, b, seed, width=5, weights=None):
                  sum_recip=acc.sum_recip.copy(), coreach=acc.coreach.copy(),
                  closeness=ref.finalize_closeness(acc), harmonic=ref.finalize_harmonic(acc),
                  lin=ref.finalize_lin(acc))
+    for spec in discounts:
+        final[f"disc_{spec.name}"] = ref.finalize_discounted(acc, spec.name)
     return dict(t=int(state.t), nch=nchs, reg_digests=regs, est_digests=ests,
                 negative_deltas=clamps), final, state
 
@@ -161,10 +181,15 @@ def drive(gT, b, seed, width=5, weights=None):
 def main():
     cases, arrays = [], {}
 
-    def add(name, gT, b, seed, width, stored, digest=None, weights=None, wseed=None):
+    def add(name, gT, b, seed, width, stored, digest=None, weights=None, wseed=None,
+            discounts=()):
         meta, final, state = drive(gT, b, seed, width,
-                                   None if weights is None else ref.NodeWeights.from_values(weights))
+                                   None if weights is None else ref.NodeWeights.from_values(weights),
+                                   discounts)
         key = f"{name}_b{b}_s{seed % 1000}_w{width}" + ("" if wseed is None else f"_nw{wseed}")
+        if discounts:
+            key += "_disc"
+            meta["discounts"] = [[nm, tab] for nm, tab in DISCOUNT_SPECS]
         meta.update(key=key, graph=name, n=int(gT.n), m=int(gT.m), b=b, seed=str(seed),
                     width=width, graph_stored=stored, graph_digest=digest,
                     weights_seed=wseed)
@@ -192,6 +217,9 @@ def main():
         gT = ref.transpose(build())
         wts = np.random.default_rng(wseed).integers(1, 6, gT.n)
         add(name, gT, b, s, w, True, weights=wts, wseed=wseed)
+    for name, build, b, s in DISCOUNT_CASES:
+        gT = ref.transpose(build())
+        add(name, gT, b, s, 5, True, discounts=ref_discounts())
     for name, build, bs, seeds in GEN:
         g = build()
         digest = gen.graph_digest(g)

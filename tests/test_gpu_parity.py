@@ -193,3 +193,30 @@ def test_engine_on_device_graph():
     st = hb.run(g, hb.HyperBallConfig(params=hb.CounterParams(b=7, seed=42)), [acc])
     assert st.t == case["t"]
     assert sha(st.register_matrix()) == case["reg_digests"][-1]
+
+
+def _specs(case):
+    out = []
+    for name, tab in case["discounts"]:
+        out.append(hb.DiscountSpec.preset(name) if tab is None
+                   else hb.DiscountSpec.from_table(tab[0], tab[1], name="table"))
+    return out
+
+
+@pytest.mark.parametrize("key", [c["key"] for c in CASES if c.get("discounts")])
+def test_fused_discounts_match_reference(key):
+    case = next(c for c in CASES if c["key"] == key)
+    off, suc = golden_graph(case)
+    g = hb.CsrGraph(off, suc)
+    specs = _specs(case)
+    acc = hb.CentralityAccumulator(g.n, specs)
+    st = hb.run(g, hb.HyperBallConfig(params=hb.CounterParams(b=case["b"],
+                                                             seed=int(case["seed"]))), [acc])
+    assert acc._binding is not None        # fused on the device, not the host observer path
+    assert st.t == case["t"]
+    _, arrays = golden()
+    for spec in specs:
+        got = hb.finalize_discounted(acc, spec.name)
+        want = arrays[f"{key}/disc_{spec.name}"]
+        assert bits_equal(got, want), spec.name
+    assert bits_equal(hb.finalize_harmonic(acc), arrays[f"{key}/harmonic"])

@@ -148,3 +148,18 @@ def test_partition_bounds_cover(n, w):
     assert b[0] == 0 and b[-1] == n and all(b[i] <= b[i + 1] for i in range(w))
     # round-robin deal sizes
     assert [b[r + 1] - b[r] for r in range(w)] == [len(range(r, n, w)) for r in range(w)]
+
+
+def test_discount_spec_mirrors_reference_validation():
+    from paper_1308_2144_b200 import DiscountSpec
+    with pytest.raises(ValueError):
+        DiscountSpec("nope")
+    with pytest.raises(ValueError):
+        DiscountSpec.from_table([1.0, 2.0], 0.5)          # increasing
+    with pytest.raises(ValueError):
+        DiscountSpec(kind="table", table=(1.0,))          # no tail
+    assert DiscountSpec.preset("log").name == "log" and DiscountSpec.preset("log").kind == "logarithmic"
+    t = DiscountSpec.from_table([1.0, 0.5], 0.25)
+    assert [t.value(k) for k in (1, 2, 3, 9)] == [1.0, 0.5, 0.25, 0.25]
+    assert DiscountSpec.preset("harmonic").device_factor(4) == (True, 0.0)
+    assert DiscountSpec.preset("quad").device_factor(4) == (False, 1.0 / 16.0)
