@@ -248,3 +248,16 @@ def finalize_lin(acc) -> np.ndarray:
 def finalize_discounted(acc, name: str) -> np.ndarray:
     """The accumulated discounted-gain sum for one discount spec (centrality.py:174-176)."""
     return np.array(acc.discounted[name], dtype=np.float64, copy=True)
+
+
+def multi_run_aggregate(runs: Sequence[np.ndarray]):
+    """Per-node mean and sample standard deviation (ddof=1) across runs; std is None for
+    a single run (centrality.py:179-193)."""
+    if not runs:
+        raise ValueError("need at least one run")
+    sizes = sorted({len(r) for r in runs})
+    if len(sizes) != 1:
+        raise ValueError(f"runs have mismatched lengths: {sizes}")
+    stack = np.stack([np.asarray(r, dtype=np.float64) for r in runs])
+    mean = stack.mean(axis=0)
+    return (mean, None) if len(runs) < 2 else (mean, stack.std(axis=0, ddof=1))

@@ -316,6 +316,26 @@ class _Device:
         self.launches = 0             # kernels launched by hb_union_step calls
         self.launches_at_last_step = 0
 
+    def fresh(self, config: HyperBallConfig) -> "_Device":
+        """A new device state for another run on the same graph and schedule."""
+        other = object.__new__(_Device)
+        other.__dict__.update(self.__dict__)
+        other.params = config.params
+        n, p = self.n, self.p
+        dv = self.device
+        other.cur = torch.empty((n, p), dtype=torch.uint8, device=dv)
+        other.nxt = torch.empty((n, p), dtype=torch.uint8, device=dv)
+        other.chg_prev = torch.full_like(self.chg_prev, -1)
+        other.chg_now = torch.zeros_like(self.chg_now)
+        other.est = torch.zeros(n, dtype=torch.float64, device=dv)
+        other.counts = torch.zeros(2, dtype=torch.int64, device=dv)
+        other.merged_total = 0
+        other.prev_all = True
+        other.full_pass = True
+        other.launches = 0
+        other.launches_at_last_step = 0
+        return other
+
     # -- graph ---------------------------------------------------------------
     def _build_graph(self, g) -> None:
         off, suc = _graph_arrays(g)
@@ -674,3 +694,33 @@ class _PendingState(HyperBallState):
             return m
         return super().register_matrix()
 
+
+
+def run_multi(g, config: HyperBallConfig, runs: int, discounts=(), observers_factory=None):
+    """The reference CLI's repeated runs (cli.py:222-254): run r uses seed config.seed + r
+    and its own CentralityAccumulator.  The graph is uploaded and scheduled once and every
+    run reuses it (only the counters are re-seeded).  Returns [(state, accumulator)]; feed
+    finalize_* of each accumulator to multi_run_aggregate."""
+    from dataclasses import replace
+    if runs < 1:
+        raise ValueError("runs must be >= 1")
+    out = []
+    dev = None
+    for r in range(runs):
+        params = replace(config.params, seed=config.params.seed + r)
+        cfg = replace(config, params=params)
+        n = (g.offsets.numel() if isinstance(g.offsets, torch.Tensor)
+             else np.asarray(g.offsets).shape[0]) - 1
+        acc = CentralityAccumulator(n, discounts)
+        obs = [acc] + (list(observers_factory(r)) if observers_factory else [])
+        w = _weights_array(cfg.weights, n)
+        if w is not None:
+            _check_weighted_width(cfg.params, w)
+        if dev is None:
+            dev = _Device(g, cfg)
+        else:                               # same graph and schedule, fresh counters
+            dev = dev.fresh(cfg)
+        state = HyperBallState(cfg, n, dev)
+        dev.seed(w)
+        out.append((resume(g, state, obs), acc))
+    return out

@@ -220,3 +220,23 @@ def test_fused_discounts_match_reference(key):
         want = arrays[f"{key}/disc_{spec.name}"]
         assert bits_equal(got, want), spec.name
     assert bits_equal(hb.finalize_harmonic(acc), arrays[f"{key}/harmonic"])
+
+
+def test_run_multi_matches_independent_runs():
+    """cli.py:222-254 repeated runs: run r uses seed + r; every run must equal an
+    independent run (golden for r = 0, the oracle for r = 1, 2)."""
+    case = next(c for c in CASES if c["key"] == "config1_b6_s42_w5")
+    off, suc = golden_graph(case)
+    g = hb.CsrGraph(off, suc)
+    res = hb.run_multi(g, hb.HyperBallConfig(params=hb.CounterParams(b=6, seed=42)), runs=3)
+    _, arrays = golden()
+    assert res[0][0].t == case["t"]
+    assert bits_equal(hb.finalize_harmonic(res[0][1]), arrays["config1_b6_s42_w5/harmonic"])
+    for r in (1, 2):
+        ref = orc.run_oracle(off, suc, 6, 42 + r, workers=4)
+        assert res[r][0].t == ref.t
+        assert bits_equal(hb.finalize_harmonic(res[r][1]), ref.harmonic)
+        assert bits_equal(hb.finalize_lin(res[r][1]), ref.lin)
+    mean, std = hb.multi_run_aggregate([hb.finalize_harmonic(a) for _, a in res])
+    stack = np.vstack([hb.finalize_harmonic(a) for _, a in res])
+    assert bits_equal(mean, stack.mean(axis=0)) and bits_equal(std, stack.std(axis=0, ddof=1))

@@ -163,3 +163,16 @@ def test_discount_spec_mirrors_reference_validation():
     assert [t.value(k) for k in (1, 2, 3, 9)] == [1.0, 0.5, 0.25, 0.25]
     assert DiscountSpec.preset("harmonic").device_factor(4) == (True, 0.0)
     assert DiscountSpec.preset("quad").device_factor(4) == (False, 1.0 / 16.0)
+
+
+def test_multi_run_aggregate_semantics():
+    runs = [np.array([1.0, 2.0, 4.0]), np.array([3.0, 2.0, 0.0])]
+    mean, std = hb.multi_run_aggregate(runs)
+    assert mean.tolist() == [2.0, 2.0, 2.0]
+    assert np.allclose(std, np.vstack(runs).std(axis=0, ddof=1))
+    m1, s1 = hb.multi_run_aggregate(runs[:1])
+    assert s1 is None and m1.tolist() == [1.0, 2.0, 4.0]
+    with pytest.raises(ValueError):
+        hb.multi_run_aggregate([])
+    with pytest.raises(ValueError):
+        hb.multi_run_aggregate([np.zeros(2), np.zeros(3)])
