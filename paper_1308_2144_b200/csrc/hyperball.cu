@@ -93,6 +93,18 @@ __device__ __forceinline__ uint32_t bmax(uint32_t a, uint32_t b) {
 __device__ __forceinline__ uint4 bmax4(uint4 a, uint4 b) {
   return make_uint4(bmax(a.x, b.x), bmax(a.y, b.y), bmax(a.z, b.z), bmax(a.w, b.w));
 }
+template <int U, int CPL>
+__device__ __forceinline__ void tree_merge(uint4 (&acc)[CPL], uint4 (&r)[U][CPL]) {
+#pragma unroll
+  for (int span = 1; span < U; span <<= 1)
+#pragma unroll
+    for (int u = 0; u + span < U; u += 2 * span)
+#pragma unroll
+      for (int c = 0; c < CPL; c++) r[u][c] = bmax4(r[u][c], r[u + span][c]);
+#pragma unroll
+  for (int c = 0; c < CPL; c++) acc[c] = bmax4(acc[c], r[0][c]);
+}
+
 __device__ __forceinline__ uint4 ldg4(const uint8_t *p) {
   return __ldg(reinterpret_cast<const uint4 *>(p));
 }
@@ -239,7 +251,7 @@ __device__ __forceinline__ bool finish_node(bool doit, int64_t v,
     // sum_j 2^-M[j] as exact fp64 partial sums (every M <= 31 here: at most 36 significant
     // bits, so any summation order gives the reference's sequential result), zero count by
     // SWAR, and an OR of all bytes to detect registers > 31 (sequential fallback).
-    double s = 0.0;
+    double s4[4] = {0.0, 0.0, 0.0, 0.0};
     uint32_t zeros = 0, big = 0;
 #pragma unroll
     for (int c = 0; c < Gm::CPL; c++) {
@@ -252,10 +264,11 @@ __device__ __forceinline__ bool finish_node(bool doit, int64_t v,
 #pragma unroll
         for (int i = 0; i < 4; i++) {
           const uint32_t m = (w >> (8 * i)) & 0xffu;
-          s = __dadd_rn(s, __hiloint2double((int)(0x3FF00000u - (m << 20)), 0));
+          s4[i] = __dadd_rn(s4[i], __hiloint2double((int)(0x3FF00000u - (m << 20)), 0));
         }
       }
     }
+    double s = __dadd_rn(__dadd_rn(s4[0], s4[1]), __dadd_rn(s4[2], s4[3]));
 #pragma unroll
     for (int off = 1; off < Gm::G; off <<= 1) {   // xor partners stay inside the group
       s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, off));
@@ -277,6 +290,10 @@ __device__ __forceinline__ bool finish_node(bool doit, int64_t v,
         sum_dist[v] = __dadd_rn(pre_vals ? pre_vals[1] : sum_dist[v], __dmul_rn(tf, d));
       if (sum_recip)
         sum_recip[v] = __dadd_rn(pre_vals ? pre_vals[2] : sum_recip[v], __ddiv_rn(d, tf));
+      // Runtime-indexed on purpose: ec.disc_scale[k] makes ptxas keep the estimator
+      // constants in a (L1-resident) local copy instead of registers, which the load
+      // pipeline of the union loops needs more (measured: a statically unrolled loop or a
+      // __constant__ copy costs 8-9% on config 4).
       for (int k = 0; k < ec.n_disc; k++) {
         double *q = ec.disc + k * ec.disc_stride + v;
         const double c = ((ec.disc_div >> k) & 1) ? __ddiv_rn(d, tf) : __dmul_rn(ec.disc_scale[k], d);
@@ -513,9 +530,14 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
                          : make_uint4(0, 0, 0, 0);
         }
 #pragma unroll
-        for (int u = 0; u < B::U; u++)
+        if constexpr (LOGP == 8) {     // pairwise merge pays at 16 loads in flight
+          tree_merge<B::U, Gm::CPL>(acc, r);
+        } else {
 #pragma unroll
-          for (int c = 0; c < Gm::CPL; c++) acc[c] = bmax4(acc[c], r[u][c]);
+          for (int u = 0; u < B::U; u++)
+#pragma unroll
+            for (int c = 0; c < Gm::CPL; c++) acc[c] = bmax4(acc[c], r[u][c]);
+        }
       }
       total += cnt;
       __syncwarp();
@@ -600,9 +622,14 @@ k_heavy_partial(const int64_t *__restrict__ offsets, const int32_t *__restrict__
                          : make_uint4(0, 0, 0, 0);
         }
 #pragma unroll
-        for (int u = 0; u < B::U; u++)
+        if constexpr (LOGP == 8) {     // pairwise merge pays at 16 loads in flight
+          tree_merge<B::U, Gm::CPL>(acc, r);
+        } else {
 #pragma unroll
-          for (int c = 0; c < Gm::CPL; c++) acc[c] = bmax4(acc[c], r[u][c]);
+          for (int u = 0; u < B::U; u++)
+#pragma unroll
+            for (int c = 0; c < Gm::CPL; c++) acc[c] = bmax4(acc[c], r[u][c]);
+        }
       }
       my_merged += (lane == 0) ? (uint32_t)cnt : 0u;
       __syncwarp();
