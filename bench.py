@@ -277,7 +277,7 @@ def run_b200(args):
             s.light_max_deg, s.heavy_nodes.data_ptr(), s.item_first.data_ptr(), s.n_heavy,
             s.finish_order.data_ptr(), s.n_mega, s.item_node.data_ptr(), s.item_beg.data_ptr(), s.n_items, s.item_arcs,
             s.partial.data_ptr(), dev.counts.data_ptr(), dev.counts.data_ptr() + 8,
-            s.hot_rows, None, 0, 0, None, 0, stream.cuda_stream), "hb_union_step")
+            s.hot_rows, None, 0, 0, None, 0, None, stream.cuda_stream), "hb_union_step")
         if ev1 is not None:
             ev1.record(stream)
         nch, merged = (int(x) for x in dev.counts.cpu())   # the per-iteration termination read

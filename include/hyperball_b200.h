@@ -31,6 +31,9 @@
  *   hb_gen_rmat_keys / hb_keys_to_csr
  *                     graph.py:52-80 (from_edges: sort, dedup, CSR) + 145-155 (transpose),
  *                     for the synthetic R-MAT configs, on the device
+ *   hb_forward_keys / hb_mark_active
+ *                     frontier of a sparse iteration (no reference counterpart: the
+ *                     reference scans every node's successor list, _kernels.py:82-87)
  *   hb_hash_items     hll.py:79-88 hash_items (device twin, used by tests)
  *
  * Layout:
@@ -104,7 +107,9 @@ int hb_estimate_rows(const uint8_t *regs, int64_t lo, int64_t hi, int b,
  * the most-read rows); 0 leaves the cache policy alone.  Discounted-gain sums
  * (centrality.py:26-101,149-150), at most 8: disc (device fp64 [n_disc, disc_stride])
  * gets disc[k][v] += (bit k of disc_div) ? delta / t : disc_scale[k] * delta for every
- * changed v (n_disc <= 8); disc_scale is a HOST array of the n_disc factors f_k(t) for this step. */
+ * changed v (n_disc <= 8); disc_scale is a HOST array of the n_disc factors f_k(t) for this step.
+ * active (device uint32 bitmap, may be NULL): frontier mode -- only nodes whose bit is set
+ * are visited (hb_mark_active); NULL visits every node. */
 int hb_union_step(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets,
                   const int32_t *succ, const uint8_t *cur, uint8_t *nxt,
                   const uint32_t *chg_prev, uint32_t *chg_now, int clear_chg_now,
@@ -115,7 +120,8 @@ int hb_union_step(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets,
                   const int32_t *item_node, const int64_t *item_beg,
                   int64_t n_items, int64_t item_arcs, uint8_t *partial, uint64_t *nch_out,
                   uint64_t *merged_out, int64_t hot_rows, double *disc, int64_t disc_stride,
-                  int n_disc, const double *disc_scale, int disc_div, void *stream);
+                  int n_disc, const double *disc_scale, int disc_div, const uint32_t *active,
+                  void *stream);
 
 /* Finalizers (centrality.py:153-171) over device sums in internal order, written in
  * original order: out[o] uses internal row rank[o] (rank NULL = identity).
@@ -158,6 +164,22 @@ int hb_relabel_csr(int64_t n, const int64_t *old_offsets, const int32_t *old_suc
 int hb_sort_rows(int64_t n, const int64_t *offsets, const int64_t *host_offsets, int32_t *ids,
                  int32_t *alt, void *temp, uint64_t *temp_bytes, int *result_in_alt,
                  void *stream);
+
+/* Frontier mode for sparse iterations.
+ * hb_forward_keys: keys[k] = succ[k] << 32 | row(k) for the transpose CSR (offsets, succ);
+ *   hb_keys_to_csr on them yields the forward graph (out-neighbours, internal ids).
+ * hb_mark_active: active = chg_prev | out-neighbours(chg_prev) (device bitmaps over n
+ *   nodes), the only nodes the source-skip rule can touch this iteration. */
+int hb_forward_keys(int64_t n, const int64_t *offsets, const int32_t *succ, uint64_t *keys,
+                    void *stream);
+/* hb_forward_csr: the forward graph by counting sort -- fwd_offsets (device int64 [n+1]),
+ *   cursor (device int64 [n], scratch), fwd_dst (device int32 [m]); rows unordered.
+ *   temp == NULL queries *temp_bytes (scan scratch). */
+int hb_forward_csr(int64_t n, const int64_t *offsets, const int32_t *succ, int64_t m,
+                   int64_t *fwd_offsets, int64_t *cursor, int32_t *fwd_dst, void *temp,
+                   uint64_t *temp_bytes, void *stream);
+int hb_mark_active(int64_t n, const int64_t *fwd_offsets, const int32_t *fwd_succ,
+                   const uint32_t *chg_prev, uint32_t *active, void *stream);
 
 /* GPU graph build.
  * hb_gen_rmat_keys: m R-MAT arcs (scale levels, 32-bit quadrant thresholds thr_a <= thr_ab

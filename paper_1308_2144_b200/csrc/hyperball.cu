@@ -17,6 +17,7 @@
 //     is exact.
 #include <cuda_runtime.h>
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_sort.cuh>
 #include <cub/device/device_select.cuh>
 #include <cub/iterator/transform_input_iterator.cuh>
@@ -405,7 +406,8 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
         const uint32_t *__restrict__ chg_prev, uint32_t *__restrict__ chg_now,
         double *__restrict__ est, double *__restrict__ sum_dist, double *__restrict__ sum_recip,
         EstConst ec, int64_t lo, int64_t hi, int64_t max_deg, int dense, double tf,
-        unsigned long long *__restrict__ nch_out, unsigned long long *__restrict__ merged_out) {
+        unsigned long long *__restrict__ nch_out, unsigned long long *__restrict__ merged_out,
+        const uint32_t *__restrict__ active) {
   using Gm = Geo<LOGP>;
   using B = Batch<LOGP>;
   __shared__ int32_t sids[kThreads / 32][B::WARP_IDS];
@@ -443,7 +445,7 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
     if (sum_recip) l2_prefetch(sum_recip + pb, (pe - pb) * 8);
   };
   int64_t pf_a0 = -1, pf_a1 = -1;
-  if (lane == 0) {
+  if (lane == 0 && !active) {
     l2_prefetch(offsets + vb, (ve - vb + 1) * 8);
     const int64_t pe = vb + (int64_t)kLookRounds * Gm::NPW < ve ? vb + (int64_t)kLookRounds * Gm::NPW : ve;
     stream_prefetch(vb, pe);
@@ -451,7 +453,10 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
     l2_prefetch(succ + a0, (a1 - a0) * 4);
   }
   for (int64_t base = vb; base < ve; base += Gm::NPW) {
-    if (lane == 0) {
+    // frontier mode: only nodes with a changed in-neighbour (or a changed own row) work
+    const bool act_v = !active || ((base + grp < ve) && test_bit(active, base + grp));
+    if (active && !__any_sync(0xffffffffu, act_v)) continue;
+    if (lane == 0 && !active) {
       if (pf_a0 >= 0) {                        // ids of the batch announced last round
         l2_prefetch(succ + pf_a0, (pf_a1 - pf_a0) * 4);
         pf_a0 = -1;
@@ -467,7 +472,7 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
       }
     }
     const int64_t v = base + grp;
-    bool valid = (v >= lo) && (v < ve);
+    bool valid = (v >= lo) && (v < ve) && act_v;
     int64_t beg = 0, end = 0;
     if (valid) {
       beg = __ldg(offsets + v);
@@ -568,7 +573,7 @@ k_heavy_partial(const int64_t *__restrict__ offsets, const int32_t *__restrict__
                 const uint8_t *__restrict__ cur, const uint32_t *__restrict__ chg_prev,
                 const int32_t *__restrict__ item_node, const int64_t *__restrict__ item_beg,
                 int64_t n_items, int64_t item_arcs, int dense, uint8_t *__restrict__ partial,
-                unsigned long long *__restrict__ merged_out) {
+                unsigned long long *__restrict__ merged_out, const uint32_t *__restrict__ active) {
   using Gm = Geo<LOGP>;
   using B = Batch<LOGP>;
   __shared__ int32_t sids[kThreads / 32][B::HEAVY_IDS];
@@ -582,6 +587,7 @@ k_heavy_partial(const int64_t *__restrict__ offsets, const int32_t *__restrict__
   uint32_t my_merged = 0;
   for (int64_t it = warp; it < n_items; it += nwarps) {
     const int64_t v = __ldg(item_node + it);
+    if (active && !test_bit(active, v)) continue;   // warp-uniform: one node per item
     const int64_t beg = __ldg(item_beg + it);
     int64_t end = __ldg(offsets + v + 1);
     if (end > beg + item_arcs) end = beg + item_arcs;
@@ -660,7 +666,7 @@ k_heavy_finish(const int32_t *__restrict__ heavy_nodes, const int32_t *__restric
                const uint32_t *__restrict__ chg_prev, uint32_t *__restrict__ chg_now,
                double *__restrict__ est, double *__restrict__ sum_dist,
                double *__restrict__ sum_recip, EstConst ec, double tf,
-               unsigned long long *__restrict__ nch_out) {
+               unsigned long long *__restrict__ nch_out, const uint32_t *__restrict__ active) {
   using Gm = Geo<LOGP>;
   constexpr int UF = 4;
   const int lane = threadIdx.x & 31;
@@ -702,7 +708,7 @@ k_heavy_finish(const int32_t *__restrict__ heavy_nodes, const int32_t *__restric
 #pragma unroll
         for (int c = 0; c < Gm::CPL; c++) acc[c] = bmax4(acc[c], shfl_xor4(acc[c], off));
     }
-    const bool owner = valid && (!mega || grp == 0);
+    const bool owner = valid && (!mega || grp == 0) && (!active || test_bit(active, v));
     bool any = false;
 #pragma unroll
     for (int c = 0; c < Gm::CPL; c++) any |= nz4(acc[c]);
@@ -831,6 +837,88 @@ __global__ void k_refresh_rows(int64_t n, int64_t lo, int64_t hi,
         reinterpret_cast<uint4 *>(dst + (size_t)v * p)[q] =
             __ldg(reinterpret_cast<const uint4 *>(src + (size_t)v * p) + q);
     }
+  }
+}
+
+// ---- frontier mode (sparse iterations) -------------------------------------------------
+// active = chg_prev | out-neighbours(chg_prev) over the forward graph G: exactly the nodes
+// the source-skip rule can change this iteration, plus the changed rows themselves (their
+// recycled-buffer copy must be refreshed).  Warp per bitmap word of chg_prev.
+__global__ void k_mark_active(int64_t n, const int64_t *__restrict__ fwd_off,
+                              const int32_t *__restrict__ fwd_succ,
+                              const uint32_t *__restrict__ chg_prev,
+                              uint32_t *__restrict__ active) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t words = (n + 31) >> 5;
+  for (int64_t wd = warp; wd < words; wd += nwarps) {
+    uint32_t m = __ldg(chg_prev + wd);
+    if ((wd << 5) + 32 > n) m &= (n - (wd << 5) >= 32) ? ~0u : ((1u << (n - (wd << 5))) - 1u);
+    if (m == 0) continue;
+    if (lane == 0) atomicOr(active + wd, m);
+    while (m) {
+      const int64_t w = (wd << 5) + __ffs(m) - 1;
+      m &= m - 1;
+      const int64_t b0 = __ldg(fwd_off + w), b1 = __ldg(fwd_off + w + 1);
+      for (int64_t k = b0 + lane; k < b1; k += 32) {
+        const int32_t d = __ldg(fwd_succ + k);
+        atomicOr(active + (d >> 5), 1u << (d & 31));
+      }
+    }
+  }
+}
+
+// Forward CSR by counting sort (row order inside a forward row is irrelevant for marking):
+// count out-degrees with atomics, exclusive scan, scatter with per-source cursors.
+// Warp-aggregated: lanes holding the same source (hubs on R-MAT) issue one atomic.
+__global__ void k_count_src(int64_t m, const int32_t *__restrict__ succ,
+                            unsigned long long *__restrict__ cnt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < m; base += stride) {
+    const int64_t k = base + threadIdx.x;
+    const bool ok = k < m;
+    const int32_t src = ok ? __ldg(succ + k) : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, src);
+    if (ok && lane == __ffs(peers) - 1) atomicAdd(cnt + src, (unsigned long long)__popc(peers));
+  }
+}
+
+__global__ void k_scatter_fwd(int64_t n, const int64_t *__restrict__ off,
+                              const int32_t *__restrict__ succ,
+                              unsigned long long *__restrict__ cursor,
+                              int32_t *__restrict__ fwd_dst) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = warp; v < n; v += nwarps) {
+    const int64_t b0 = __ldg(off + v), b1 = __ldg(off + v + 1);
+    for (int64_t kb = b0; kb < b1; kb += 32) {     // warp-uniform trip count
+      const int64_t k = kb + lane;
+      const bool ok = k < b1;
+      const int32_t src = ok ? __ldg(succ + k) : -1;
+      const unsigned peers = __match_any_sync(0xffffffffu, src);
+      const int leader = __ffs(peers) - 1;
+      unsigned long long pos = 0;
+      if (ok && lane == leader) pos = atomicAdd(cursor + src, (unsigned long long)__popc(peers));
+      pos = __shfl_sync(0xffffffffu, pos, leader);
+      if (ok) fwd_dst[pos + __popc(peers & ((1u << lane) - 1u))] = (int32_t)v;
+    }
+  }
+}
+
+// keys (src << 32 | dst) of every arc of the transpose CSR: sorting them gives the forward
+// graph (hb_keys_to_csr).  Warp per row.
+__global__ void k_forward_keys(int64_t n, const int64_t *__restrict__ off,
+                               const int32_t *__restrict__ succ, uint64_t *__restrict__ keys) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = warp; v < n; v += nwarps) {
+    const int64_t b0 = __ldg(off + v), b1 = __ldg(off + v + 1);
+    for (int64_t k = b0 + lane; k < b1; k += 32)
+      keys[k] = ((uint64_t)(uint32_t)__ldg(succ + k) << 32) | (uint64_t)v;
   }
 }
 
@@ -1002,7 +1090,8 @@ int union_step_impl(int64_t lo, int64_t hi, const int64_t *offsets, const int32_
                     const int32_t *finish_order, int64_t n_mega,
                     const int32_t *item_node, const int64_t *item_beg, int64_t n_items,
                     int64_t item_arcs, uint8_t *partial, unsigned long long *nch,
-                    unsigned long long *merged, int64_t hot_rows, cudaStream_t s) {
+                    unsigned long long *merged, int64_t hot_rows, const uint32_t *active,
+                    cudaStream_t s) {
   using Gm = Geo<LOGP>;
   if (hot_rows > 0) {
     cudaCtxResetPersistingL2Cache();    // lines of last iteration's buffer stop persisting
@@ -1011,28 +1100,28 @@ int union_step_impl(int64_t lo, int64_t hi, const int64_t *offsets, const int32_
   if (n_items > 0) {
     k_heavy_partial<LOGP><<<grid_for_warps(n_items), kThreads, 0, s>>>(
         offsets, succ, cur, chg_prev, item_node, item_beg, n_items, item_arcs, dense, partial,
-        merged);
+        merged, active);
     if (int e = check_launch("k_heavy_partial")) return e;
   }
   if (hi > lo) {
     const int64_t warps = (hi - lo + Gm::NPW - 1) / Gm::NPW + 1;   // capped at the resident set
     k_light<LOGP><<<grid_for_warps(warps), kThreads, 0, s>>>(
         offsets, succ, cur, nxt, chg_prev, chg_now, est, sum_dist, sum_recip, ec, lo, hi,
-        light_max_deg, dense, tf, nch, merged);
+        light_max_deg, dense, tf, nch, merged, active);
     if (int e = check_launch("k_light")) return e;
   }
   if (n_heavy > 0) {
     if (n_mega > 0) {
       k_heavy_finish<LOGP><<<grid_for_warps(n_mega), kThreads, 0, s>>>(
           heavy_nodes, item_first, finish_order, 0, n_mega, 1, partial, cur, nxt, chg_prev,
-          chg_now, est, sum_dist, sum_recip, ec, tf, nch);
+          chg_now, est, sum_dist, sum_recip, ec, tf, nch, active);
       if (int e = check_launch("k_heavy_finish(mega)")) return e;
     }
     if (n_heavy > n_mega)
       k_heavy_finish<LOGP><<<grid_for_warps((n_heavy - n_mega + Gm::NPW - 1) / Gm::NPW), kThreads,
                              0, s>>>(heavy_nodes, item_first, finish_order, n_mega, n_heavy, 0,
                                      partial, cur, nxt, chg_prev, chg_now, est, sum_dist,
-                                     sum_recip, ec, tf, nch);
+                                     sum_recip, ec, tf, nch, active);
     if (int e = check_launch("k_heavy_finish")) return e;
   }
   if (hot_rows > 0) set_hot_window(s, nullptr, 0);
@@ -1122,7 +1211,8 @@ int hb_union_step(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets,
                   const int32_t *item_node, const int64_t *item_beg,
                   int64_t n_items, int64_t item_arcs, uint8_t *partial, uint64_t *nch_out,
                   uint64_t *merged_out, int64_t hot_rows, double *disc, int64_t disc_stride,
-                  int n_disc, const double *disc_scale, int disc_div, void *stream) {
+                  int n_disc, const double *disc_scale, int disc_div, const uint32_t *active,
+                  void *stream) {
   if (n_disc < 0 || n_disc > kMaxDisc || (n_disc > 0 && (!disc || !disc_scale)))
     return set_err_msg("hb_union_step: bad discount arguments (at most 8 fused)");
   if (n < 0 || lo < 0 || hi > n || lo > hi || t < 1 || !nch_out)
@@ -1151,7 +1241,7 @@ int hb_union_step(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets,
                      sum_recip, tf, ec, dense, light_max_deg, heavy_nodes, item_first, n_heavy,
                      finish_order, n_mega, item_node, item_beg, n_items, item_arcs, partial,
                      reinterpret_cast<unsigned long long *>(nch_out),
-                     reinterpret_cast<unsigned long long *>(merged_out), hot_rows, s));
+                     reinterpret_cast<unsigned long long *>(merged_out), hot_rows, active, s));
   return 0;
 }
 
@@ -1237,6 +1327,55 @@ int hb_sort_rows(int64_t n, const int64_t *offsets, const int64_t *host_offsets,
   }
   if (result_in_alt) *result_in_alt = 0;
   return check_launch("hb_sort_rows");
+}
+
+int hb_mark_active(int64_t n, const int64_t *fwd_offsets, const int32_t *fwd_succ,
+                   const uint32_t *chg_prev, uint32_t *active, void *stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n <= 0) return 0;
+  cudaError_t e = cudaMemsetAsync(active, 0, sizeof(uint32_t) * (size_t)((n + 31) / 32), s);
+  if (e != cudaSuccess) return set_err("hb_mark_active memset", e);
+  k_mark_active<<<grid_for_warps((n + 31) / 32), kThreads, 0, s>>>(n, fwd_offsets, fwd_succ,
+                                                                   chg_prev, active);
+  return check_launch("k_mark_active");
+}
+
+int hb_forward_csr(int64_t n, const int64_t *offsets, const int32_t *succ, int64_t m,
+                   int64_t *fwd_offsets, int64_t *cursor, int32_t *fwd_dst, void *temp,
+                   uint64_t *temp_bytes, void *stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!temp_bytes) return set_err_msg("hb_forward_csr: temp_bytes");
+  size_t need = 0;
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, need, fwd_offsets, fwd_offsets,
+                                                n + 1, s);
+  if (e != cudaSuccess) return set_err("hb_forward_csr scan size", e);
+  if (!temp) {
+    *temp_bytes = need;
+    return 0;
+  }
+  if (n <= 0) return 0;
+  e = cudaMemsetAsync(fwd_offsets, 0, sizeof(int64_t) * (size_t)(n + 1), s);
+  if (e != cudaSuccess) return set_err("hb_forward_csr memset", e);
+  if (m > 0)
+    k_count_src<<<grid_for_threads(m), kThreads, 0, s>>>(
+        m, succ, reinterpret_cast<unsigned long long *>(fwd_offsets));
+  size_t bytes = *temp_bytes;
+  e = cub::DeviceScan::ExclusiveSum(temp, bytes, fwd_offsets, fwd_offsets, n + 1, s);
+  if (e != cudaSuccess) return set_err("hb_forward_csr scan", e);
+  e = cudaMemcpyAsync(cursor, fwd_offsets, sizeof(int64_t) * (size_t)n,
+                      cudaMemcpyDeviceToDevice, s);
+  if (e != cudaSuccess) return set_err("hb_forward_csr cursor", e);
+  k_scatter_fwd<<<grid_for_warps(n), kThreads, 0, s>>>(
+      n, offsets, succ, reinterpret_cast<unsigned long long *>(cursor), fwd_dst);
+  return check_launch("hb_forward_csr");
+}
+
+int hb_forward_keys(int64_t n, const int64_t *offsets, const int32_t *succ, uint64_t *keys,
+                    void *stream) {
+  if (n <= 0) return 0;
+  k_forward_keys<<<grid_for_warps(n), kThreads, 0, (cudaStream_t)stream>>>(n, offsets, succ,
+                                                                           keys);
+  return check_launch("k_forward_keys");
 }
 
 int hb_gen_rmat_keys(int scale, int64_t m, uint64_t thr_a, uint64_t thr_ab, uint64_t thr_abc,

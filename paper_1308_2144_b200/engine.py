@@ -37,6 +37,14 @@ from .centrality import BallObserver, CentralityAccumulator, fusable
 from .hll import CounterArray, CounterParams, estimator_constants, lc_table
 from .schedule import Schedule, build_schedule
 
+import os as _os
+
+# frontier mode when fewer than n / FRONTIER_DIV counters changed in the last iteration
+FRONTIER_DIV = int(_os.environ.get("HB_FRONTIER_DIV", "8"))
+# ... and only from the FRONTIER_AFTER-th consecutive such iteration on (building the
+# forward graph costs several full scans; short tails do not repay it)
+FRONTIER_AFTER = int(_os.environ.get("HB_FRONTIER_AFTER", "4"))
+
 CHECKPOINT_MAGIC = b"HBCK"
 CHECKPOINT_VERSION = 1
 
@@ -66,6 +74,7 @@ class HyperBallConfig:
     progress: IO[str] | None = None
     device: object | None = None        # B200: CUDA device (index, "cuda:k" or None = current)
     schedule: str = "auto"              # B200: "auto" | "identity" | "degree" (schedule.py)
+    frontier: bool = True               # B200: sparse iterations visit only the frontier
 
     def __post_init__(self) -> None:
         self.backend = _BACKEND_ALIASES.get(self.backend, self.backend)
@@ -315,6 +324,10 @@ class _Device:
         self.full_pass = True         # zero in-degree nodes may still need their copy
         self.launches = 0             # kernels launched by hb_union_step calls
         self.launches_at_last_step = 0
+        self.frontier = config.frontier
+        self.fwd = None               # forward CSR (internal ids), built on first use
+        self.active = None
+        self.last_nch = None
 
     def fresh(self, config: HyperBallConfig) -> "_Device":
         """A new device state for another run on the same graph and schedule."""
@@ -334,6 +347,9 @@ class _Device:
         other.full_pass = True
         other.launches = 0
         other.launches_at_last_step = 0
+        other.active = None
+        other.last_nch = None
+        other._sparse_run = 0
         return other
 
     # -- graph ---------------------------------------------------------------
@@ -404,8 +420,53 @@ class _Device:
         self.launches += 1 if self.n else 0
         self._seed_weights = w
 
+    def _forward(self):
+        """Forward CSR (out-neighbours, internal ids, rows unordered) for frontier marking;
+        built once by counting sort (hb_forward_csr)."""
+        if self.fwd is None:
+            import ctypes
+            s, L, st = self.sched, _lib.hb(), self.stream.cuda_stream
+            m = s.succ.numel()
+            off = torch.empty(self.n + 1, dtype=torch.int64, device=self.device)
+            cursor = torch.empty(max(self.n, 1), dtype=torch.int64, device=self.device)
+            dst = torch.empty(max(m, 1), dtype=torch.int32, device=self.device)
+            tb = ctypes.c_uint64(0)
+            _lib.check(L.hb_forward_csr(self.n, s.offsets.data_ptr(), s.succ.data_ptr(), m,
+                                        off.data_ptr(), cursor.data_ptr(), dst.data_ptr(),
+                                        None, ctypes.byref(tb), st), "hb_forward_csr(size)")
+            temp = torch.empty(max(int(tb.value), 1), dtype=torch.uint8, device=self.device)
+            _lib.check(L.hb_forward_csr(self.n, s.offsets.data_ptr(), s.succ.data_ptr(), m,
+                                        off.data_ptr(), cursor.data_ptr(), dst.data_ptr(),
+                                        temp.data_ptr(), ctypes.byref(tb), st),
+                       "hb_forward_csr")
+            del cursor, temp
+            self.fwd = (off, dst)
+            self.launches += 2
+        return self.fwd
+
+    def _frontier_ptr(self, dense: bool):
+        """Device bitmap of the nodes a sparse iteration can touch, or None (full scan).
+        Used when fewer than 1/FRONTIER_DIV of the nodes changed last iteration."""
+        sparse = (not dense and self.frontier and self.last_nch is not None and self.n > 0
+                  and self.last_nch * FRONTIER_DIV < self.n)
+        self._sparse_run = getattr(self, "_sparse_run", 0) + 1 if sparse else 0
+        # the forward graph costs about one atomic per arc (several full scans of the
+        # successor lists) to build: only for long sparse tails, or once it exists
+        if not sparse or (self.fwd is None and self._sparse_run < FRONTIER_AFTER
+                          and FRONTIER_DIV > 1):
+            return None
+        off, dst = self._forward()
+        if self.active is None:
+            self.active = torch.empty_like(self.chg_now)
+        _lib.check(_lib.hb().hb_mark_active(self.n, off.data_ptr(), dst.data_ptr(),
+                                            self.chg_prev.data_ptr(), self.active.data_ptr(),
+                                            self.stream.cuda_stream), "hb_mark_active")
+        self.launches += 1
+        return self.active.data_ptr()
+
     def union_step(self, t: int, dense: bool, sums: _DeviceSums | None) -> int:
         s = self.sched
+        active = self._frontier_ptr(dense)
         light_hi = s.light_hi if self.full_pass else s.light_hi_steady
         sd = sums.sum_dist.data_ptr() if sums is not None else None
         sr = sums.sum_recip.data_ptr() if sums is not None else None
@@ -418,10 +479,11 @@ class _Device:
             s.heavy_nodes.data_ptr(), s.item_first.data_ptr(), s.n_heavy,
             s.finish_order.data_ptr(), s.n_mega, s.item_node.data_ptr(), s.item_beg.data_ptr(), s.n_items, s.item_arcs,
             s.partial.data_ptr(), self.counts.data_ptr(), self.counts.data_ptr() + 8,
-            s.hot_rows, *dargs, self.stream.cuda_stream), "hb_union_step")
+            s.hot_rows, *dargs, active, self.stream.cuda_stream), "hb_union_step")
         self.launches += (light_hi > s.light_lo) + (s.n_items > 0) + (s.n_heavy > 0)
         self.launches_at_last_step = self.launches
         nch, merged = (int(x) for x in self.counts.cpu())
+        self.last_nch = nch
         self.last_merged = merged
         self.merged_total += merged
         return nch

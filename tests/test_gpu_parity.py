@@ -240,3 +240,35 @@ def test_run_multi_matches_independent_runs():
     mean, std = hb.multi_run_aggregate([hb.finalize_harmonic(a) for _, a in res])
     stack = np.vstack([hb.finalize_harmonic(a) for _, a in res])
     assert bits_equal(mean, stack.mean(axis=0)) and bits_equal(std, stack.std(axis=0, ddof=1))
+
+
+@pytest.mark.parametrize("mode", ["always", "off"])
+@pytest.mark.parametrize("key", ["sparse2000_b4_s42_w5", "disc14_b4_s42_w5", "rmat12_b7_s42_w5",
+                                 "islands400_b11_s3_w5", "config1_b6_s42_w5", "web14_b8_s42_w5"])
+def test_frontier_mode_matches_reference(key, mode, monkeypatch):
+    """Sparse iterations visiting only chg_prev | out-neighbours(chg_prev) (hb_mark_active)
+    give the reference's bits; 'always' uses the frontier whenever fewer than n counters
+    changed, 'off' never."""
+    from paper_1308_2144_b200 import engine as E
+    monkeypatch.setattr(E, "FRONTIER_DIV", 1)
+    case = next(c for c in CASES if c["key"] == key)
+    off, suc = golden_graph(case)
+    g = hb.CsrGraph(off, suc)
+    cfg = hb.HyperBallConfig(params=hb.CounterParams(b=case["b"], seed=int(case["seed"])),
+                             frontier=(mode == "always"))
+    acc = hb.CentralityAccumulator(g.n)
+    st = hb.initialize(g, cfg)
+    regs, merged = [], []
+    while True:
+        nch = hb.iterate(g, st, [acc])
+        regs.append(sha(st.register_matrix()))
+        merged.append(st._dev.last_merged)
+        if nch == 0:
+            break
+    acc.on_converged(st.est)
+    assert st.t == case["t"]
+    assert regs == case["reg_digests"][1:]
+    _, arrays = golden()
+    assert bits_equal(hb.finalize_lin(acc), arrays[f"{key}/lin"])
+    if mode == "always":
+        assert st._dev.fwd is not None
