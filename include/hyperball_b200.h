@@ -31,7 +31,7 @@
  *   hb_gen_rmat_keys / hb_keys_to_csr
  *                     graph.py:52-80 (from_edges: sort, dedup, CSR) + 145-155 (transpose),
  *                     for the synthetic R-MAT configs, on the device
- *   hb_forward_keys / hb_mark_active
+ *   hb_forward_csr / hb_mark_active
  *                     frontier of a sparse iteration (no reference counterpart: the
  *                     reference scans every node's successor list, _kernels.py:82-87)
  *   hb_hash_items     hll.py:79-88 hash_items (device twin, used by tests)
@@ -166,12 +166,8 @@ int hb_sort_rows(int64_t n, const int64_t *offsets, const int64_t *host_offsets,
                  void *stream);
 
 /* Frontier mode for sparse iterations.
- * hb_forward_keys: keys[k] = succ[k] << 32 | row(k) for the transpose CSR (offsets, succ);
- *   hb_keys_to_csr on them yields the forward graph (out-neighbours, internal ids).
  * hb_mark_active: active = chg_prev | out-neighbours(chg_prev) (device bitmaps over n
  *   nodes), the only nodes the source-skip rule can touch this iteration. */
-int hb_forward_keys(int64_t n, const int64_t *offsets, const int32_t *succ, uint64_t *keys,
-                    void *stream);
 /* hb_forward_csr: the forward graph by counting sort -- fwd_offsets (device int64 [n+1]),
  *   cursor (device int64 [n], scratch), fwd_dst (device int32 [m]); rows unordered.
  *   temp == NULL queries *temp_bytes (scan scratch). */

@@ -44,7 +44,6 @@ HB_SIGNATURES = {
                              _vp, _i64, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _i64,
                              _vp, _i64, _int, _vp, _int, _vp, _vp]),
     "hb_mark_active": (_int, [_i64, _vp, _vp, _vp, _vp, _vp]),
-    "hb_forward_keys": (_int, [_i64, _vp, _vp, _vp, _vp]),
     "hb_forward_csr": (_int, [_i64, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "hb_finalize": (_int, [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "hb_gather_changed": (_int, [_i64, _i64, _vp, _vp, _int, _vp, _vp, _vp, _vp]),

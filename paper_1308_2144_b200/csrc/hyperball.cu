@@ -362,31 +362,6 @@ __device__ __forceinline__ void l2_prefetch(const void *p, int64_t bytes) {
                : "memory");
 }
 
-// Smallest v in [lo, hi] with off[v] + v >= target (f(hi) >= target), by a warp-wide
-// 32-ary search: every lane probes one point per round.
-__device__ __forceinline__ int64_t warp_lower_bound(const int64_t *__restrict__ off, int64_t lo,
-                                                    int64_t hi, int64_t target, int lane) {
-  int64_t L = lo, R = hi;
-  while (R > L) {
-    const int64_t step = (R - L + 31) / 32;
-    const int64_t probe = L + (int64_t)lane * step;
-    const bool ge = probe >= R || (__ldg(off + probe) + probe >= target);
-    const unsigned b = __ballot_sync(0xffffffffu, ge);
-    if (b == 0) {
-      L = L + 31 * step + 1;
-    } else {
-      const int f = __ffs(b) - 1;
-      if (f == 0) {
-        R = L;
-      } else {
-        R = L + (int64_t)f * step;
-        L = L + (int64_t)(f - 1) * step + 1;
-      }
-    }
-  }
-  return L;
-}
-
 constexpr int kLookRounds = 4;    // L2 prefetch distance of the light kernel, in warp rounds
 // warp rounds per grid-stride chunk of the light kernel (resident warps x chunk nodes is
 // the id window the GPU sweeps): 16 for p >= 256, 4 below (measured on configs 3-5)
@@ -908,20 +883,6 @@ __global__ void k_scatter_fwd(int64_t n, const int64_t *__restrict__ off,
   }
 }
 
-// keys (src << 32 | dst) of every arc of the transpose CSR: sorting them gives the forward
-// graph (hb_keys_to_csr).  Warp per row.
-__global__ void k_forward_keys(int64_t n, const int64_t *__restrict__ off,
-                               const int32_t *__restrict__ succ, uint64_t *__restrict__ keys) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t v = warp; v < n; v += nwarps) {
-    const int64_t b0 = __ldg(off + v), b1 = __ldg(off + v + 1);
-    for (int64_t k = b0 + lane; k < b1; k += 32)
-      keys[k] = ((uint64_t)(uint32_t)__ldg(succ + k) << 32) | (uint64_t)v;
-  }
-}
-
 // ---- GPU graph build ---------------------------------------------
 // Counter-based R-MAT arcs, bit-identical to graphgen.c's rmat_fn (same splitmix chain,
 // same 32-bit quadrant thresholds), packed as (dst << 32 | src) keys of the TRANSPOSE;
@@ -1368,14 +1329,6 @@ int hb_forward_csr(int64_t n, const int64_t *offsets, const int32_t *succ, int64
   k_scatter_fwd<<<grid_for_warps(n), kThreads, 0, s>>>(
       n, offsets, succ, reinterpret_cast<unsigned long long *>(cursor), fwd_dst);
   return check_launch("hb_forward_csr");
-}
-
-int hb_forward_keys(int64_t n, const int64_t *offsets, const int32_t *succ, uint64_t *keys,
-                    void *stream) {
-  if (n <= 0) return 0;
-  k_forward_keys<<<grid_for_warps(n), kThreads, 0, (cudaStream_t)stream>>>(n, offsets, succ,
-                                                                           keys);
-  return check_launch("k_forward_keys");
 }
 
 int hb_gen_rmat_keys(int scale, int64_t m, uint64_t thr_a, uint64_t thr_ab, uint64_t thr_abc,
