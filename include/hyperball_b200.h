@@ -135,17 +135,19 @@ int hb_finalize(int64_t n, const int32_t *rank, const double *sum_dist, const do
 
 /* Multi-GPU exchange.
  * hb_gather_changed: for every v in [lo, hi) with chg_bits bit v set, append v to ids_out
- *   and rows[v] (p = 2^b bytes) to rows_out; *count_out (device uint64, zeroed by the
- *   call) receives the number appended.  Order is unspecified.
- * hb_scatter_rows: dst[ids[i]] = rows[i] for i < k and set bit ids[i] of chg_bits
- *   (chg_bits may be NULL).
+ *   and rows[v] to rows_out -- p = 2^b bytes per row, or hb_packed_row_bytes(b) bytes of
+ *   5-bit fields when packed != 0 (only valid for register_width <= 5); *count_out
+ *   (device uint64, zeroed by the call) receives the number appended.  Order unspecified.
+ * hb_scatter_rows: dst[ids[i]] = rows[i] (unpacked when packed != 0) for i < k and set bit
+ *   ids[i] of chg_bits (chg_bits may be NULL).
  * hb_refresh_rows: dst[v] = src[v] for every v in [0, n) outside [lo, hi) whose bit is
  *   set in bits (keeps the lazy double buffer of rows owned by other ranks). */
+int hb_packed_row_bytes(int b);
 int hb_gather_changed(int64_t lo, int64_t hi, const uint32_t *chg_bits, const uint8_t *rows,
-                      int b, int32_t *ids_out, uint8_t *rows_out, uint64_t *count_out,
-                      void *stream);
-int hb_scatter_rows(int64_t k, const int32_t *ids, const uint8_t *rows, int b, uint8_t *dst,
-                    uint32_t *chg_bits, void *stream);
+                      int b, int packed, int32_t *ids_out, uint8_t *rows_out,
+                      uint64_t *count_out, void *stream);
+int hb_scatter_rows(int64_t k, const int32_t *ids, const uint8_t *rows, int b, int packed,
+                    uint8_t *dst, uint32_t *chg_bits, void *stream);
 int hb_refresh_rows(int64_t n, int64_t lo, int64_t hi, const uint32_t *bits, const uint8_t *src,
                     uint8_t *dst, int b, void *stream);
 

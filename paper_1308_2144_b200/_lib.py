@@ -46,8 +46,9 @@ HB_SIGNATURES = {
     "hb_mark_active": (_int, [_i64, _vp, _vp, _vp, _vp, _vp]),
     "hb_forward_csr": (_int, [_i64, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "hb_finalize": (_int, [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
-    "hb_gather_changed": (_int, [_i64, _i64, _vp, _vp, _int, _vp, _vp, _vp, _vp]),
-    "hb_scatter_rows": (_int, [_i64, _vp, _vp, _int, _vp, _vp, _vp]),
+    "hb_packed_row_bytes": (_int, [_int]),
+    "hb_gather_changed": (_int, [_i64, _i64, _vp, _vp, _int, _int, _vp, _vp, _vp, _vp]),
+    "hb_scatter_rows": (_int, [_i64, _vp, _vp, _int, _int, _vp, _vp, _vp]),
     "hb_refresh_rows": (_int, [_i64, _i64, _i64, _vp, _vp, _vp, _int, _vp]),
     "hb_relabel_csr": (_int, [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "hb_sort_rows": (_int, [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),

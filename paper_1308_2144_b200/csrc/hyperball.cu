@@ -743,14 +743,69 @@ k_estimate_rows(const uint8_t *__restrict__ regs, int64_t lo, int64_t hi, EstCon
 // Pack the rows of [lo, hi) whose chg_now bit is set: ids_out[k] = v, rows_out[k] = nxt[v].
 // One warp per bitmap word; positions by one atomicAdd per word (order is irrelevant:
 // receivers scatter by id).
+// 5-bit exchange format (register_width <= 5: every register fits 5 bits): 32 registers
+// -> 5 words, a p-register row -> packed_row_bytes(p) bytes (p = 16: 12 bytes, p = 256:
+// 160) -- 37.5% fewer NVLink bytes than the byte rows for p >= 32.
+__host__ __device__ __forceinline__ int packed_row_bytes(int p) { return ((p * 5 + 31) / 32) * 4; }
+
+__device__ __forceinline__ void pack_row5(const uint8_t *__restrict__ row, int p,
+                                          uint32_t *__restrict__ out) {
+  for (int g = 0; g < p; g += 32) {
+    uint32_t w[5] = {0, 0, 0, 0, 0};
+    const int cnt = p - g < 32 ? p - g : 32;
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      if (h * 16 >= cnt) break;
+      const uint4 q = __ldg(reinterpret_cast<const uint4 *>(row + g + 16 * h));
+      const uint32_t qs[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int i = 0; i < 16; i++) {
+        const int r = 16 * h + i, bit = 5 * r;
+        const uint32_t val = (qs[i >> 2] >> (8 * (i & 3))) & 31u;
+        w[bit >> 5] |= val << (bit & 31);
+        if ((bit & 31) > 27) w[(bit >> 5) + 1] |= val >> (32 - (bit & 31));
+      }
+    }
+    const int words = (cnt * 5 + 31) / 32;
+    for (int i = 0; i < words; i++) out[(g / 32) * 5 + i] = w[i];
+  }
+}
+
+__device__ __forceinline__ void unpack_row5(const uint32_t *__restrict__ in, int p,
+                                            uint8_t *__restrict__ row) {
+  for (int g = 0; g < p; g += 32) {
+    const int cnt = p - g < 32 ? p - g : 32;
+    const int words = (cnt * 5 + 31) / 32;
+    uint32_t w[6] = {0, 0, 0, 0, 0, 0};
+    for (int i = 0; i < words; i++) w[i] = __ldg(in + (g / 32) * 5 + i);
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      if (h * 16 >= cnt) break;
+      uint32_t qs[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int i = 0; i < 16; i++) {
+        const int r = 16 * h + i, bit = 5 * r;
+        uint32_t val = w[bit >> 5] >> (bit & 31);
+        if ((bit & 31) > 27) val |= w[(bit >> 5) + 1] << (32 - (bit & 31));
+        qs[i >> 2] |= (val & 31u) << (8 * (i & 3));
+      }
+      *reinterpret_cast<uint4 *>(row + g + 16 * h) = make_uint4(qs[0], qs[1], qs[2], qs[3]);
+    }
+  }
+}
+
+// Pack the rows of [lo, hi) whose chg_now bit is set: ids_out[k] = v, rows_out[k] = nxt[v]
+// (byte rows, or 5-bit packed rows when packed != 0).  One warp per bitmap word;
+// positions by one atomicAdd per word (order is irrelevant: receivers scatter by id).
 __global__ void k_gather_changed(int64_t lo, int64_t hi, const uint32_t *__restrict__ bits,
-                                 const uint8_t *__restrict__ src, int p,
+                                 const uint8_t *__restrict__ src, int p, int packed,
                                  int32_t *__restrict__ ids_out, uint8_t *__restrict__ rows_out,
                                  unsigned long long *__restrict__ count) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t w0 = lo >> 5, w1 = (hi + 31) >> 5;
+  const int rb = packed ? packed_row_bytes(p) : p;
   for (int64_t w = w0 + warp; w < w1; w += nwarps) {
     uint32_t m = __ldg(bits + w);
     const int64_t v0 = w << 5;
@@ -765,17 +820,34 @@ __global__ void k_gather_changed(int64_t lo, int64_t hi, const uint32_t *__restr
       const int bit = __fns(m, 0, lane + 1);
       const int64_t v = v0 + bit;
       ids_out[base + lane] = (int32_t)v;
-      const uint4 *s4 = reinterpret_cast<const uint4 *>(src + (size_t)v * p);
-      uint4 *d4 = reinterpret_cast<uint4 *>(rows_out + (size_t)(base + lane) * p);
-      for (int q = 0; q < p / 16; q++) d4[q] = __ldg(s4 + q);
+      uint8_t *dst = rows_out + (size_t)(base + lane) * rb;
+      if (packed) {
+        pack_row5(src + (size_t)v * p, p, reinterpret_cast<uint32_t *>(dst));
+      } else {
+        const uint4 *s4 = reinterpret_cast<const uint4 *>(src + (size_t)v * p);
+        uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+        for (int q = 0; q < p / 16; q++) d4[q] = __ldg(s4 + q);
+      }
     }
   }
 }
 
-// Apply received rows: dst[ids[k]] = rows[k] and set their change bits.
+// Apply received rows: dst[ids[k]] = rows[k] (byte rows: thread per 16-byte chunk; 5-bit
+// packed rows: thread per row) and set their change bits.
 __global__ void k_scatter_rows(int64_t k, const int32_t *__restrict__ ids,
-                               const uint8_t *__restrict__ rows, int p,
+                               const uint8_t *__restrict__ rows, int p, int packed,
                                uint8_t *__restrict__ dst, uint32_t *__restrict__ bits) {
+  if (packed) {
+    const int rb = packed_row_bytes(p);
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < k;
+         r += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t v = __ldg(ids + r);
+      unpack_row5(reinterpret_cast<const uint32_t *>(rows + (size_t)r * rb), p,
+                  dst + (size_t)v * p);
+      if (bits) atomicOr(bits + (v >> 5), 1u << (v & 31));
+    }
+    return;
+  }
   const int64_t chunks = p / 16;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < k * chunks;
        t += (int64_t)gridDim.x * blockDim.x) {
@@ -1218,24 +1290,26 @@ int hb_finalize(int64_t n, const int32_t *rank, const double *sum_dist, const do
   return check_launch("k_finalize");
 }
 
+int hb_packed_row_bytes(int b) { return packed_row_bytes(1 << b); }
+
 int hb_gather_changed(int64_t lo, int64_t hi, const uint32_t *chg_bits, const uint8_t *rows,
-                      int b, int32_t *ids_out, uint8_t *rows_out, uint64_t *count_out,
-                      void *stream) {
+                      int b, int packed, int32_t *ids_out, uint8_t *rows_out,
+                      uint64_t *count_out, void *stream) {
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e = cudaMemsetAsync(count_out, 0, sizeof(uint64_t), s);
   if (e != cudaSuccess) return set_err("hb_gather_changed memset", e);
   if (hi <= lo) return 0;
   k_gather_changed<<<grid_for_warps(((hi + 31) >> 5) - (lo >> 5)), kThreads, 0, s>>>(
-      lo, hi, chg_bits, rows, 1 << b, ids_out, rows_out,
+      lo, hi, chg_bits, rows, 1 << b, packed, ids_out, rows_out,
       reinterpret_cast<unsigned long long *>(count_out));
   return check_launch("k_gather_changed");
 }
 
-int hb_scatter_rows(int64_t k, const int32_t *ids, const uint8_t *rows, int b, uint8_t *dst,
-                    uint32_t *chg_bits, void *stream) {
+int hb_scatter_rows(int64_t k, const int32_t *ids, const uint8_t *rows, int b, int packed,
+                    uint8_t *dst, uint32_t *chg_bits, void *stream) {
   if (k <= 0) return 0;
-  k_scatter_rows<<<grid_for_threads(k * ((1 << b) / 16)), kThreads, 0, (cudaStream_t)stream>>>(
-      k, ids, rows, 1 << b, dst, chg_bits);
+  k_scatter_rows<<<grid_for_threads(packed ? k : k * ((1 << b) / 16)), kThreads, 0,
+                   (cudaStream_t)stream>>>(k, ids, rows, 1 << b, packed, dst, chg_bits);
   return check_launch("k_scatter_rows");
 }
 

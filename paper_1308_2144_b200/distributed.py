@@ -96,7 +96,7 @@ class TorchComm:
 class CudaRankState:
     """One rank's device state: full register replica, owned range [lo, hi)."""
 
-    def __init__(self, g, config: HyperBallConfig, world: int, rank: int):
+    def __init__(self, g, config: HyperBallConfig, world: int, rank: int, packed: bool = True):
         n = (g.offsets.numel() if isinstance(g.offsets, torch.Tensor)
              else np.asarray(g.offsets).shape[0]) - 1
         w = _weights_array(config.weights, n)
@@ -108,8 +108,11 @@ class CudaRankState:
         self.lo, self.hi = self.dev.sched.lo, self.dev.sched.hi
         cap = max(self.hi - self.lo, 1)
         dv = self.dev.device
+        # rows travel 5-bit packed when every register fits (register_width <= 5)
+        self.packed = int(config.params.register_width <= 5 and packed)
+        self.row_bytes = (_lib.hb().hb_packed_row_bytes(self.b) if self.packed else self.p)
         self.ids_buf = torch.empty(cap, dtype=torch.int32, device=dv)
-        self.rows_buf = torch.empty((cap, self.p), dtype=torch.uint8, device=dv)
+        self.rows_buf = torch.empty((cap, self.row_bytes), dtype=torch.uint8, device=dv)
         self.count = torch.zeros(1, dtype=torch.int64, device=dv)
         self.sums = None
 
@@ -135,7 +138,7 @@ class CudaRankState:
     def gather_changed(self):
         d = self.dev
         _lib.check(_lib.hb().hb_gather_changed(self.lo, self.hi, d.chg_now.data_ptr(),
-                                               d.nxt.data_ptr(), self.b,
+                                               d.nxt.data_ptr(), self.b, self.packed,
                                                self.ids_buf.data_ptr(),
                                                self.rows_buf.data_ptr(),
                                                self.count.data_ptr(), d.stream.cuda_stream),
@@ -150,7 +153,8 @@ class CudaRankState:
         if k == 0:
             return
         _lib.check(_lib.hb().hb_scatter_rows(k, ids.data_ptr(), rows.contiguous().data_ptr(),
-                                             self.b, d.nxt.data_ptr(), d.chg_now.data_ptr(),
+                                             self.b, self.packed, d.nxt.data_ptr(),
+                                             d.chg_now.data_ptr(),
                                              d.stream.cuda_stream), "hb_scatter_rows")
         d.launches += 1
 
@@ -243,11 +247,12 @@ def run_distributed(g, config: HyperBallConfig, observers: Iterable = (), group=
     return res
 
 
-def run_simulated(g, config: HyperBallConfig, world: int, observers: Iterable = ()):
+def run_simulated(g, config: HyperBallConfig, world: int, observers: Iterable = (),
+                  packed: bool = True):
     """All `world` ranks in one process on one GPU, phase by phase (no kernel waits on
     another rank).  Exercises the partition and every exchange kernel; results must be
     bit-identical to the single-GPU run."""
-    states = [CudaRankState(g, config, world, r) for r in range(world)]
+    states = [CudaRankState(g, config, world, r, packed) for r in range(world)]
     observers = list(observers)
     accs = [o for o in observers if fusable(o, states[0].n)]
     if accs:

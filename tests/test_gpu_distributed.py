@@ -24,18 +24,19 @@ def sha(a):
     return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
 
 
+@pytest.mark.parametrize("packed", [True, False])
 @pytest.mark.parametrize("world", [2, 3, 8])
 @pytest.mark.parametrize("schedule", ["identity", "degree"])
 @pytest.mark.parametrize("key", ["random300_b6_s42_w5", "disc14_b4_s42_w5", "rmat12_b7_s42_w5",
                                  "config1_b6_s42_w5", "sparse2000_b4_s42_w5"])
-def test_simulated_ranks_match_reference(key, world, schedule):
+def test_simulated_ranks_match_reference(key, world, schedule, packed):
     case = CASES[key]
     off, suc = golden_graph(case)
     g = hb.CsrGraph(off, suc)
     acc = hb.CentralityAccumulator(g.n)
     cfg = hb.HyperBallConfig(params=hb.CounterParams(b=case["b"], seed=int(case["seed"])),
                              schedule=schedule)
-    res = run_simulated(g, cfg, world, [acc])
+    res = run_simulated(g, cfg, world, [acc], packed=packed)
     assert res.t == case["t"]
     for regs in res.registers:        # every replica holds the final registers
         assert sha(regs) == case["reg_digests"][-1]
