@@ -249,13 +249,17 @@ def run_b200(args):
     # ---------------------------------------------------------------- device-resident step
     cfg = hb.HyperBallConfig(params=params, device=local)
     acc = hb.CentralityAccumulator(n)
-    rs = comm = st = None
+    rs = comm = st = symm = None
     if world > 1:
         from paper_1308_2144_b200.distributed import CudaRankState, TorchComm
         comm = TorchComm()
         rs = CudaRankState(g, cfg, world, rank)
         sums = rs.bind_sums()
         dev = rs.dev
+        symm = None
+        if args.exchange == "push":
+            from paper_1308_2144_b200.distributed import _ptr_array, setup_push
+            symm = setup_push(rs)
     else:
         from paper_1308_2144_b200.engine import _bind_sums
         st = hb.initialize(g, cfg)
@@ -266,22 +270,33 @@ def run_b200(args):
     L = _lib.hb()
 
     def step(ev0=None, ev1=None):
-        """One dense iteration: union kernels (+ exchange of changed rows when N > 1)."""
+        """One dense iteration: union kernels (+ exchange of changed rows when N > 1: fused
+        into the union epilogue with --exchange push, else pack / all-gather / scatter)."""
+        npeer, pn, pc, clear = 0, None, None, 1
+        if symm is not None:
+            pnl, pcl = symm.peer_pointers(dev)
+            npeer, pn, pc, clear = len(pnl), _ptr_array(pnl), _ptr_array(pcl), 0
         if ev0 is not None:
             ev0.record(stream)
         _lib.check(L.hb_union_step(
             n, s.light_lo, s.light_hi, s.offsets.data_ptr(), s.succ.data_ptr(),
             dev.cur.data_ptr(), dev.nxt.data_ptr(), dev.chg_prev.data_ptr(),
-            dev.chg_now.data_ptr(), 1, dev.est.data_ptr(), sums.sum_dist.data_ptr(),
+            dev.chg_now.data_ptr(), clear, dev.est.data_ptr(), sums.sum_dist.data_ptr(),
             sums.sum_recip.data_ptr(), 1, dev.lc.data_ptr(), dev.alpha_p2, dev.lc_cut, b, 1,
             s.light_max_deg, s.heavy_nodes.data_ptr(), s.item_first.data_ptr(), s.n_heavy,
             s.finish_order.data_ptr(), s.n_mega, s.item_node.data_ptr(), s.item_beg.data_ptr(), s.n_items, s.item_arcs,
             s.partial.data_ptr(), dev.counts.data_ptr(), dev.counts.data_ptr() + 8,
-            s.hot_rows, None, 0, 0, None, 0, None, stream.cuda_stream), "hb_union_step")
+            s.hot_rows, None, 0, 0, None, 0, None, npeer, pn, pc, stream.cuda_stream),
+            "hb_union_step")
         if ev1 is not None:
             ev1.record(stream)
         nch, merged = (int(x) for x in dev.counts.cpu())   # the per-iteration termination read
-        if rs is not None:
+        if symm is not None:
+            # the all-reduce of the changed count is the barrier after which every peer's
+            # pushed rows are visible; chg_prev stays all-ones so each step is iteration 1
+            tot = torch.tensor([nch], dtype=torch.int64, device=dev.device)
+            dist.all_reduce(tot)
+        elif rs is not None:
             rs.refresh_unowned()
             ids, rows, k = rs.gather_changed()
             _, parts = comm.exchange(ids, rows, k)
@@ -290,7 +305,7 @@ def run_b200(args):
         return nch, merged
 
     launches_per_step = (s.light_hi > s.light_lo) + (s.n_items > 0) + (s.n_heavy > 0)
-    if world > 1:
+    if world > 1 and symm is None:
         launches_per_step += 2 + (world - 1)   # refresh, gather, one scatter per peer
     for _ in range(args.warmup):
         step()
@@ -362,7 +377,7 @@ def run_b200(args):
             cfg2 = hb.HyperBallConfig(params=params, device=local)
             if world > 1:
                 from paper_1308_2144_b200.distributed import run_distributed
-                st2 = run_distributed(gp, cfg2, [acc2])
+                st2 = run_distributed(gp, cfg2, [acc2], exchange=args.exchange)
             else:
                 st2 = hb.run(gp, cfg2, [acc2])
             har = hb.finalize_harmonic(acc2)
@@ -419,7 +434,8 @@ def run_b200(args):
                                "fused harmonic/closeness/Lin accumulate",
                        "l2": "inputs larger than L2 (%.2f GB of registers), no flush"
                              % (n * p / 1e9),
-                       "parallelism": f"node-partition x{world}" if world > 1 else "single GPU"},
+                       "parallelism": (f"node-partition x{world}, {args.exchange} exchange"
+                                       if world > 1 else "single GPU")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": B, "kernel_ms": k_ms,
@@ -444,6 +460,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--config", default="config4")
+    ap.add_argument("--exchange", choices=["push", "allgather"], default="push",
+                    help="N > 1: fused push over symmetric memory, or all-gather")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-warmup", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")

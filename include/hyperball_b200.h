@@ -109,7 +109,12 @@ int hb_estimate_rows(const uint8_t *regs, int64_t lo, int64_t hi, int b,
  * gets disc[k][v] += (bit k of disc_div) ? delta / t : disc_scale[k] * delta for every
  * changed v (n_disc <= 8); disc_scale is a HOST array of the n_disc factors f_k(t) for this step.
  * active (device uint32 bitmap, may be NULL): frontier mode -- only nodes whose bit is set
- * are visited (hb_mark_active); NULL visits every node. */
+ * are visited (hb_mark_active); NULL visits every node.  Fused push (multi-GPU, DESIGN.md
+ * section 6): n_peers > 0 (at most 7) additionally stores every written nxt row into
+ * peer_nxt[q] (device addresses of the peers' nxt replicas, same layout) and sets its
+ * change bit in peer_chg[q]; peer_nxt / peer_chg are HOST arrays of those pointers.  The
+ * caller must not clear chg_now (clear_chg_now = 0) while peers may be pushing, and must
+ * barrier all ranks before reading what the peers pushed. */
 int hb_union_step(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets,
                   const int32_t *succ, const uint8_t *cur, uint8_t *nxt,
                   const uint32_t *chg_prev, uint32_t *chg_now, int clear_chg_now,
@@ -121,6 +126,7 @@ int hb_union_step(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets,
                   int64_t n_items, int64_t item_arcs, uint8_t *partial, uint64_t *nch_out,
                   uint64_t *merged_out, int64_t hot_rows, double *disc, int64_t disc_stride,
                   int n_disc, const double *disc_scale, int disc_div, const uint32_t *active,
+                  int n_peers, uint8_t *const *peer_nxt, uint32_t *const *peer_chg,
                   void *stream);
 
 /* Finalizers (centrality.py:153-171) over device sums in internal order, written in

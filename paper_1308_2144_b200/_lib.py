@@ -42,7 +42,7 @@ HB_SIGNATURES = {
     "hb_union_step": (_int, [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _int, _vp, _vp,
                              _vp, _i64, _vp, _dbl, _dbl, _int, _int, _i64, _vp, _vp, _i64,
                              _vp, _i64, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _i64,
-                             _vp, _i64, _int, _vp, _int, _vp, _vp]),
+                             _vp, _i64, _int, _vp, _int, _vp, _int, _vp, _vp, _vp]),
     "hb_mark_active": (_int, [_i64, _vp, _vp, _vp, _vp, _vp]),
     "hb_forward_csr": (_int, [_i64, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "hb_finalize": (_int, [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),

@@ -209,6 +209,18 @@ __device__ double estimate_row_thread(const uint8_t *row, const EstConst &ec) {
   return finish_estimate(s, zeros, ec);
 }
 
+// Fused push (multi-GPU): every row a rank writes into its own nxt
+// buffer (the lazy-write set chg_prev | chg_now) is also stored straight into the nxt
+// replica of every peer over NVLink, and its change bit OR-ed into every peer's chg_now,
+// so no separate all-gather runs after the union.  Pointers are peer device addresses
+// (symmetric-memory / IPC mappings); n == 0 disables.
+constexpr int kMaxPeers = 7;
+struct Peers {
+  int n;
+  uint8_t *nxt[kMaxPeers];
+  uint32_t *chg[kMaxPeers];
+};
+
 // numpy.maximum(x, 0.0) (centrality.py:134)
 __device__ __forceinline__ double np_max0(double x) { return (x >= 0.0 || x != x) ? x : 0.0; }
 
@@ -218,8 +230,8 @@ __device__ __forceinline__ double np_max0(double x) { return (x >= 0.0 || x != x
 // warp calls it (groups with nothing to do pass doit = false), so all collectives use the
 // full mask and no group's divergence serialises the others.  Returns the group's changed
 // flag.
-template <int LOGP>
-__device__ __forceinline__ bool finish_node(bool doit, int64_t v,
+template <int LOGP, bool PUSH>
+__device__ __forceinline__ bool finish_node(const Peers &peers, bool doit, int64_t v,
                                             const uint4 (&acc)[Geo<LOGP>::CPL],
                                             const uint4 (&pre)[Geo<LOGP>::CPL], bool have_pre,
                                             bool self_chg, int grp, int gl,
@@ -247,6 +259,14 @@ __device__ __forceinline__ bool finish_node(bool doit, int64_t v,
 #pragma unroll
     for (int c = 0; c < Gm::CPL; c++)
       *reinterpret_cast<uint4 *>(nrow + 16 * (c * Gm::G + gl)) = nw[c];
+    if constexpr (PUSH) {
+      for (int q = 0; q < peers.n; q++) {
+        uint8_t *prow = peers.nxt[q] + (size_t)v * Gm::P;
+#pragma unroll
+        for (int c = 0; c < Gm::CPL; c++)
+          *reinterpret_cast<uint4 *>(prow + 16 * (c * Gm::G + gl)) = nw[c];
+      }
+    }
   }
   if (bal != 0u) {   // warp-uniform
     // sum_j 2^-M[j] as exact fp64 partial sums (every M <= 31 here: at most 36 significant
@@ -374,7 +394,7 @@ __host__ __device__ constexpr int chunk_rounds() { return LOGP >= 8 ? 16 : 4; }
 // prefetches them into L2 kLookRounds rounds ahead, leaving the random source-row
 // gather as the only exposed memory latency of a round.
 // _kernels.py:67-114 restated with the source-skip rule.
-template <int LOGP>
+template <int LOGP, bool PUSH>
 __global__ void __launch_bounds__(kThreads, Batch<LOGP>::MINB)
 k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
         const uint8_t *__restrict__ cur, uint8_t *__restrict__ nxt,
@@ -382,7 +402,7 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
         double *__restrict__ est, double *__restrict__ sum_dist, double *__restrict__ sum_recip,
         EstConst ec, int64_t lo, int64_t hi, int64_t max_deg, int dense, double tf,
         unsigned long long *__restrict__ nch_out, unsigned long long *__restrict__ merged_out,
-        const uint32_t *__restrict__ active) {
+        const uint32_t *__restrict__ active, Peers peers) {
   using Gm = Geo<LOGP>;
   using B = Batch<LOGP>;
   __shared__ int32_t sids[kThreads / 32][B::WARP_IDS];
@@ -523,7 +543,7 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
       __syncwarp();
     }
     my_merged += (gl == 0) ? (uint32_t)total : 0u;
-    const bool changed = finish_node<LOGP>(valid && (total > 0 || self_chg), v, acc, self, pre,
+    const bool changed = finish_node<LOGP, PUSH>(peers, valid && (total > 0 || self_chg), v, acc, self, pre,
                                            self_chg, grp, gl, cur, nxt, est, sum_dist,
                                            sum_recip, ec, tf, pre ? vals : nullptr);
     // Warp-level aggregation of the NPW change bits (they share one bitmap word).
@@ -533,10 +553,13 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
 #pragma unroll
       for (int g = 0; g < Gm::NPW; g++) m |= ((bb >> (g * Gm::G)) & 1u) << g;
       atomicOr(chg_now + (base >> 5), m << (base & 31));
+      if constexpr (PUSH)
+        for (int q = 0; q < peers.n; q++) atomicOr(peers.chg[q] + (base >> 5), m << (base & 31));
       my_nch += __popc(m);
     }
   }
   }  // chunk
+  if constexpr (PUSH) __threadfence_system();   // remote rows/bits before the barrier
   block_add2(my_nch, my_merged, nch_out, merged_out);
 }
 
@@ -632,7 +655,7 @@ k_heavy_partial(const int64_t *__restrict__ offsets, const int32_t *__restrict__
 // order[o0, o1) lists heavy indices j.  mega == 0: one lane group per node (nodes with few
 // items); mega != 0: one warp per node, its NPW slots striding over the items (hubs with
 // hundreds of items), merged by a shuffle tree.  Partial loads are unrolled 4-deep.
-template <int LOGP>
+template <int LOGP, bool PUSH>
 __global__ void __launch_bounds__(kThreads)
 k_heavy_finish(const int32_t *__restrict__ heavy_nodes, const int32_t *__restrict__ item_first,
                const int32_t *__restrict__ order, int64_t o0, int64_t o1, int mega,
@@ -641,7 +664,8 @@ k_heavy_finish(const int32_t *__restrict__ heavy_nodes, const int32_t *__restric
                const uint32_t *__restrict__ chg_prev, uint32_t *__restrict__ chg_now,
                double *__restrict__ est, double *__restrict__ sum_dist,
                double *__restrict__ sum_recip, EstConst ec, double tf,
-               unsigned long long *__restrict__ nch_out, const uint32_t *__restrict__ active) {
+               unsigned long long *__restrict__ nch_out, const uint32_t *__restrict__ active,
+               Peers peers) {
   using Gm = Geo<LOGP>;
   constexpr int UF = 4;
   const int lane = threadIdx.x & 31;
@@ -689,14 +713,17 @@ k_heavy_finish(const int32_t *__restrict__ heavy_nodes, const int32_t *__restric
     for (int c = 0; c < Gm::CPL; c++) any |= nz4(acc[c]);
     any = ((__ballot_sync(0xffffffffu, any) >> (grp * Gm::G)) & lowmask) != 0u;
     const bool self_chg = owner && test_bit(chg_prev, v);
-    const bool changed = finish_node<LOGP>(owner && (any || self_chg), v, acc, acc, false,
+    const bool changed = finish_node<LOGP, PUSH>(peers, owner && (any || self_chg), v, acc, acc, false,
                                            self_chg, grp, gl, cur, nxt, est, sum_dist,
                                            sum_recip, ec, tf);
     if (changed && gl == 0) {
       atomicOr(chg_now + (v >> 5), 1u << (v & 31));
+      if constexpr (PUSH)
+        for (int q = 0; q < peers.n; q++) atomicOr(peers.chg[q] + (v >> 5), 1u << (v & 31));
       my_nch++;
     }
   }
+  if constexpr (PUSH) __threadfence_system();
   block_add2(my_nch, 0u, nch_out, nullptr);
 }
 
@@ -1114,7 +1141,7 @@ unsigned grid_for_warps(int64_t work_warps) {
 }
 unsigned grid_for_threads(int64_t work) { return grid_for_warps((work + 31) / 32); }
 
-template <int LOGP>
+template <int LOGP, bool PUSH>
 int union_step_impl(int64_t lo, int64_t hi, const int64_t *offsets, const int32_t *succ,
                     const uint8_t *cur, uint8_t *nxt, const uint32_t *chg_prev,
                     uint32_t *chg_now, double *est, double *sum_dist, double *sum_recip,
@@ -1124,7 +1151,7 @@ int union_step_impl(int64_t lo, int64_t hi, const int64_t *offsets, const int32_
                     const int32_t *item_node, const int64_t *item_beg, int64_t n_items,
                     int64_t item_arcs, uint8_t *partial, unsigned long long *nch,
                     unsigned long long *merged, int64_t hot_rows, const uint32_t *active,
-                    cudaStream_t s) {
+                    const Peers &peers, cudaStream_t s) {
   using Gm = Geo<LOGP>;
   if (hot_rows > 0) {
     cudaCtxResetPersistingL2Cache();    // lines of last iteration's buffer stop persisting
@@ -1138,23 +1165,23 @@ int union_step_impl(int64_t lo, int64_t hi, const int64_t *offsets, const int32_
   }
   if (hi > lo) {
     const int64_t warps = (hi - lo + Gm::NPW - 1) / Gm::NPW + 1;   // capped at the resident set
-    k_light<LOGP><<<grid_for_warps(warps), kThreads, 0, s>>>(
+    k_light<LOGP, PUSH><<<grid_for_warps(warps), kThreads, 0, s>>>(
         offsets, succ, cur, nxt, chg_prev, chg_now, est, sum_dist, sum_recip, ec, lo, hi,
-        light_max_deg, dense, tf, nch, merged, active);
+        light_max_deg, dense, tf, nch, merged, active, peers);
     if (int e = check_launch("k_light")) return e;
   }
   if (n_heavy > 0) {
     if (n_mega > 0) {
-      k_heavy_finish<LOGP><<<grid_for_warps(n_mega), kThreads, 0, s>>>(
+      k_heavy_finish<LOGP, PUSH><<<grid_for_warps(n_mega), kThreads, 0, s>>>(
           heavy_nodes, item_first, finish_order, 0, n_mega, 1, partial, cur, nxt, chg_prev,
-          chg_now, est, sum_dist, sum_recip, ec, tf, nch, active);
+          chg_now, est, sum_dist, sum_recip, ec, tf, nch, active, peers);
       if (int e = check_launch("k_heavy_finish(mega)")) return e;
     }
     if (n_heavy > n_mega)
-      k_heavy_finish<LOGP><<<grid_for_warps((n_heavy - n_mega + Gm::NPW - 1) / Gm::NPW), kThreads,
-                             0, s>>>(heavy_nodes, item_first, finish_order, n_mega, n_heavy, 0,
-                                     partial, cur, nxt, chg_prev, chg_now, est, sum_dist,
-                                     sum_recip, ec, tf, nch, active);
+      k_heavy_finish<LOGP, PUSH>
+          <<<grid_for_warps((n_heavy - n_mega + Gm::NPW - 1) / Gm::NPW), kThreads, 0, s>>>(
+              heavy_nodes, item_first, finish_order, n_mega, n_heavy, 0, partial, cur, nxt,
+              chg_prev, chg_now, est, sum_dist, sum_recip, ec, tf, nch, active, peers);
     if (int e = check_launch("k_heavy_finish")) return e;
   }
   if (hot_rows > 0) set_hot_window(s, nullptr, 0);
@@ -1245,7 +1272,17 @@ int hb_union_step(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets,
                   int64_t n_items, int64_t item_arcs, uint8_t *partial, uint64_t *nch_out,
                   uint64_t *merged_out, int64_t hot_rows, double *disc, int64_t disc_stride,
                   int n_disc, const double *disc_scale, int disc_div, const uint32_t *active,
+                  int n_peers, uint8_t *const *peer_nxt, uint32_t *const *peer_chg,
                   void *stream) {
+  if (n_peers < 0 || n_peers > kMaxPeers || (n_peers > 0 && (!peer_nxt || !peer_chg)))
+    return set_err_msg("hb_union_step: bad peer arguments (at most 7 peers)");
+  Peers peers;
+  memset(&peers, 0, sizeof(peers));
+  peers.n = n_peers;
+  for (int q = 0; q < n_peers; q++) {
+    peers.nxt[q] = peer_nxt[q];
+    peers.chg[q] = peer_chg[q];
+  }
   if (n_disc < 0 || n_disc > kMaxDisc || (n_disc > 0 && (!disc || !disc_scale)))
     return set_err_msg("hb_union_step: bad discount arguments (at most 8 fused)");
   if (n < 0 || lo < 0 || hi > n || lo > hi || t < 1 || !nch_out)
@@ -1269,12 +1306,22 @@ int hb_union_step(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets,
   EstConst ec{alpha_p2, lc_cut, lc_table, disc, disc_stride, n_disc, disc_div, {0, 0, 0, 0, 0, 0, 0, 0}};
   for (int k = 0; k < n_disc; k++) ec.disc_scale[k] = disc_scale[k];
   const double tf = (double)t;
-  HB_DISPATCH(b, return union_step_impl<LB>(
+  if (n_peers > 0) {
+    HB_DISPATCH(b, return (union_step_impl<LB, true>(
+                       lo, hi, offsets, succ, cur, nxt, chg_prev, chg_now, est, sum_dist,
+                       sum_recip, tf, ec, dense, light_max_deg, heavy_nodes, item_first, n_heavy,
+                       finish_order, n_mega, item_node, item_beg, n_items, item_arcs, partial,
+                       reinterpret_cast<unsigned long long *>(nch_out),
+                       reinterpret_cast<unsigned long long *>(merged_out), hot_rows, active,
+                       peers, s)));
+  }
+  HB_DISPATCH(b, return (union_step_impl<LB, false>(
                      lo, hi, offsets, succ, cur, nxt, chg_prev, chg_now, est, sum_dist,
                      sum_recip, tf, ec, dense, light_max_deg, heavy_nodes, item_first, n_heavy,
                      finish_order, n_mega, item_node, item_beg, n_items, item_arcs, partial,
                      reinterpret_cast<unsigned long long *>(nch_out),
-                     reinterpret_cast<unsigned long long *>(merged_out), hot_rows, active, s));
+                     reinterpret_cast<unsigned long long *>(merged_out), hot_rows, active, peers,
+                     s)));
   return 0;
 }
 

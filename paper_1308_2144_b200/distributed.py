@@ -197,11 +197,37 @@ class DistributedResult:
         return self.est.copy()
 
 
+def setup_push(state: "CudaRankState", group=None):
+    """Move the rank's buffers into symmetric memory for the fused push; None if the
+    platform has no symmetric memory (the all-gather exchange is used instead)."""
+    try:
+        return SymmetricBuffers(state, group)
+    except Exception as exc:   # no NVLink / symmetric memory: fall back, loudly
+        import warnings
+        warnings.warn(f"fused push unavailable ({exc!r}); using the all-gather exchange")
+        return None
+
+
+def iterate_push(state: "CudaRankState", symm: SymmetricBuffers, t: int, dense: bool,
+                 group=None) -> int:
+    """One fused-push iteration: union epilogue stores into the peers, then one NCCL
+    all-reduce of the changed count -- the termination test (engine.py:390) and the
+    barrier after which every rank's pushed rows are visible -- then swap."""
+    peer_nxt, peer_chg = symm.peer_pointers(state.dev)
+    nch = push_step(state, t, dense, peer_nxt, peer_chg)
+    tot = torch.tensor([nch], dtype=torch.int64, device=state.dev.device)
+    dist.all_reduce(tot, group=group)
+    state.swap()
+    return int(tot.item())
+
+
 def run_distributed(g, config: HyperBallConfig, observers: Iterable = (), group=None,
-                    state_factory=None) -> DistributedResult:
+                    state_factory=None, exchange: str = "push") -> DistributedResult:
     """``run`` (engine.py:402-435) over every rank of `group`; call it on every rank with
-    the same graph.  Fused ``CentralityAccumulator`` observers are supported (filled on
-    every rank after convergence); other observers get ``on_converged`` only."""
+    the same graph.  exchange="push" (default on NCCL) fuses the row exchange into the
+    union epilogue over symmetric memory; "allgather" packs, all-gathers and scatters the
+    changed rows.  Fused ``CentralityAccumulator`` observers are supported (filled on every
+    rank after convergence); other observers get ``on_converged`` only."""
     comm = TorchComm(group)
     factory = state_factory or (lambda: CudaRankState(g, config, comm.world, comm.rank))
     st = factory()
@@ -209,12 +235,20 @@ def run_distributed(g, config: HyperBallConfig, observers: Iterable = (), group=
     accs = [o for o in observers if fusable(o, st.n)]
     if accs:
         st.bind_sums()
+    symm = None
+    if (exchange == "push" and comm.world > 1 and isinstance(st, CudaRankState)
+            and dist.get_backend(group) == "nccl" and st.n > 0):
+        symm = setup_push(st, group)
     t = 0
     nch = st.n
     if st.n > 0:
         while True:
             started = time.perf_counter()
-            nch = iterate_rank(st, comm, t + 1, dense=(t == 0 or not config.skip_stable_nodes))
+            dense = t == 0 or not config.skip_stable_nodes
+            if symm is not None:
+                nch = iterate_push(st, symm, t + 1, dense, group)
+            else:
+                nch = iterate_rank(st, comm, t + 1, dense)
             t += 1
             if config.progress is not None and comm.rank == 0:
                 config.progress.write(f"t={t} changed={nch} elapsed_ms="
@@ -247,8 +281,61 @@ def run_distributed(g, config: HyperBallConfig, observers: Iterable = (), group=
     return res
 
 
+# ---------------------------------------------------------------- fused push exchange
+
+def _ptr_array(ptrs):
+    import ctypes
+    arr = (ctypes.c_void_p * max(len(ptrs), 1))(*ptrs)
+    return arr
+
+
+def push_step(state: "CudaRankState", t: int, dense: bool, peer_nxt, peer_chg) -> int:
+    """Union step whose epilogue stores this rank's written rows and change bits straight
+    into every peer's replica (hb_union_step with peers).  Afterwards this rank's chg_prev
+    is cleared: it becomes chg_now of the next step, into which peers may push only after
+    the barrier that follows.  Returns the LOCAL changed count."""
+    d = state.dev
+    n_peers = len(peer_nxt)
+    nch = d.union_step(t, dense, state.sums,
+                       peers=(n_peers, _ptr_array(peer_nxt), _ptr_array(peer_chg)),
+                       clear_chg_now=False)
+    d.chg_prev.zero_()
+    return nch
+
+
+class SymmetricBuffers:
+    """The register double buffer and the two change bitmaps of one rank in symmetric
+    memory (torch.distributed._symmetric_memory): every peer maps them, so the union
+    epilogue can store into them over NVLink."""
+
+    def __init__(self, state: "CudaRankState", group=None):
+        import torch.distributed._symmetric_memory as symm
+        d = state.dev
+        n, p = d.n, d.p
+        words = d.chg_prev.numel()
+        self.regs = symm.empty((2, n, p), dtype=torch.uint8, device=d.device)
+        self.bits = symm.empty((2, words), dtype=torch.int32, device=d.device)
+        self.regs[0].copy_(d.cur)
+        self.bits[0].fill_(-1)
+        self.bits[1].zero_()
+        d.cur, d.nxt = self.regs[0], self.regs[1]
+        d.chg_prev, d.chg_now = self.bits[0], self.bits[1]
+        gname = group.group_name if group is not None else dist.group.WORLD.group_name
+        self.h_regs = symm.rendezvous(self.regs, gname)
+        self.h_bits = symm.rendezvous(self.bits, gname)
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def peer_pointers(self, d):
+        on = d.nxt.data_ptr() - self.regs.data_ptr()
+        oc = d.chg_now.data_ptr() - self.bits.data_ptr()
+        qs = [q for q in range(self.world) if q != self.rank]
+        return ([int(self.h_regs.buffer_ptrs[q]) + on for q in qs],
+                [int(self.h_bits.buffer_ptrs[q]) + oc for q in qs])
+
+
 def run_simulated(g, config: HyperBallConfig, world: int, observers: Iterable = (),
-                  packed: bool = True):
+                  packed: bool = True, exchange: str = "allgather"):
     """All `world` ranks in one process on one GPU, phase by phase (no kernel waits on
     another rank).  Exercises the partition and every exchange kernel; results must be
     bit-identical to the single-GPU run."""
@@ -263,15 +350,24 @@ def run_simulated(g, config: HyperBallConfig, world: int, observers: Iterable = 
     if nch > 0:
         while True:
             dense = t == 0 or not config.skip_stable_nodes
-            for s in states:
-                s.local_step(t + 1, dense)
-                s.refresh_unowned()
-            packed = [s.gather_changed() for s in states]
-            nch = sum(k for _, _, k in packed)
-            for r, s in enumerate(states):
-                for q, (ids, rows, k) in enumerate(packed):
-                    if q != r and k:
-                        s.apply_remote(ids, rows)
+            if exchange == "push":
+                # every rank's epilogue writes into the other ranks' buffers; the ranks
+                # run one after another, so no kernel ever waits on another
+                nch = 0
+                for s in states:
+                    peers = [q for q in states if q is not s]
+                    nch += push_step(s, t + 1, dense, [q.dev.nxt.data_ptr() for q in peers],
+                                     [q.dev.chg_now.data_ptr() for q in peers])
+            else:
+                for s in states:
+                    s.local_step(t + 1, dense)
+                    s.refresh_unowned()
+                packed_rows = [s.gather_changed() for s in states]
+                nch = sum(k for _, _, k in packed_rows)
+                for r, s in enumerate(states):
+                    for q, (ids, rows, k) in enumerate(packed_rows):
+                        if q != r and k:
+                            s.apply_remote(ids, rows)
             for s in states:
                 s.swap()
             t += 1

@@ -464,9 +464,13 @@ class _Device:
         self.launches += 1
         return self.active.data_ptr()
 
-    def union_step(self, t: int, dense: bool, sums: _DeviceSums | None) -> int:
+    def union_step(self, t: int, dense: bool, sums: _DeviceSums | None, peers=None,
+                   clear_chg_now: bool = True) -> int:
+        """One hb_union_step.  peers: (n, host uint8** array, host uint32** array) of peer
+        nxt / chg_now device addresses for the fused multi-GPU push (distributed.py)."""
         s = self.sched
-        active = self._frontier_ptr(dense)
+        active = self._frontier_ptr(dense) if peers is None else None
+        n_peers, peer_nxt, peer_chg = peers if peers is not None else (0, None, None)
         light_hi = s.light_hi if self.full_pass else s.light_hi_steady
         sd = sums.sum_dist.data_ptr() if sums is not None else None
         sr = sums.sum_recip.data_ptr() if sums is not None else None
@@ -474,12 +478,14 @@ class _Device:
         _lib.check(_lib.hb().hb_union_step(
             self.n, s.light_lo, light_hi, s.offsets.data_ptr(), s.succ.data_ptr(),
             self.cur.data_ptr(), self.nxt.data_ptr(), self.chg_prev.data_ptr(),
-            self.chg_now.data_ptr(), 1, self.est.data_ptr(), sd, sr, t, self.lc.data_ptr(),
+            self.chg_now.data_ptr(), int(clear_chg_now), self.est.data_ptr(), sd, sr, t,
+            self.lc.data_ptr(),
             self.alpha_p2, self.lc_cut, self.b, int(dense), s.light_max_deg,
             s.heavy_nodes.data_ptr(), s.item_first.data_ptr(), s.n_heavy,
             s.finish_order.data_ptr(), s.n_mega, s.item_node.data_ptr(), s.item_beg.data_ptr(), s.n_items, s.item_arcs,
             s.partial.data_ptr(), self.counts.data_ptr(), self.counts.data_ptr() + 8,
-            s.hot_rows, *dargs, active, self.stream.cuda_stream), "hb_union_step")
+            s.hot_rows, *dargs, active, n_peers, peer_nxt, peer_chg, self.stream.cuda_stream),
+            "hb_union_step")
         self.launches += (light_hi > s.light_lo) + (s.n_items > 0) + (s.n_heavy > 0)
         self.launches_at_last_step = self.launches
         nch, merged = (int(x) for x in self.counts.cpu())
