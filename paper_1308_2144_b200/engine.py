@@ -35,7 +35,7 @@ import torch
 from . import _lib
 from .centrality import BallObserver, CentralityAccumulator, fusable
 from .hll import CounterArray, CounterParams, estimator_constants, lc_table
-from .schedule import Schedule, build_schedule
+from .schedule import Schedule, build_schedule, pack_bits, unpack_bits
 
 import os as _os
 
@@ -121,23 +121,6 @@ def _resolve_device(dev) -> torch.device:
     if d.type != "cuda":
         raise ValueError(f"device must be a CUDA device, got {dev!r}")
     return d if d.index is not None else torch.device("cuda", torch.cuda.current_device())
-
-
-def pack_bits(flags: torch.Tensor) -> torch.Tensor:
-    """bool [n] -> int32 bitmap [ceil(n/32)], bit v & 31 of word v >> 5."""
-    n = flags.numel()
-    words = (n + 31) // 32
-    padded = torch.zeros(words * 32, dtype=torch.int64, device=flags.device)
-    padded[:n] = flags.to(torch.int64)
-    shifts = torch.arange(32, dtype=torch.int64, device=flags.device)
-    w = (padded.view(words, 32) << shifts).sum(dim=1)
-    return torch.where(w >= 2**31, w - 2**32, w).to(torch.int32)
-
-
-def unpack_bits(words: torch.Tensor, n: int) -> torch.Tensor:
-    shifts = torch.arange(32, dtype=torch.int64, device=words.device)
-    bits = (words.to(torch.int64).unsqueeze(1) >> shifts) & 1
-    return bits.view(-1)[:n].to(torch.bool)
 
 
 class _PinnedPool:

@@ -68,6 +68,33 @@ class Schedule:
     def to_original(self, x: torch.Tensor) -> torch.Tensor:
         return x if self.rank is None else x.index_select(0, self.rank.long())
 
+    def to_internal_bits(self, words: torch.Tensor, n: int) -> torch.Tensor:
+        """Change bitmap (int32 words) from original to internal node order."""
+        if self.perm is None:
+            return words
+        return pack_bits(self.to_internal(unpack_bits(words, n)))
+
+    def to_original_bits(self, words: torch.Tensor, n: int) -> torch.Tensor:
+        """Change bitmap (int32 words, internal order) -> bool [n] in original order."""
+        return self.to_original(unpack_bits(words, n))
+
+
+def pack_bits(flags: torch.Tensor) -> torch.Tensor:
+    """bool [n] -> int32 bitmap [ceil(n/32)], bit v & 31 of word v >> 5."""
+    n = flags.numel()
+    words = (n + 31) // 32
+    padded = torch.zeros(words * 32, dtype=torch.int64, device=flags.device)
+    padded[:n] = flags.to(torch.int64)
+    shifts = torch.arange(32, dtype=torch.int64, device=flags.device)
+    w = (padded.view(words, 32) << shifts).sum(dim=1)
+    return torch.where(w >= 2**31, w - 2**32, w).to(torch.int32)
+
+
+def unpack_bits(words: torch.Tensor, n: int) -> torch.Tensor:
+    shifts = torch.arange(32, dtype=torch.int64, device=words.device)
+    bits = (words.to(torch.int64).unsqueeze(1) >> shifts) & 1
+    return bits.view(-1)[:n].to(torch.bool)
+
 
 MEGA_ITEMS = 16   # heavy nodes with more work items than this are finished one warp each
 

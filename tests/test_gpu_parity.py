@@ -272,3 +272,43 @@ def test_frontier_mode_matches_reference(key, mode, monkeypatch):
     assert bits_equal(hb.finalize_lin(acc), arrays[f"{key}/lin"])
     if mode == "always":
         assert st._dev.fwd is not None
+
+
+@pytest.mark.parametrize("key", ["random300_b6_s42_w5", "rmat12_b7_s42_w5", "sparse2000_b4_s42_w5"])
+@pytest.mark.parametrize("schedule", ["identity", "degree"])
+def test_reference_protocol_backend(key, schedule):
+    """CudaBackend driven exactly like the reference engine drives its backends
+    (engine.py:362-399: seed, union_range over [0, n), observers on host arrays, swap)."""
+    from paper_1308_2144_b200.reference_backend import CudaBackend
+    case = next(c for c in CASES if c["key"] == key)
+    off, suc = golden_graph(case)
+    g = hb.CsrGraph(off, suc)
+    n = g.n
+    params = hb.CounterParams(b=case["b"], seed=int(case["seed"]))
+    be = CudaBackend(n, params, g, schedule=schedule)
+    est = np.zeros(n)
+    new_est = np.zeros(n)
+    be.seed(None, est)
+    changed_prev = np.ones(n, dtype=bool)
+    changed_now = np.zeros(n, dtype=bool)
+    acc = hb.CentralityAccumulator(n)
+    regs = [sha(be.register_matrix())]
+    ests = [sha(est)]
+    t = 0
+    while True:
+        nch = be.union_range(0, n, g.offsets, g.successors, changed_prev, changed_now, est,
+                             new_est, True)
+        t += 1
+        acc.on_step(t, est, new_est)          # host observer path, exactly as the reference
+        be.swap()
+        est, new_est = new_est, est
+        changed_prev, changed_now = changed_now, changed_prev
+        regs.append(sha(be.register_matrix()))
+        ests.append(sha(est))
+        if nch == 0:
+            break
+    acc.on_converged(est)
+    assert t == case["t"]
+    assert regs == case["reg_digests"] and ests == case["est_digests"]
+    _, arrays = golden()
+    assert bits_equal(hb.finalize_lin(acc), arrays[f"{key}/lin"])
