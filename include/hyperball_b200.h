@@ -31,6 +31,9 @@
  *   hb_gen_rmat_keys / hb_keys_to_csr
  *                     graph.py:52-80 (from_edges: sort, dedup, CSR) + 145-155 (transpose),
  *                     for the synthetic R-MAT configs, on the device
+ *   hb_exact_seed / hb_exact_union_step
+ *                     engine.py:194-206 _ExactBackend.seed / union_range
+ *                     (-> _kernels.py:117-172 bitset_union_range, weighted_popcount_row)
  *   hb_forward_csr / hb_mark_active
  *                     frontier of a sparse iteration (no reference counterpart: the
  *                     reference scans every node's successor list, _kernels.py:82-87)
@@ -172,6 +175,23 @@ int hb_relabel_csr(int64_t n, const int64_t *old_offsets, const int32_t *old_suc
 int hb_sort_rows(int64_t n, const int64_t *offsets, const int64_t *host_offsets, int32_t *ids,
                  int32_t *alt, void *temp, uint64_t *temp_bytes, int *result_in_alt,
                  void *stream);
+
+/* Exact backend (engine.py:178-213, _kernels.py:117-172): one bitset of n bits per node,
+ * MSB-first bytes (the reference's rows), padded to row_stride bytes (multiple of 16,
+ * >= ceil(n/8)).  hb_exact_seed: zero every row, set node v's own bit, est[v] = weight
+ * (weights: device int64 [n] or NULL = 1).  hb_exact_union_step: one step over all nodes
+ * with the source-skip rule -- OR of the changed sources' rows into nxt, change test,
+ * est = weighted popcount (exact), fused accumulate and discounted sums as hb_union_step;
+ * nch_out / merged_out as hb_union_step; chg_now is cleared by the call. */
+int hb_exact_seed(int64_t n, int64_t row_stride, uint8_t *bits, double *est,
+                  const int64_t *weights, void *stream);
+int hb_exact_union_step(int64_t n, const int64_t *offsets, const int32_t *succ,
+                        const uint8_t *cur, uint8_t *nxt, int64_t row_stride,
+                        const uint32_t *chg_prev, uint32_t *chg_now, double *est,
+                        double *sum_dist, double *sum_recip, int64_t t, int dense,
+                        const int64_t *weights, double *disc, int64_t disc_stride, int n_disc,
+                        const double *disc_scale, int disc_div, uint64_t *nch_out,
+                        uint64_t *merged_out, void *stream);
 
 /* Frontier mode for sparse iterations.
  * hb_mark_active: active = chg_prev | out-neighbours(chg_prev) (device bitmaps over n

@@ -215,3 +215,71 @@ def run_oracle(offsets, succ, b: int, seed: int = 0, width: int = 5, workers: in
     res.t, res.registers, res.est = t, cur, est
     res.coreach, res.closeness, res.harmonic, res.lin = coreach, clo, har, lin
     return res
+
+
+def exact_union_pass(offsets, succ, cur, chg_prev, est, weights, skip: bool = True):
+    """One bitset_union_range pass over all nodes (_kernels.py:133-172), vectorised:
+    a node is active when it or one of its in-neighbours changed; an active row is the OR
+    of its own row and all its in-neighbours' rows; a changed row's estimate is the
+    weighted popcount of its MSB-first bits (_kernels.py:117-130) as float."""
+    offsets = _c(offsets, np.int64)
+    succ = _c(succ, np.int64)
+    n = offsets.shape[0] - 1
+    nxt = cur.copy()
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(offsets))
+    prev = np.asarray(chg_prev).astype(bool)
+    act = prev.copy()
+    if succ.size:
+        np.logical_or.at(act, rows, prev[succ])
+    sel = act[rows] if skip else np.ones(rows.shape, bool)
+    if sel.any():
+        np.bitwise_or.at(nxt, rows[sel], cur[succ[sel]])
+    changed = (nxt != cur).any(axis=1) if n else np.zeros(0, bool)
+    new_est = est.copy()
+    if changed.any():
+        bits = np.unpackbits(nxt[changed], axis=1)[:, :n].astype(np.int64)
+        new_est[changed] = (bits @ np.asarray(weights, np.int64)).astype(np.float64)
+    return int(changed.sum()), nxt, changed.astype(np.uint8), new_est
+
+
+def run_exact_oracle(offsets, succ, weights=None, skip: bool = True,
+                     record: bool = True) -> OracleResult:
+    """engine.run with backend="exact" (engine.py:178-213) restated: seed one bit per
+    node (engine.py:194-200), iterate exact_union_pass to convergence, accumulate and
+    finalize as run_oracle."""
+    offsets = _c(offsets, np.int64)
+    n = offsets.shape[0] - 1
+    w = np.ones(n, np.int64) if weights is None else _c(weights, np.int64)
+    cur = np.zeros((n, (n + 7) // 8), np.uint8)
+    v = np.arange(n)
+    cur[v, v >> 3] |= (0x80 >> (v & 7)).astype(np.uint8)
+    est = w.astype(np.float64)
+    chg_prev = np.ones(n, np.uint8)
+    sum_dist = np.zeros(n, np.float64)
+    sum_recip = np.zeros(n, np.float64)
+    res = OracleResult(0, cur, est, sum_dist, sum_recip, None, None, None, None)
+    if record:
+        res.reg_digests.append(sha(cur))
+        res.est_digests.append(sha(est))
+    t = 0
+    if n > 0:
+        while True:
+            nch, nxt, chg_now, new_est = exact_union_pass(offsets, succ, cur, chg_prev, est,
+                                                          w, skip)
+            t += 1
+            lib().orc_accumulate(n, t, _p(est), _p(new_est), _p(sum_dist), _p(sum_recip))
+            cur, est, chg_prev = nxt, new_est, chg_now
+            res.nch.append(nch)
+            if record:
+                res.reg_digests.append(sha(cur))
+                res.est_digests.append(sha(est))
+            if nch == 0:
+                break
+    coreach = est.copy()
+    clo, har, lin = np.zeros(n), np.zeros(n), np.zeros(n)
+    if n:
+        lib().orc_finalize(n, _p(sum_dist), _p(sum_recip), _p(coreach), _p(clo), _p(har),
+                           _p(lin))
+    res.t, res.registers, res.est = t, cur, est
+    res.coreach, res.closeness, res.harmonic, res.lin = coreach, clo, har, lin
+    return res

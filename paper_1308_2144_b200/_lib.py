@@ -44,6 +44,10 @@ HB_SIGNATURES = {
                              _vp, _i64, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _i64,
                              _vp, _i64, _int, _vp, _int, _vp, _int, _vp, _vp, _vp]),
     "hb_mark_active": (_int, [_i64, _vp, _vp, _vp, _vp, _vp]),
+    "hb_exact_seed": (_int, [_i64, _i64, _vp, _vp, _vp, _vp]),
+    "hb_exact_union_step": (_int, [_i64, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp,
+                                   _i64, _int, _vp, _vp, _i64, _int, _vp, _int, _vp, _vp,
+                                   _vp]),
     "hb_forward_csr": (_int, [_i64, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "hb_finalize": (_int, [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "hb_packed_row_bytes": (_int, [_int]),

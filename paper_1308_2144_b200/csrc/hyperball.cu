@@ -914,6 +914,112 @@ __global__ void k_refresh_rows(int64_t n, int64_t lo, int64_t hi,
   }
 }
 
+// ---- exact backend ---------------------------------------------------
+// The reference's validation backend (engine.py:178-213, _kernels.py:117-172): one bitset
+// of n bits per node (MSB-first bytes, exactly the reference's rows), OR instead of max,
+// weighted popcount instead of the HLL estimate -- the engine becomes a BFS oracle.  Rows
+// are padded to a 16-byte stride rs.  One warp per node; the OR accumulates in the node's
+// nxt row (each lane owns its chunks), so any row length works.
+__global__ void k_exact_seed(int64_t n, int64_t rs, uint8_t *__restrict__ bits,
+                             double *__restrict__ est, const int64_t *__restrict__ weights) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    bits[(size_t)v * rs + (v >> 3)] = (uint8_t)(0x80u >> (v & 7));
+    est[v] = weights ? (double)__ldg(weights + v) : 1.0;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads)
+k_exact_union(int64_t n, const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
+              const uint8_t *__restrict__ cur, uint8_t *__restrict__ nxt, int64_t rs,
+              const uint32_t *__restrict__ chg_prev, uint32_t *__restrict__ chg_now,
+              double *__restrict__ est, double *__restrict__ sum_dist,
+              double *__restrict__ sum_recip, double tf, int dense,
+              const int64_t *__restrict__ weights, const EstConst ec,
+              unsigned long long *__restrict__ nch_out,
+              unsigned long long *__restrict__ merged_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t chunks = rs / 16;
+  uint32_t my_nch = 0, my_merged = 0;
+  for (int64_t v = warp; v < n; v += nwarps) {
+    const bool self_chg = test_bit(chg_prev, v);
+    const int64_t b0 = __ldg(offsets + v), b1 = __ldg(offsets + v + 1);
+    const uint4 *crow = reinterpret_cast<const uint4 *>(cur + (size_t)v * rs);
+    uint4 *nrow = reinterpret_cast<uint4 *>(nxt + (size_t)v * rs);
+    bool started = false;
+    for (int64_t kb = b0; kb < b1; kb += 32) {
+      const int64_t k = kb + lane;
+      const int32_t id = k < b1 ? __ldg(succ + k) : -1;
+      const bool act = id >= 0 && (dense || test_bit(chg_prev, id));
+      unsigned mask = __ballot_sync(0xffffffffu, act);
+      if (mask && !started) {           // first active source: nxt[v] = cur[v]
+        for (int64_t c = lane; c < chunks; c += 32) nrow[c] = __ldg(crow + c);
+        started = true;
+      }
+      my_merged += lane == 0 ? (uint32_t)__popc(mask) : 0u;
+      while (mask) {
+        const int src = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const int32_t w = __shfl_sync(0xffffffffu, id, src);
+        const uint4 *wrow = reinterpret_cast<const uint4 *>(cur + (size_t)w * rs);
+        for (int64_t c = lane; c < chunks; c += 32) {
+          uint4 a = nrow[c];
+          const uint4 q = __ldg(wrow + c);
+          a.x |= q.x; a.y |= q.y; a.z |= q.z; a.w |= q.w;
+          nrow[c] = a;
+        }
+      }
+    }
+    if (!started) {
+      if (self_chg)                     // lazy double buffer: refresh the recycled row
+        for (int64_t c = lane; c < chunks; c += 32) nrow[c] = __ldg(crow + c);
+      continue;
+    }
+    bool diff = false;
+    unsigned long long cnt = 0;
+    for (int64_t c = lane; c < chunks; c += 32) {
+      const uint4 a = nrow[c], q = __ldg(crow + c);
+      diff |= ((a.x ^ q.x) | (a.y ^ q.y) | (a.z ^ q.z) | (a.w ^ q.w)) != 0u;
+      if (!weights) {
+        cnt += __popc(a.x) + __popc(a.y) + __popc(a.z) + __popc(a.w);
+      } else {
+        const uint32_t ws[4] = {a.x, a.y, a.z, a.w};
+        for (int q4 = 0; q4 < 4; q4++) {
+          uint32_t x = ws[q4];
+          while (x) {                   // byte j of the word, bit 7-k of the byte -> node
+            const int bit = __ffs(x) - 1;
+            x &= x - 1;
+            const int64_t node = (c * 16 + q4 * 4 + (bit >> 3)) * 8 + (7 - (bit & 7));
+            cnt += (unsigned long long)__ldg(weights + node);
+          }
+        }
+      }
+    }
+    const bool changed = __any_sync(0xffffffffu, diff);
+    if (changed) {
+      for (int off = 16; off > 0; off >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, off);
+      if (lane == 0) {
+        const double e = (double)cnt;
+        const double d = np_max0(__dsub_rn(e, est[v]));
+        est[v] = e;
+        if (sum_dist) sum_dist[v] = __dadd_rn(sum_dist[v], __dmul_rn(tf, d));
+        if (sum_recip) sum_recip[v] = __dadd_rn(sum_recip[v], __ddiv_rn(d, tf));
+        for (int k = 0; k < ec.n_disc; k++) {
+          double *q = ec.disc + k * ec.disc_stride + v;
+          const double c = ((ec.disc_div >> k) & 1) ? __ddiv_rn(d, tf)
+                                                    : __dmul_rn(ec.disc_scale[k], d);
+          *q = __dadd_rn(*q, c);
+        }
+        atomicOr(chg_now + (v >> 5), 1u << (v & 31));
+        my_nch++;
+      }
+    }
+  }
+  block_add2(my_nch, my_merged, nch_out, merged_out);
+}
+
 // ---- frontier mode (sparse iterations) -------------------------------------------------
 // active = chg_prev | out-neighbours(chg_prev) over the forward graph G: exactly the nodes
 // the source-skip rule can change this iteration, plus the changed rows themselves (their
@@ -1409,6 +1515,44 @@ int hb_sort_rows(int64_t n, const int64_t *offsets, const int64_t *host_offsets,
   }
   if (result_in_alt) *result_in_alt = 0;
   return check_launch("hb_sort_rows");
+}
+
+int hb_exact_seed(int64_t n, int64_t row_stride, uint8_t *bits, double *est,
+                  const int64_t *weights, void *stream) {
+  if (n <= 0) return 0;
+  if (row_stride % 16 || row_stride * 8 < n) return set_err_msg("hb_exact_seed: bad row_stride");
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(bits, 0, (size_t)n * (size_t)row_stride, s);
+  if (e != cudaSuccess) return set_err("hb_exact_seed memset", e);
+  k_exact_seed<<<grid_for_threads(n), kThreads, 0, s>>>(n, row_stride, bits, est, weights);
+  return check_launch("k_exact_seed");
+}
+
+int hb_exact_union_step(int64_t n, const int64_t *offsets, const int32_t *succ,
+                        const uint8_t *cur, uint8_t *nxt, int64_t row_stride,
+                        const uint32_t *chg_prev, uint32_t *chg_now, double *est,
+                        double *sum_dist, double *sum_recip, int64_t t, int dense,
+                        const int64_t *weights, double *disc, int64_t disc_stride, int n_disc,
+                        const double *disc_scale, int disc_div, uint64_t *nch_out,
+                        uint64_t *merged_out, void *stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n < 0 || t < 1 || !nch_out || row_stride % 16)
+    return set_err_msg("hb_exact_union_step: bad arguments");
+  if (n_disc < 0 || n_disc > kMaxDisc || (n_disc > 0 && (!disc || !disc_scale)))
+    return set_err_msg("hb_exact_union_step: bad discount arguments (at most 8 fused)");
+  EstConst ec{0.0, 0.0, nullptr, disc, disc_stride, n_disc, disc_div, {0, 0, 0, 0, 0, 0, 0, 0}};
+  for (int k = 0; k < n_disc; k++) ec.disc_scale[k] = disc_scale[k];
+  cudaError_t e = cudaMemsetAsync(nch_out, 0, sizeof(uint64_t), s);
+  if (e == cudaSuccess && merged_out) e = cudaMemsetAsync(merged_out, 0, sizeof(uint64_t), s);
+  if (e == cudaSuccess && n > 0)
+    e = cudaMemsetAsync(chg_now, 0, sizeof(uint32_t) * (size_t)((n + 31) / 32), s);
+  if (e != cudaSuccess) return set_err("hb_exact_union_step memset", e);
+  if (n == 0) return 0;
+  k_exact_union<<<grid_for_warps(n), kThreads, 0, s>>>(
+      n, offsets, succ, cur, nxt, row_stride, chg_prev, chg_now, est, sum_dist, sum_recip,
+      (double)t, dense, weights, ec, reinterpret_cast<unsigned long long *>(nch_out),
+      reinterpret_cast<unsigned long long *>(merged_out));
+  return check_launch("k_exact_union");
 }
 
 int hb_mark_active(int64_t n, const int64_t *fwd_offsets, const int32_t *fwd_succ,

@@ -97,6 +97,9 @@ class CudaRankState:
     """One rank's device state: full register replica, owned range [lo, hi)."""
 
     def __init__(self, g, config: HyperBallConfig, world: int, rank: int, packed: bool = True):
+        if config.backend != "probabilistic":
+            raise ValueError("multi-GPU runs use the probabilistic backend; the exact bitset "
+                             "backend is a single-device validation tool")
         n = (g.offsets.numel() if isinstance(g.offsets, torch.Tensor)
              else np.asarray(g.offsets).shape[0]) - 1
         w = _weights_array(config.weights, n)

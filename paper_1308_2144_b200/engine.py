@@ -314,7 +314,7 @@ class _Device:
 
     def fresh(self, config: HyperBallConfig) -> "_Device":
         """A new device state for another run on the same graph and schedule."""
-        other = object.__new__(_Device)
+        other = object.__new__(type(self))
         other.__dict__.update(self.__dict__)
         other.params = config.params
         n, p = self.n, self.p
@@ -484,6 +484,129 @@ class _Device:
         self.full_pass = False
 
 
+class _IdentityOrder:
+    """Node order of the exact backend: original ids, the CSR uploaded as is."""
+
+    perm = None
+    rank = None
+
+    def __init__(self, g, device: torch.device):
+        off, suc = _graph_arrays(g)
+        if not isinstance(off, torch.Tensor):
+            off, suc = torch.from_numpy(np.array(off)), torch.from_numpy(np.array(suc))
+        self.offsets = off.to(device=device, dtype=torch.int64).contiguous()
+        self.succ = suc.to(device=device, dtype=torch.int32).contiguous()
+        self.n = int(self.offsets.numel()) - 1
+
+    @staticmethod
+    def to_internal(x):
+        return x
+
+    @staticmethod
+    def to_original(x):
+        return x
+
+
+class _ExactDevice(_Device):
+    """Device state of the exact backend (engine.py:178-213): one bitset row of n bits per
+    node (the reference's MSB-first bytes, padded to a 16-byte stride), OR-union and
+    weighted popcount in hb_exact_union_step.  Identity node order; no frontier mode."""
+
+    def __init__(self, g, config: HyperBallConfig):
+        self.params = config.params
+        self.b = config.params.b
+        self.device = _resolve_device(config.device)
+        self.stream = torch.cuda.current_stream(self.device)
+        self.order = "identity"
+        self.world, self.rank_id = 1, 0
+        self._build_graph(g)
+        n = self.n
+        self.row_bytes = (n + 7) // 8
+        self.row_stride = max(16, (self.row_bytes + 15) // 16 * 16)
+        self.p = self.row_stride                    # row length of cur / nxt in bytes
+        words = max((n + 31) // 32, 1)
+        dv = self.device
+        self.cur = torch.zeros((n, self.row_stride), dtype=torch.uint8, device=dv)
+        self.nxt = torch.zeros((n, self.row_stride), dtype=torch.uint8, device=dv)
+        self.chg_prev = torch.full((words,), -1, dtype=torch.int32, device=dv)
+        self.chg_now = torch.zeros((words,), dtype=torch.int32, device=dv)
+        self.est = torch.zeros(n, dtype=torch.float64, device=dv)
+        self.counts = torch.zeros(2, dtype=torch.int64, device=dv)
+        self.weights = np.ones(n, dtype=np.int64)
+        self._w_dev = None
+        self.merged_total = 0
+        self.prev_all = True
+        self.full_pass = True
+        self.launches = 0
+        self.launches_at_last_step = 0
+        self.frontier = False
+        self.fwd = None
+        self.active = None
+        self.last_nch = None
+
+    def fresh(self, config: HyperBallConfig) -> "_ExactDevice":
+        other = super().fresh(config)
+        other.cur = torch.zeros_like(self.cur)
+        other.nxt = torch.zeros_like(self.nxt)
+        return other
+
+    def _build_graph(self, g) -> None:
+        self.sched = _IdentityOrder(g, self.device)
+        self.n = self.sched.n
+        self.graph_key = _graph_key(g)
+
+    def seed(self, weights: np.ndarray | None) -> None:
+        if weights is not None:
+            self.weights = np.ascontiguousarray(weights, dtype=np.int64)
+            self._w_dev = torch.from_numpy(self.weights).to(self.device)
+        else:
+            self.weights, self._w_dev = np.ones(self.n, dtype=np.int64), None
+        _lib.check(_lib.hb().hb_exact_seed(
+            self.n, self.row_stride, self.cur.data_ptr(), self.est.data_ptr(),
+            self._w_dev.data_ptr() if self._w_dev is not None else None,
+            self.stream.cuda_stream), "hb_exact_seed")
+        self.launches += 1 if self.n else 0
+
+    def set_weights(self, weights: np.ndarray) -> None:
+        """Weights of a loaded checkpoint (no re-seed)."""
+        self.weights = np.ascontiguousarray(weights, dtype=np.int64)
+        ones = self.n == 0 or bool((self.weights == 1).all())
+        self._w_dev = None if ones else torch.from_numpy(self.weights).to(self.device)
+
+    def _frontier_ptr(self, dense: bool):
+        return None
+
+    def union_step(self, t: int, dense: bool, sums: _DeviceSums | None, peers=None,
+                   clear_chg_now: bool = True) -> int:
+        if peers is not None:
+            raise ValueError("the exact backend runs on one device")
+        s = self.sched
+        sd = sums.sum_dist.data_ptr() if sums is not None else None
+        sr = sums.sum_recip.data_ptr() if sums is not None else None
+        dargs = sums.disc_args(t) if hasattr(sums, "disc_args") else (None, 0, 0, None, 0)
+        _lib.check(_lib.hb().hb_exact_union_step(
+            self.n, s.offsets.data_ptr(), s.succ.data_ptr(), self.cur.data_ptr(),
+            self.nxt.data_ptr(), self.row_stride, self.chg_prev.data_ptr(),
+            self.chg_now.data_ptr(), self.est.data_ptr(), sd, sr, t, int(dense),
+            self._w_dev.data_ptr() if self._w_dev is not None else None, *dargs,
+            self.counts.data_ptr(), self.counts.data_ptr() + 8, self.stream.cuda_stream),
+            "hb_exact_union_step")
+        self.launches += 1
+        self.launches_at_last_step = self.launches
+        nch, merged = (int(x) for x in self.counts.cpu())
+        self.last_nch = nch
+        self.last_merged = merged
+        self.merged_total += merged
+        return nch
+
+
+def _make_device(g, config: HyperBallConfig) -> _Device:
+    if config.backend == BACKEND_EXACT:
+        return _ExactDevice(g, config)
+    return _Device(g, config)
+
+
+
 class HyperBallState:
     """Engine state resident on the device; host views are copies in original node order.
 
@@ -517,31 +640,56 @@ class HyperBallState:
         d = self._dev
         return d.to_host(unpack_bits(d.chg_prev, d.n))
 
+    @property
+    def _exact(self) -> bool:
+        return self.config.backend == BACKEND_EXACT
+
     def register_matrix(self) -> np.ndarray:
-        """Host copy of the working counter rows, uint8 [n, p], original order, read-only."""
+        """Host copy of the working counter rows, original order, read-only: uint8 [n, p]
+        registers, or for the exact backend the [n, ceil(n/8)] bitset rows."""
         if self._dev is None:
-            m = np.zeros((0, self.config.params.p), dtype=np.uint8)
+            width = (self.n + 7) // 8 if self._exact else self.config.params.p
+            m = np.zeros((0, width), dtype=np.uint8)
+        elif self._exact:
+            d = self._dev
+            m = np.ascontiguousarray(d.to_host(d.cur)[:, :d.row_bytes])
         else:
             m = self._dev.to_host(self._dev.cur)
         m.setflags(write=False)
         return m
 
     def counters(self) -> CounterArray:
-        """Bit-packed snapshot of the current counters."""
+        """Bit-packed snapshot of the current counters (probabilistic only)."""
+        if self._exact:
+            raise ValueError("packed counters exist only for the probabilistic backend")
         return CounterArray.from_dense(self.register_matrix(), self.config.params)
+
+    def ball_members(self, v: int) -> np.ndarray:
+        """Exact backend: the node ids in v's current ball (engine.py:209-211)."""
+        if not self._exact:
+            raise ValueError("ball members exist only for the exact backend")
+        return np.flatnonzero(np.unpackbits(self.register_matrix()[v])[:self.n])
+
+    def _exact_weights(self) -> np.ndarray:
+        if self._dev is not None:
+            return np.asarray(self._dev.weights, dtype=np.int64)
+        return np.asarray(self._host[3], dtype=np.int64)
 
     @property
     def kernel_launches(self) -> int:
         return 0 if self._dev is None else self._dev.launches
 
-    # checkpointing (engine.py:254-280, HBCK v1, probabilistic kind) -------------
+    # checkpointing (engine.py:254-280, HBCK v1, both kinds) ---------------------
     def save(self, path) -> None:
         pr = self.config.params
-        blob_cur = CounterArray.from_dense(self.register_matrix(), pr).to_blob()
-        blob_nxt = CounterArray(self.n, pr).to_blob()
+        if self._exact:
+            blob_cur, blob_nxt, kind = self.register_matrix().tobytes(), b"", 1
+        else:
+            blob_cur = CounterArray.from_dense(self.register_matrix(), pr).to_blob()
+            blob_nxt, kind = CounterArray(self.n, pr).to_blob(), 0
         buf = io.BytesIO()
         buf.write(CHECKPOINT_MAGIC)
-        buf.write(struct.pack("<HBQQQ", CHECKPOINT_VERSION, 0, self.n, self.t,
+        buf.write(struct.pack("<HBQQQ", CHECKPOINT_VERSION, kind, self.n, self.t,
                               self.num_changed))
         buf.write(struct.pack("<BBQ", pr.b, pr.register_width, pr.seed & ((1 << 64) - 1)))
         for blob in (blob_cur, blob_nxt):
@@ -549,6 +697,8 @@ class HyperBallState:
             buf.write(blob)
         buf.write(self.changed_prev.astype(np.bool_).tobytes())
         buf.write(self.est.astype(np.float64).tobytes())
+        if self._exact:
+            buf.write(self._exact_weights().tobytes())
         with open(path, "wb") as fh:
             fh.write(buf.getvalue())
 
@@ -559,13 +709,10 @@ def initialize(g, config: HyperBallConfig) -> HyperBallState:
     """Seed one counter per node with item (v, 1) (or its weight replicas) on the device."""
     off = g.offsets
     n = (off.numel() if isinstance(off, torch.Tensor) else np.asarray(off).shape[0]) - 1
-    if config.backend != BACKEND_PROBABILISTIC:
-        raise ValueError("the B200 engine implements the probabilistic (HyperLogLog) backend "
-                         "only; the exact bitset backend is a CPU validation tool")
     w = _weights_array(config.weights, n)
     if w is not None:
         _check_weighted_width(config.params, w)
-    dev = _Device(g, config)
+    dev = _make_device(g, config)
     state = HyperBallState(config, n, dev)
     dev.seed(w)
     return state
@@ -676,8 +823,8 @@ def load_state(path, config: HyperBallConfig | None = None, graph=None) -> Hyper
     version, kind, n, t, num_changed = struct.unpack("<HBQQQ", data[4:31])
     if version != CHECKPOINT_VERSION:
         raise ValueError(f"unsupported checkpoint version {version}")
-    if kind != 0:
-        raise ValueError("only probabilistic checkpoints can be resumed on the B200 engine")
+    if kind not in (0, 1):
+        raise ValueError(f"unknown checkpoint kind {kind}")
     b, width, seed = struct.unpack("<BBQ", data[31:41])
     params = CounterParams(b=b, register_width=width, seed=seed)
     pos = 41
@@ -690,11 +837,20 @@ def load_state(path, config: HyperBallConfig | None = None, graph=None) -> Hyper
     changed_prev = np.frombuffer(data, dtype=np.bool_, count=n, offset=pos).copy()
     pos += n
     est = np.frombuffer(data, dtype=np.float64, count=n, offset=pos).copy()
-    dense = CounterArray.from_blob(blobs[0]).to_dense() if n else np.zeros((0, params.p),
-                                                                           np.uint8)
+    pos += 8 * n
+    weights = None
+    if kind == 0:
+        dense = CounterArray.from_blob(blobs[0]).to_dense() if n else np.zeros((0, params.p),
+                                                                               np.uint8)
+    else:
+        weights = np.frombuffer(data, dtype=np.int64, count=n, offset=pos).copy()
+        dense = np.frombuffer(blobs[0], dtype=np.uint8).reshape(n, (n + 7) // 8).copy()
     if config is None:
-        config = HyperBallConfig(params=params)
-    state = _PendingState(config, n, (dense, changed_prev, est))
+        config = HyperBallConfig(params=params, weights=weights,
+                                 backend=BACKEND_PROBABILISTIC if kind == 0 else BACKEND_EXACT)
+    elif (config.backend == BACKEND_EXACT) != (kind == 1):
+        raise ValueError(f"checkpoint kind {kind} does not match backend {config.backend!r}")
+    state = _PendingState(config, n, (dense, changed_prev, est, weights))
     state.t = t
     state.num_changed = num_changed
     if graph is not None:
@@ -712,10 +868,15 @@ class _PendingState(HyperBallState):
     def _attach(self, g) -> None:
         if self._dev is not None:
             return
-        dense, changed_prev, est = self._host
-        dev = _Device(g, self.config)
+        dense, changed_prev, est, weights = self._host
+        dev = _make_device(g, self.config)
         if dev.n != self.n:
             raise ValueError(f"graph has {dev.n} nodes, checkpoint has {self.n}")
+        if weights is not None:
+            dev.set_weights(weights)
+            padded = np.zeros((self.n, dev.row_stride), dtype=np.uint8)
+            padded[:, :dense.shape[1]] = dense
+            dense = padded
         cur = torch.from_numpy(dense).to(dev.device)
         dev.restore_original(cur, cur.clone(), torch.from_numpy(est).to(dev.device),
                              torch.from_numpy(changed_prev).to(dev.device))
@@ -768,7 +929,7 @@ def run_multi(g, config: HyperBallConfig, runs: int, discounts=(), observers_fac
         if w is not None:
             _check_weighted_width(cfg.params, w)
         if dev is None:
-            dev = _Device(g, cfg)
+            dev = _make_device(g, cfg)
         else:                               # same graph and schedule, fresh counters
             dev = dev.fresh(cfg)
         state = HyperBallState(cfg, n, dev)

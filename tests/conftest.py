@@ -61,6 +61,12 @@ def golden_cases():
     return meta["cases"]
 
 
+def exact_cases():
+    """Golden runs of the reference's exact bitset backend (engine.py:178-213)."""
+    meta, _ = golden()
+    return meta["exact_cases"]
+
+
 @pytest.fixture(scope="session")
 def pins():
     meta, arrays = golden()

@@ -141,6 +141,23 @@ DISCOUNT_CASES = [  # fused discounted-gain sums (centrality.py:26-101,149-150)
 ]
 
 
+EXACT_CASES = [  # the exact bitset backend (engine.py:178-213, _kernels.py:117-172)
+    # (name, builder, weights seed or None, with discounts)
+    ("path8", lambda: path_graph(8), None, False),
+    ("cycle5", lambda: cycle_graph(5), None, False),
+    ("star6", lambda: star_graph(6), None, False),
+    ("complete7", lambda: complete_graph(7), None, False),
+    ("random300", lambda: random_graph(7, 300, 3.0), None, True),
+    ("dag300", lambda: random_dag(8, 300, 2.0), None, False),
+    ("islands400", lambda: islands(9, 400, 1.5), 2, False),
+    ("random300", lambda: random_graph(7, 300, 3.0), 1, False),
+    ("sparse2000", lambda: random_graph(10, 2000, 1.1), None, False),
+    ("isolated5", lambda: empty_graph(5), None, False),
+    ("single1", lambda: empty_graph(1), None, False),
+    ("empty0", lambda: empty_graph(0), None, False),
+]
+
+
 def ref_discounts():
     out = []
     for name, tab in DISCOUNT_SPECS:
@@ -151,9 +168,9 @@ def ref_discounts():
     return out
 
 
-def drive(gT, b, seed, width=5, weights=None, discounts=()):
+def drive(gT, b, seed, width=5, weights=None, discounts=(), backend="probabilistic"):
     cfg = ref.HyperBallConfig(params=ref.CounterParams(b=b, register_width=width, seed=seed),
-                              workers=1, weights=weights)
+                              workers=1, weights=weights, backend=backend)
     acc = ref.CentralityAccumulator(gT.n, discounts)
     state = ref.initialize(gT, cfg)
     regs, ests, nchs, clamps = [sha(state.register_matrix())], [sha(state.est)], [], 0
@@ -228,6 +245,28 @@ def main():
             for s in seeds:
                 add(name, gT, b, s, 5, False, digest)
 
+    exact_cases = []
+    for name, build, wseed, with_disc in EXACT_CASES:
+        gT = ref.transpose(build())
+        wts = None if wseed is None else np.random.default_rng(wseed).integers(1, 6, gT.n)
+        discs = ref_discounts() if with_disc else ()
+        meta, final, _ = drive(gT, 6, 42, 5,
+                               None if wts is None else ref.NodeWeights.from_values(wts),
+                               discs, backend="exact")
+        key = f"exact_{name}" + ("" if wseed is None else f"_nw{wseed}") + (
+            "_disc" if with_disc else "")
+        meta.update(key=key, graph=name, n=int(gT.n), m=int(gT.m), b=6, seed="42", width=5,
+                    graph_stored=True, graph_digest=None, weights_seed=wseed,
+                    backend="exact")
+        if with_disc:
+            meta["discounts"] = [[nm, tab] for nm, tab in DISCOUNT_SPECS]
+        if wts is not None:
+            arrays[f"{key}/weights"] = np.asarray(wts, np.int64)
+        for k, v in final.items():
+            arrays[f"{key}/{k}"] = v
+        exact_cases.append(meta)
+        print(f"{key}: n={gT.n} m={gT.m} t={meta['t']} nch={meta['nch']}", flush=True)
+
     # ---------------------------------------------------------------- pins
     pins = {}
     items = np.array([0, 1, 2, 3, 1000, 2**31 - 1, 2**40 + 7, 2**64 - 1], dtype=np.uint64)
@@ -290,9 +329,22 @@ def main():
         path = os.path.join(td, "ck.bin")
         st.save(path)
         pins["hbck_random300_b6_t2"] = hashlib.sha256(open(path, "rb").read()).hexdigest()
+    # exact-kind HBCK (raw bitset rows + weights) after 2 iterations of weighted islands400
+    gT = ref.transpose(islands(9, 400, 1.5))
+    wts = ref.NodeWeights.from_values(np.random.default_rng(2).integers(1, 6, gT.n))
+    cfg = ref.HyperBallConfig(params=ref.CounterParams(b=6, seed=42), weights=wts,
+                              backend="exact")
+    st = ref.initialize(gT, cfg)
+    ref.iterate(gT, st)
+    ref.iterate(gT, st)
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, "ck.bin")
+        st.save(path)
+        pins["hbck_exact_islands400_nw2_t2"] = hashlib.sha256(
+            open(path, "rb").read()).hexdigest()
 
     with open(os.path.join(HERE, "cases.json"), "w") as fh:
-        json.dump(dict(cases=cases, pins=pins), fh, indent=1)
+        json.dump(dict(cases=cases, exact_cases=exact_cases, pins=pins), fh, indent=1)
     np.savez_compressed(os.path.join(HERE, "arrays.npz"), **arrays)
     print("wrote", len(cases), "cases")
 

@@ -8,6 +8,7 @@ import re
 
 import numpy as np
 import pytest
+import torch
 
 import paper_1308_2144_b200 as hb
 from paper_1308_2144_b200 import _lib, generators as gen
@@ -104,9 +105,16 @@ def test_engine_fails_loudly_without_cuda():
         hb.run(g, hb.HyperBallConfig(params=CounterParams(b=4)))
 
 
-def test_exact_backend_rejected():
-    g = hb.CsrGraph([0, 1, 1], [1])
+def test_exact_backend_config():
+    """backend="exact" is accepted (and still needs the device: no CPU fallback);
+    unknown backends are rejected (engine.py:82-97)."""
+    assert hb.HyperBallConfig(backend="exact").backend == "exact"
     with pytest.raises(ValueError):
+        hb.HyperBallConfig(backend="bitmap")
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    g = hb.CsrGraph([0, 1, 1], [1])
+    with pytest.raises(RuntimeError, match="CUDA"):
         hb.initialize(g, hb.HyperBallConfig(backend="exact"))
 
 

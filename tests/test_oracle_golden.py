@@ -11,7 +11,7 @@ import numpy as np
 import pytest
 
 import oracle as orc
-from conftest import golden, golden_cases, golden_graph
+from conftest import exact_cases, golden, golden_cases, golden_graph
 
 CASES = golden_cases()
 
@@ -74,3 +74,32 @@ def test_alpha_pins(pins):
     p, _ = pins
     for ps, a2 in p["alpha_p2"].items():
         assert orc.constants(int(ps).bit_length() - 1)[0] == a2
+
+
+EXACT = exact_cases()
+
+
+@pytest.mark.parametrize("case", EXACT, ids=[c["key"] for c in EXACT])
+def test_exact_oracle_matches_reference(case):
+    """The exact-backend restatement (oracle.run_exact_oracle) reproduces the reference's
+    exact runs: per-iteration bitset rows, estimates, sums and centralities."""
+    off, suc = golden_graph(case)
+    _, arrays = golden()
+    key = case["key"]
+    w = arrays[f"{key}/weights"] if case.get("weights_seed") is not None else None
+    res = orc.run_exact_oracle(off, suc, weights=w)
+    assert res.t == case["t"]
+    assert res.nch == case["nch"]
+    assert res.reg_digests == case["reg_digests"]
+    assert res.est_digests == case["est_digests"]
+    for name in ("sum_dist", "sum_recip", "coreach", "closeness", "harmonic", "lin"):
+        got = getattr(res, name)
+        assert np.array_equal(got.view(np.uint64), arrays[f"{key}/{name}"].view(np.uint64)), name
+
+
+def test_exact_oracle_skip_equals_naive():
+    case = next(c for c in EXACT if c["key"] == "exact_sparse2000")
+    off, suc = golden_graph(case)
+    a = orc.run_exact_oracle(off, suc, skip=True)
+    b = orc.run_exact_oracle(off, suc, skip=False)
+    assert a.reg_digests == b.reg_digests and a.est_digests == b.est_digests
