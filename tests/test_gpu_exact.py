@@ -161,3 +161,33 @@ def test_exact_run_multi():
     for st, acc in out:                     # seeds differ, exact results do not
         assert st.t == case["t"]
         assert bits_equal(hb.finalize_harmonic(acc), arrays["exact_random300_nw1/harmonic"])
+
+
+@pytest.mark.parametrize("key", ["exact_random300_nw1", "exact_sparse2000", "exact_cycle5"])
+def test_reference_protocol_exact_backend(key):
+    """CudaExactBackend driven the way engine.py:362-399 drives _ExactBackend."""
+    from paper_1308_2144_b200.reference_backend import CudaExactBackend
+    case = next(c for c in EXACT if c["key"] == key)
+    off, suc = golden_graph(case)
+    _, arrays = golden()
+    w = arrays[f"{key}/weights"] if case.get("weights_seed") is not None else None
+    g = hb.CsrGraph(off, suc)
+    n = g.n
+    be = CudaExactBackend(n, hb.CounterParams(b=6, seed=42), w, g)
+    est, new_est = np.zeros(n), np.zeros(n)
+    be.seed(w, est)
+    changed_prev, changed_now = np.ones(n, dtype=bool), np.zeros(n, dtype=bool)
+    regs, ests, t = [sha(be.cur)], [sha(est)], 0
+    while True:
+        nch = be.union_range(0, n, g.offsets, g.successors, changed_prev, changed_now, est,
+                             new_est, True)
+        t += 1
+        be.swap()
+        est, new_est = new_est, est
+        changed_prev, changed_now = changed_now, changed_prev
+        regs.append(sha(be.cur))
+        ests.append(sha(est))
+        if nch == 0:
+            break
+    assert t == case["t"]
+    assert regs == case["reg_digests"] and ests == case["est_digests"]
