@@ -16,6 +16,7 @@
 //   * registers are < 128 (rho_max = 65 - b <= 61), so the 7-bit-safe SIMD byte max below
 //     is exact.
 #include <cuda_runtime.h>
+#include <type_traits>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_sort.cuh>
@@ -104,6 +105,72 @@ __device__ __forceinline__ void tree_merge(uint4 (&acc)[CPL], uint4 (&r)[U][CPL]
       for (int c = 0; c < CPL; c++) r[u][c] = bmax4(r[u][c], r[u + span][c]);
 #pragma unroll
   for (int c = 0; c < CPL; c++) acc[c] = bmax4(acc[c], r[0][c]);
+}
+
+// Per-byte max accumulator on the 16x2 integer max unit (VIMNMX.U16x2, one ALU-pipe op).
+// The max of two u16 lanes always carries the larger high byte, whatever the low bytes,
+// so `hi` accumulates the raw words (odd bytes valid) and `lo` the words shifted up by 8
+// (even bytes valid; the shift is an IMAD on the FMA pipe).  3 instructions per merged word
+// with 2 on the ALU pipe, against 4 (3 ALU) for bmax; exact for any byte values.
+__device__ __forceinline__ uint32_t vmax16(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("max.u16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+template <int CPL>
+struct MaxAcc {
+  uint4 hi[CPL], lo[CPL];
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int c = 0; c < CPL; c++) hi[c] = lo[c] = make_uint4(0, 0, 0, 0);
+  }
+  __device__ __forceinline__ void add(int c, uint4 r) {
+    hi[c].x = vmax16(hi[c].x, r.x); lo[c].x = vmax16(lo[c].x, r.x << 8);
+    hi[c].y = vmax16(hi[c].y, r.y); lo[c].y = vmax16(lo[c].y, r.y << 8);
+    hi[c].z = vmax16(hi[c].z, r.z); lo[c].z = vmax16(lo[c].z, r.z << 8);
+    hi[c].w = vmax16(hi[c].w, r.w); lo[c].w = vmax16(lo[c].w, r.w << 8);
+  }
+  // byte 2k+1 from hi, byte 2k from lo's byte 2k+1
+  __device__ __forceinline__ static uint32_t join(uint32_t h, uint32_t l) {
+    uint32_t r;
+    asm("prmt.b32 %0, %1, %2, 0x3715;" : "=r"(r) : "r"(h), "r"(l));
+    return r;
+  }
+  __device__ __forceinline__ uint4 get(int c) const {
+    return make_uint4(join(hi[c].x, lo[c].x), join(hi[c].y, lo[c].y),
+                      join(hi[c].z, lo[c].z), join(hi[c].w, lo[c].w));
+  }
+};
+// The SWAR alternative with the same interface (one register set, 4 ops per word).
+template <int CPL>
+struct BmaxAcc {
+  uint4 a[CPL];
+  __device__ __forceinline__ void init() {
+#pragma unroll
+    for (int c = 0; c < CPL; c++) a[c] = make_uint4(0, 0, 0, 0);
+  }
+  __device__ __forceinline__ void add(int c, uint4 r) { a[c] = bmax4(a[c], r); }
+  __device__ __forceinline__ uint4 get(int c) const { return a[c]; }
+};
+// VIMNMX accumulation from p = 128 up (ALU-bound loops); below, the loops are latency-bound
+// and the second register set costs more than the saved ALU ops (measured, configs 3, 5s).
+// Padded (unconditional) loads from p = 64 up; at p = 16 / 32 the extra L1 wavefronts of
+// padded slots cost more than the predicates.
+#ifndef HB_VMAX_MIN_LOGP
+#define HB_VMAX_MIN_LOGP 7
+#endif
+#ifndef HB_PAD_MIN_LOGP
+#define HB_PAD_MIN_LOGP 6
+#endif
+template <int LOGP>
+using RowAcc = typename std::conditional<(LOGP >= HB_VMAX_MIN_LOGP), MaxAcc<Geo<LOGP>::CPL>,
+                                         BmaxAcc<Geo<LOGP>::CPL>>::type;
+
+// Source-row chunk load with 32-bit index arithmetic (one IMAD + one IMAD.WIDE.U32 per
+// address): rows * chunks-per-row < 2^32 for every array the C-ABI accepts.
+__device__ __forceinline__ uint4 ld_chunk(const uint4 *__restrict__ cur4, int32_t w, uint32_t ch,
+                                          uint32_t k) {
+  return __ldg(cur4 + ((uint32_t)w * ch + k));
 }
 
 __device__ __forceinline__ uint4 ldg4(const uint8_t *p) {
@@ -361,8 +428,22 @@ struct Batch {
   using Gm = Geo<LOGP>;
   // 16-byte row loads in flight per lane and resident CTAs per SM of the light kernel,
   // per p (swept on configs 3, 4, 5s: more registers per thread pay at p = 64 / 256)
-  static constexpr int LOADS = LOGP == 8 ? 16 : 8;
-  static constexpr int MINB = LOGP >= 10 ? 2 : (LOGP == 8 ? 2 : (LOGP >= 6 ? 3 : 4));
+#ifndef HB_LOADS_P16
+#define HB_LOADS_P16 8
+#endif
+#ifndef HB_MINB_P16
+#define HB_MINB_P16 4
+#endif
+#ifndef HB_LOADS_P64
+#define HB_LOADS_P64 8
+#endif
+#ifndef HB_MINB_P64
+#define HB_MINB_P64 3
+#endif
+  static constexpr int LOADS = LOGP == 8 ? 16 : (LOGP == 6 ? HB_LOADS_P64
+                                                             : (LOGP <= 5 ? HB_LOADS_P16 : 8));
+  static constexpr int MINB = LOGP >= 10 ? 2 : (LOGP == 8 ? 2 : (LOGP == 6 ? HB_MINB_P64 :
+                              (LOGP == 7 ? 3 : HB_MINB_P16)));
   static constexpr int U = Gm::CPL >= LOADS ? 1 : LOADS / Gm::CPL;  // rows in flight per lane
   static constexpr int NB = Gm::G > 8 ? Gm::G : 8;            // light: ids per group batch
   static constexpr int J = NB / Gm::G;                        // light: ids loaded per lane
@@ -413,6 +494,7 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
   const unsigned gmask = lowmask << (grp * Gm::G);
   const unsigned below = (1u << gl) - 1u;
   int32_t *my_ids = &sids[threadIdx.x >> 5][grp * B::NB];
+  const uint4 *cur4 = reinterpret_cast<const uint4 *>(cur);
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   uint32_t my_nch = 0, my_merged = 0;
@@ -484,6 +566,11 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
       acc[c] = make_uint4(0, 0, 0, 0);
       self[c] = pre ? ldg4(cur + (size_t)v * Gm::P + 16 * (c * Gm::G + gl)) : acc[c];
     }
+    // own row: part of the union anyway, so it pads the group's unused load slots (and is
+    // L1-hot); groups past the range use row lo
+    const int32_t fb = (int32_t)(v < ve ? v : lo);
+    RowAcc<LOGP> macc;
+    macc.init();
     double vals[3] = {0.0, 0.0, 0.0};
     if (pre && gl == 0) {
       vals[0] = est[v];
@@ -519,29 +606,29 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
       __syncwarp();
       const int cmax = __reduce_max_sync(0xffffffffu, (unsigned)cnt);
       for (int i = 0; i < cmax; i += B::U) {
+        // from p = 64 up, slots past the group's count load the fallback row instead of
+        // being predicated off: merging a row that is already part of the union changes
+        // nothing, and the loads stay unconditional (no zero-fill, no per-slot predicates)
         uint4 r[B::U][Gm::CPL];
 #pragma unroll
         for (int u = 0; u < B::U; u++) {
           const bool ok = i + u < cnt;
-          const int32_t w = ok ? my_ids[i + u] : 0;
+          const int32_t w = ok ? my_ids[i + u] : fb;
 #pragma unroll
           for (int c = 0; c < Gm::CPL; c++)
-            r[u][c] = ok ? ldg4(cur + (size_t)w * Gm::P + 16 * (c * Gm::G + gl))
-                         : make_uint4(0, 0, 0, 0);
+            r[u][c] = (LOGP >= HB_PAD_MIN_LOGP || ok) ? ld_chunk(cur4, w, Gm::CH, c * Gm::G + gl)
+                                                      : make_uint4(0, 0, 0, 0);
         }
 #pragma unroll
-        if constexpr (LOGP == 8) {     // pairwise merge pays at 16 loads in flight
-          tree_merge<B::U, Gm::CPL>(acc, r);
-        } else {
+        for (int u = 0; u < B::U; u++)
 #pragma unroll
-          for (int u = 0; u < B::U; u++)
-#pragma unroll
-            for (int c = 0; c < Gm::CPL; c++) acc[c] = bmax4(acc[c], r[u][c]);
-        }
+          for (int c = 0; c < Gm::CPL; c++) macc.add(c, r[u][c]);
       }
       total += cnt;
       __syncwarp();
     }
+#pragma unroll
+    for (int c = 0; c < Gm::CPL; c++) acc[c] = macc.get(c);
     my_merged += (gl == 0) ? (uint32_t)total : 0u;
     const bool changed = finish_node<LOGP, PUSH>(peers, valid && (total > 0 || self_chg), v, acc, self, pre,
                                            self_chg, grp, gl, cur, nxt, est, sum_dist,
@@ -580,6 +667,7 @@ k_heavy_partial(const int64_t *__restrict__ offsets, const int32_t *__restrict__
   const int slot = lane / Gm::G;
   const unsigned below = (1u << lane) - 1u;
   int32_t *wids = sids[threadIdx.x >> 5];
+  const uint4 *cur4 = reinterpret_cast<const uint4 *>(cur);
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   uint32_t my_merged = 0;
@@ -590,8 +678,8 @@ k_heavy_partial(const int64_t *__restrict__ offsets, const int32_t *__restrict__
     int64_t end = __ldg(offsets + v + 1);
     if (end > beg + item_arcs) end = beg + item_arcs;
     uint4 acc[Gm::CPL];
-#pragma unroll
-    for (int c = 0; c < Gm::CPL; c++) acc[c] = make_uint4(0, 0, 0, 0);
+    RowAcc<LOGP> macc;
+    macc.init();
     int32_t idr[B::HJ];
 #pragma unroll
     for (int j = 0; j < B::HJ; j++) {
@@ -614,30 +702,29 @@ k_heavy_partial(const int64_t *__restrict__ offsets, const int32_t *__restrict__
       }
       __syncwarp();
       for (int i = slot; i < cnt; i += Gm::NPW * B::U) {
+        // slots past cnt re-load the batch's first row (already merged: no effect), from
+        // p = 64 up; predicated off below
         uint4 r[B::U][Gm::CPL];
 #pragma unroll
         for (int u = 0; u < B::U; u++) {
           const int e = i + u * Gm::NPW;
           const bool ok = e < cnt;
-          const int32_t w = ok ? wids[e] : 0;
+          const int32_t w = wids[ok ? e : 0];
 #pragma unroll
           for (int c = 0; c < Gm::CPL; c++)
-            r[u][c] = ok ? ldg4(cur + (size_t)w * Gm::P + 16 * (c * Gm::G + gl))
-                         : make_uint4(0, 0, 0, 0);
+            r[u][c] = (LOGP >= HB_PAD_MIN_LOGP || ok) ? ld_chunk(cur4, w, Gm::CH, c * Gm::G + gl)
+                                                      : make_uint4(0, 0, 0, 0);
         }
 #pragma unroll
-        if constexpr (LOGP == 8) {     // pairwise merge pays at 16 loads in flight
-          tree_merge<B::U, Gm::CPL>(acc, r);
-        } else {
+        for (int u = 0; u < B::U; u++)
 #pragma unroll
-          for (int u = 0; u < B::U; u++)
-#pragma unroll
-            for (int c = 0; c < Gm::CPL; c++) acc[c] = bmax4(acc[c], r[u][c]);
-        }
+          for (int c = 0; c < Gm::CPL; c++) macc.add(c, r[u][c]);
       }
       my_merged += (lane == 0) ? (uint32_t)cnt : 0u;
       __syncwarp();
     }
+#pragma unroll
+    for (int c = 0; c < Gm::CPL; c++) acc[c] = macc.get(c);
 #pragma unroll
     for (int off = Gm::G; off < 32; off <<= 1)
 #pragma unroll
