@@ -247,7 +247,7 @@ def run_b200(args):
     params = hb.CounterParams(b=b, seed=seed)
 
     # ---------------------------------------------------------------- device-resident step
-    cfg = hb.HyperBallConfig(params=params, device=local)
+    cfg = hb.HyperBallConfig(params=params, device=local, schedule=args.schedule)
     acc = hb.CentralityAccumulator(n)
     rs = comm = st = symm = None
     if world > 1:
@@ -374,7 +374,7 @@ def run_b200(args):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             acc2 = hb.CentralityAccumulator(n)
-            cfg2 = hb.HyperBallConfig(params=params, device=local)
+            cfg2 = hb.HyperBallConfig(params=params, device=local, schedule=args.schedule)
             if world > 1:
                 from paper_1308_2144_b200.distributed import run_distributed
                 st2 = run_distributed(gp, cfg2, [acc2], exchange=args.exchange)
@@ -460,6 +460,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--config", default="config4")
+    ap.add_argument("--schedule", default="auto", choices=["auto", "identity", "degree", "window"])
     ap.add_argument("--exchange", choices=["push", "allgather"], default="push",
                     help="N > 1: fused push over symmetric memory, or all-gather")
     ap.add_argument("--e2e-steps", type=int, default=3)

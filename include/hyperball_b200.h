@@ -228,6 +228,10 @@ int hb_hash_items(int64_t n, const uint64_t *items, const uint64_t *replicas, ui
 /* Number of work items / recommended item size for heavy-node splitting at log2m b. */
 int64_t hb_item_arcs(int b);
 int64_t hb_light_max_deg(int b);
+/* Light-kernel geometry at log2m b: nodes per warp round (npw) and nodes per grid-stride
+ * chunk (window); the "window" schedule sorts nodes by in-degree inside each window. */
+int64_t hb_light_npw(int b);
+int64_t hb_light_window(int b);
 
 #ifdef __cplusplus
 }

@@ -61,6 +61,8 @@ HB_SIGNATURES = {
     "hb_hash_items": (_int, [_i64, _vp, _vp, _u64, _vp, _vp]),
     "hb_item_arcs": (_i64, [_int]),
     "hb_light_max_deg": (_i64, [_int]),
+    "hb_light_npw": (_i64, [_int]),
+    "hb_light_window": (_i64, [_int]),
 }
 
 GRAPH_SIGNATURES = {

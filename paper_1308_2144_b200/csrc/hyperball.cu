@@ -1421,6 +1421,11 @@ int64_t row_batch_end(const int64_t *h_off, int64_t n, int64_t r0) {
 }
 
 // ------------------------------------------------------------------ C-ABI
+template <int LOGP>
+static int64_t light_npw_t() { return Geo<LOGP>::NPW; }
+template <int LOGP>
+static int64_t light_window_t() { return (int64_t)Geo<LOGP>::NPW * chunk_rounds<LOGP>(); }
+
 extern "C" {
 
 const char *hb_version(void) { return "hyperball_b200 0.1 (sm_100a)"; }
@@ -1429,6 +1434,26 @@ int hb_min_log2m(void) { return HB_MIN_B; }
 int hb_max_log2m(void) { return HB_MAX_B; }
 int64_t hb_item_arcs(int b) { return item_arcs_for(b); }
 int64_t hb_light_max_deg(int b) { (void)b; return kLightMaxDeg; }
+int64_t hb_light_npw(int b) {
+  switch (b) {
+    case 4: return light_npw_t<4>();   case 5: return light_npw_t<5>();
+    case 6: return light_npw_t<6>();   case 7: return light_npw_t<7>();
+    case 8: return light_npw_t<8>();   case 9: return light_npw_t<9>();
+    case 10: return light_npw_t<10>(); case 11: return light_npw_t<11>();
+    case 12: return light_npw_t<12>();
+  }
+  return 1;
+}
+int64_t hb_light_window(int b) {
+  switch (b) {
+    case 4: return light_window_t<4>();   case 5: return light_window_t<5>();
+    case 6: return light_window_t<6>();   case 7: return light_window_t<7>();
+    case 8: return light_window_t<8>();   case 9: return light_window_t<9>();
+    case 10: return light_window_t<10>(); case 11: return light_window_t<11>();
+    case 12: return light_window_t<12>();
+  }
+  return 1;
+}
 
 int hb_seed(uint8_t *regs, double *est, int64_t n, int b, int register_width, uint64_t seed,
             const int32_t *perm, const int64_t *weights, const double *lc_table,

@@ -82,7 +82,7 @@ class HyperBallConfig:
             raise ValueError(f"unknown counter backend {self.backend!r}")
         if self.workers < 1:
             raise ValueError("workers must be >= 1")
-        if self.schedule not in ("auto", "identity", "degree"):
+        if self.schedule not in ("auto", "identity", "degree", "window"):
             raise ValueError(f"unknown schedule {self.schedule!r}")
 
 

@@ -4,8 +4,9 @@ The reference walks nodes in id order with one CPU thread per arc-balanced range
 (engine.py:351-390).  On the B200 the union kernel assigns lane groups to nodes, so the
 schedule decides:
 
-* ``order``: ``identity`` keeps node ids (best when in-degrees are flat and ids carry
-  locality, e.g. config 4's +-1024 window); ``degree`` relabels nodes by descending
+* ``order``: ``identity`` keeps node ids; ``window`` keeps them inside the light
+  kernel's grid-stride chunks but sorts each chunk by in-degree (best when ids carry
+  locality, e.g. config 4's +-1024 window, and in-degrees vary); ``degree`` relabels nodes by descending
   in-degree (stable), so every warp sees neighbours of equal degree, hubs sit first and
   their hot register rows share cache lines, and zero in-degree nodes trail.  The
   relabelling is internal: hashes use original ids and every host-visible array is
@@ -109,9 +110,38 @@ def _as_device(a, dtype, device) -> torch.Tensor:
     return t.to(device=device, non_blocking=True).to(dtype)
 
 
-def choose_order(max_deg: int, light_max_deg: int) -> str:
-    """auto: relabel by degree when any node needs the heavy path (skewed in-degree)."""
-    return "degree" if max_deg > light_max_deg else "identity"
+WINDOW_MIN_NODES = 1 << 23
+
+
+def choose_order(max_deg: int, light_max_deg: int, n: int = 0) -> str:
+    """auto: relabel by degree when any node needs the heavy path (skewed in-degree); else
+    sort inside the light kernel's chunks on large graphs (the relabel costs about one
+    pass over the CSR, repaid by the dense iterations from ~2^23 nodes: config 4 dense step
+    10.98 -> 10.05 ms, run 0.156 -> 0.150 s; config 3 (2^22) step 0.64 -> 0.57 ms but run
+    12.8 -> 13.4 ms); identity otherwise."""
+    if max_deg > light_max_deg:
+        return "degree"
+    return "window" if n >= WINDOW_MIN_NODES else "identity"
+
+
+def window_order(deg: torch.Tensor, b: int, bounds, max_deg: int) -> torch.Tensor:
+    """Node order of the "window" schedule: ids stay inside the light kernel's grid-stride
+    chunk (hb_light_window nodes, aligned as the kernel aligns them per rank), sorted by
+    descending in-degree there -- the NPW nodes of a warp round then have near-equal
+    in-degrees, so the round's warp-uniform loop wastes few load slots, while id locality
+    (e.g. config 4's +-1024 window) is kept to within one chunk."""
+    n = deg.numel()
+    dv = deg.device
+    L = _lib.hb()
+    win = int(L.hb_light_window(b))
+    npw = int(L.hb_light_npw(b))
+    v = torch.arange(n, dtype=torch.int64, device=dv)
+    bt = torch.tensor(bounds, dtype=torch.int64, device=dv)
+    r = torch.searchsorted(bt, v, right=True) - 1
+    lo_al = (bt[:-1] // npw) * npw
+    w = (v - lo_al[r]) // win
+    key = (r * (n // win + 2) + w) * (max_deg + 1) + (max_deg - deg)
+    return torch.sort(key, stable=True).indices
 
 
 def partition_bounds(n: int, world: int):
@@ -141,10 +171,26 @@ def build_schedule(offsets, successors, b: int, device, order: str = "auto", wor
     deg = off[1:] - off[:-1]
     max_deg = int(deg.max().item()) if n else 0
     if order == "auto":
-        order = choose_order(max_deg, light_max_deg)
-    if order not in ("identity", "degree"):
+        order = choose_order(max_deg, light_max_deg, n)
+    if order not in ("identity", "degree", "window"):
         raise ValueError(f"unknown schedule order {order!r}")
     perm = rank = None
+    if order == "window" and n > 0:
+        srt = window_order(deg, b, bounds, max_deg)
+        perm = srt.to(torch.int32)
+        rank = torch.empty_like(perm)
+        rank[srt] = torch.arange(n, dtype=torch.int32, device=device)
+        new_deg = deg[srt]
+        new_off = torch.zeros(n + 1, dtype=torch.int64, device=device)
+        torch.cumsum(new_deg, 0, out=new_off[1:])
+        new_succ = torch.empty(m, dtype=torch.int32, device=device)
+        s = stream if stream is not None else torch.cuda.current_stream(device)
+        _lib.check(L.hb_relabel_csr(n, off.data_ptr(), succ.data_ptr(), perm.data_ptr(),
+                                    rank.data_ptr(), new_off.data_ptr(), new_succ.data_ptr(),
+                                    s.cuda_stream), "hb_relabel_csr")
+        # ids move by less than a window: rows stay nearly ascending, no re-sort needed
+        off, succ, deg = new_off, new_succ, new_deg
+        del srt
     if order == "degree" and n > 0:
         srt = torch.sort(deg, descending=True, stable=True).indices
         if world > 1:

@@ -26,7 +26,7 @@ def sha(a):
 
 @pytest.mark.parametrize("packed", [True, False])
 @pytest.mark.parametrize("world", [2, 3, 8])
-@pytest.mark.parametrize("schedule", ["identity", "degree"])
+@pytest.mark.parametrize("schedule", ["identity", "degree", "window"])
 @pytest.mark.parametrize("key", ["random300_b6_s42_w5", "disc14_b4_s42_w5", "rmat12_b7_s42_w5",
                                  "config1_b6_s42_w5", "sparse2000_b4_s42_w5"])
 def test_simulated_ranks_match_reference(key, world, schedule, packed):

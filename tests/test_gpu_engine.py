@@ -155,10 +155,11 @@ class TestRegisterSemantics:
     def test_schedule_invariance(self, b):
         """Worker-count invariance (test_engine.py:231-239) for the B200 schedules."""
         g = random_graph(7, 500, 3.0)
-        outs = [hb.run(g, cfg(b=b, seed=9, schedule=s)) for s in ("identity", "degree")]
-        assert outs[0].t == outs[1].t
-        assert np.array_equal(outs[0].register_matrix(), outs[1].register_matrix())
-        assert np.array_equal(outs[0].est.view(np.uint64), outs[1].est.view(np.uint64))
+        outs = [hb.run(g, cfg(b=b, seed=9, schedule=s)) for s in ("identity", "degree", "window")]
+        for o in outs[1:]:
+            assert outs[0].t == o.t
+            assert np.array_equal(outs[0].register_matrix(), o.register_matrix())
+            assert np.array_equal(outs[0].est.view(np.uint64), o.est.view(np.uint64))
 
     def test_counters_pack_registers(self):
         g = random_graph(3, 100, 2.0)

@@ -54,7 +54,7 @@ def drive(off, suc, b, seed, width=5, schedule="auto", skip=True, weights=None):
     return st, acc, regs, ests, nchs
 
 
-@pytest.mark.parametrize("schedule", ["auto", "identity", "degree"])
+@pytest.mark.parametrize("schedule", ["auto", "identity", "degree", "window"])
 @pytest.mark.parametrize("case", CASES, ids=[c["key"] for c in CASES])
 def test_golden_case(case, schedule):
     off, suc = golden_graph(case)
@@ -119,7 +119,7 @@ def test_rmat_heavy_split_vs_oracle(b):
     _oracle_compare(g, b, 42)
 
 
-@pytest.mark.parametrize("schedule", ["identity", "degree"])
+@pytest.mark.parametrize("schedule", ["identity", "degree", "window"])
 def test_rmat16_both_schedules(schedule):
     g = gen.rmat_t(16, 16 << 16, seed=22)
     _oracle_compare(g, 4, 7, schedule)
