@@ -34,7 +34,7 @@
  *   hb_exact_seed / hb_exact_union_step
  *                     engine.py:194-206 _ExactBackend.seed / union_range
  *                     (-> _kernels.py:117-172 bitset_union_range, weighted_popcount_row)
- *   hb_forward_csr / hb_mark_active
+ *   hb_forward_csr / hb_mark_active / hb_mark_pull
  *                     frontier of a sparse iteration (no reference counterpart: the
  *                     reference scans every node's successor list, _kernels.py:82-87)
  *   hb_hash_items     hll.py:79-88 hash_items (device twin, used by tests)
@@ -204,6 +204,10 @@ int hb_forward_csr(int64_t n, const int64_t *offsets, const int32_t *succ, int64
                    uint64_t *temp_bytes, void *stream);
 int hb_mark_active(int64_t n, const int64_t *fwd_offsets, const int32_t *fwd_succ,
                    const uint32_t *chg_prev, uint32_t *active, void *stream);
+/* hb_mark_pull: the same active bitmap from the CSR of G^T alone (no forward graph): one
+ *   streaming pass over the successor ids (short sparse tails). */
+int hb_mark_pull(int64_t n, const int64_t *offsets, const int32_t *succ,
+                 const uint32_t *chg_prev, uint32_t *active, void *stream);
 
 /* GPU graph build.
  * hb_gen_rmat_keys: m R-MAT arcs (scale levels, 32-bit quadrant thresholds thr_a <= thr_ab

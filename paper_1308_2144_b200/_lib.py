@@ -44,6 +44,7 @@ HB_SIGNATURES = {
                              _vp, _i64, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _i64,
                              _vp, _i64, _int, _vp, _int, _vp, _int, _vp, _vp, _vp]),
     "hb_mark_active": (_int, [_i64, _vp, _vp, _vp, _vp, _vp]),
+    "hb_mark_pull": (_int, [_i64, _vp, _vp, _vp, _vp, _vp]),
     "hb_exact_seed": (_int, [_i64, _i64, _vp, _vp, _vp, _vp]),
     "hb_exact_union_step": (_int, [_i64, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp,
                                    _i64, _int, _vp, _vp, _i64, _int, _vp, _int, _vp, _vp,

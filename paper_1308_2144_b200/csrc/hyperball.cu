@@ -1136,6 +1136,39 @@ __global__ void k_mark_active(int64_t n, const int64_t *__restrict__ fwd_off,
   }
 }
 
+// The same frontier without a forward graph: active[v] = chg_prev[v] | any chg_prev[id],
+// id in row v of G^T.  One warp per 32 consecutive nodes streams their (contiguous) ids
+// coalesced; a changed source marks its row's owner, found by a vote over the 33 row
+// offsets held one per lane.  One pass over the ids at streaming rate, against the
+// latency-bound id scan of a full union pass.  Every bitmap word is written by one warp.
+__global__ void k_mark_pull(int64_t n, const int64_t *__restrict__ offsets,
+                            const int32_t *__restrict__ succ,
+                            const uint32_t *__restrict__ chg_prev, uint32_t *__restrict__ active) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v0 = warp * 32; v0 < n; v0 += nwarps * 32) {
+    const int64_t v = v0 + lane;
+    const int64_t my_off = __ldg(offsets + (v < n ? v : n));
+    const int64_t a0 = __shfl_sync(0xffffffffu, my_off, 0);
+    const int64_t a1 = __ldg(offsets + (v0 + 32 < n ? v0 + 32 : n));
+    bool mark = v < n && test_bit(chg_prev, v);
+    for (int64_t kb = a0; kb < a1; kb += 32) {
+      const int64_t k = kb + lane;
+      const bool hit = k < a1 && test_bit(chg_prev, __ldg(succ + k));
+      unsigned bal = __ballot_sync(0xffffffffu, hit);
+      while (bal) {                       // warp-uniform
+        const int64_t kk = kb + __ffs(bal) - 1;
+        bal &= bal - 1;
+        const int owner = __popc(__ballot_sync(0xffffffffu, my_off <= kk)) - 1;
+        mark |= lane == owner;
+      }
+    }
+    const unsigned word = __ballot_sync(0xffffffffu, mark);
+    if (lane == 0) active[v0 >> 5] = word;
+  }
+}
+
 // Forward CSR by counting sort (row order inside a forward row is irrelevant for marking):
 // count out-degrees with atomics, exclusive scan, scatter with per-source cursors.
 // Warp-aggregated: lanes holding the same source (hubs on R-MAT) issue one atomic.
@@ -1676,6 +1709,15 @@ int hb_mark_active(int64_t n, const int64_t *fwd_offsets, const int32_t *fwd_suc
   k_mark_active<<<grid_for_warps((n + 31) / 32), kThreads, 0, s>>>(n, fwd_offsets, fwd_succ,
                                                                    chg_prev, active);
   return check_launch("k_mark_active");
+}
+
+int hb_mark_pull(int64_t n, const int64_t *offsets, const int32_t *succ,
+                 const uint32_t *chg_prev, uint32_t *active, void *stream) {
+  if (n <= 0) return 0;
+  if (!offsets || !succ || !chg_prev || !active) return set_err_msg("hb_mark_pull: bad arguments");
+  k_mark_pull<<<grid_for_warps((n + 31) / 32), kThreads, 0, (cudaStream_t)stream>>>(
+      n, offsets, succ, chg_prev, active);
+  return check_launch("k_mark_pull");
 }
 
 int hb_forward_csr(int64_t n, const int64_t *offsets, const int32_t *succ, int64_t m,

@@ -41,8 +41,9 @@ import os as _os
 
 # frontier mode when fewer than n / FRONTIER_DIV counters changed in the last iteration
 FRONTIER_DIV = int(_os.environ.get("HB_FRONTIER_DIV", "8"))
-# ... and only from the FRONTIER_AFTER-th consecutive such iteration on (building the
-# forward graph costs several full scans; short tails do not repay it)
+# ... marked by one streaming pass over G^T's ids (hb_mark_pull) up to the FRONTIER_AFTER-th
+# consecutive such iteration, from the forward graph (hb_mark_active) after it (building
+# the forward graph costs several full scans; short tails do not repay it)
 FRONTIER_AFTER = int(_os.environ.get("HB_FRONTIER_AFTER", "4"))
 
 CHECKPOINT_MAGIC = b"HBCK"
@@ -433,17 +434,24 @@ class _Device:
         sparse = (not dense and self.frontier and self.last_nch is not None and self.n > 0
                   and self.last_nch * FRONTIER_DIV < self.n)
         self._sparse_run = getattr(self, "_sparse_run", 0) + 1 if sparse else 0
-        # the forward graph costs about one atomic per arc (several full scans of the
-        # successor lists) to build: only for long sparse tails, or once it exists
-        if not sparse or (self.fwd is None and self._sparse_run < FRONTIER_AFTER
-                          and FRONTIER_DIV > 1):
+        if not sparse:
             return None
-        off, dst = self._forward()
         if self.active is None:
             self.active = torch.empty_like(self.chg_now)
-        _lib.check(_lib.hb().hb_mark_active(self.n, off.data_ptr(), dst.data_ptr(),
-                                            self.chg_prev.data_ptr(), self.active.data_ptr(),
-                                            self.stream.cuda_stream), "hb_mark_active")
+        s = self.sched
+        # the forward graph costs about one atomic per arc (several full scans of the
+        # successor lists) to build: only for long sparse tails, or once it exists;
+        # before that, one streaming pass over the CSR of G^T marks the frontier
+        if self.fwd is None and self._sparse_run < FRONTIER_AFTER:
+            _lib.check(_lib.hb().hb_mark_pull(self.n, s.offsets.data_ptr(), s.succ.data_ptr(),
+                                              self.chg_prev.data_ptr(), self.active.data_ptr(),
+                                              self.stream.cuda_stream), "hb_mark_pull")
+        else:
+            off, dst = self._forward()
+            _lib.check(_lib.hb().hb_mark_active(self.n, off.data_ptr(), dst.data_ptr(),
+                                                self.chg_prev.data_ptr(),
+                                                self.active.data_ptr(),
+                                                self.stream.cuda_stream), "hb_mark_active")
         self.launches += 1
         return self.active.data_ptr()
 

@@ -242,20 +242,22 @@ def test_run_multi_matches_independent_runs():
     assert bits_equal(mean, stack.mean(axis=0)) and bits_equal(std, stack.std(axis=0, ddof=1))
 
 
-@pytest.mark.parametrize("mode", ["always", "off"])
+@pytest.mark.parametrize("mode", ["forward", "pull", "off"])
 @pytest.mark.parametrize("key", ["sparse2000_b4_s42_w5", "disc14_b4_s42_w5", "rmat12_b7_s42_w5",
                                  "islands400_b11_s3_w5", "config1_b6_s42_w5", "web14_b8_s42_w5"])
 def test_frontier_mode_matches_reference(key, mode, monkeypatch):
-    """Sparse iterations visiting only chg_prev | out-neighbours(chg_prev) (hb_mark_active)
-    give the reference's bits; 'always' uses the frontier whenever fewer than n counters
-    changed, 'off' never."""
+    """Sparse iterations visiting only chg_prev | out-neighbours(chg_prev) give the
+    reference's bits; the frontier is used whenever fewer than n counters changed, marked
+    from the forward graph (hb_mark_active, 'forward') or by the pull pass over G^T
+    (hb_mark_pull, 'pull'); 'off' never."""
     from paper_1308_2144_b200 import engine as E
     monkeypatch.setattr(E, "FRONTIER_DIV", 1)
+    monkeypatch.setattr(E, "FRONTIER_AFTER", 0 if mode == "forward" else 10**9)
     case = next(c for c in CASES if c["key"] == key)
     off, suc = golden_graph(case)
     g = hb.CsrGraph(off, suc)
     cfg = hb.HyperBallConfig(params=hb.CounterParams(b=case["b"], seed=int(case["seed"])),
-                             frontier=(mode == "always"))
+                             frontier=(mode != "off"))
     acc = hb.CentralityAccumulator(g.n)
     st = hb.initialize(g, cfg)
     regs, merged = [], []
@@ -270,8 +272,10 @@ def test_frontier_mode_matches_reference(key, mode, monkeypatch):
     assert regs == case["reg_digests"][1:]
     _, arrays = golden()
     assert bits_equal(hb.finalize_lin(acc), arrays[f"{key}/lin"])
-    if mode == "always":
+    if mode == "forward":
         assert st._dev.fwd is not None
+    if mode == "pull":
+        assert st._dev.fwd is None and st._dev.active is not None
 
 
 @pytest.mark.parametrize("key", ["random300_b6_s42_w5", "rmat12_b7_s42_w5", "sparse2000_b4_s42_w5"])
