@@ -168,11 +168,14 @@ int hb_relabel_csr(int64_t n, const int64_t *old_offsets, const int32_t *old_suc
                    int32_t *new_succ, void *stream);
 
 /* Sort the ids of every CSR row ascending (schedule setup, after hb_relabel_csr): offsets
- * (device int64 [n+1]) and host_offsets (HOST copy of the same array) describe the rows of
- * ids (device int32 [m]); alt (device int32 [m]) is scratch of the same size.  Call with
- * temp == NULL to get the scratch size in *temp_bytes, then again with that buffer.  The
- * sorted ids end in `ids` (*result_in_alt, if given, is set to 0). */
-int hb_sort_rows(int64_t n, const int64_t *offsets, const int64_t *host_offsets, int32_t *ids,
+ * (device int64 [n+1]) describe the rows of ids (device int32 [m]); alt (device int32 [m])
+ * is scratch of the same size.  The rows are sorted in n_batches batches of < 2^31 arcs:
+ * batch q covers rows [host_batch_rows[q], host_batch_rows[q+1]) whose arcs start at
+ * host_batch_arcs[q] (= offsets[host_batch_rows[q]]; both HOST arrays of n_batches + 1).
+ * Call with temp == NULL to get the scratch size in *temp_bytes, then again with that
+ * buffer.  The sorted ids end in `ids` (*result_in_alt, if given, is set to 0). */
+int hb_sort_rows(int64_t n, const int64_t *offsets, int64_t n_batches,
+                 const int64_t *host_batch_rows, const int64_t *host_batch_arcs, int32_t *ids,
                  int32_t *alt, void *temp, uint64_t *temp_bytes, int *result_in_alt,
                  void *stream);
 
@@ -205,9 +208,13 @@ int hb_forward_csr(int64_t n, const int64_t *offsets, const int32_t *succ, int64
 int hb_mark_active(int64_t n, const int64_t *fwd_offsets, const int32_t *fwd_succ,
                    const uint32_t *chg_prev, uint32_t *active, void *stream);
 /* hb_mark_pull: the same active bitmap from the CSR of G^T alone (no forward graph): one
- *   streaming pass over the successor ids (short sparse tails). */
+ *   streaming pass over the successor ids (short sparse tails).  Rows with in-degree >
+ *   light_max_deg are marked through the schedule's work items (item_node / item_beg /
+ *   n_items / item_arcs, as for hb_union_step), which must cover them. */
 int hb_mark_pull(int64_t n, const int64_t *offsets, const int32_t *succ,
-                 const uint32_t *chg_prev, uint32_t *active, void *stream);
+                 const uint32_t *chg_prev, uint32_t *active, int64_t light_max_deg,
+                 const int32_t *item_node, const int64_t *item_beg, int64_t n_items,
+                 int64_t item_arcs, void *stream);
 
 /* GPU graph build.
  * hb_gen_rmat_keys: m R-MAT arcs (scale levels, 32-bit quadrant thresholds thr_a <= thr_ab

@@ -1137,35 +1137,74 @@ __global__ void k_mark_active(int64_t n, const int64_t *__restrict__ fwd_off,
 }
 
 // The same frontier without a forward graph: active[v] = chg_prev[v] | any chg_prev[id],
-// id in row v of G^T.  One warp per 32 consecutive nodes streams their (contiguous) ids
-// coalesced; a changed source marks its row's owner, found by a vote over the 33 row
-// offsets held one per lane.  One pass over the ids at streaming rate, against the
-// latency-bound id scan of a full union pass.  Every bitmap word is written by one warp.
+// id in row v of G^T.  Light rows: one warp per 32 consecutive nodes; when their rows
+// are short in total the warp streams the whole (contiguous) id range coalesced and a
+// changed source marks its row's owner, found by a vote over the 33 row offsets held one
+// per lane; otherwise it walks the light rows one by one.  Heavy rows (in-degree >
+// light_max_deg) are skipped here and marked by k_mark_items over the schedule's work
+// items, so every warp streams a bounded number of ids.  Every bitmap word is written by
+// one warp of k_mark_pull (k_mark_items, launched after it, only ORs bits in).
 __global__ void k_mark_pull(int64_t n, const int64_t *__restrict__ offsets,
                             const int32_t *__restrict__ succ,
-                            const uint32_t *__restrict__ chg_prev, uint32_t *__restrict__ active) {
+                            const uint32_t *__restrict__ chg_prev, uint32_t *__restrict__ active,
+                            int64_t light_max_deg) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t v0 = warp * 32; v0 < n; v0 += nwarps * 32) {
     const int64_t v = v0 + lane;
     const int64_t my_off = __ldg(offsets + (v < n ? v : n));
+    const int64_t my_end = __ldg(offsets + (v + 1 < n ? v + 1 : n));
     const int64_t a0 = __shfl_sync(0xffffffffu, my_off, 0);
-    const int64_t a1 = __ldg(offsets + (v0 + 32 < n ? v0 + 32 : n));
+    const int64_t a1 = __shfl_sync(0xffffffffu, my_end, 31);
     bool mark = v < n && test_bit(chg_prev, v);
-    for (int64_t kb = a0; kb < a1; kb += 32) {
-      const int64_t k = kb + lane;
-      const bool hit = k < a1 && test_bit(chg_prev, __ldg(succ + k));
-      unsigned bal = __ballot_sync(0xffffffffu, hit);
-      while (bal) {                       // warp-uniform
-        const int64_t kk = kb + __ffs(bal) - 1;
-        bal &= bal - 1;
-        const int owner = __popc(__ballot_sync(0xffffffffu, my_off <= kk)) - 1;
-        mark |= lane == owner;
+    const bool heavy = v < n && my_end - my_off > light_max_deg;
+    const unsigned heavy_mask = __ballot_sync(0xffffffffu, heavy);
+    if (heavy_mask == 0u && a1 - a0 <= 32 * 64) {
+      for (int64_t kb = a0; kb < a1; kb += 32) {
+        const int64_t k = kb + lane;
+        const bool hit = k < a1 && test_bit(chg_prev, __ldg(succ + k));
+        unsigned bal = __ballot_sync(0xffffffffu, hit);
+        while (bal) {                     // warp-uniform
+          const int64_t kk = kb + __ffs(bal) - 1;
+          bal &= bal - 1;
+          const int owner = __popc(__ballot_sync(0xffffffffu, my_off <= kk)) - 1;
+          mark |= lane == owner;
+        }
+      }
+    } else {
+      for (int r = 0; r < 32; r++) {      // light rows one by one (<= light_max_deg ids)
+        const int64_t b0 = __shfl_sync(0xffffffffu, my_off, r);
+        const int64_t b1 = __shfl_sync(0xffffffffu, my_end, r);
+        if (((heavy_mask >> r) & 1u) || v0 + r >= n) continue;
+        bool any = false;
+        for (int64_t k = b0 + lane; k < b1; k += 32) any |= test_bit(chg_prev, __ldg(succ + k));
+        if (__any_sync(0xffffffffu, any)) mark |= lane == r;
       }
     }
     const unsigned word = __ballot_sync(0xffffffffu, mark);
     if (lane == 0) active[v0 >> 5] = word;
+  }
+}
+
+// Heavy rows of the pull marking: one warp per work item (<= item_arcs ids of one node).
+__global__ void k_mark_items(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
+                             const uint32_t *__restrict__ chg_prev,
+                             const int32_t *__restrict__ item_node,
+                             const int64_t *__restrict__ item_beg, int64_t n_items,
+                             int64_t item_arcs, uint32_t *__restrict__ active) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t it = warp; it < n_items; it += nwarps) {
+    const int64_t v = __ldg(item_node + it);
+    const int64_t beg = __ldg(item_beg + it);
+    int64_t end = __ldg(offsets + v + 1);
+    if (end > beg + item_arcs) end = beg + item_arcs;
+    bool any = false;
+    for (int64_t k = beg + lane; k < end; k += 32) any |= test_bit(chg_prev, __ldg(succ + k));
+    if (__any_sync(0xffffffffu, any) && lane == 0 && !test_bit(active, v))
+      atomicOr(active + (v >> 5), 1u << (v & 31));
   }
 }
 
@@ -1442,16 +1481,6 @@ struct ShiftOff {
 };
 using OffIt = cub::TransformInputIterator<int, ShiftOff, const int64_t *>;
 
-int64_t row_batch_end(const int64_t *h_off, int64_t n, int64_t r0) {
-  // largest r1 <= n with h_off[r1] - h_off[r0] < 2^31 (at least r0 + 1)
-  const int64_t lim = h_off[r0] + ((int64_t)1 << 31) - 1;
-  int64_t lo = r0 + 1, hi = n;
-  while (lo < hi) {
-    const int64_t mid = (lo + hi + 1) / 2;
-    if (h_off[mid] <= lim) lo = mid; else hi = mid - 1;
-  }
-  return lo;
-}
 
 // ------------------------------------------------------------------ C-ABI
 template <int LOGP>
@@ -1619,15 +1648,22 @@ int hb_refresh_rows(int64_t n, int64_t lo, int64_t hi, const uint32_t *bits, con
   return check_launch("k_refresh_rows");
 }
 
-int hb_sort_rows(int64_t n, const int64_t *offsets, const int64_t *host_offsets, int32_t *ids,
+int hb_sort_rows(int64_t n, const int64_t *offsets, int64_t n_batches,
+                 const int64_t *host_batch_rows, const int64_t *host_batch_arcs, int32_t *ids,
                  int32_t *alt, void *temp, uint64_t *temp_bytes, int *result_in_alt,
                  void *stream) {
   cudaStream_t s = (cudaStream_t)stream;
-  if (!host_offsets || !temp_bytes) return set_err_msg("hb_sort_rows: host_offsets/temp_bytes");
+  if (!host_batch_rows || !host_batch_arcs || !temp_bytes || n_batches < 0)
+    return set_err_msg("hb_sort_rows: batch arrays / temp_bytes");
+  for (int64_t q = 0; q < n_batches; q++)
+    if (host_batch_rows[q + 1] < host_batch_rows[q] ||
+        host_batch_arcs[q + 1] - host_batch_arcs[q] >= ((int64_t)1 << 31))
+      return set_err_msg("hb_sort_rows: a batch must hold < 2^31 arcs");
   size_t need = 0;
-  for (int64_t r0 = 0; r0 < n;) {                  // temp size: max over batches
-    const int64_t r1 = row_batch_end(host_offsets, n, r0);
-    const int64_t a0 = host_offsets[r0], items = host_offsets[r1] - a0;
+  for (int64_t q = 0; q < n_batches; q++) {       // temp size: max over batches
+    const int64_t r0 = host_batch_rows[q], r1 = host_batch_rows[q + 1];
+    const int64_t a0 = host_batch_arcs[q], items = host_batch_arcs[q + 1] - a0;
+    if (r1 == r0) continue;
     cub::DoubleBuffer<int32_t> keys(ids + a0, alt + a0);
     OffIt beg(offsets + r0, ShiftOff{a0}), end(offsets + r0 + 1, ShiftOff{a0});
     size_t bytes = 0;
@@ -1635,16 +1671,16 @@ int hb_sort_rows(int64_t n, const int64_t *offsets, const int64_t *host_offsets,
                                                        (int)(r1 - r0), beg, end, s);
     if (e != cudaSuccess) return set_err("hb_sort_rows (size)", e);
     need = bytes > need ? bytes : need;
-    r0 = r1;
   }
   if (!temp) {                                     // size query
     *temp_bytes = need;
     return 0;
   }
   if (*temp_bytes < need) return set_err_msg("hb_sort_rows: temp buffer too small");
-  for (int64_t r0 = 0; r0 < n;) {
-    const int64_t r1 = row_batch_end(host_offsets, n, r0);
-    const int64_t a0 = host_offsets[r0], items = host_offsets[r1] - a0;
+  for (int64_t q = 0; q < n_batches; q++) {
+    const int64_t r0 = host_batch_rows[q], r1 = host_batch_rows[q + 1];
+    const int64_t a0 = host_batch_arcs[q], items = host_batch_arcs[q + 1] - a0;
+    if (r1 == r0) continue;
     cub::DoubleBuffer<int32_t> keys(ids + a0, alt + a0);
     OffIt beg(offsets + r0, ShiftOff{a0}), end(offsets + r0 + 1, ShiftOff{a0});
     size_t bytes = need;
@@ -1656,7 +1692,6 @@ int hb_sort_rows(int64_t n, const int64_t *offsets, const int64_t *host_offsets,
                           cudaMemcpyDeviceToDevice, s);
       if (e != cudaSuccess) return set_err("hb_sort_rows copy", e);
     }
-    r0 = r1;
   }
   if (result_in_alt) *result_in_alt = 0;
   return check_launch("hb_sort_rows");
@@ -1712,12 +1747,22 @@ int hb_mark_active(int64_t n, const int64_t *fwd_offsets, const int32_t *fwd_suc
 }
 
 int hb_mark_pull(int64_t n, const int64_t *offsets, const int32_t *succ,
-                 const uint32_t *chg_prev, uint32_t *active, void *stream) {
+                 const uint32_t *chg_prev, uint32_t *active, int64_t light_max_deg,
+                 const int32_t *item_node, const int64_t *item_beg, int64_t n_items,
+                 int64_t item_arcs, void *stream) {
   if (n <= 0) return 0;
-  if (!offsets || !succ || !chg_prev || !active) return set_err_msg("hb_mark_pull: bad arguments");
-  k_mark_pull<<<grid_for_warps((n + 31) / 32), kThreads, 0, (cudaStream_t)stream>>>(
-      n, offsets, succ, chg_prev, active);
-  return check_launch("k_mark_pull");
+  if (!offsets || !succ || !chg_prev || !active || (n_items > 0 && (!item_node || !item_beg)))
+    return set_err_msg("hb_mark_pull: bad arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  k_mark_pull<<<grid_for_warps((n + 31) / 32), kThreads, 0, s>>>(n, offsets, succ, chg_prev,
+                                                                active, light_max_deg);
+  if (int e = check_launch("k_mark_pull")) return e;
+  if (n_items > 0) {
+    k_mark_items<<<grid_for_warps(n_items), kThreads, 0, s>>>(
+        offsets, succ, chg_prev, item_node, item_beg, n_items, item_arcs, active);
+    return check_launch("k_mark_items");
+  }
+  return 0;
 }
 
 int hb_forward_csr(int64_t n, const int64_t *offsets, const int32_t *succ, int64_t m,

@@ -443,9 +443,12 @@ class _Device:
         # successor lists) to build: only for long sparse tails, or once it exists;
         # before that, one streaming pass over the CSR of G^T marks the frontier
         if self.fwd is None and self._sparse_run < FRONTIER_AFTER:
-            _lib.check(_lib.hb().hb_mark_pull(self.n, s.offsets.data_ptr(), s.succ.data_ptr(),
-                                              self.chg_prev.data_ptr(), self.active.data_ptr(),
-                                              self.stream.cuda_stream), "hb_mark_pull")
+            _lib.check(_lib.hb().hb_mark_pull(
+                self.n, s.offsets.data_ptr(), s.succ.data_ptr(), self.chg_prev.data_ptr(),
+                self.active.data_ptr(), s.light_max_deg, s.item_node.data_ptr(),
+                s.item_beg.data_ptr(), s.n_items, s.item_arcs, self.stream.cuda_stream),
+                "hb_mark_pull")
+            self.launches += 1 if s.n_items else 0
         else:
             off, dst = self._forward()
             _lib.check(_lib.hb().hb_mark_active(self.n, off.data_ptr(), dst.data_ptr(),

@@ -111,6 +111,12 @@ def _as_device(a, dtype, device) -> torch.Tensor:
 
 
 WINDOW_MIN_NODES = 1 << 23
+# Re-sorting the rows after the degree relabel (hb_sort_rows) makes a hub's consecutive
+# arcs read neighbouring register rows: 1-4% off a dense iteration (config 5s 1.80 ->
+# 1.74 ms, config 5 38.0 -> 37.5 ms) for a segmented sort of every arc (30 ms at config
+# 5s, 0.37 s at config 5) -- a loss for any run of fewer than ~500 iterations.  Off by
+# default; HB_SORT_ROWS=1 turns it on.
+SORT_ROWS = bool(int(__import__("os").environ.get("HB_SORT_ROWS", "0")))
 
 
 def choose_order(max_deg: int, light_max_deg: int, n: int = 0) -> str:
@@ -142,6 +148,25 @@ def window_order(deg: torch.Tensor, b: int, bounds, max_deg: int) -> torch.Tenso
     w = (v - lo_al[r]) // win
     key = (r * (n // win + 2) + w) * (max_deg + 1) + (max_deg - deg)
     return torch.sort(key, stable=True).indices
+
+
+def _row_batches(off: torch.Tensor, n: int, m: int, limit: int = (1 << 31) - 1):
+    """Row batches of < 2^31 arcs for hb_sort_rows (cub segment sorts take int offsets):
+    host arrays of batch start rows and start arcs, found by device searchsorted (no copy
+    of the offsets to the host)."""
+    rows, arcs = [0], [0]
+    while rows[-1] < n:
+        a0 = arcs[-1]
+        if m - a0 <= limit:
+            r1 = n
+        else:
+            r1 = int(torch.searchsorted(off, torch.tensor([a0 + limit], dtype=off.dtype,
+                                                            device=off.device),
+                                        right=True).item()) - 1
+            r1 = max(r1, rows[-1] + 1)    # a single row above the limit: sorted alone
+        rows.append(min(r1, n))
+        arcs.append(m if r1 >= n else int(off[r1].item()))
+    return np.asarray(rows, dtype=np.int64), np.asarray(arcs, dtype=np.int64)
 
 
 def partition_bounds(n: int, world: int):
@@ -208,22 +233,25 @@ def build_schedule(offsets, successors, b: int, device, order: str = "auto", wor
         _lib.check(L.hb_relabel_csr(n, off.data_ptr(), succ.data_ptr(), perm.data_ptr(),
                                     rank.data_ptr(), new_off.data_ptr(), new_succ.data_ptr(),
                                     s.cuda_stream), "hb_relabel_csr")
-        # restore ascending ids inside every row (graph.py's normalisation), now in
+        # optionally restore ascending ids inside every row (graph.py's normalisation), in
         # internal ids: a hub's consecutive arcs then read neighbouring register rows
-        host_off = new_off.cpu().numpy()
-        if isinstance(successors, torch.Tensor) and successors.data_ptr() == succ.data_ptr():
-            succ = torch.empty_like(succ)       # never scribble on the caller's tensor
-        import ctypes
-        tb = ctypes.c_uint64(0)
-        hp = host_off.ctypes.data_as(ctypes.c_void_p)
-        _lib.check(L.hb_sort_rows(n, new_off.data_ptr(), hp, new_succ.data_ptr(),
-                                  succ.data_ptr(), None, ctypes.byref(tb), None,
-                                  s.cuda_stream), "hb_sort_rows(size)")
-        temp = torch.empty(max(int(tb.value), 1), dtype=torch.uint8, device=device)
-        _lib.check(L.hb_sort_rows(n, new_off.data_ptr(), hp, new_succ.data_ptr(),
-                                  succ.data_ptr(), temp.data_ptr(), ctypes.byref(tb), None,
-                                  s.cuda_stream), "hb_sort_rows")
-        del temp
+        if SORT_ROWS:
+            brows, barcs = _row_batches(new_off, n, m)
+            if isinstance(successors, torch.Tensor) and successors.data_ptr() == succ.data_ptr():
+                succ = torch.empty_like(succ)       # never scribble on the caller's tensor
+            import ctypes
+            tb = ctypes.c_uint64(0)
+            br = brows.ctypes.data_as(ctypes.c_void_p)
+            ba = barcs.ctypes.data_as(ctypes.c_void_p)
+            nb = brows.size - 1
+            _lib.check(L.hb_sort_rows(n, new_off.data_ptr(), nb, br, ba, new_succ.data_ptr(),
+                                      succ.data_ptr(), None, ctypes.byref(tb), None,
+                                      s.cuda_stream), "hb_sort_rows(size)")
+            temp = torch.empty(max(int(tb.value), 1), dtype=torch.uint8, device=device)
+            _lib.check(L.hb_sort_rows(n, new_off.data_ptr(), nb, br, ba, new_succ.data_ptr(),
+                                      succ.data_ptr(), temp.data_ptr(), ctypes.byref(tb), None,
+                                      s.cuda_stream), "hb_sort_rows")
+            del temp
         off, succ, deg = new_off, new_succ, new_deg
         del srt
     dloc = deg[lo:hi]

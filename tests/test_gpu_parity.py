@@ -316,3 +316,40 @@ def test_reference_protocol_backend(key, schedule):
     assert regs == case["reg_digests"] and ests == case["est_digests"]
     _, arrays = golden()
     assert bits_equal(hb.finalize_lin(acc), arrays[f"{key}/lin"])
+
+
+def test_sorted_rows_schedule(monkeypatch):
+    """HB_SORT_ROWS=1: degree relabel + per-row sort (hb_sort_rows) keeps the bits; rows
+    come out ascending; multi-batch sorting (batches < 2^31 arcs) equals a host sort."""
+    import ctypes
+    from paper_1308_2144_b200 import _lib, schedule as S
+    monkeypatch.setattr(S, "SORT_ROWS", True)
+    case = next(c for c in CASES if c["key"] == "rmat12_b7_s42_w5")
+    off, suc = golden_graph(case)
+    g = hb.CsrGraph(off, suc)
+    st = hb.run(g, hb.HyperBallConfig(params=hb.CounterParams(b=7, seed=42), schedule="degree"))
+    assert st.t == case["t"] and sha(st.register_matrix()) == case["reg_digests"][-1]
+    s = st._dev.sched
+    o, v = s.offsets.cpu().numpy(), s.succ.cpu().numpy()
+    assert all(np.all(np.diff(v[o[i]:o[i + 1]]) > 0) for i in range(s.n))
+    # several batches
+    rng = np.random.default_rng(5)
+    deg = rng.integers(0, 40, 3000)
+    offs = np.concatenate([[0], np.cumsum(deg)]).astype(np.int64)
+    ids = rng.integers(0, 3000, int(offs[-1])).astype(np.int32)
+    d_off = torch.from_numpy(offs).cuda()
+    d_ids = torch.from_numpy(ids).cuda()
+    alt = torch.empty_like(d_ids)
+    br, ba = S._row_batches(d_off, 3000, int(offs[-1]), limit=7000)
+    assert br.size > 3
+    tb = ctypes.c_uint64(0)
+    L = _lib.hb()
+    args = (3000, d_off.data_ptr(), br.size - 1, br.ctypes.data_as(ctypes.c_void_p),
+            ba.ctypes.data_as(ctypes.c_void_p), d_ids.data_ptr(), alt.data_ptr())
+    _lib.check(L.hb_sort_rows(*args, None, ctypes.byref(tb), None, None), "size")
+    temp = torch.empty(max(int(tb.value), 1), dtype=torch.uint8, device="cuda")
+    _lib.check(L.hb_sort_rows(*args, temp.data_ptr(), ctypes.byref(tb), None, None), "sort")
+    torch.cuda.synchronize()
+    got = d_ids.cpu().numpy()
+    want = np.concatenate([np.sort(ids[offs[i]:offs[i + 1]]) for i in range(3000)])
+    assert np.array_equal(got, want)
