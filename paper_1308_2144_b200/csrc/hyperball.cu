@@ -440,10 +440,22 @@ struct Batch {
 #ifndef HB_MINB_P64
 #define HB_MINB_P64 3
 #endif
-  static constexpr int LOADS = LOGP == 8 ? 16 : (LOGP == 6 ? HB_LOADS_P64
-                                                             : (LOGP <= 5 ? HB_LOADS_P16 : 8));
-  static constexpr int MINB = LOGP >= 10 ? 2 : (LOGP == 8 ? 2 : (LOGP == 6 ? HB_MINB_P64 :
-                              (LOGP == 7 ? 3 : HB_MINB_P16)));
+#ifndef HB_LOADS_P256
+#define HB_LOADS_P256 16
+#endif
+#ifndef HB_MINB_P256
+#define HB_MINB_P256 2
+#endif
+#ifndef HB_LOADS_P128
+#define HB_LOADS_P128 8
+#endif
+#ifndef HB_MINB_P128
+#define HB_MINB_P128 3
+#endif
+  static constexpr int LOADS = LOGP == 8 ? HB_LOADS_P256 : (LOGP == 6 ? HB_LOADS_P64 :
+                               (LOGP <= 5 ? HB_LOADS_P16 : (LOGP == 7 ? HB_LOADS_P128 : 8)));
+  static constexpr int MINB = LOGP >= 10 ? 2 : (LOGP == 8 ? HB_MINB_P256 : (LOGP == 6 ? HB_MINB_P64 :
+                              (LOGP == 7 ? HB_MINB_P128 : HB_MINB_P16)));
   static constexpr int U = Gm::CPL >= LOADS ? 1 : LOADS / Gm::CPL;  // rows in flight per lane
   static constexpr int NB = Gm::G > 8 ? Gm::G : 8;            // light: ids per group batch
   static constexpr int J = NB / Gm::G;                        // light: ids loaded per lane
@@ -619,6 +631,8 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
             r[u][c] = (LOGP >= HB_PAD_MIN_LOGP || ok) ? ld_chunk(cur4, w, Gm::CH, c * Gm::G + gl)
                                                       : make_uint4(0, 0, 0, 0);
         }
+        // sequential accumulate: a pairwise tree (shorter chains) measured 20% slower on
+        // config 4 (more live registers at 127/thread)
 #pragma unroll
         for (int u = 0; u < B::U; u++)
 #pragma unroll
@@ -1161,15 +1175,26 @@ __global__ void k_mark_pull(int64_t n, const int64_t *__restrict__ offsets,
     const bool heavy = v < n && my_end - my_off > light_max_deg;
     const unsigned heavy_mask = __ballot_sync(0xffffffffu, heavy);
     if (heavy_mask == 0u && a1 - a0 <= 32 * 64) {
-      for (int64_t kb = a0; kb < a1; kb += 32) {
-        const int64_t k = kb + lane;
-        const bool hit = k < a1 && test_bit(chg_prev, __ldg(succ + k));
-        unsigned bal = __ballot_sync(0xffffffffu, hit);
-        while (bal) {                     // warp-uniform
-          const int64_t kk = kb + __ffs(bal) - 1;
-          bal &= bal - 1;
-          const int owner = __popc(__ballot_sync(0xffffffffu, my_off <= kk)) - 1;
-          mark |= lane == owner;
+      constexpr int IL = 4;               // independent id loads per lane in flight
+      for (int64_t kb = a0; kb < a1; kb += 32 * IL) {
+        int32_t id[IL];
+#pragma unroll
+        for (int j = 0; j < IL; j++) {
+          const int64_t k = kb + j * 32 + lane;
+          id[j] = k < a1 ? __ldg(succ + k) : -1;
+        }
+        bool hit[IL];
+#pragma unroll
+        for (int j = 0; j < IL; j++) hit[j] = id[j] >= 0 && test_bit(chg_prev, id[j]);
+#pragma unroll
+        for (int j = 0; j < IL; j++) {
+          unsigned bal = __ballot_sync(0xffffffffu, hit[j]);
+          while (bal) {                   // warp-uniform
+            const int64_t kk = kb + j * 32 + __ffs(bal) - 1;
+            bal &= bal - 1;
+            const int owner = __popc(__ballot_sync(0xffffffffu, my_off <= kk)) - 1;
+            mark |= lane == owner;
+          }
         }
       }
     } else {
