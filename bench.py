@@ -279,7 +279,8 @@ def run_b200(args):
         if ev0 is not None:
             ev0.record(stream)
         _lib.check(L.hb_union_step(
-            n, s.light_lo, s.light_hi, s.offsets.data_ptr(), s.succ.data_ptr(),
+            n, s.light_lo, s.light_hi if dev.full_pass else s.light_hi_steady,
+            s.offsets.data_ptr(), s.succ.data_ptr(),
             dev.cur.data_ptr(), dev.nxt.data_ptr(), dev.chg_prev.data_ptr(),
             dev.chg_now.data_ptr(), clear, dev.est.data_ptr(), sums.sum_dist.data_ptr(),
             sums.sum_recip.data_ptr(), 1, dev.lc.data_ptr(), dev.alpha_p2, dev.lc_cut, b, 1,
