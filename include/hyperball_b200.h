@@ -31,6 +31,9 @@
  *   hb_gen_rmat_keys / hb_keys_to_csr
  *                     graph.py:52-80 (from_edges: sort, dedup, CSR) + 145-155 (transpose),
  *                     for the synthetic R-MAT configs, on the device
+ *   hb_union_step_runs
+ *                     cli.py:222-254 repeated runs (engine.run per seed), batched: R runs
+ *                     in one union pass
  *   hb_exact_seed / hb_exact_union_step
  *                     engine.py:194-206 _ExactBackend.seed / union_range
  *                     (-> _kernels.py:117-172 bitset_union_range, weighted_popcount_row)
@@ -178,6 +181,29 @@ int hb_sort_rows(int64_t n, const int64_t *offsets, int64_t n_batches,
                  const int64_t *host_batch_rows, const int64_t *host_batch_arcs, int32_t *ids,
                  int32_t *alt, void *temp, uint64_t *temp_bytes, int *result_in_alt,
                  void *stream);
+
+/* Batched runs (run_multi, cli.py:222-254): R = 2^log2_runs runs with
+ * the same log2m b share one CSR scan.  cur / nxt hold n rows of R * p bytes (run r's
+ * registers at bytes [r*p, (r+1)*p) of a row; R * p <= 256), est / sum_dist / sum_recip
+ * are [R, run_stride] fp64 (run r at + r * run_stride, run_stride >= n).  chg_prev /
+ * chg_now are the OR over runs of the change flags (source skip and lazy double buffer,
+ * as hb_union_step; chg_now is cleared by the call), chg_runs (device uint32 [R, ceil(n/32)],
+ * cleared by the call) receives each run's change bits and run_nch_out (device uint64 [R])
+ * each run's changed count; *nch_out counts nodes with any run changed.  The schedule
+ * arrays are those of build at log2m b + log2_runs (the wide row).  Every run's bits equal
+ * an independent hb_union_step run with its own seed. */
+int hb_union_step_runs(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets,
+                       const int32_t *succ, const uint8_t *cur, uint8_t *nxt,
+                       const uint32_t *chg_prev, uint32_t *chg_now, uint32_t *chg_runs,
+                       double *est, double *sum_dist, double *sum_recip, int64_t run_stride,
+                       int64_t t, const double *lc_table, double alpha_p2, double lc_cut, int b,
+                       int log2_runs, int dense, int64_t light_max_deg,
+                       const int32_t *heavy_nodes, const int32_t *item_first, int64_t n_heavy,
+                       const int32_t *finish_order, int64_t n_mega, const int32_t *item_node,
+                       const int64_t *item_beg, int64_t n_items, int64_t item_arcs,
+                       uint8_t *partial, uint64_t *nch_out, uint64_t *merged_out,
+                       uint64_t *run_nch_out, int64_t hot_rows, const uint32_t *active,
+                       void *stream);
 
 /* Exact backend (engine.py:178-213, _kernels.py:117-172): one bitset of n bits per node,
  * MSB-first bytes (the reference's rows), padded to row_stride bytes (multiple of 16,

@@ -43,6 +43,10 @@ HB_SIGNATURES = {
                              _vp, _i64, _vp, _dbl, _dbl, _int, _int, _i64, _vp, _vp, _i64,
                              _vp, _i64, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _i64,
                              _vp, _i64, _int, _vp, _int, _vp, _int, _vp, _vp, _vp]),
+    "hb_union_step_runs": (_int, [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                  _vp, _vp, _i64, _i64, _vp, _dbl, _dbl, _int, _int, _int,
+                                  _i64, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _i64, _i64, _vp,
+                                  _vp, _vp, _vp, _i64, _vp, _vp]),
     "hb_mark_active": (_int, [_i64, _vp, _vp, _vp, _vp, _vp]),
     "hb_mark_pull": (_int, [_i64, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _i64, _i64, _vp]),
     "hb_exact_seed": (_int, [_i64, _i64, _vp, _vp, _vp, _vp]),

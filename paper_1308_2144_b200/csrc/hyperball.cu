@@ -392,6 +392,114 @@ __device__ __forceinline__ bool finish_node(const Peers &peers, bool doit, int64
   return changed;
 }
 
+// Batched runs (run_multi): a row of cur holds R = 2^LOGR independent runs' registers side
+// by side (p1 = P / R bytes each, run r at bytes [r*p1, (r+1)*p1)).  The union is the same
+// byte-wise max over the wide row; this epilogue then does per run what finish_node does
+// per row: change test, estimate, accumulate -- est / sums are [R, stride] (run r at
+// + r * stride) and run r's change bit goes to ra.chg[r * ra.words + v/32].  The row is
+// written iff any run changed or the row changed last iteration (lazy double buffer over
+// the OR of the runs' flags, which also drives the source skip).  A run's CPR = p1/16
+// chunks sit on CPR consecutive lanes of one chunk slot (CPR <= G for every p1 >= 16 and
+// P <= 256), so its partial sums reduce by xor-shuffles inside that lane block.
+struct RunArgs {
+  uint32_t *chg;      // [R, words] per-run change bitmaps
+  int64_t words;
+  int64_t stride;     // est / sum_dist / sum_recip run stride (>= n)
+};
+
+template <int LOGP, int LOGR>
+__device__ __forceinline__ bool finish_runs(bool doit, int64_t v,
+                                            const uint4 (&acc)[Geo<LOGP>::CPL],
+                                            const uint4 (&pre)[Geo<LOGP>::CPL], bool have_pre,
+                                            bool self_chg, int gl,
+                                            const uint8_t *__restrict__ cur,
+                                            uint8_t *__restrict__ nxt, double *__restrict__ est,
+                                            double *__restrict__ sum_dist,
+                                            double *__restrict__ sum_recip, const EstConst &ec,
+                                            double tf, const RunArgs &ra) {
+  using Gm = Geo<LOGP>;
+  constexpr int P1 = Gm::P >> LOGR;
+  constexpr int CPR = P1 / 16;
+  static_assert(CPR >= 1 && CPR <= Gm::G && Gm::G % CPR == 0, "run chunks must share a lane block");
+  const uint8_t *crow = cur + (size_t)v * Gm::P;
+  uint8_t *nrow = nxt + (size_t)v * Gm::P;
+  uint4 nw[Gm::CPL];
+  unsigned my_runs = 0;
+#pragma unroll
+  for (int c = 0; c < Gm::CPL; c++) {
+    uint4 self = pre[c];
+    if (doit && !have_pre) self = ldg4(crow + 16 * (c * Gm::G + gl));
+    nw[c] = bmax4(acc[c], self);
+    if (doit && neq4(nw[c], self)) my_runs |= 1u << ((c * Gm::G + gl) / CPR);
+  }
+  unsigned runs = my_runs;
+#pragma unroll
+  for (int off = 1; off < Gm::G; off <<= 1) runs |= __shfl_xor_sync(0xffffffffu, runs, off);
+  const bool changed = runs != 0u;
+  if (doit && (changed || self_chg)) {
+#pragma unroll
+    for (int c = 0; c < Gm::CPL; c++)
+      *reinterpret_cast<uint4 *>(nrow + 16 * (c * Gm::G + gl)) = nw[c];
+  }
+  if (__any_sync(0xffffffffu, changed)) {   // warp-uniform
+    double s[Gm::CPL];
+    uint32_t zeros[Gm::CPL], big[Gm::CPL];
+#pragma unroll
+    for (int c = 0; c < Gm::CPL; c++) {
+      double s4[4] = {0.0, 0.0, 0.0, 0.0};
+      const uint32_t ws[4] = {nw[c].x, nw[c].y, nw[c].z, nw[c].w};
+      zeros[c] = 0;
+      big[c] = 0;
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        const uint32_t w = ws[q];
+        zeros[c] += __popc(~(((w & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | w) & 0x80808080u);
+        big[c] |= w;
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+          const uint32_t m = (w >> (8 * i)) & 0xffu;
+          s4[i] = __dadd_rn(s4[i], __hiloint2double((int)(0x3FF00000u - (m << 20)), 0));
+        }
+      }
+      s[c] = __dadd_rn(__dadd_rn(s4[0], s4[1]), __dadd_rn(s4[2], s4[3]));
+#pragma unroll
+      for (int off = 1; off < CPR; off <<= 1) {   // inside the run's lane block
+        s[c] = __dadd_rn(s[c], __shfl_xor_sync(0xffffffffu, s[c], off));
+        zeros[c] += __shfl_xor_sync(0xffffffffu, zeros[c], off);
+        big[c] |= __shfl_xor_sync(0xffffffffu, big[c], off);
+      }
+    }
+    bool need_seq = false;
+#pragma unroll
+    for (int c = 0; c < Gm::CPL; c++) {
+      const int r = (c * Gm::G + gl) / CPR;
+      need_seq |= ((runs >> r) & 1u) && (big[c] & 0xE0E0E0E0u) != 0u;
+    }
+    if (__any_sync(0xffffffffu, need_seq)) __syncwarp();   // stored rows visible
+    if (gl % CPR == 0) {
+#pragma unroll
+      for (int c = 0; c < Gm::CPL; c++) {
+        const int r = (c * Gm::G + gl) / CPR;
+        if (!((runs >> r) & 1u)) continue;
+        double sr = s[c];
+        if ((big[c] & 0xE0E0E0E0u) != 0u) {   // reference order: ascending-j fp64 sum
+          sr = 0.0;
+          for (int j = 0; j < P1; j++) sr = __dadd_rn(sr, pow2neg(nrow[r * P1 + j]));
+        }
+        const double e = finish_estimate(sr, (int)zeros[c], ec);
+        const int64_t at = (int64_t)r * ra.stride + v;
+        const double old = est[at];
+        est[at] = e;
+        const double d = np_max0(__dsub_rn(e, old));
+        if (sum_dist) sum_dist[at] = __dadd_rn(sum_dist[at], __dmul_rn(tf, d));
+        if (sum_recip) sum_recip[at] = __dadd_rn(sum_recip[at], __ddiv_rn(d, tf));
+        atomicOr(ra.chg + r * ra.words + (v >> 5), 1u << (v & 31));
+      }
+    }
+  }
+  return changed;
+}
+
 // Block-wide sum of two per-thread counters, one atomicAdd per block and counter.
 __device__ __forceinline__ void block_add2(uint32_t a, uint32_t b, unsigned long long *out_a,
                                            unsigned long long *out_b) {
@@ -487,7 +595,7 @@ __host__ __device__ constexpr int chunk_rounds() { return LOGP >= 8 ? 16 : 4; }
 // prefetches them into L2 kLookRounds rounds ahead, leaving the random source-row
 // gather as the only exposed memory latency of a round.
 // _kernels.py:67-114 restated with the source-skip rule.
-template <int LOGP, bool PUSH>
+template <int LOGP, bool PUSH, int LOGR = 0>
 __global__ void __launch_bounds__(kThreads, Batch<LOGP>::MINB)
 k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
         const uint8_t *__restrict__ cur, uint8_t *__restrict__ nxt,
@@ -495,7 +603,8 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
         double *__restrict__ est, double *__restrict__ sum_dist, double *__restrict__ sum_recip,
         EstConst ec, int64_t lo, int64_t hi, int64_t max_deg, int dense, double tf,
         unsigned long long *__restrict__ nch_out, unsigned long long *__restrict__ merged_out,
-        const uint32_t *__restrict__ active, Peers peers) {
+        const uint32_t *__restrict__ active, Peers peers, RunArgs ra) {
+  static_assert(LOGR == 0 || !PUSH, "batched runs are single-device");
   using Gm = Geo<LOGP>;
   using B = Batch<LOGP>;
   __shared__ int32_t sids[kThreads / 32][B::WARP_IDS];
@@ -584,7 +693,7 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
     RowAcc<LOGP> macc;
     macc.init();
     double vals[3] = {0.0, 0.0, 0.0};
-    if (pre && gl == 0) {
+    if (LOGR == 0 && pre && gl == 0) {
       vals[0] = est[v];
       if (sum_dist) vals[1] = sum_dist[v];
       if (sum_recip) vals[2] = sum_recip[v];
@@ -644,9 +753,15 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
 #pragma unroll
     for (int c = 0; c < Gm::CPL; c++) acc[c] = macc.get(c);
     my_merged += (gl == 0) ? (uint32_t)total : 0u;
-    const bool changed = finish_node<LOGP, PUSH>(peers, valid && (total > 0 || self_chg), v, acc, self, pre,
-                                           self_chg, grp, gl, cur, nxt, est, sum_dist,
-                                           sum_recip, ec, tf, pre ? vals : nullptr);
+    bool changed;
+    if constexpr (LOGR == 0)
+      changed = finish_node<LOGP, PUSH>(peers, valid && (total > 0 || self_chg), v, acc, self,
+                                        pre, self_chg, grp, gl, cur, nxt, est, sum_dist,
+                                        sum_recip, ec, tf, pre ? vals : nullptr);
+    else
+      changed = finish_runs<LOGP, LOGR>(valid && (total > 0 || self_chg), v, acc, self, pre,
+                                        self_chg, gl, cur, nxt, est, sum_dist, sum_recip, ec,
+                                        tf, ra);
     // Warp-level aggregation of the NPW change bits (they share one bitmap word).
     const unsigned bb = __ballot_sync(0xffffffffu, changed && gl == 0);
     if (lane == 0 && bb) {
@@ -756,7 +871,7 @@ k_heavy_partial(const int64_t *__restrict__ offsets, const int32_t *__restrict__
 // order[o0, o1) lists heavy indices j.  mega == 0: one lane group per node (nodes with few
 // items); mega != 0: one warp per node, its NPW slots striding over the items (hubs with
 // hundreds of items), merged by a shuffle tree.  Partial loads are unrolled 4-deep.
-template <int LOGP, bool PUSH>
+template <int LOGP, bool PUSH, int LOGR = 0>
 __global__ void __launch_bounds__(kThreads)
 k_heavy_finish(const int32_t *__restrict__ heavy_nodes, const int32_t *__restrict__ item_first,
                const int32_t *__restrict__ order, int64_t o0, int64_t o1, int mega,
@@ -766,7 +881,7 @@ k_heavy_finish(const int32_t *__restrict__ heavy_nodes, const int32_t *__restric
                double *__restrict__ est, double *__restrict__ sum_dist,
                double *__restrict__ sum_recip, EstConst ec, double tf,
                unsigned long long *__restrict__ nch_out, const uint32_t *__restrict__ active,
-               Peers peers) {
+               Peers peers, RunArgs ra) {
   using Gm = Geo<LOGP>;
   constexpr int UF = 4;
   const int lane = threadIdx.x & 31;
@@ -814,9 +929,15 @@ k_heavy_finish(const int32_t *__restrict__ heavy_nodes, const int32_t *__restric
     for (int c = 0; c < Gm::CPL; c++) any |= nz4(acc[c]);
     any = ((__ballot_sync(0xffffffffu, any) >> (grp * Gm::G)) & lowmask) != 0u;
     const bool self_chg = owner && test_bit(chg_prev, v);
-    const bool changed = finish_node<LOGP, PUSH>(peers, owner && (any || self_chg), v, acc, acc, false,
-                                           self_chg, grp, gl, cur, nxt, est, sum_dist,
-                                           sum_recip, ec, tf);
+    bool changed;
+    if constexpr (LOGR == 0)
+      changed = finish_node<LOGP, PUSH>(peers, owner && (any || self_chg), v, acc, acc, false,
+                                        self_chg, grp, gl, cur, nxt, est, sum_dist, sum_recip,
+                                        ec, tf);
+    else
+      changed = finish_runs<LOGP, LOGR>(owner && (any || self_chg), v, acc, acc, false,
+                                        self_chg, gl, cur, nxt, est, sum_dist, sum_recip, ec,
+                                        tf, ra);
     if (changed && gl == 0) {
       atomicOr(chg_now + (v >> 5), 1u << (v & 31));
       if constexpr (PUSH)
@@ -1368,6 +1489,24 @@ __global__ void k_hash(int64_t n, const uint64_t *__restrict__ items,
     out[i] = hash_item(items[i], replicas[i], seed);
 }
 
+// out[r] = popcount of bitmap row r (rows of `words` uint32): per-run changed counts of a
+// batched step.  One block per row.
+__global__ void k_count_bits(const uint32_t *__restrict__ bits, int64_t words,
+                             unsigned long long *__restrict__ out) {
+  const uint32_t *row = bits + (int64_t)blockIdx.x * words;
+  uint32_t c = 0;
+  for (int64_t i = threadIdx.x; i < words; i += blockDim.x) c += __popc(__ldg(row + i));
+  __shared__ uint32_t red[32];
+  c = __reduce_add_sync(0xffffffffu, c);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    uint32_t x = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0u;
+    x = __reduce_add_sync(0xffffffffu, x);
+    if (threadIdx.x == 0) out[blockIdx.x] = x;
+  }
+}
+
 // ------------------------------------------------------------------ launch helpers
 // Persisting-L2 window over the hot head of the register array.  In degree order the
 // internal ids sort nodes by in-degree, which on the R-MAT configs is also the read
@@ -1431,7 +1570,7 @@ unsigned grid_for_warps(int64_t work_warps) {
 }
 unsigned grid_for_threads(int64_t work) { return grid_for_warps((work + 31) / 32); }
 
-template <int LOGP, bool PUSH>
+template <int LOGP, bool PUSH, int LOGR = 0>
 int union_step_impl(int64_t lo, int64_t hi, const int64_t *offsets, const int32_t *succ,
                     const uint8_t *cur, uint8_t *nxt, const uint32_t *chg_prev,
                     uint32_t *chg_now, double *est, double *sum_dist, double *sum_recip,
@@ -1441,7 +1580,7 @@ int union_step_impl(int64_t lo, int64_t hi, const int64_t *offsets, const int32_
                     const int32_t *item_node, const int64_t *item_beg, int64_t n_items,
                     int64_t item_arcs, uint8_t *partial, unsigned long long *nch,
                     unsigned long long *merged, int64_t hot_rows, const uint32_t *active,
-                    const Peers &peers, cudaStream_t s) {
+                    const Peers &peers, cudaStream_t s, RunArgs ra = RunArgs{nullptr, 0, 0}) {
   using Gm = Geo<LOGP>;
   if (hot_rows > 0) {
     cudaCtxResetPersistingL2Cache();    // lines of last iteration's buffer stop persisting
@@ -1455,23 +1594,23 @@ int union_step_impl(int64_t lo, int64_t hi, const int64_t *offsets, const int32_
   }
   if (hi > lo) {
     const int64_t warps = (hi - lo + Gm::NPW - 1) / Gm::NPW + 1;   // capped at the resident set
-    k_light<LOGP, PUSH><<<grid_for_warps(warps), kThreads, 0, s>>>(
+    k_light<LOGP, PUSH, LOGR><<<grid_for_warps(warps), kThreads, 0, s>>>(
         offsets, succ, cur, nxt, chg_prev, chg_now, est, sum_dist, sum_recip, ec, lo, hi,
-        light_max_deg, dense, tf, nch, merged, active, peers);
+        light_max_deg, dense, tf, nch, merged, active, peers, ra);
     if (int e = check_launch("k_light")) return e;
   }
   if (n_heavy > 0) {
     if (n_mega > 0) {
-      k_heavy_finish<LOGP, PUSH><<<grid_for_warps(n_mega), kThreads, 0, s>>>(
+      k_heavy_finish<LOGP, PUSH, LOGR><<<grid_for_warps(n_mega), kThreads, 0, s>>>(
           heavy_nodes, item_first, finish_order, 0, n_mega, 1, partial, cur, nxt, chg_prev,
-          chg_now, est, sum_dist, sum_recip, ec, tf, nch, active, peers);
+          chg_now, est, sum_dist, sum_recip, ec, tf, nch, active, peers, ra);
       if (int e = check_launch("k_heavy_finish(mega)")) return e;
     }
     if (n_heavy > n_mega)
-      k_heavy_finish<LOGP, PUSH>
+      k_heavy_finish<LOGP, PUSH, LOGR>
           <<<grid_for_warps((n_heavy - n_mega + Gm::NPW - 1) / Gm::NPW), kThreads, 0, s>>>(
               heavy_nodes, item_first, finish_order, n_mega, n_heavy, 0, partial, cur, nxt,
-              chg_prev, chg_now, est, sum_dist, sum_recip, ec, tf, nch, active, peers);
+              chg_prev, chg_now, est, sum_dist, sum_recip, ec, tf, nch, active, peers, ra);
     if (int e = check_launch("k_heavy_finish")) return e;
   }
   if (hot_rows > 0) set_hot_window(s, nullptr, 0);
@@ -1628,6 +1767,67 @@ int hb_union_step(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets,
                      reinterpret_cast<unsigned long long *>(merged_out), hot_rows, active, peers,
                      s)));
   return 0;
+}
+
+int hb_union_step_runs(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets,
+                       const int32_t *succ, const uint8_t *cur, uint8_t *nxt,
+                       const uint32_t *chg_prev, uint32_t *chg_now, uint32_t *chg_runs,
+                       double *est, double *sum_dist, double *sum_recip, int64_t run_stride,
+                       int64_t t, const double *lc_table, double alpha_p2, double lc_cut, int b,
+                       int log2_runs, int dense, int64_t light_max_deg,
+                       const int32_t *heavy_nodes, const int32_t *item_first, int64_t n_heavy,
+                       const int32_t *finish_order, int64_t n_mega, const int32_t *item_node,
+                       const int64_t *item_beg, int64_t n_items, int64_t item_arcs,
+                       uint8_t *partial, uint64_t *nch_out, uint64_t *merged_out,
+                       uint64_t *run_nch_out, int64_t hot_rows, const uint32_t *active,
+                       void *stream) {
+  const int wb = b + log2_runs;
+  if (log2_runs < 1 || log2_runs > 4 || b < HB_MIN_B || wb > 8)
+    return set_err_msg("hb_union_step_runs: need 2..16 runs and runs * p <= 256");
+  if (n < 0 || lo < 0 || hi > n || lo > hi || t < 1 || !nch_out || !chg_runs || !run_nch_out ||
+      run_stride < n)
+    return set_err_msg("hb_union_step_runs: bad arguments");
+  if ((n_items > 0 && (!item_node || !item_beg || !partial)) ||
+      (n_heavy > 0 && (!heavy_nodes || !item_first || !finish_order || !partial)) ||
+      n_mega < 0 || n_mega > n_heavy)
+    return set_err_msg("hb_union_step_runs: heavy schedule arrays missing");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t words = (n + 31) / 32;
+  const int runs = 1 << log2_runs;
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(nch_out, 0, sizeof(uint64_t), s)) != cudaSuccess ||
+      (merged_out && (e = cudaMemsetAsync(merged_out, 0, sizeof(uint64_t), s)) != cudaSuccess))
+    return set_err("hb_union_step_runs memset", e);
+  if (n == 0) return cudaMemsetAsync(run_nch_out, 0, sizeof(uint64_t) * runs, s) == cudaSuccess
+                         ? 0 : set_err_msg("hb_union_step_runs memset");
+  if ((e = cudaMemsetAsync(chg_now, 0, sizeof(uint32_t) * (size_t)words, s)) != cudaSuccess ||
+      (e = cudaMemsetAsync(chg_runs, 0, sizeof(uint32_t) * (size_t)words * runs, s)) !=
+          cudaSuccess)
+    return set_err("hb_union_step_runs memset", e);
+  EstConst ec{alpha_p2, lc_cut, lc_table, nullptr, 0, 0, 0, {0, 0, 0, 0, 0, 0, 0, 0}};
+  Peers peers;
+  memset(&peers, 0, sizeof(peers));
+  const RunArgs ra{chg_runs, words, run_stride};
+  const double tf = (double)t;
+  int rc = 0;
+#define HB_RUNS_CASE(WB, LR)                                                                   \
+  if (wb == WB && log2_runs == LR)                                                             \
+    rc = union_step_impl<WB, false, LR>(                                                       \
+        lo, hi, offsets, succ, cur, nxt, chg_prev, chg_now, est, sum_dist, sum_recip, tf, ec,  \
+        dense, light_max_deg, heavy_nodes, item_first, n_heavy, finish_order, n_mega,          \
+        item_node, item_beg, n_items, item_arcs, partial,                                      \
+        reinterpret_cast<unsigned long long *>(nch_out),                                       \
+        reinterpret_cast<unsigned long long *>(merged_out), hot_rows, active, peers, s, ra);   \
+  else
+  HB_RUNS_CASE(5, 1) HB_RUNS_CASE(6, 1) HB_RUNS_CASE(6, 2) HB_RUNS_CASE(7, 1)
+  HB_RUNS_CASE(7, 2) HB_RUNS_CASE(7, 3) HB_RUNS_CASE(8, 1) HB_RUNS_CASE(8, 2)
+  HB_RUNS_CASE(8, 3) HB_RUNS_CASE(8, 4)
+  return set_err_msg("hb_union_step_runs: unsupported (p, runs)");
+#undef HB_RUNS_CASE
+  if (rc) return rc;
+  k_count_bits<<<runs, 256, 0, s>>>(chg_runs, words,
+                                    reinterpret_cast<unsigned long long *>(run_nch_out));
+  return check_launch("k_count_bits");
 }
 
 int hb_finalize(int64_t n, const int32_t *rank, const double *sum_dist, const double *sum_recip,

@@ -268,6 +268,17 @@ class _DeviceSums:
     def invalidate(self) -> None:
         self.stale = True
 
+    def reorder(self, old, new) -> None:
+        """The device state moved to schedule `new`: reorder the sums from `old`."""
+        def mv(x):
+            return new.to_internal(old.to_original(x)).contiguous()
+        self.sum_dist, self.sum_recip = mv(self.sum_dist), mv(self.sum_recip)
+        if self.disc.numel():
+            self.disc = torch.stack([mv(row) for row in self.disc])
+        if self.coreach_dev is not None:
+            self.coreach_dev = mv(self.coreach_dev)
+        self._fin_cache = None
+
     def still_valid(self) -> bool:
         if self.stale:
             return False
@@ -345,17 +356,22 @@ class _Device:
         self.n = self.sched.n
         self.graph_key = _graph_key(g)
 
-    def bind_graph(self, g) -> None:
+    def bind_graph(self, g):
+        """Schedule `g` (a no-op for the graph already bound).  Returns the previous
+        Schedule when it was replaced (per-node device arrays kept elsewhere, e.g. the
+        accumulator sums, must then be reordered), else None."""
         if _graph_key(g) == self.graph_key:
-            return
+            return None
         off, _ = _graph_arrays(g)
         n_new = (off.numel() if isinstance(off, torch.Tensor) else np.asarray(off).shape[0]) - 1
         if n_new != self.n:
             raise ValueError(f"graph has {n_new} nodes, state has {self.n}")
         # different graph object: carry the state over in original order
         snap = self.snapshot_original()
+        old = self.sched
         self._build_graph(g)
         self.restore_original(*snap)
+        return old
 
     # -- order conversion ----------------------------------------------------
     def to_internal(self, host_or_dev) -> torch.Tensor:
@@ -781,7 +797,9 @@ def iterate(g, state: HyperBallState, observers: Iterable = ()) -> int:
         state.t = t_next
         state.num_changed = 0
         return 0
-    dev.bind_graph(g)
+    old_sched = dev.bind_graph(g)
+    if old_sched is not None and state._sums is not None:
+        state._sums.reorder(old_sched, dev.sched)
     fused, generic = _split_observers(state, observers)
     sums = _bind_sums(state, fused)
     old = dev.est.clone() if generic else None
@@ -928,23 +946,43 @@ class _PendingState(HyperBallState):
 
 
 
-def run_multi(g, config: HyperBallConfig, runs: int, discounts=(), observers_factory=None):
+def run_multi(g, config: HyperBallConfig, runs: int, discounts=(), observers_factory=None,
+              batch: int | None = None):
     """The reference CLI's repeated runs (cli.py:222-254): run r uses seed config.seed + r
-    and its own CentralityAccumulator.  The graph is uploaded and scheduled once and every
-    run reuses it (only the counters are re-seeded).  Returns [(state, accumulator)]; feed
-    finalize_* of each accumulator to multi_run_aggregate."""
+    and its own CentralityAccumulator.  Returns [(state, accumulator)]; feed finalize_* of
+    each accumulator to multi_run_aggregate.
+
+    batch: runs sharing one union pass (multirun.py; a power of two, batch * p <= 256).
+    None picks multirun.batch_size (p = 16: 4, p = 32: 2, else 1).  Batching needs the
+    probabilistic backend, no discounts and no progress stream; otherwise, and for
+    batch = 1, the runs go one after the other, the graph uploaded and scheduled once and
+    only the counters re-seeded.  Either way every run's bits equal an independent run."""
     from dataclasses import replace
+    from . import multirun
     if runs < 1:
         raise ValueError("runs must be >= 1")
+    n = (g.offsets.numel() if isinstance(g.offsets, torch.Tensor)
+         else np.asarray(g.offsets).shape[0]) - 1
+    if batch is None:
+        batch = multirun.batch_size(config.params.p, runs)
+    if batch < 1:
+        raise ValueError("batch must be >= 1")
+    accs = [CentralityAccumulator(n, discounts) for _ in range(runs)]
+    obs = [[accs[r]] + (list(observers_factory(r)) if observers_factory else [])
+           for r in range(runs)]
+    seeds = [config.params.seed + r for r in range(runs)]
     out = []
     dev = None
-    for r in range(runs):
-        params = replace(config.params, seed=config.params.seed + r)
-        cfg = replace(config, params=params)
-        n = (g.offsets.numel() if isinstance(g.offsets, torch.Tensor)
-             else np.asarray(g.offsets).shape[0]) - 1
-        acc = CentralityAccumulator(n, discounts)
-        obs = [acc] + (list(observers_factory(r)) if observers_factory else [])
+    r = 0
+    while r < runs:
+        k = min(batch, runs - r)
+        k = 1 << (k.bit_length() - 1)                  # largest power of two <= k
+        if k >= 2 and not discounts and multirun.supported(config, k):
+            states = multirun.run_batched(g, config, seeds[r:r + k], obs[r:r + k])
+            out.extend(zip(states, accs[r:r + k]))
+            r += k
+            continue
+        cfg = replace(config, params=replace(config.params, seed=seeds[r]))
         w = _weights_array(cfg.weights, n)
         if w is not None:
             _check_weighted_width(cfg.params, w)
@@ -954,5 +992,6 @@ def run_multi(g, config: HyperBallConfig, runs: int, discounts=(), observers_fac
             dev = dev.fresh(cfg)
         state = HyperBallState(cfg, n, dev)
         dev.seed(w)
-        out.append((resume(g, state, obs), acc))
+        out.append((resume(g, state, obs[r]), accs[r]))
+        r += 1
     return out
