@@ -319,7 +319,8 @@ class SymmetricBuffers:
         self.regs = symm.empty((2, n, p), dtype=torch.uint8, device=d.device)
         self.bits = symm.empty((2, words), dtype=torch.int32, device=d.device)
         self.regs[0].copy_(d.cur)
-        self.bits[0].fill_(-1)
+        self.regs[1].copy_(d.nxt)      # seeded rows the first iteration may skip (_Device.seed)
+        self.bits[0].copy_(d.chg_prev)
         self.bits[1].zero_()
         d.cur, d.nxt = self.regs[0], self.regs[1]
         d.chg_prev, d.chg_now = self.bits[0], self.bits[1]

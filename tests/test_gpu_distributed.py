@@ -80,3 +80,58 @@ def test_fused_push_matches_reference(key, world, schedule):
     _, arrays = golden()
     assert np.array_equal(hb.finalize_lin(acc).view(np.uint64),
                           arrays[f"{key}/lin"].view(np.uint64))
+
+
+_ONE_RANK = r"""
+import hashlib, json, sys
+import numpy as np, torch, torch.distributed as dist
+sys.path.insert(0, sys.argv[1])
+import paper_1308_2144_b200 as hb
+from paper_1308_2144_b200.distributed import CudaRankState, SymmetricBuffers, iterate_push
+dist.init_process_group("nccl", init_method="tcp://127.0.0.1:" + sys.argv[2], rank=0,
+                        world_size=1, device_id=torch.device("cuda", 0))
+d = np.load(sys.argv[3])
+g = hb.CsrGraph(d["off"], d["suc"])
+cfg = hb.HyperBallConfig(params=hb.CounterParams(b=int(sys.argv[4]), seed=int(sys.argv[5])),
+                         schedule=sys.argv[6])
+st = CudaRankState(g, cfg, 1, 0)
+symm = SymmetricBuffers(st)
+t = 0
+while True:
+    t += 1
+    nch = iterate_push(st, symm, t, t == 1)
+    if nch == 0:
+        break
+regs = st.dev.to_host(st.dev.cur)
+est = st.dev.to_host(st.dev.est)
+print(json.dumps({"t": t, "regs": hashlib.sha256(regs.tobytes()).hexdigest(),
+                  "est": hashlib.sha256(np.ascontiguousarray(est).tobytes()).hexdigest()}))
+dist.destroy_process_group()
+"""
+
+
+@pytest.mark.parametrize("schedule", ["identity", "degree"])
+def test_symmetric_buffers_one_rank(tmp_path, schedule):
+    """The real fused-push plumbing (symmetric-memory double buffer, NCCL all-reduce as
+    the barrier) on a one-rank NCCL group in a subprocess: the seeded buffers are carried
+    into symmetric memory (incl. rows iteration 1 skips) and the run matches the golden."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+    case = CASES["rmat12_b7_s42_w5"]
+    off, suc = golden_graph(case)
+    path = tmp_path / "g.npz"
+    np.savez(path, off=off, suc=suc)
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", _ONE_RANK, repo, str(port), str(path), "7", "42",
+                          schedule], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    res = json.loads(out.stdout.strip().splitlines()[-1])
+    assert res["t"] == case["t"]
+    assert res["regs"] == case["reg_digests"][-1]
+    assert res["est"] == case["est_digests"][-1]
