@@ -17,6 +17,7 @@
 //     is exact.
 #include <cuda_runtime.h>
 #include <type_traits>
+#include <algorithm>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_sort.cuh>
@@ -171,6 +172,34 @@ using RowAcc = typename std::conditional<(LOGP >= HB_VMAX_MIN_LOGP), MaxAcc<Geo<
 __device__ __forceinline__ uint4 ld_chunk(const uint4 *__restrict__ cur4, int32_t w, uint32_t ch,
                                           uint32_t k) {
   return __ldg(cur4 + ((uint32_t)w * ch + k));
+}
+
+// L2 eviction priorities for the DRAM-bound small-p kernels (p <= 32, degree order): one
+// uniform range policy over cur -- rows in the hot head (the most-read rows, first
+// hb_union_step hot_lim rows) evict_last, the rest evict_first, so the random cold
+// gather stops pushing the hot rows out of L2.  Config 5: 35.9 -> 34.0 ms per dense step
+// at a 64 MB head (16-192 MB swept; HB_HINT_MB).  A per-lane choice between two policies
+// costs more than it saves (the policy lives in the load's uniform descriptor).
+#ifndef HB_HINT_MAX_LOGP
+#define HB_HINT_MAX_LOGP 5
+#endif
+__device__ __forceinline__ uint4 ld_pol(const uint4 *p, uint64_t pol) {
+  uint4 r;
+  asm("ld.global.nc.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "l"(p), "l"(pol));
+  return r;
+}
+// [base, base + hot) evict_last, [base + hot, base + total) evict_first.
+__device__ __forceinline__ uint64_t range_policy(const void *base, uint32_t hot, uint32_t total) {
+  uint64_t pol;
+  asm("createpolicy.range.global.L2::evict_last.L2::evict_first.b64 %0, [%1], %2, %3;"
+      : "=l"(pol) : "l"(base), "r"(hot), "r"(total));
+  return pol;
+}
+__device__ __forceinline__ uint4 ld_chunk_hint(const uint4 *__restrict__ cur4, int32_t w,
+                                               uint32_t ch, uint32_t k, uint64_t pol) {
+  return ld_pol(cur4 + ((uint32_t)w * ch + k), pol);
 }
 
 __device__ __forceinline__ uint4 ldg4(const uint8_t *p) {
@@ -595,7 +624,7 @@ __host__ __device__ constexpr int chunk_rounds() { return LOGP >= 8 ? 16 : 4; }
 // prefetches them into L2 kLookRounds rounds ahead, leaving the random source-row
 // gather as the only exposed memory latency of a round.
 // _kernels.py:67-114 restated with the source-skip rule.
-template <int LOGP, bool PUSH, int LOGR = 0>
+template <int LOGP, bool PUSH, int LOGR = 0, bool HINT = false>
 __global__ void __launch_bounds__(kThreads, Batch<LOGP>::MINB)
 k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
         const uint8_t *__restrict__ cur, uint8_t *__restrict__ nxt,
@@ -603,8 +632,11 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
         double *__restrict__ est, double *__restrict__ sum_dist, double *__restrict__ sum_recip,
         EstConst ec, int64_t lo, int64_t hi, int64_t max_deg, int dense, double tf,
         unsigned long long *__restrict__ nch_out, unsigned long long *__restrict__ merged_out,
-        const uint32_t *__restrict__ active, Peers peers, RunArgs ra) {
+        const uint32_t *__restrict__ active, Peers peers, RunArgs ra, int64_t hot_lim) {
   static_assert(LOGR == 0 || !PUSH, "batched runs are single-device");
+  constexpr bool kHint = HINT;
+  uint64_t pol = 0;
+  if (kHint) pol = range_policy(cur, (uint32_t)((uint64_t)hot_lim << LOGP), 0xFFFFFFF0u);
   using Gm = Geo<LOGP>;
   using B = Batch<LOGP>;
   __shared__ int32_t sids[kThreads / 32][B::WARP_IDS];
@@ -737,8 +769,10 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
           const int32_t w = ok ? my_ids[i + u] : fb;
 #pragma unroll
           for (int c = 0; c < Gm::CPL; c++)
-            r[u][c] = (LOGP >= HB_PAD_MIN_LOGP || ok) ? ld_chunk(cur4, w, Gm::CH, c * Gm::G + gl)
-                                                      : make_uint4(0, 0, 0, 0);
+            r[u][c] = (LOGP >= HB_PAD_MIN_LOGP || ok)
+                          ? (kHint ? ld_chunk_hint(cur4, w, Gm::CH, c * Gm::G + gl, pol)
+                                   : ld_chunk(cur4, w, Gm::CH, c * Gm::G + gl))
+                          : make_uint4(0, 0, 0, 0);
         }
         // sequential accumulate: a pairwise tree (shorter chains) measured 20% slower on
         // config 4 (more live registers at 127/thread)
@@ -781,13 +815,17 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
 
 // Heavy nodes, phase 1: one warp per work item (a slice of one node's arcs) leaves the
 // max over the slice's changed sources as a partial row.
-template <int LOGP>
+template <int LOGP, bool HINT = false>
 __global__ void __launch_bounds__(kThreads, (LOGP >= 10 ? 2 : 4))
 k_heavy_partial(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
                 const uint8_t *__restrict__ cur, const uint32_t *__restrict__ chg_prev,
                 const int32_t *__restrict__ item_node, const int64_t *__restrict__ item_beg,
                 int64_t n_items, int64_t item_arcs, int dense, uint8_t *__restrict__ partial,
-                unsigned long long *__restrict__ merged_out, const uint32_t *__restrict__ active) {
+                unsigned long long *__restrict__ merged_out, const uint32_t *__restrict__ active,
+                int64_t hot_lim) {
+  constexpr bool kHint = HINT;
+  uint64_t pol = 0;
+  if (kHint) pol = range_policy(cur, (uint32_t)((uint64_t)hot_lim << LOGP), 0xFFFFFFF0u);
   using Gm = Geo<LOGP>;
   using B = Batch<LOGP>;
   __shared__ int32_t sids[kThreads / 32][B::HEAVY_IDS];
@@ -841,8 +879,10 @@ k_heavy_partial(const int64_t *__restrict__ offsets, const int32_t *__restrict__
           const int32_t w = wids[ok ? e : 0];
 #pragma unroll
           for (int c = 0; c < Gm::CPL; c++)
-            r[u][c] = (LOGP >= HB_PAD_MIN_LOGP || ok) ? ld_chunk(cur4, w, Gm::CH, c * Gm::G + gl)
-                                                      : make_uint4(0, 0, 0, 0);
+            r[u][c] = (LOGP >= HB_PAD_MIN_LOGP || ok)
+                          ? (kHint ? ld_chunk_hint(cur4, w, Gm::CH, c * Gm::G + gl, pol)
+                                   : ld_chunk(cur4, w, Gm::CH, c * Gm::G + gl))
+                          : make_uint4(0, 0, 0, 0);
         }
 #pragma unroll
         for (int u = 0; u < B::U; u++)
@@ -1531,6 +1571,24 @@ size_t persist_bytes() {
   return b;
 }
 
+// Bytes of the evict_last head (HB_HINT_MB, default 64); HB_PERSIST_WINDOW=0 turns the
+// persisting access-policy window off.
+int64_t hint_bytes() {
+  static int64_t b = [] {
+    int64_t mb = 64;
+    if (const char *e = getenv("HB_HINT_MB")) mb = atoll(e);
+    return mb << 20;
+  }();
+  return b;
+}
+bool persist_window_on() {
+  static bool on = [] {
+    const char *e = getenv("HB_PERSIST_WINDOW");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
+
 void set_hot_window(cudaStream_t s, const void *base, size_t hot_bytes) {
   cudaStreamAttrValue attr;
   memset(&attr, 0, sizeof(attr));
@@ -1582,21 +1640,38 @@ int union_step_impl(int64_t lo, int64_t hi, const int64_t *offsets, const int32_
                     unsigned long long *merged, int64_t hot_rows, const uint32_t *active,
                     const Peers &peers, cudaStream_t s, RunArgs ra = RunArgs{nullptr, 0, 0}) {
   using Gm = Geo<LOGP>;
-  if (hot_rows > 0) {
+  if (hot_rows > 0 && persist_window_on()) {
     cudaCtxResetPersistingL2Cache();    // lines of last iteration's buffer stop persisting
     set_hot_window(s, cur, (size_t)hot_rows * Gm::P);
   }
+  const int64_t hot_lim = hot_rows > 0 ? std::min<int64_t>(hot_rows, hint_bytes() / Gm::P) : 0;
+  constexpr bool kCanHint = LOGP <= HB_HINT_MAX_LOGP;
+  const bool hint = kCanHint && hot_lim > 0;
   if (n_items > 0) {
-    k_heavy_partial<LOGP><<<grid_for_warps(n_items), kThreads, 0, s>>>(
-        offsets, succ, cur, chg_prev, item_node, item_beg, n_items, item_arcs, dense, partial,
-        merged, active);
+    if constexpr (kCanHint) {
+      if (hint)
+        k_heavy_partial<LOGP, true><<<grid_for_warps(n_items), kThreads, 0, s>>>(
+            offsets, succ, cur, chg_prev, item_node, item_beg, n_items, item_arcs, dense,
+            partial, merged, active, hot_lim);
+    }
+    if (!hint)
+      k_heavy_partial<LOGP, false><<<grid_for_warps(n_items), kThreads, 0, s>>>(
+          offsets, succ, cur, chg_prev, item_node, item_beg, n_items, item_arcs, dense,
+          partial, merged, active, hot_lim);
     if (int e = check_launch("k_heavy_partial")) return e;
   }
   if (hi > lo) {
     const int64_t warps = (hi - lo + Gm::NPW - 1) / Gm::NPW + 1;   // capped at the resident set
-    k_light<LOGP, PUSH, LOGR><<<grid_for_warps(warps), kThreads, 0, s>>>(
-        offsets, succ, cur, nxt, chg_prev, chg_now, est, sum_dist, sum_recip, ec, lo, hi,
-        light_max_deg, dense, tf, nch, merged, active, peers, ra);
+    if constexpr (kCanHint) {
+      if (hint)
+        k_light<LOGP, PUSH, LOGR, true><<<grid_for_warps(warps), kThreads, 0, s>>>(
+            offsets, succ, cur, nxt, chg_prev, chg_now, est, sum_dist, sum_recip, ec, lo, hi,
+            light_max_deg, dense, tf, nch, merged, active, peers, ra, hot_lim);
+    }
+    if (!hint)
+      k_light<LOGP, PUSH, LOGR, false><<<grid_for_warps(warps), kThreads, 0, s>>>(
+          offsets, succ, cur, nxt, chg_prev, chg_now, est, sum_dist, sum_recip, ec, lo, hi,
+          light_max_deg, dense, tf, nch, merged, active, peers, ra, hot_lim);
     if (int e = check_launch("k_light")) return e;
   }
   if (n_heavy > 0) {
@@ -1613,7 +1688,7 @@ int union_step_impl(int64_t lo, int64_t hi, const int64_t *offsets, const int32_
               chg_prev, chg_now, est, sum_dist, sum_recip, ec, tf, nch, active, peers, ra);
     if (int e = check_launch("k_heavy_finish")) return e;
   }
-  if (hot_rows > 0) set_hot_window(s, nullptr, 0);
+  if (hot_rows > 0 && persist_window_on()) set_hot_window(s, nullptr, 0);
   return 0;
 }
 
