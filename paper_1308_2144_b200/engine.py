@@ -51,7 +51,8 @@ CHECKPOINT_VERSION = 1
 
 BACKEND_PROBABILISTIC = "probabilistic"
 BACKEND_EXACT = "exact"
-_BACKEND_ALIASES = {"hll": BACKEND_PROBABILISTIC}
+# "cuda": the name a reference-side registration would use for this engine
+_BACKEND_ALIASES = {"hll": BACKEND_PROBABILISTIC, "cuda": BACKEND_PROBABILISTIC}
 
 
 class ConvergenceError(RuntimeError):

@@ -109,6 +109,8 @@ def test_exact_backend_config():
     """backend="exact" is accepted (and still needs the device: no CPU fallback);
     unknown backends are rejected (engine.py:82-97)."""
     assert hb.HyperBallConfig(backend="exact").backend == "exact"
+    assert hb.HyperBallConfig(backend="cuda").backend == "probabilistic"
+    assert hb.HyperBallConfig(backend="hll").backend == "probabilistic"
     with pytest.raises(ValueError):
         hb.HyperBallConfig(backend="bitmap")
     if torch.cuda.is_available():
