@@ -10,6 +10,7 @@ import paper_1308_2144_b200 as hb  # noqa: E402
 from paper_1308_2144_b200 import generators as gen, schedule as S  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "config5s"
+ORDER = sys.argv[3] if len(sys.argv) > 3 else "auto"
 cfgd = gen.CONFIGS[name]
 g = cfgd.build()
 n, m = g.n, g.m
@@ -41,7 +42,7 @@ for rep in range(3):
     T.clear()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    s = S.build_schedule(off_pin, suc_pin, cfgd.log2m, dev, "auto")
+    s = S.build_schedule(off_pin, suc_pin, cfgd.log2m, dev, ORDER)
     torch.cuda.synchronize()
     T["build_schedule_total"] = time.perf_counter() - t0
     print(rep, s.order, {k: round(v * 1000, 2) for k, v in T.items()})
@@ -50,6 +51,6 @@ for rep in range(3):
 if len(sys.argv) > 2 and sys.argv[2] == "torchprof":
     from torch.profiler import ProfilerActivity, profile
     with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
-        s = S.build_schedule(off_pin, suc_pin, cfgd.log2m, dev, "auto")
+        s = S.build_schedule(off_pin, suc_pin, cfgd.log2m, dev, ORDER)
         torch.cuda.synchronize()
     print(prof.key_averages().table(sort_by="cpu_time_total", row_limit=25))
