@@ -31,6 +31,9 @@
  *   hb_gen_rmat_keys / hb_keys_to_csr
  *                     graph.py:52-80 (from_edges: sort, dedup, CSR) + 145-155 (transpose),
  *                     for the synthetic R-MAT configs, on the device
+ *   hb_pack_registers / hb_unpack_registers
+ *                     hll.py:145-177 (CounterArray packing, to_blob / from_blob body),
+ *                     for counters(), save() and load_state() (engine.py:254-327)
  *   hb_union_step_runs
  *                     cli.py:222-254 repeated runs (engine.run per seed), batched: R runs
  *                     in one union pass
@@ -181,6 +184,17 @@ int hb_sort_rows(int64_t n, const int64_t *offsets, int64_t n_batches,
                  const int64_t *host_batch_rows, const int64_t *host_batch_arcs, int32_t *ids,
                  int32_t *alt, void *temp, uint64_t *temp_bytes, int *result_in_alt,
                  void *stream);
+
+/* At-rest register format (hll.py:128-132 CounterArray.registers, hll.py:161-177 HLLA blob
+ * body): every register's `width` low bits MSB-first, rows of p*width/8 bytes back to back.
+ * hb_pack_registers: regs (device uint8 [*, p], p = 2^b) -> out (device uint8
+ * [n, p*width/8]), packed row i taken from regs row order[i] (order: device int32 [n] or
+ * NULL = identity; pass the schedule's rank to pack in original node order).
+ * hb_unpack_registers: the inverse, regs row i from packed row order[i] (pass perm). */
+int hb_pack_registers(int64_t n, int b, int width, const uint8_t *regs, const int32_t *order,
+                      uint8_t *out, void *stream);
+int hb_unpack_registers(int64_t n, int b, int width, const uint8_t *packed, const int32_t *order,
+                        uint8_t *regs, void *stream);
 
 /* Batched runs (run_multi, cli.py:222-254): R = 2^log2_runs runs with
  * the same log2m b share one CSR scan.  cur / nxt hold n rows of R * p bytes (run r's

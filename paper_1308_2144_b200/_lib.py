@@ -48,6 +48,8 @@ HB_SIGNATURES = {
                                   _i64, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _i64, _i64, _vp,
                                   _vp, _vp, _vp, _i64, _vp, _vp]),
     "hb_mark_active": (_int, [_i64, _vp, _vp, _vp, _vp, _vp]),
+    "hb_pack_registers": (_int, [_i64, _int, _int, _vp, _vp, _vp, _vp]),
+    "hb_unpack_registers": (_int, [_i64, _int, _int, _vp, _vp, _vp, _vp]),
     "hb_mark_pull": (_int, [_i64, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _i64, _i64, _vp]),
     "hb_exact_seed": (_int, [_i64, _i64, _vp, _vp, _vp, _vp]),
     "hb_exact_union_step": (_int, [_i64, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp,

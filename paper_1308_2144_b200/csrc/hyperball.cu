@@ -1529,6 +1529,56 @@ __global__ void k_hash(int64_t n, const uint64_t *__restrict__ items,
     out[i] = hash_item(items[i], replicas[i], seed);
 }
 
+// The at-rest register format (hll.py:128-132, 161-177: CounterArray.registers and the HLLA
+// blob): each register's `width` low bits, most significant first, concatenated over the
+// row, rows back to back (p * width / 8 bytes each).  8 registers make `width` whole
+// bytes, so one thread packs / unpacks one group of 8.  `order` (may be NULL) reorders rows:
+// packed row i <-> register row order[i] (the schedule's rank / perm).
+__global__ void k_pack_registers(int64_t n, int p, int width, const uint8_t *__restrict__ regs,
+                                 const int32_t *__restrict__ order, uint8_t *__restrict__ out) {
+  const int groups = p / 8;
+  const int64_t total = n * groups;
+  const uint32_t mask = (1u << width) - 1u;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / groups;
+    const int g = (int)(i - row * groups);
+    const int64_t src = order ? (int64_t)__ldg(order + row) : row;
+    const uint2 r = __ldg(reinterpret_cast<const uint2 *>(regs + src * p + g * 8));
+    uint64_t acc = 0;
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      const uint32_t m = ((j < 4 ? r.x : r.y) >> (8 * (j & 3))) & mask;
+      acc = (acc << width) | m;
+    }
+    uint8_t *o = out + row * ((int64_t)p * width / 8) + (int64_t)g * width;
+    for (int k = 0; k < width; k++) o[k] = (uint8_t)(acc >> (8 * (width - 1 - k)));
+  }
+}
+
+__global__ void k_unpack_registers(int64_t n, int p, int width, const uint8_t *__restrict__ in,
+                                   const int32_t *__restrict__ order, uint8_t *__restrict__ regs) {
+  const int groups = p / 8;
+  const int64_t total = n * groups;
+  const uint32_t mask = (1u << width) - 1u;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / groups;
+    const int g = (int)(i - row * groups);
+    const int64_t src = order ? (int64_t)__ldg(order + row) : row;
+    const uint8_t *q = in + src * ((int64_t)p * width / 8) + (int64_t)g * width;
+    uint64_t acc = 0;
+    for (int k = 0; k < width; k++) acc = (acc << 8) | __ldg(q + k);
+    uint32_t lo = 0, hi = 0;
+#pragma unroll
+    for (int j = 0; j < 8; j++) {
+      const uint32_t m = (uint32_t)(acc >> (width * (7 - j))) & mask;
+      if (j < 4) lo |= m << (8 * j); else hi |= m << (8 * (j - 4));
+    }
+    *reinterpret_cast<uint2 *>(regs + row * p + g * 8) = make_uint2(lo, hi);
+  }
+}
+
 // out[r] = popcount of bitmap row r (rows of `words` uint32): per-run changed counts of a
 // batched step.  One block per row.
 __global__ void k_count_bits(const uint32_t *__restrict__ bits, int64_t words,
@@ -1903,6 +1953,28 @@ int hb_union_step_runs(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets
   k_count_bits<<<runs, 256, 0, s>>>(chg_runs, words,
                                     reinterpret_cast<unsigned long long *>(run_nch_out));
   return check_launch("k_count_bits");
+}
+
+int hb_pack_registers(int64_t n, int b, int width, const uint8_t *regs, const int32_t *order,
+                      uint8_t *out, void *stream) {
+  if (n <= 0) return 0;
+  if (b < HB_MIN_B || b > 16 || width < 1 || width > 8 || !regs || !out)
+    return set_err_msg("hb_pack_registers: bad arguments");
+  const int p = 1 << b;
+  k_pack_registers<<<grid_for_threads(n * (p / 8)), kThreads, 0, (cudaStream_t)stream>>>(
+      n, p, width, regs, order, out);
+  return check_launch("k_pack_registers");
+}
+
+int hb_unpack_registers(int64_t n, int b, int width, const uint8_t *packed, const int32_t *order,
+                        uint8_t *regs, void *stream) {
+  if (n <= 0) return 0;
+  if (b < HB_MIN_B || b > 16 || width < 1 || width > 8 || !packed || !regs)
+    return set_err_msg("hb_unpack_registers: bad arguments");
+  const int p = 1 << b;
+  k_unpack_registers<<<grid_for_threads(n * (p / 8)), kThreads, 0, (cudaStream_t)stream>>>(
+      n, p, width, packed, order, regs);
+  return check_launch("k_unpack_registers");
 }
 
 int hb_finalize(int64_t n, const int32_t *rank, const double *sum_dist, const double *sum_recip,

@@ -696,10 +696,21 @@ class HyperBallState:
         return m
 
     def counters(self) -> CounterArray:
-        """Bit-packed snapshot of the current counters (probabilistic only)."""
+        """Bit-packed snapshot of the current counters (probabilistic only), packed on the
+        device (hb_pack_registers) in original node order."""
         if self._exact:
             raise ValueError("packed counters exist only for the probabilistic backend")
-        return CounterArray.from_dense(self.register_matrix(), self.config.params)
+        pr = self.config.params
+        if self._dev is None or self.n == 0:
+            return CounterArray.from_dense(self.register_matrix(), pr)
+        d = self._dev
+        out = torch.empty((self.n, pr.row_bytes), dtype=torch.uint8, device=d.device)
+        rank = d.sched.rank
+        _lib.check(_lib.hb().hb_pack_registers(
+            self.n, pr.b, pr.register_width, d.cur.data_ptr(),
+            rank.data_ptr() if rank is not None else None, out.data_ptr(),
+            d.stream.cuda_stream), "hb_pack_registers")
+        return CounterArray(self.n, pr, d.to_host_raw(out).copy())
 
     def ball_members(self, v: int) -> np.ndarray:
         """Exact backend: the node ids in v's current ball (engine.py:209-211)."""
@@ -722,7 +733,7 @@ class HyperBallState:
         if self._exact:
             blob_cur, blob_nxt, kind = self.register_matrix().tobytes(), b"", 1
         else:
-            blob_cur = CounterArray.from_dense(self.register_matrix(), pr).to_blob()
+            blob_cur = self.counters().to_blob()
             blob_nxt, kind = CounterArray(self.n, pr).to_blob(), 0
         buf = io.BytesIO()
         buf.write(CHECKPOINT_MAGIC)
@@ -879,8 +890,7 @@ def load_state(path, config: HyperBallConfig | None = None, graph=None) -> Hyper
     pos += 8 * n
     weights = None
     if kind == 0:
-        dense = CounterArray.from_blob(blobs[0]).to_dense() if n else np.zeros((0, params.p),
-                                                                               np.uint8)
+        dense = CounterArray.from_blob(blobs[0])     # unpacked on the device in _attach
     else:
         weights = np.frombuffer(data, dtype=np.int64, count=n, offset=pos).copy()
         dense = np.frombuffer(blobs[0], dtype=np.uint8).reshape(n, (n + 7) // 8).copy()
@@ -911,14 +921,30 @@ class _PendingState(HyperBallState):
         dev = _make_device(g, self.config)
         if dev.n != self.n:
             raise ValueError(f"graph has {dev.n} nodes, checkpoint has {self.n}")
-        if weights is not None:
-            dev.set_weights(weights)
-            padded = np.zeros((self.n, dev.row_stride), dtype=np.uint8)
-            padded[:, :dense.shape[1]] = dense
-            dense = padded
-        cur = torch.from_numpy(dense).to(dev.device)
-        dev.restore_original(cur, cur.clone(), torch.from_numpy(est).to(dev.device),
-                             torch.from_numpy(changed_prev).to(dev.device))
+        if isinstance(dense, CounterArray):           # packed registers: unpack on device
+            pr = dense.params
+            packed = torch.from_numpy(np.ascontiguousarray(dense.registers)).to(dev.device)
+            cur = torch.empty((self.n, pr.p), dtype=torch.uint8, device=dev.device)
+            perm = dev.sched.perm
+            if self.n:
+                _lib.check(_lib.hb().hb_unpack_registers(
+                    self.n, pr.b, pr.register_width, packed.data_ptr(),
+                    perm.data_ptr() if perm is not None else None, cur.data_ptr(),
+                    dev.stream.cuda_stream), "hb_unpack_registers")
+            del packed
+            dev.cur = cur
+            dev.nxt = cur.clone()
+            dev.est = dev.to_internal(torch.from_numpy(est))
+            dev.chg_prev = pack_bits(dev.to_internal(torch.from_numpy(changed_prev)))
+        else:
+            if weights is not None:
+                dev.set_weights(weights)
+                padded = np.zeros((self.n, dev.row_stride), dtype=np.uint8)
+                padded[:, :dense.shape[1]] = dense
+                dense = padded
+            cur = torch.from_numpy(dense).to(dev.device)
+            dev.restore_original(cur, cur.clone(), torch.from_numpy(est).to(dev.device),
+                                 torch.from_numpy(changed_prev).to(dev.device))
         # the recycled buffer must hold the current rows (lazy double-buffer invariant)
         dev.nxt.copy_(dev.cur)
         dev.prev_all = bool(changed_prev.all()) if self.n else False
@@ -940,10 +966,16 @@ class _PendingState(HyperBallState):
 
     def register_matrix(self):
         if self._dev is None:
-            m = self._host[0].copy()
+            h = self._host[0]
+            m = h.to_dense() if isinstance(h, CounterArray) else h.copy()
             m.setflags(write=False)
             return m
         return super().register_matrix()
+
+    def counters(self) -> CounterArray:
+        if self._dev is None and isinstance(self._host[0], CounterArray):
+            return self._host[0].copy()
+        return super().counters()
 
 
 

@@ -353,3 +353,34 @@ def test_sorted_rows_schedule(monkeypatch):
     got = d_ids.cpu().numpy()
     want = np.concatenate([np.sort(ids[offs[i]:offs[i + 1]]) for i in range(3000)])
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("b,width", [(4, 5), (5, 3), (6, 6), (7, 8), (8, 5), (12, 5), (4, 1)])
+def test_device_register_packing(b, width):
+    """hb_pack_registers / hb_unpack_registers == hll.pack_rows / unpack_rows (the HLLA
+    layout, hll.py:145-177), with and without a row order."""
+    from paper_1308_2144_b200 import _lib
+    from paper_1308_2144_b200.hll import pack_rows, unpack_rows
+    rng = np.random.default_rng(b * 10 + width)
+    n, p = 1000, 1 << b
+    regs = rng.integers(0, 1 << width, (n, p)).astype(np.uint8)
+    order = rng.permutation(n).astype(np.int32)
+    L = _lib.hb()
+    d_regs = torch.from_numpy(regs).cuda()
+    d_ord = torch.from_numpy(order).cuda()
+    rb = p * width // 8
+    for o in (None, d_ord):
+        out = torch.empty((n, rb), dtype=torch.uint8, device="cuda")
+        _lib.check(L.hb_pack_registers(n, b, width, d_regs.data_ptr(),
+                                       o.data_ptr() if o is not None else None,
+                                       out.data_ptr(), None), "pack")
+        want = pack_rows(regs if o is None else regs[order], width)
+        assert np.array_equal(out.cpu().numpy(), want)
+        back = torch.empty_like(d_regs)
+        _lib.check(L.hb_unpack_registers(n, b, width, out.data_ptr(),
+                                         o.data_ptr() if o is not None else None,
+                                         back.data_ptr(), None), "unpack")
+        # unpack with the same order array: row i <- packed row order[i]
+        exp = unpack_rows(want, p, width)
+        exp = exp if o is None else exp[order]
+        assert np.array_equal(back.cpu().numpy(), exp)
