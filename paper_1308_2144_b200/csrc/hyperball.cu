@@ -1823,6 +1823,7 @@ int hb_estimate_rows(const uint8_t *regs, int64_t lo, int64_t hi, int b,
                      const double *lc_table, double alpha_p2, double lc_cut, double *out,
                      void *stream) {
   if (hi <= lo) return 0;
+  if (lo < 0 || !regs || !lc_table || !out) return set_err_msg("hb_estimate_rows: bad arguments");
   cudaStream_t s = (cudaStream_t)stream;
   EstConst ec{alpha_p2, lc_cut, lc_table, nullptr, 0, 0, 0, {0, 0, 0, 0, 0, 0, 0, 0}};
   HB_DISPATCH(b, (k_estimate_rows<LB><<<grid_for_threads(hi - lo), kThreads, 0, s>>>(
@@ -1856,6 +1857,9 @@ int hb_union_step(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets,
     return set_err_msg("hb_union_step: bad discount arguments (at most 8 fused)");
   if (n < 0 || lo < 0 || hi > n || lo > hi || t < 1 || !nch_out)
     return set_err_msg("hb_union_step: bad range / t / nch_out");
+  if (n > 0 && (!offsets || !succ || !cur || !nxt || !chg_prev || !chg_now || !est ||
+                !lc_table))
+    return set_err_msg("hb_union_step: null graph / register / flag / estimate array");
   if ((n_items > 0 && (!item_node || !item_beg || !partial)) ||
       (n_heavy > 0 && (!heavy_nodes || !item_first || !finish_order || !partial)) ||
       n_mega < 0 || n_mega > n_heavy)
@@ -1910,7 +1914,8 @@ int hb_union_step_runs(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets
   if (log2_runs < 1 || log2_runs > 4 || b < HB_MIN_B || wb > 8)
     return set_err_msg("hb_union_step_runs: need 2..16 runs and runs * p <= 256");
   if (n < 0 || lo < 0 || hi > n || lo > hi || t < 1 || !nch_out || !chg_runs || !run_nch_out ||
-      run_stride < n)
+      run_stride < n || (n > 0 && (!offsets || !succ || !cur || !nxt || !chg_prev || !chg_now ||
+                                   !est || !lc_table)))
     return set_err_msg("hb_union_step_runs: bad arguments");
   if ((n_items > 0 && (!item_node || !item_beg || !partial)) ||
       (n_heavy > 0 && (!heavy_nodes || !item_first || !finish_order || !partial)) ||
@@ -1995,6 +2000,9 @@ int hb_gather_changed(int64_t lo, int64_t hi, const uint32_t *chg_bits, const ui
                       int b, int packed, int32_t *ids_out, uint8_t *rows_out,
                       uint64_t *count_out, void *stream) {
   cudaStream_t s = (cudaStream_t)stream;
+  if (!count_out || lo < 0 || (hi > lo && (!chg_bits || !rows || !ids_out || !rows_out)) ||
+      b < HB_MIN_B || b > HB_MAX_B)
+    return set_err_msg("hb_gather_changed: bad arguments");
   cudaError_t e = cudaMemsetAsync(count_out, 0, sizeof(uint64_t), s);
   if (e != cudaSuccess) return set_err("hb_gather_changed memset", e);
   if (hi <= lo) return 0;
@@ -2007,6 +2015,8 @@ int hb_gather_changed(int64_t lo, int64_t hi, const uint32_t *chg_bits, const ui
 int hb_scatter_rows(int64_t k, const int32_t *ids, const uint8_t *rows, int b, int packed,
                     uint8_t *dst, uint32_t *chg_bits, void *stream) {
   if (k <= 0) return 0;
+  if (!ids || !rows || !dst || !chg_bits || b < HB_MIN_B || b > HB_MAX_B)
+    return set_err_msg("hb_scatter_rows: bad arguments");
   k_scatter_rows<<<grid_for_threads(packed ? k : k * ((1 << b) / 16)), kThreads, 0,
                    (cudaStream_t)stream>>>(k, ids, rows, 1 << b, packed, dst, chg_bits);
   return check_launch("k_scatter_rows");
@@ -2015,6 +2025,8 @@ int hb_scatter_rows(int64_t k, const int32_t *ids, const uint8_t *rows, int b, i
 int hb_refresh_rows(int64_t n, int64_t lo, int64_t hi, const uint32_t *bits, const uint8_t *src,
                     uint8_t *dst, int b, void *stream) {
   if (n <= 0) return 0;
+  if (!bits || !src || !dst || lo < 0 || hi > n || lo > hi || b < HB_MIN_B || b > HB_MAX_B)
+    return set_err_msg("hb_refresh_rows: bad arguments");
   k_refresh_rows<<<grid_for_warps((n + 31) >> 5), kThreads, 0, (cudaStream_t)stream>>>(
       n, lo, hi, bits, src, dst, 1 << b);
   return check_launch("k_refresh_rows");
@@ -2111,6 +2123,8 @@ int hb_mark_active(int64_t n, const int64_t *fwd_offsets, const int32_t *fwd_suc
                    const uint32_t *chg_prev, uint32_t *active, void *stream) {
   cudaStream_t s = (cudaStream_t)stream;
   if (n <= 0) return 0;
+  if (!fwd_offsets || !fwd_succ || !chg_prev || !active)
+    return set_err_msg("hb_mark_active: bad arguments");
   cudaError_t e = cudaMemsetAsync(active, 0, sizeof(uint32_t) * (size_t)((n + 31) / 32), s);
   if (e != cudaSuccess) return set_err("hb_mark_active memset", e);
   k_mark_active<<<grid_for_warps((n + 31) / 32), kThreads, 0, s>>>(n, fwd_offsets, fwd_succ,
@@ -2217,6 +2231,8 @@ int hb_relabel_csr(int64_t n, const int64_t *old_offsets, const int32_t *old_suc
                    const int32_t *perm, const int32_t *rank, const int64_t *new_offsets,
                    int32_t *new_succ, void *stream) {
   if (n <= 0) return 0;
+  if (!old_offsets || !old_succ || !perm || !rank || !new_offsets || !new_succ)
+    return set_err_msg("hb_relabel_csr: bad arguments");
   k_relabel<<<grid_for_warps(n), kThreads, 0, (cudaStream_t)stream>>>(
       n, old_offsets, old_succ, perm, rank, new_offsets, new_succ);
   return check_launch("k_relabel");
@@ -2225,6 +2241,7 @@ int hb_relabel_csr(int64_t n, const int64_t *old_offsets, const int32_t *old_suc
 int hb_hash_items(int64_t n, const uint64_t *items, const uint64_t *replicas, uint64_t seed,
                   uint64_t *out, void *stream) {
   if (n <= 0) return 0;
+  if (!items || !replicas || !out) return set_err_msg("hb_hash_items: bad arguments");
   k_hash<<<grid_for_threads(n), kThreads, 0, (cudaStream_t)stream>>>(n, items, replicas, seed,
                                                                       out);
   return check_launch("k_hash");

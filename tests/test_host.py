@@ -39,6 +39,44 @@ def test_library_metadata_calls():
     assert L.hb_item_arcs(4) == 512 and L.hb_item_arcs(8) == 64
 
 
+def _abi_args(name, **at):
+    """Neutral arguments for C-ABI function `name` (NULL pointers, zeros, 1.0), with
+    positional overrides at={index: value}."""
+    out = []
+    for k, ty in enumerate(_lib.HB_SIGNATURES[name][1]):
+        v = None if ty is ctypes.c_void_p else (1.0 if ty is ctypes.c_double else 0)
+        out.append(at.get(f"a{k}", v))
+    return out
+
+
+def test_c_abi_rejects_bad_arguments():
+    """Argument validation happens before any CUDA call: error code -1 and a message
+    (hb_last_error), on a host without a GPU too."""
+    L = _lib.hb()
+
+    def err(rc):
+        assert rc == -1
+        return L.hb_last_error().decode()
+    # hb_union_step(n, lo, hi, ... t at 13, b at 17, nch_out at 30)
+    base = dict(a0=10, a2=10, a13=1, a17=4, a30=ctypes.c_void_p(8))
+    assert "null" in err(L.hb_union_step(*_abi_args("hb_union_step", **base)))
+    assert "t" in err(L.hb_union_step(*_abi_args("hb_union_step", **{**base, "a13": 0})))
+    assert "range" in err(L.hb_union_step(*_abi_args("hb_union_step", **{**base, "a2": 11})))
+    assert "register_width" in err(L.hb_seed(*_abi_args("hb_seed", a2=5, a3=4, a4=9)))
+    assert "hb_pack_registers" in err(L.hb_pack_registers(*_abi_args(
+        "hb_pack_registers", a0=5, a1=2, a2=5)))
+    assert "hb_unpack_registers" in err(L.hb_unpack_registers(*_abi_args(
+        "hb_unpack_registers", a0=5, a1=4, a2=0)))
+    assert "hb_sort_rows" in err(L.hb_sort_rows(*_abi_args("hb_sort_rows", a0=5, a2=1)))
+    assert "hb_union_step_runs" in err(L.hb_union_step_runs(*_abi_args(
+        "hb_union_step_runs", a0=10, a2=10, a14=1, a18=4, a19=5)))
+    assert "hb_exact_seed" in err(L.hb_exact_seed(*_abi_args("hb_exact_seed", a0=100, a1=8)))
+    assert "hb_estimate_rows" in err(L.hb_estimate_rows(*_abi_args(
+        "hb_estimate_rows", a2=5, a3=4)))
+    assert "hb_gather_changed" in err(L.hb_gather_changed(*_abi_args(
+        "hb_gather_changed", a1=5, a4=4)))
+
+
 def test_hash_and_register_pins(pins):
     p, _ = pins
     items = np.array([int(x) for x in p["hash_items"]["items"]], dtype=np.uint64)
