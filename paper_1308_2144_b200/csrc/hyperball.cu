@@ -1857,8 +1857,7 @@ int hb_union_step(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets,
     return set_err_msg("hb_union_step: bad discount arguments (at most 8 fused)");
   if (n < 0 || lo < 0 || hi > n || lo > hi || t < 1 || !nch_out)
     return set_err_msg("hb_union_step: bad range / t / nch_out");
-  if (n > 0 && (!offsets || !succ || !cur || !nxt || !chg_prev || !chg_now || !est ||
-                !lc_table))
+  if (n > 0 && (!offsets || !cur || !nxt || !chg_prev || !chg_now || !est || !lc_table))
     return set_err_msg("hb_union_step: null graph / register / flag / estimate array");
   if ((n_items > 0 && (!item_node || !item_beg || !partial)) ||
       (n_heavy > 0 && (!heavy_nodes || !item_first || !finish_order || !partial)) ||
@@ -1914,7 +1913,7 @@ int hb_union_step_runs(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets
   if (log2_runs < 1 || log2_runs > 4 || b < HB_MIN_B || wb > 8)
     return set_err_msg("hb_union_step_runs: need 2..16 runs and runs * p <= 256");
   if (n < 0 || lo < 0 || hi > n || lo > hi || t < 1 || !nch_out || !chg_runs || !run_nch_out ||
-      run_stride < n || (n > 0 && (!offsets || !succ || !cur || !nxt || !chg_prev || !chg_now ||
+      run_stride < n || (n > 0 && (!offsets || !cur || !nxt || !chg_prev || !chg_now ||
                                    !est || !lc_table)))
     return set_err_msg("hb_union_step_runs: bad arguments");
   if ((n_items > 0 && (!item_node || !item_beg || !partial)) ||
@@ -2137,7 +2136,7 @@ int hb_mark_pull(int64_t n, const int64_t *offsets, const int32_t *succ,
                  const int32_t *item_node, const int64_t *item_beg, int64_t n_items,
                  int64_t item_arcs, void *stream) {
   if (n <= 0) return 0;
-  if (!offsets || !succ || !chg_prev || !active || (n_items > 0 && (!item_node || !item_beg)))
+  if (!offsets || !chg_prev || !active || (n_items > 0 && (!item_node || !item_beg)))
     return set_err_msg("hb_mark_pull: bad arguments");
   cudaStream_t s = (cudaStream_t)stream;
   k_mark_pull<<<grid_for_warps((n + 31) / 32), kThreads, 0, s>>>(n, offsets, succ, chg_prev,
@@ -2231,7 +2230,7 @@ int hb_relabel_csr(int64_t n, const int64_t *old_offsets, const int32_t *old_suc
                    const int32_t *perm, const int32_t *rank, const int64_t *new_offsets,
                    int32_t *new_succ, void *stream) {
   if (n <= 0) return 0;
-  if (!old_offsets || !old_succ || !perm || !rank || !new_offsets || !new_succ)
+  if (!old_offsets || !perm || !rank || !new_offsets)   // succ arrays may be empty (NULL)
     return set_err_msg("hb_relabel_csr: bad arguments");
   k_relabel<<<grid_for_warps(n), kThreads, 0, (cudaStream_t)stream>>>(
       n, old_offsets, old_succ, perm, rank, new_offsets, new_succ);
