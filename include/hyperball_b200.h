@@ -203,9 +203,10 @@ int hb_unpack_registers(int64_t n, int b, int width, const uint8_t *packed, cons
  * chg_now are the OR over runs of the change flags (source skip and lazy double buffer,
  * as hb_union_step; chg_now is cleared by the call), chg_runs (device uint32 [R, ceil(n/32)],
  * cleared by the call) receives each run's change bits and run_nch_out (device uint64 [R])
- * each run's changed count; *nch_out counts nodes with any run changed.  The schedule
- * arrays are those of build at log2m b + log2_runs (the wide row).  Every run's bits equal
- * an independent hb_union_step run with its own seed. */
+ * each run's changed count; *nch_out counts nodes with any run changed.  Discounted sums
+ * as hb_union_step, disc laid out [R, n_disc, disc_stride].  The schedule arrays are
+ * those of build at log2m b + log2_runs (the wide row).  Every run's bits equal an
+ * independent hb_union_step run with its own seed. */
 int hb_union_step_runs(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets,
                        const int32_t *succ, const uint8_t *cur, uint8_t *nxt,
                        const uint32_t *chg_prev, uint32_t *chg_now, uint32_t *chg_runs,
@@ -216,8 +217,9 @@ int hb_union_step_runs(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets
                        const int32_t *finish_order, int64_t n_mega, const int32_t *item_node,
                        const int64_t *item_beg, int64_t n_items, int64_t item_arcs,
                        uint8_t *partial, uint64_t *nch_out, uint64_t *merged_out,
-                       uint64_t *run_nch_out, int64_t hot_rows, const uint32_t *active,
-                       void *stream);
+                       uint64_t *run_nch_out, int64_t hot_rows, double *disc,
+                       int64_t disc_stride, int n_disc, const double *disc_scale, int disc_div,
+                       const uint32_t *active, void *stream);
 
 /* Exact backend (engine.py:178-213, _kernels.py:117-172): one bitset of n bits per node,
  * MSB-first bytes (the reference's rows), padded to row_stride bytes (multiple of 16,

@@ -46,7 +46,7 @@ HB_SIGNATURES = {
     "hb_union_step_runs": (_int, [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                   _vp, _vp, _i64, _i64, _vp, _dbl, _dbl, _int, _int, _int,
                                   _i64, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _i64, _i64, _vp,
-                                  _vp, _vp, _vp, _i64, _vp, _vp]),
+                                  _vp, _vp, _vp, _i64, _vp, _i64, _int, _vp, _int, _vp, _vp]),
     "hb_mark_active": (_int, [_i64, _vp, _vp, _vp, _vp, _vp]),
     "hb_pack_registers": (_int, [_i64, _int, _int, _vp, _vp, _vp, _vp]),
     "hb_unpack_registers": (_int, [_i64, _int, _int, _vp, _vp, _vp, _vp]),

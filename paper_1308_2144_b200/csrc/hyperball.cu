@@ -522,6 +522,12 @@ __device__ __forceinline__ bool finish_runs(bool doit, int64_t v,
         const double d = np_max0(__dsub_rn(e, old));
         if (sum_dist) sum_dist[at] = __dadd_rn(sum_dist[at], __dmul_rn(tf, d));
         if (sum_recip) sum_recip[at] = __dadd_rn(sum_recip[at], __ddiv_rn(d, tf));
+        for (int k = 0; k < ec.n_disc; k++) {   // run r's discounts: [R, n_disc, stride]
+          double *q = ec.disc + ((int64_t)r * ec.n_disc + k) * ec.disc_stride + v;
+          const double cc = ((ec.disc_div >> k) & 1) ? __ddiv_rn(d, tf)
+                                                     : __dmul_rn(ec.disc_scale[k], d);
+          *q = __dadd_rn(*q, cc);
+        }
         atomicOr(ra.chg + r * ra.words + (v >> 5), 1u << (v & 31));
       }
     }
@@ -1907,8 +1913,9 @@ int hb_union_step_runs(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets
                        const int32_t *finish_order, int64_t n_mega, const int32_t *item_node,
                        const int64_t *item_beg, int64_t n_items, int64_t item_arcs,
                        uint8_t *partial, uint64_t *nch_out, uint64_t *merged_out,
-                       uint64_t *run_nch_out, int64_t hot_rows, const uint32_t *active,
-                       void *stream) {
+                       uint64_t *run_nch_out, int64_t hot_rows, double *disc,
+                       int64_t disc_stride, int n_disc, const double *disc_scale, int disc_div,
+                       const uint32_t *active, void *stream) {
   const int wb = b + log2_runs;
   if (log2_runs < 1 || log2_runs > 4 || b < HB_MIN_B || wb > 8)
     return set_err_msg("hb_union_step_runs: need 2..16 runs and runs * p <= 256");
@@ -1933,7 +1940,10 @@ int hb_union_step_runs(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets
       (e = cudaMemsetAsync(chg_runs, 0, sizeof(uint32_t) * (size_t)words * runs, s)) !=
           cudaSuccess)
     return set_err("hb_union_step_runs memset", e);
-  EstConst ec{alpha_p2, lc_cut, lc_table, nullptr, 0, 0, 0, {0, 0, 0, 0, 0, 0, 0, 0}};
+  if (n_disc < 0 || n_disc > kMaxDisc || (n_disc > 0 && (!disc || !disc_scale)))
+    return set_err_msg("hb_union_step_runs: bad discount arguments (at most 8 fused)");
+  EstConst ec{alpha_p2, lc_cut, lc_table, disc, disc_stride, n_disc, disc_div, {0, 0, 0, 0, 0, 0, 0, 0}};
+  for (int k = 0; k < n_disc; k++) ec.disc_scale[k] = disc_scale[k];
   Peers peers;
   memset(&peers, 0, sizeof(peers));
   const RunArgs ra{chg_runs, words, run_stride};

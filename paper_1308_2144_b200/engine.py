@@ -987,7 +987,7 @@ def run_multi(g, config: HyperBallConfig, runs: int, discounts=(), observers_fac
 
     batch: runs sharing one union pass (multirun.py; a power of two, batch * p <= 256).
     None picks multirun.batch_size (p = 16: 4, p = 32: 2, else 1).  Batching needs the
-    probabilistic backend, no discounts and no progress stream; otherwise, and for
+    probabilistic backend and at most 8 device-fusable discounts; otherwise, and for
     batch = 1, the runs go one after the other, the graph uploaded and scheduled once and
     only the counters re-seeded.  Either way every run's bits equal an independent run."""
     from dataclasses import replace
@@ -1010,8 +1010,8 @@ def run_multi(g, config: HyperBallConfig, runs: int, discounts=(), observers_fac
     while r < runs:
         k = min(batch, runs - r)
         k = 1 << (k.bit_length() - 1)                  # largest power of two <= k
-        if k >= 2 and not discounts and multirun.supported(config, k):
-            states = multirun.run_batched(g, config, seeds[r:r + k], obs[r:r + k])
+        if k >= 2 and multirun.supported(config, k, discounts):
+            states = multirun.run_batched(g, config, seeds[r:r + k], obs[r:r + k], discounts)
             out.extend(zip(states, accs[r:r + k]))
             r += k
             continue

@@ -22,6 +22,8 @@ device as after ``run``.
 
 from __future__ import annotations
 
+import ctypes
+import time
 import weakref
 from dataclasses import replace
 
@@ -29,7 +31,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .centrality import CentralityAccumulator
+from .centrality import MAX_FUSED_DISCOUNTS, CentralityAccumulator
 from .engine import (FRONTIER_DIV, ConvergenceError, HyperBallConfig, HyperBallState, _Device,
                      _DeviceSums, _PINNED, _check_weighted_width, _graph_arrays,
                      _resolve_device, _weights_array)
@@ -48,18 +50,20 @@ def batch_size(p: int, runs: int) -> int:
     return min(runs, 64 // p)
 
 
-def supported(config: HyperBallConfig, batch: int) -> bool:
+def supported(config: HyperBallConfig, batch: int, discounts=()) -> bool:
     p = config.params.p
     return (batch >= 2 and batch & (batch - 1) == 0 and batch <= MAX_RUNS
             and batch * p <= MAX_ROW_BYTES and config.backend == "probabilistic"
-            and config.progress is None)
+            and len(discounts) <= MAX_FUSED_DISCOUNTS
+            and all(hasattr(d, "device_factor") for d in discounts))
 
 
 class _Batch:
     """Device state of R = 2^k runs sharing one wide-row register array."""
 
-    def __init__(self, g, config: HyperBallConfig, seeds, weights):
+    def __init__(self, g, config: HyperBallConfig, seeds, weights, discounts=()):
         pr = config.params
+        self.specs = list(discounts)
         self.R = len(seeds)
         self.log2r = self.R.bit_length() - 1
         self.b, self.p = pr.b, pr.p
@@ -79,6 +83,7 @@ class _Batch:
         self.est = torch.zeros((R, n), dtype=torch.float64, device=dv)
         self.sum_dist = torch.zeros((R, n), dtype=torch.float64, device=dv)
         self.sum_recip = torch.zeros((R, n), dtype=torch.float64, device=dv)
+        self.disc = torch.zeros((R, len(self.specs), n), dtype=torch.float64, device=dv)
         self.chg_prev = torch.full((words,), -1, dtype=torch.int32, device=dv)
         self.chg_now = torch.zeros((words,), dtype=torch.int32, device=dv)
         self.chg_runs = torch.zeros((R, words), dtype=torch.int32, device=dv)
@@ -131,6 +136,13 @@ class _Batch:
         active = self._frontier(dense) if frontier else None
         light_hi = s.light_hi if self.full_pass else s.light_hi_steady
         c = self.counts
+        k = len(self.specs)
+        scale = (ctypes.c_double * max(k, 1))()
+        div = 0
+        for i, spec in enumerate(self.specs):
+            dflag, f = spec.device_factor(t)
+            scale[i] = f
+            div |= int(dflag) << i
         _lib.check(_lib.hb().hb_union_step_runs(
             self.n, s.light_lo, light_hi, s.offsets.data_ptr(), s.succ.data_ptr(),
             self.cur.data_ptr(), self.nxt.data_ptr(), self.chg_prev.data_ptr(),
@@ -140,7 +152,9 @@ class _Batch:
             s.light_max_deg, s.heavy_nodes.data_ptr(), s.item_first.data_ptr(), s.n_heavy,
             s.finish_order.data_ptr(), s.n_mega, s.item_node.data_ptr(), s.item_beg.data_ptr(),
             s.n_items, s.item_arcs, s.partial.data_ptr(), c.data_ptr(), c.data_ptr() + 8,
-            c.data_ptr() + 16, s.hot_rows, active, self.stream.cuda_stream),
+            c.data_ptr() + 16, s.hot_rows, self.disc.data_ptr() if k else None, self.n, k,
+            ctypes.cast(scale, ctypes.c_void_p) if k else None, div, active,
+            self.stream.cuda_stream),
             "hb_union_step_runs")
         self.launches += ((light_hi > s.light_lo) + (s.n_items > 0) + (s.n_heavy > 0)
                           + (s.n_mega > 0 and s.n_heavy > s.n_mega) + 1)
@@ -164,10 +178,11 @@ def _to_host(x: torch.Tensor, stream) -> np.ndarray:
     return arr.copy()
 
 
-def run_batched(g, config: HyperBallConfig, seeds, observers):
+def run_batched(g, config: HyperBallConfig, seeds, observers, discounts=()):
     """Runs with `seeds` (len a power of two, <= 16, len * p <= 256) in one batch.
-    observers[r]: run r's observers (a CentralityAccumulator among them is folded on the
-    device).  Returns the per-run HyperBallStates."""
+    observers[r]: run r's observers (a CentralityAccumulator among them, with `discounts`,
+    is folded on the device).  Progress lines (config.progress) are written run after run
+    once the batch is done, in the reference's format.  Returns the per-run states."""
     n = (g.offsets.numel() if isinstance(g.offsets, torch.Tensor)
          else np.asarray(g.offsets).shape[0]) - 1
     w = _weights_array(config.weights, n)
@@ -178,9 +193,11 @@ def run_batched(g, config: HyperBallConfig, seeds, observers):
     if n == 0:
         from .engine import run
         return [run(g, c, obs) for c, obs in zip(cfgs, observers)]
-    bt = _Batch(g, config, seeds, w)
+    bt = _Batch(g, config, seeds, w, discounts)
+    names = [d.name for d in discounts]
     fused = [next((o for o in obs if isinstance(o, CentralityAccumulator) and o.n == n
-                   and not o.discounts), None) for obs in observers]
+                   and [d.name for d in o.discounts] == names), None) for obs in observers]
+    lines = [[] for _ in range(R)]
     generic = [[o for o in obs if o is not f] for obs, f in zip(observers, fused)]
     need_old = any(generic)
     done = [False] * R
@@ -188,12 +205,16 @@ def run_batched(g, config: HyperBallConfig, seeds, observers):
     t = 0
     while True:
         t += 1
+        started = time.perf_counter()
         dense = bt.prev_all or not config.skip_stable_nodes
         old = bt.est.clone() if need_old else None
         _, per_run = bt.step(t, dense, config.frontier)
+        elapsed_ms = (time.perf_counter() - started) * 1000.0
         for r in range(R):
             if done[r]:
                 continue
+            if config.progress is not None:
+                lines[r].append(f"t={t} changed={per_run[r]} elapsed_ms={elapsed_ms:.0f}\n")
             if generic[r]:
                 o_h, n_h = bt.host_est(r, old), bt.host_est(r)
                 o_h.setflags(write=False)
@@ -206,6 +227,9 @@ def run_batched(g, config: HyperBallConfig, seeds, observers):
                 raise ConvergenceError(t, per_run[r])
         if all(done):
             break
+    if config.progress is not None:
+        for r in range(R):
+            config.progress.write("".join(lines[r]))
     # hand every run an ordinary single-run state: its device arrays are sliced out of the
     # batch (internal order of the batch schedule); the single-run schedule is only built
     # if the state is iterated again (graph_key None -> _Device.bind_graph relabels)
@@ -217,7 +241,8 @@ def run_batched(g, config: HyperBallConfig, seeds, observers):
         st = HyperBallState(cfgs[r], n, dev)
         st.t, st.num_changed = t_run[r], 0
         if fused[r] is not None:
-            _bind_batch_sums(st, fused[r], bt.sum_dist[r], bt.sum_recip[r])
+            _bind_batch_sums(st, fused[r], bt.sum_dist[r], bt.sum_recip[r], bt.disc[r],
+                             bt.specs)
         final = st.est
         final.setflags(write=False)
         for obs in observers[r]:
@@ -253,7 +278,7 @@ def _parked_device(bt: _Batch, cfg: HyperBallConfig, cur: torch.Tensor,
 
 
 def _bind_batch_sums(st: HyperBallState, acc, sum_dist: torch.Tensor,
-                     sum_recip: torch.Tensor) -> None:
+                     sum_recip: torch.Tensor, disc: torch.Tensor, specs) -> None:
     """Leave run r's sums on the device as the accumulator's binding (device finalize);
     reference accumulators (foreign classes) get host copies."""
     dev = st._dev
@@ -266,9 +291,9 @@ def _bind_batch_sums(st: HyperBallState, acc, sum_dist: torch.Tensor,
     sums._acc = weakref.ref(acc)
     sums.foreign = False
     sums.host_ids = (id(acc._sum_dist), id(acc._sum_recip))
-    sums.specs = []
+    sums.specs = list(specs)
     sums.sum_dist, sums.sum_recip = sum_dist, sum_recip
-    sums.disc = torch.zeros((0, dev.n), dtype=torch.float64, device=dev.device)
+    sums.disc = disc
     sums.dirty, sums.stale = True, False
     acc._binding = sums
     acc._fresh = False

@@ -143,3 +143,29 @@ def test_batch_size_policy():
     cfg = hb.HyperBallConfig(params=hb.CounterParams(b=4))
     assert multirun.supported(cfg, 4) and multirun.supported(cfg, 16)
     assert not multirun.supported(cfg, 3) and not multirun.supported(cfg, 32)
+
+
+def test_batched_discounts_and_progress():
+    """Fused discounts per run ([R, k, n] on the device) and the per-run progress lines of
+    the reference loop (engine.py:420-425), written run after run."""
+    import io
+    import re
+    case = CASES["random300_b4_s42_w5"]
+    off, suc = golden_graph(case)
+    g = hb.CsrGraph(off, suc)
+    specs = [hb.DiscountSpec.preset("harmonic"), hb.DiscountSpec.preset("log"),
+             hb.DiscountSpec.from_table((1.0, 0.5, 0.25), 0.125, name="table")]
+    outs, prog = {}, {}
+    for batch in (1, 4):
+        prog[batch] = io.StringIO()
+        cfg = hb.HyperBallConfig(params=hb.CounterParams(b=4, seed=42), progress=prog[batch])
+        outs[batch] = hb.run_multi(g, cfg, 4, discounts=specs, batch=batch)
+    for (sa, aa), (sb, ab) in zip(outs[1], outs[4]):
+        assert sa.t == sb.t
+        for spec in specs:
+            assert np.array_equal(bits(hb.finalize_discounted(aa, spec.name)),
+                                  bits(hb.finalize_discounted(ab, spec.name))), spec.name
+        assert np.array_equal(bits(hb.finalize_harmonic(aa)), bits(hb.finalize_harmonic(ab)))
+    strip = [re.sub(r"elapsed_ms=\d+", "", prog[b].getvalue()) for b in (1, 4)]
+    assert strip[0] == strip[1] and strip[0].count("\n") == sum(s.t for s, _ in outs[1])
+    assert outs[4][0][1]._binding is not None          # discounts stayed on the device
