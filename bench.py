@@ -268,6 +268,10 @@ def run_b200(args):
     s = dev.sched
     stream = dev.stream
     L = _lib.hb()
+    # the config's outputs (BASELINE: config 5 is harmonic only): closeness and Lin need
+    # sum_dist, harmonic needs sum_recip
+    outputs = tuple(cfgd.outputs)
+    need_dist = "closeness" in outputs or "lin" in outputs
 
     def step(ev0=None, ev1=None):
         """One dense iteration: union kernels (+ exchange of changed rows when N > 1: fused
@@ -282,7 +286,8 @@ def run_b200(args):
             n, s.light_lo, s.light_hi if dev.full_pass else s.light_hi_steady,
             s.offsets.data_ptr(), s.succ.data_ptr(),
             dev.cur.data_ptr(), dev.nxt.data_ptr(), dev.chg_prev.data_ptr(),
-            dev.chg_now.data_ptr(), clear, dev.est.data_ptr(), sums.sum_dist.data_ptr(),
+            dev.chg_now.data_ptr(), clear, dev.est.data_ptr(),
+            sums.sum_dist.data_ptr() if need_dist else None,
             sums.sum_recip.data_ptr(), 1, dev.lc.data_ptr(), dev.alpha_p2, dev.lc_cut, b, 1,
             s.light_max_deg, s.heavy_nodes.data_ptr(), s.item_first.data_ptr(), s.n_heavy,
             s.finish_order.data_ptr(), s.n_mega, s.item_node.data_ptr(), s.item_beg.data_ptr(), s.n_items, s.item_arcs,
@@ -381,14 +386,12 @@ def run_b200(args):
                 st2 = run_distributed(gp, cfg2, [acc2], exchange=args.exchange)
             else:
                 st2 = hb.run(gp, cfg2, [acc2])
-            har = hb.finalize_harmonic(acc2)
-            clo = hb.finalize_closeness(acc2)
-            lin = hb.finalize_lin(acc2)
+            fins = [getattr(hb, f"finalize_{o}")(acc2) for o in outputs]
             torch.cuda.synchronize()
             dt = time.perf_counter() - t0
             merged_total = (st2._dev.merged_total if world == 1 else st2.merged_total)
             iters = st2.t
-            del st2, acc2, har, clo, lin
+            del st2, acc2, fins
             if i >= args.e2e_warmup:
                 runs.append((dt, merged_total, iters))
         dt = max(r[0] for r in runs) if runs else float("nan")
@@ -403,12 +406,12 @@ def run_b200(args):
         mean_dt = sum_dt / len(dts)
         e2e = {"value": merged_total * p / mean_dt, "unit": UNIT,
                "h2d_bytes_per_step": int(off_pin.numel() * 8 + suc_pin.numel() * 4),
-               "d2h_bytes_per_step": int(n * 8 * 3 + 16 * iters),
+               "d2h_bytes_per_step": int(n * 8 * len(outputs) + 16 * iters),
                "seconds_per_run": mean_dt, "iterations": iters,
                "merged_arcs_per_run": merged_total,
-               "what": "run(g, config, [CentralityAccumulator]) + finalize_{harmonic,closeness,"
-                       "lin} from pinned host CSR; graph upload, schedule, seed, all "
-                       "iterations to convergence and result download timed"}
+               "what": "run(g, config, [CentralityAccumulator]) + finalize_{%s} from pinned "
+                       "host CSR; graph upload, schedule, seed, all iterations to convergence "
+                       "and result download timed" % ",".join(outputs)}
         whole = {"iterations": iters, "merged_arcs": merged_total,
                  "dense_equivalent_arcs": m * iters}
 
@@ -432,9 +435,12 @@ def run_b200(args):
                        "log2m": b, "register_width": 5, "hash_seed": seed,
                        "schedule": s.order, "heavy_nodes": s.n_heavy, "items": s.n_items,
                        "step": "one dense iteration (all sources changed): union + estimate + "
-                               "fused harmonic/closeness/Lin accumulate",
-                       "l2": "inputs larger than L2 (%.2f GB of registers), no flush"
-                             % (n * p / 1e9),
+                               "fused accumulate for %s" % "/".join(outputs),
+                       "l2": ("inputs larger than L2 (%.2f GB of registers + %.2f GB of CSR), "
+                              "no flush" if n * p > 126e6 else
+                              "registers (%.2f GB) + CSR (%.2f GB) partly L2-resident, no "
+                              "flush: a small-graph line") % (n * p / 1e9,
+                                                             (8 * (n + 1) + 4 * m) / 1e9),
                        "parallelism": (f"node-partition x{world}, {args.exchange} exchange"
                                        if world > 1 else "single GPU")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -226,8 +226,9 @@ class _DeviceSums:
     _fin_cache = None   # (key, {name: host array}, {name: handed out once})
 
     def finalize(self, which: str) -> np.ndarray:
-        """closeness / harmonic / lin on the device (one hb_finalize for all three, one
-        pinned device->host copy), original order; later calls reuse the copy."""
+        """closeness / harmonic / lin on the device (one hb_finalize computes all three in
+        original order and keeps them there); each is copied to the host (pinned) on its
+        first request only, so a harmonic-only caller downloads n doubles, not 3n."""
         dev = self.dev
         key = (dev.launches_at_last_step, self.coreach_host_id)
         if self._fin_cache is None or self._fin_cache[0] != key:
@@ -242,16 +243,15 @@ class _DeviceSums:
                 out[1].data_ptr(), out[2].data_ptr() if with_lin else None,
                 dev.stream.cuda_stream), "hb_finalize")
             dev.launches += 1
-            host = dev.to_host_raw(out)
-            names = ["closeness", "harmonic", "lin"][:host.shape[0]]
-            self._fin_cache = (key, {nm: host[i] for i, nm in enumerate(names)}, set())
-        _, arrays, given = self._fin_cache
-        if which not in arrays:
+            names = ["closeness", "harmonic", "lin"][:out.shape[0]]
+            self._fin_cache = (key, {nm: out[i] for i, nm in enumerate(names)}, {})
+        _, device_rows, host = self._fin_cache
+        if which not in device_rows:
             return None
-        if which in given:                 # the reference returns a fresh array per call
-            return arrays[which].copy()
-        given.add(which)
-        return arrays[which]
+        if which in host:                  # the reference returns a fresh array per call
+            return host[which].copy()
+        host[which] = dev.to_host_raw(device_rows[which])
+        return host[which]
 
     def pull_into(self, acc) -> None:
         sd = self.dev.to_host(self.sum_dist)
