@@ -35,7 +35,7 @@ import torch.distributed as dist
 
 from . import _lib
 from .centrality import CentralityAccumulator, fusable
-from .engine import (ConvergenceError, HyperBallConfig, _Device, _weights_array,
+from .engine import (DENSE_FRAC, ConvergenceError, HyperBallConfig, _Device, _weights_array,
                      _check_weighted_width)
 
 
@@ -247,7 +247,8 @@ def run_distributed(g, config: HyperBallConfig, observers: Iterable = (), group=
     if st.n > 0:
         while True:
             started = time.perf_counter()
-            dense = t == 0 or not config.skip_stable_nodes
+            dense = (t == 0 or not config.skip_stable_nodes
+                     or nch >= DENSE_FRAC * st.n)   # every rank sees the same global nch
             if symm is not None:
                 nch = iterate_push(st, symm, t + 1, dense, group)
             else:
@@ -353,7 +354,8 @@ def run_simulated(g, config: HyperBallConfig, world: int, observers: Iterable = 
     nch = states[0].n
     if nch > 0:
         while True:
-            dense = t == 0 or not config.skip_stable_nodes
+            dense = (t == 0 or not config.skip_stable_nodes
+                     or nch >= DENSE_FRAC * states[0].n)
             if exchange == "push":
                 # every rank's epilogue writes into the other ranks' buffers; the ranks
                 # run one after another, so no kernel ever waits on another

@@ -46,6 +46,10 @@ FRONTIER_DIV = int(_os.environ.get("HB_FRONTIER_DIV", "8"))
 # the forward graph costs several full scans; short tails do not repay it)
 FRONTIER_AFTER = int(_os.environ.get("HB_FRONTIER_AFTER", "4"))
 
+# a step runs dense (no per-source change test) when at least this fraction of the counters
+# changed in the previous iteration
+DENSE_FRAC = float(_os.environ.get("HB_DENSE_FRAC", "0.95"))
+
 CHECKPOINT_MAGIC = b"HBCK"
 CHECKPOINT_VERSION = 1
 
@@ -421,14 +425,17 @@ class _Device:
         self.launches += 1 if self.n else 0
         self._seed_weights = w
         s = self.sched
-        if s.light_hi_steady < s.light_hi:
+        if s.light_hi_steady < s.light_hi or self.world > 1:
             # Degree order: the zero in-degree suffix never changes, so seed its rows into
             # both buffers (one copy per run) and let iteration 1 skip those nodes too --
             # on R-MAT about half of all nodes (config 5: ~1.7 ms per dense iteration).
-            # Every replica copies all n rows (other ranks' suffixes are never pushed).
+            # With several ranks every replica copies all n rows whatever its own slice
+            # looks like: a peer's skipped suffix is never pushed, and dense steps read
+            # every source row.
             with torch.cuda.stream(self.stream):
                 self.nxt.copy_(self.cur)
-            self.full_pass = False
+            if s.light_hi_steady < s.light_hi:
+                self.full_pass = False
 
     def _forward(self):
         """Forward CSR (out-neighbours, internal ids, rows unordered) for frontier marking;
@@ -815,7 +822,11 @@ def iterate(g, state: HyperBallState, observers: Iterable = ()) -> int:
     fused, generic = _split_observers(state, observers)
     sums = _bind_sums(state, fused)
     old = dev.est.clone() if generic else None
-    dense = dev.prev_all or not state.config.skip_stable_nodes
+    # Merging an unchanged source is a no-op, so when nearly every counter
+    # changed last iteration the step skips the per-source bitmap tests (dense mode):
+    # identical bits, less work per arc.
+    dense = (dev.prev_all or not state.config.skip_stable_nodes
+             or (dev.last_nch is not None and dev.last_nch >= DENSE_FRAC * dev.n))
     nch = dev.union_step(t_next, dense, sums)
     if generic:
         old_h, new_h = dev.to_host(old), dev.to_host(dev.est)

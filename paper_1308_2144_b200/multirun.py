@@ -32,7 +32,7 @@ import torch
 
 from . import _lib
 from .centrality import MAX_FUSED_DISCOUNTS, CentralityAccumulator
-from .engine import (FRONTIER_DIV, ConvergenceError, HyperBallConfig, HyperBallState, _Device,
+from .engine import (DENSE_FRAC, FRONTIER_DIV, ConvergenceError, HyperBallConfig, HyperBallState, _Device,
                      _DeviceSums, _PINNED, _check_weighted_width, _graph_arrays,
                      _resolve_device, _weights_array)
 from .hll import estimator_constants, lc_table
@@ -206,7 +206,8 @@ def run_batched(g, config: HyperBallConfig, seeds, observers, discounts=()):
     while True:
         t += 1
         started = time.perf_counter()
-        dense = bt.prev_all or not config.skip_stable_nodes
+        dense = (bt.prev_all or not config.skip_stable_nodes
+                 or (bt.last_nch is not None and bt.last_nch >= DENSE_FRAC * n))
         old = bt.est.clone() if need_old else None
         _, per_run = bt.step(t, dense, config.frontier)
         elapsed_ms = (time.perf_counter() - started) * 1000.0
