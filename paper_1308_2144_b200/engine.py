@@ -295,7 +295,10 @@ class _DeviceSums:
 class _Device:
     """Per-run device resources; all per-node arrays are in internal (schedule) order."""
 
-    def __init__(self, g, config: HyperBallConfig, world: int = 1, rank_id: int = 0):
+    def __init__(self, g, config: HyperBallConfig, world: int = 1, rank_id: int = 0,
+                 seed_weights=False):
+        """seed_weights: False = do not seed; None or an int64 array = seed (as seed())
+        while the successor ids are still being uploaded (build_schedule's on_order)."""
         self.params = config.params
         self.b = config.params.b
         self.p = config.params.p
@@ -307,8 +310,9 @@ class _Device:
         self.stream = torch.cuda.current_stream(self.device)
         self.order = config.schedule
         self.world, self.rank_id = world, rank_id
-        self._build_graph(g)
-        n, p = self.n, self.p
+        off, _ = _graph_arrays(g)
+        n = (off.numel() if isinstance(off, torch.Tensor) else np.asarray(off).shape[0]) - 1
+        p = self.p
         words = max((n + 31) // 32, 1)
         dv = self.device
         self.cur = torch.empty((n, p), dtype=torch.uint8, device=dv)
@@ -328,6 +332,13 @@ class _Device:
         self.fwd = None               # forward CSR (internal ids), built on first use
         self.active = None
         self.last_nch = None
+        early = None
+        if seed_weights is not False:
+            def early(perm):
+                self._launch_seed(seed_weights, perm)
+        self._build_graph(g, on_order=early)
+        if early is not None:
+            self._after_seed()
 
     def fresh(self, config: HyperBallConfig) -> "_Device":
         """A new device state for another run on the same graph and schedule."""
@@ -353,11 +364,12 @@ class _Device:
         return other
 
     # -- graph ---------------------------------------------------------------
-    def _build_graph(self, g) -> None:
+    def _build_graph(self, g, on_order=None) -> None:
         off, suc = _graph_arrays(g)
         with torch.cuda.device(self.device):
             self.sched: Schedule = build_schedule(off, suc, self.b, self.device, self.order,
-                                                  self.world, self.rank_id, self.stream)
+                                                  self.world, self.rank_id, self.stream,
+                                                  on_order=on_order)
         self.n = self.sched.n
         self.graph_key = _graph_key(g)
 
@@ -412,18 +424,23 @@ class _Device:
 
     # -- kernels -------------------------------------------------------------
     def seed(self, weights: np.ndarray | None) -> None:
+        self._launch_seed(weights, self.sched.perm)
+        self._after_seed()
+
+    def _launch_seed(self, weights, perm) -> None:
         w = None
         if weights is not None:
             w = torch.from_numpy(np.ascontiguousarray(weights, dtype=np.int64)).to(self.device)
-        perm = self.sched.perm
         _lib.check(_lib.hb().hb_seed(
-            self.cur.data_ptr(), self.est.data_ptr(), self.n, self.b,
+            self.cur.data_ptr(), self.est.data_ptr(), self.cur.shape[0], self.b,
             self.params.register_width, self.params.seed & ((1 << 64) - 1),
             perm.data_ptr() if perm is not None else None,
             w.data_ptr() if w is not None else None, self.lc.data_ptr(), self.alpha_p2,
             self.lc_cut, self.stream.cuda_stream), "hb_seed")
-        self.launches += 1 if self.n else 0
+        self.launches += 1 if self.cur.shape[0] else 0
         self._seed_weights = w
+
+    def _after_seed(self) -> None:
         s = self.sched
         if s.light_hi_steady < s.light_hi or self.world > 1:
             # Degree order: the zero in-degree suffix never changes, so seed its rows into
@@ -767,10 +784,12 @@ def initialize(g, config: HyperBallConfig) -> HyperBallState:
     w = _weights_array(config.weights, n)
     if w is not None:
         _check_weighted_width(config.params, w)
-    dev = _make_device(g, config)
-    state = HyperBallState(config, n, dev)
-    dev.seed(w)
-    return state
+    if config.backend == BACKEND_EXACT:
+        dev = _ExactDevice(g, config)
+        dev.seed(w)
+    else:                        # seeded while the successor ids are still uploading
+        dev = _Device(g, config, seed_weights=w)
+    return HyperBallState(config, n, dev)
 
 
 def _split_observers(state: HyperBallState, observers):

@@ -100,6 +100,27 @@ def unpack_bits(words: torch.Tensor, n: int) -> torch.Tensor:
 MEGA_ITEMS = 16   # heavy nodes with more work items than this are finished one warp each
 
 
+_SIDE_STREAMS = {}
+
+
+def _upload_on_side_stream(a, device, main):
+    """int32 successor ids on the device.  A host array is copied on a side stream (the
+    copy engine) so that it overlaps the offsets-only work on `main`; returns the tensor
+    and the event `main` must wait on (None when nothing was uploaded)."""
+    if isinstance(a, torch.Tensor) and a.is_cuda:
+        return _as_device(a, torch.int32, device), None
+    side = _SIDE_STREAMS.get(device)
+    if side is None:
+        side = _SIDE_STREAMS[device] = torch.cuda.Stream(device=device)
+    side.wait_stream(main)
+    with torch.cuda.stream(side):
+        t = _as_device(a, torch.int32, device)
+        ev = torch.cuda.Event()
+        ev.record(side)
+    t.record_stream(main)
+    return t, ev
+
+
 def _as_device(a, dtype, device) -> torch.Tensor:
     if isinstance(a, torch.Tensor):
         return a.to(device=device, dtype=dtype, non_blocking=True)
@@ -181,12 +202,18 @@ def partition_bounds(n: int, world: int):
 
 
 def build_schedule(offsets, successors, b: int, device, order: str = "auto", world: int = 1,
-                   rank_id: int = 0, stream=None) -> Schedule:
+                   rank_id: int = 0, stream=None, on_order=None) -> Schedule:
     """Upload the CSR of G^T, relabel it into schedule order and split the heavy nodes of
-    this rank's internal-id range [lo, hi) into work items."""
+    this rank's internal-id range [lo, hi) into work items.
+
+    The successor ids (the bulk of the upload) travel on a side stream while the offsets-
+    only work runs (degrees, node order); on_order(perm), if given, is called once the
+    order is known and before the ids are needed, so the caller can launch work that
+    overlaps the rest of the upload (the engine seeds the counters there)."""
     L = _lib.hb()
+    s_main = stream if stream is not None else torch.cuda.current_stream(device)
     off = _as_device(offsets, torch.int64, device)
-    succ = _as_device(successors, torch.int32, device)
+    succ, ids_ready = _upload_on_side_stream(successors, device, s_main)
     n = off.numel() - 1
     m = succ.numel()
     bounds = partition_bounds(n, world)
@@ -200,16 +227,29 @@ def build_schedule(offsets, successors, b: int, device, order: str = "auto", wor
     if order not in ("identity", "degree", "window"):
         raise ValueError(f"unknown schedule order {order!r}")
     perm = rank = None
+    srt = None
     if order == "window" and n > 0:
         srt = window_order(deg, b, bounds, max_deg)
+    elif order == "degree" and n > 0:
+        srt = torch.sort(deg, descending=True, stable=True).indices
+        if world > 1:
+            # deal the degree ranking round-robin: rank r gets ranks r, r+W, r+2W, ...
+            # (bounds[r+1]-bounds[r] of them), each slice still in descending degree.
+            srt = torch.cat([srt[r::world] for r in range(world)])
+    if srt is not None:
         perm = srt.to(torch.int32)
+    if on_order is not None:
+        on_order(perm)
+    if ids_ready is not None:
+        s_main.wait_event(ids_ready)
+    if order == "window" and n > 0:
         rank = torch.empty_like(perm)
         rank[srt] = torch.arange(n, dtype=torch.int32, device=device)
         new_deg = deg[srt]
         new_off = torch.zeros(n + 1, dtype=torch.int64, device=device)
         torch.cumsum(new_deg, 0, out=new_off[1:])
         new_succ = torch.empty(m, dtype=torch.int32, device=device)
-        s = stream if stream is not None else torch.cuda.current_stream(device)
+        s = s_main
         _lib.check(L.hb_relabel_csr(n, off.data_ptr(), succ.data_ptr(), perm.data_ptr(),
                                     rank.data_ptr(), new_off.data_ptr(), new_succ.data_ptr(),
                                     s.cuda_stream), "hb_relabel_csr")
@@ -217,19 +257,13 @@ def build_schedule(offsets, successors, b: int, device, order: str = "auto", wor
         off, succ, deg = new_off, new_succ, new_deg
         del srt
     if order == "degree" and n > 0:
-        srt = torch.sort(deg, descending=True, stable=True).indices
-        if world > 1:
-            # deal the degree ranking round-robin: rank r gets ranks r, r+W, r+2W, ...
-            # (bounds[r+1]-bounds[r] of them), each slice still in descending degree.
-            srt = torch.cat([srt[r::world] for r in range(world)])
-        perm = srt.to(torch.int32)
         rank = torch.empty_like(perm)
         rank[srt] = torch.arange(n, dtype=torch.int32, device=device)
         new_deg = deg[srt]
         new_off = torch.zeros(n + 1, dtype=torch.int64, device=device)
         torch.cumsum(new_deg, 0, out=new_off[1:])
         new_succ = torch.empty(m, dtype=torch.int32, device=device)
-        s = stream if stream is not None else torch.cuda.current_stream(device)
+        s = s_main
         _lib.check(L.hb_relabel_csr(n, off.data_ptr(), succ.data_ptr(), perm.data_ptr(),
                                     rank.data_ptr(), new_off.data_ptr(), new_succ.data_ptr(),
                                     s.cuda_stream), "hb_relabel_csr")
