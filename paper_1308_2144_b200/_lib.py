@@ -17,7 +17,7 @@ import subprocess
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-HB_LIB_PATH = os.path.join(_HERE, "libhyperball_b200.so")
+HB_LIB_PATH = os.environ.get("HB_LIB") or os.path.join(_HERE, "libhyperball_b200.so")
 GRAPH_LIB_PATH = os.path.join(_HERE, "libhbgraph.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "hyperball_b200.h")
 

@@ -131,6 +131,13 @@ struct MaxAcc {
     hi[c].z = vmax16(hi[c].z, r.z); lo[c].z = vmax16(lo[c].z, r.z << 8);
     hi[c].w = vmax16(hi[c].w, r.w); lo[c].w = vmax16(lo[c].w, r.w << 8);
   }
+  // two rows at once: ptxas fuses max(acc, max(a, b)) into one 3-input VIMNMX3.U16x2
+  __device__ __forceinline__ void add2(int c, uint4 a, uint4 b) {
+    hi[c].x = vmax16(hi[c].x, vmax16(a.x, b.x)); lo[c].x = vmax16(lo[c].x, vmax16(a.x << 8, b.x << 8));
+    hi[c].y = vmax16(hi[c].y, vmax16(a.y, b.y)); lo[c].y = vmax16(lo[c].y, vmax16(a.y << 8, b.y << 8));
+    hi[c].z = vmax16(hi[c].z, vmax16(a.z, b.z)); lo[c].z = vmax16(lo[c].z, vmax16(a.z << 8, b.z << 8));
+    hi[c].w = vmax16(hi[c].w, vmax16(a.w, b.w)); lo[c].w = vmax16(lo[c].w, vmax16(a.w << 8, b.w << 8));
+  }
   // byte 2k+1 from hi, byte 2k from lo's byte 2k+1
   __device__ __forceinline__ static uint32_t join(uint32_t h, uint32_t l) {
     uint32_t r;
@@ -151,6 +158,7 @@ struct BmaxAcc {
     for (int c = 0; c < CPL; c++) a[c] = make_uint4(0, 0, 0, 0);
   }
   __device__ __forceinline__ void add(int c, uint4 r) { a[c] = bmax4(a[c], r); }
+  __device__ __forceinline__ void add2(int c, uint4 x, uint4 y) { add(c, x); add(c, y); }
   __device__ __forceinline__ uint4 get(int c) const { return a[c]; }
 };
 // VIMNMX accumulation from p = 128 up (ALU-bound loops); below, the loops are latency-bound
@@ -783,9 +791,13 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
         // sequential accumulate: a pairwise tree (shorter chains) measured 20% slower on
         // config 4 (more live registers at 127/thread)
 #pragma unroll
-        for (int u = 0; u < B::U; u++)
+        for (int u = 0; u + 1 < B::U; u += 2)
 #pragma unroll
-          for (int c = 0; c < Gm::CPL; c++) macc.add(c, r[u][c]);
+          for (int c = 0; c < Gm::CPL; c++) macc.add2(c, r[u][c], r[u + 1][c]);
+        if constexpr (B::U % 2 == 1) {
+#pragma unroll
+          for (int c = 0; c < Gm::CPL; c++) macc.add(c, r[B::U - 1][c]);
+        }
       }
       total += cnt;
       __syncwarp();
@@ -891,9 +903,13 @@ k_heavy_partial(const int64_t *__restrict__ offsets, const int32_t *__restrict__
                           : make_uint4(0, 0, 0, 0);
         }
 #pragma unroll
-        for (int u = 0; u < B::U; u++)
+        for (int u = 0; u + 1 < B::U; u += 2)
 #pragma unroll
-          for (int c = 0; c < Gm::CPL; c++) macc.add(c, r[u][c]);
+          for (int c = 0; c < Gm::CPL; c++) macc.add2(c, r[u][c], r[u + 1][c]);
+        if constexpr (B::U % 2 == 1) {
+#pragma unroll
+          for (int c = 0; c < Gm::CPL; c++) macc.add(c, r[B::U - 1][c]);
+        }
       }
       my_merged += (lane == 0) ? (uint32_t)cnt : 0u;
       __syncwarp();
