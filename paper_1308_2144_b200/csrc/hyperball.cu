@@ -721,7 +721,10 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
     if (valid) {
       beg = __ldg(offsets + v);
       end = __ldg(offsets + v + 1);
-      if (end - beg > max_deg) valid = false;  // heavy: handled by the item path
+      if (end - beg > max_deg) {               // heavy: handled by the item path
+        valid = false;
+        end = beg;
+      }
     }
     const bool self_chg = valid && test_bit(chg_prev, v);
     bool pre;                                   // own row certainly needed: load early
