@@ -24,7 +24,8 @@
  *                     multi-GPU exchange of changed counter rows (no reference
  *                     counterpart: the reference shares `cur` between threads,
  *                     engine.py:377-390)
- *   hb_relabel_csr    graph.py:145-155 transpose's output consumed in schedule order
+ *   hb_relabel_csr / hb_relabel_csr_rows
+ *                     graph.py:145-155 transpose's output consumed in schedule order
  *                     (internal relabelling; no reference counterpart)
  *   hb_sort_rows      graph.py:52-80 keeps successor lists sorted; this restores that
  *                     order after the internal relabelling
@@ -172,6 +173,13 @@ int hb_refresh_rows(int64_t n, int64_t lo, int64_t hi, const uint32_t *bits, con
 int hb_relabel_csr(int64_t n, const int64_t *old_offsets, const int32_t *old_succ,
                    const int32_t *perm, const int32_t *rank, const int64_t *new_offsets,
                    int32_t *new_succ, void *stream);
+
+/* hb_relabel_csr restricted to the new rows [r0, r1) (the other rows are left as they
+ * are): the schedule relabels the CSR slice by slice while the rest of the successor ids
+ * are still being uploaded, and iteration 1 starts on the slices already relabelled. */
+int hb_relabel_csr_rows(int64_t n, int64_t r0, int64_t r1, const int64_t *old_offsets,
+                        const int32_t *old_succ, const int32_t *perm, const int32_t *rank,
+                        const int64_t *new_offsets, int32_t *new_succ, void *stream);
 
 /* Sort the ids of every CSR row ascending (schedule setup, after hb_relabel_csr): offsets
  * (device int64 [n+1]) describe the rows of ids (device int32 [m]); alt (device int32 [m])

@@ -1531,14 +1531,14 @@ __global__ void k_finalize(int64_t n, const int32_t *__restrict__ rank,
   }
 }
 
-__global__ void k_relabel(int64_t n, const int64_t *__restrict__ old_off,
+__global__ void k_relabel(int64_t r0, int64_t r1, const int64_t *__restrict__ old_off,
                           const int32_t *__restrict__ old_succ, const int32_t *__restrict__ perm,
                           const int32_t *__restrict__ rank, const int64_t *__restrict__ new_off,
                           int32_t *__restrict__ new_succ) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t i = warp; i < n; i += nwarps) {
+  for (int64_t i = r0 + warp; i < r1; i += nwarps) {
     const int64_t o = __ldg(perm + i);
     const int64_t b0 = __ldg(old_off + o), len = __ldg(old_off + o + 1) - b0;
     const int64_t d0 = __ldg(new_off + i);
@@ -2262,7 +2262,19 @@ int hb_relabel_csr(int64_t n, const int64_t *old_offsets, const int32_t *old_suc
   if (!old_offsets || !perm || !rank || !new_offsets)   // succ arrays may be empty (NULL)
     return set_err_msg("hb_relabel_csr: bad arguments");
   k_relabel<<<grid_for_warps(n), kThreads, 0, (cudaStream_t)stream>>>(
-      n, old_offsets, old_succ, perm, rank, new_offsets, new_succ);
+      0, n, old_offsets, old_succ, perm, rank, new_offsets, new_succ);
+  return check_launch("k_relabel");
+}
+
+int hb_relabel_csr_rows(int64_t n, int64_t r0, int64_t r1, const int64_t *old_offsets,
+                        const int32_t *old_succ, const int32_t *perm, const int32_t *rank,
+                        const int64_t *new_offsets, int32_t *new_succ, void *stream) {
+  if (r0 < 0 || r1 > n || r0 > r1) return set_err_msg("hb_relabel_csr_rows: bad row range");
+  if (r1 == r0) return 0;
+  if (!old_offsets || !perm || !rank || !new_offsets)
+    return set_err_msg("hb_relabel_csr_rows: bad arguments");
+  k_relabel<<<grid_for_warps(r1 - r0), kThreads, 0, (cudaStream_t)stream>>>(
+      r0, r1, old_offsets, old_succ, perm, rank, new_offsets, new_succ);
   return check_launch("k_relabel");
 }
 

@@ -332,6 +332,7 @@ class _Device:
         self.fwd = None               # forward CSR (internal ids), built on first use
         self.active = None
         self.last_nch = None
+        self.slice_counts = None      # per-slice counters of a streamed iteration 1
         early = None
         if seed_weights is not False:
             def early(perm):
@@ -360,6 +361,7 @@ class _Device:
         other.launches_at_last_step = 0
         other.active = None
         other.last_nch = None
+        other.slice_counts = None
         other._sparse_run = 0
         return other
 
@@ -519,18 +521,41 @@ class _Device:
         sd = sums.sum_dist.data_ptr() if sums is not None else None
         sr = sums.sum_recip.data_ptr() if sums is not None else None
         dargs = sums.disc_args(t) if hasattr(sums, "disc_args") else (None, 0, 0, None, 0)
-        _lib.check(_lib.hb().hb_union_step(
-            self.n, s.light_lo, light_hi, s.offsets.data_ptr(), s.succ.data_ptr(),
-            self.cur.data_ptr(), self.nxt.data_ptr(), self.chg_prev.data_ptr(),
-            self.chg_now.data_ptr(), int(clear_chg_now), self.est.data_ptr(), sd, sr, t,
-            self.lc.data_ptr(),
-            self.alpha_p2, self.lc_cut, self.b, int(dense), s.light_max_deg,
-            s.heavy_nodes.data_ptr(), s.item_first.data_ptr(), s.n_heavy,
-            s.finish_order.data_ptr(), s.n_mega, s.item_node.data_ptr(), s.item_beg.data_ptr(), s.n_items, s.item_arcs,
-            s.partial.data_ptr(), self.counts.data_ptr(), self.counts.data_ptr() + 8,
-            s.hot_rows, *dargs, active, n_peers, peer_nxt, peer_chg, self.stream.cuda_stream),
-            "hb_union_step")
-        self.launches += (light_hi > s.light_lo) + (s.n_items > 0) + (s.n_heavy > 0)
+        # Streamed upload (schedule.py): while successor-id slices are still arriving, the
+        # step runs slice by slice, each one as soon as its ids are uploaded (and relabelled)
+        # -- the light kernel over that row range, its own counters -- so iteration 1
+        # overlaps the rest of the PCIe copy.  Rows are independent within a step.
+        parts = [(s.light_lo, light_hi, None)]
+        if (s.pending and s.n_items == 0 and n_peers == 0 and active is None
+                and s.light_lo == 0 and light_hi == self.n):
+            parts = s.take_pending()
+        elif s.pending:
+            s.ensure_ready()
+        if len(parts) > 1 and (self.slice_counts is None
+                               or self.slice_counts.shape[0] < len(parts)):
+            self.slice_counts = torch.zeros((len(parts), 2), dtype=torch.int64,
+                                            device=self.device)
+        L = _lib.hb()
+        for k, (lo, hi, ev) in enumerate(parts):
+            if ev is not None:
+                s.ready_slice(lo, hi, ev)
+            cnt = self.counts if len(parts) == 1 else self.slice_counts[k]
+            _lib.check(L.hb_union_step(
+                self.n, lo, hi, s.offsets.data_ptr(), s.succ_buf.data_ptr(),
+                self.cur.data_ptr(), self.nxt.data_ptr(), self.chg_prev.data_ptr(),
+                self.chg_now.data_ptr(), int(clear_chg_now and k == 0), self.est.data_ptr(),
+                sd, sr, t, self.lc.data_ptr(),
+                self.alpha_p2, self.lc_cut, self.b, int(dense), s.light_max_deg,
+                s.heavy_nodes.data_ptr(), s.item_first.data_ptr(), s.n_heavy,
+                s.finish_order.data_ptr(), s.n_mega, s.item_node.data_ptr(),
+                s.item_beg.data_ptr(), s.n_items, s.item_arcs,
+                s.partial.data_ptr(), cnt.data_ptr(), cnt.data_ptr() + 8,
+                s.hot_rows, *dargs, active, n_peers, peer_nxt, peer_chg,
+                self.stream.cuda_stream), "hb_union_step")
+            self.launches += (hi > lo) + (s.n_items > 0) + (s.n_heavy > 0)
+        if len(parts) > 1:
+            s.relabel = None
+            self.counts.copy_(self.slice_counts[:len(parts)].sum(0))
         self.launches_at_last_step = self.launches
         nch, merged = (int(x) for x in self.counts.cpu())
         self.last_nch = nch

@@ -18,8 +18,9 @@ schedule decides:
 
 from __future__ import annotations
 
+import os
 import warnings
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 import torch
@@ -36,7 +37,7 @@ class Schedule:
     perm: torch.Tensor | None      # int32 [n]: internal id -> original id
     rank: torch.Tensor | None      # int32 [n]: original id -> internal id
     offsets: torch.Tensor          # int64 [n+1], internal ids
-    succ: torch.Tensor             # int32 [m], internal ids
+    succ_buf: torch.Tensor         # int32 [m], internal ids (see `succ`)
     lo: int
     hi: int
     light_lo: int
@@ -53,6 +54,39 @@ class Schedule:
     partial: torch.Tensor
     max_deg: int
     hot_rows: int = 0              # degree order: head of the rows kept persisting in L2
+    # Streamed upload (window / identity order): row slices [r0, r1) whose successor ids
+    # are still in flight on the side stream (event) and, for the window order, not yet
+    # relabelled (relabel = (old offsets, old ids, perm, rank)).  Iteration 1 consumes them
+    # slice by slice (engine._Device.union_step); any other reader of `succ` first
+    # finishes them all on `stream`.
+    pending: list = field(default_factory=list)
+    relabel: tuple | None = None
+    stream: object = None
+
+    @property
+    def succ(self) -> torch.Tensor:
+        self.ensure_ready()
+        return self.succ_buf
+
+    def ready_slice(self, r0: int, r1: int, ev) -> None:
+        """Make rows [r0, r1) of succ valid on `stream` (wait for their upload, relabel)."""
+        self.stream.wait_event(ev)
+        if self.relabel is not None:
+            off, suc, perm, rank = self.relabel
+            _lib.check(_lib.hb().hb_relabel_csr_rows(
+                self.n, r0, r1, off.data_ptr(), suc.data_ptr(), perm.data_ptr(),
+                rank.data_ptr(), self.offsets.data_ptr(), self.succ_buf.data_ptr(),
+                self.stream.cuda_stream), "hb_relabel_csr_rows")
+
+    def take_pending(self) -> list:
+        """Hand the pending slices to the caller, which must ready_slice() each in order."""
+        out, self.pending = self.pending, []
+        return out
+
+    def ensure_ready(self) -> None:
+        for r0, r1, ev in self.take_pending():
+            self.ready_slice(r0, r1, ev)
+        self.relabel = None
 
     @property
     def n_heavy(self) -> int:
@@ -119,6 +153,43 @@ def _upload_on_side_stream(a, device, main):
         ev.record(side)
     t.record_stream(main)
     return t, ev
+
+
+# Streamed upload: successor ids of at least STREAM_MIN_ARCS arcs travel in STREAM_SLICES
+# row slices (one event each), so that the window relabel and iteration 1 run on the
+# slices that have arrived while the rest is still crossing PCIe.  HB_STREAM_SLICES=1
+# turns it off.
+STREAM_SLICES = int(os.environ.get("HB_STREAM_SLICES", "8"))
+STREAM_MIN_ARCS = 1 << 24
+
+
+def _upload_slices(successors, off_host: np.ndarray, device, main, nslices: int, align: int):
+    """int32 ids uploaded on the side stream in row slices aligned to `align` rows; returns
+    the device tensor and [(r0, r1, event)]."""
+    n = off_host.shape[0] - 1
+    m = int(off_host[-1])
+    side = _SIDE_STREAMS.get(device)
+    if side is None:
+        side = _SIDE_STREAMS[device] = torch.cuda.Stream(device=device)
+    side.wait_stream(main)
+    dst = torch.empty(m, dtype=torch.int32, device=device)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", UserWarning)
+        ht = torch.from_numpy(np.ascontiguousarray(successors))
+    targets = np.arange(1, nslices, dtype=np.int64) * m // nslices
+    rows = np.searchsorted(off_host, targets, side="left") // align * align
+    rows = np.unique(np.concatenate([[0], rows, [n]]))
+    slices = []
+    with torch.cuda.stream(side):
+        for r0, r1 in zip(rows[:-1].tolist(), rows[1:].tolist()):
+            a0, a1 = int(off_host[r0]), int(off_host[r1])
+            if a1 > a0:
+                dst[a0:a1].copy_(ht[a0:a1], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(side)
+            slices.append((r0, r1, ev))
+    dst.record_stream(side)
+    return dst, slices
 
 
 def _as_device(a, dtype, device) -> torch.Tensor:
@@ -213,7 +284,17 @@ def build_schedule(offsets, successors, b: int, device, order: str = "auto", wor
     L = _lib.hb()
     s_main = stream if stream is not None else torch.cuda.current_stream(device)
     off = _as_device(offsets, torch.int64, device)
-    succ, ids_ready = _upload_on_side_stream(successors, device, s_main)
+    slices = None
+    if (world == 1 and STREAM_SLICES > 1 and not isinstance(successors, torch.Tensor)
+            and not isinstance(offsets, torch.Tensor)
+            and np.asarray(successors).dtype == np.int32
+            and np.asarray(successors).shape[0] >= STREAM_MIN_ARCS):
+        off_host = np.asarray(offsets, dtype=np.int64)
+        succ, slices = _upload_slices(successors, off_host, device, s_main, STREAM_SLICES,
+                                      int(L.hb_light_window(b)))
+        ids_ready = None
+    else:
+        succ, ids_ready = _upload_on_side_stream(successors, device, s_main)
     n = off.numel() - 1
     m = succ.numel()
     bounds = partition_bounds(n, world)
@@ -242,7 +323,23 @@ def build_schedule(offsets, successors, b: int, device, order: str = "auto", wor
         on_order(perm)
     if ids_ready is not None:
         s_main.wait_event(ids_ready)
-    if order == "window" and n > 0:
+    pending, relabel = [], None
+    if slices is not None:
+        if order in ("window", "identity") and n > 0:
+            pending = slices                   # consumed by iteration 1, slice by slice
+        else:
+            for _, _, ev in slices:
+                s_main.wait_event(ev)
+    if order == "window" and n > 0 and pending:
+        rank = torch.empty_like(perm)
+        rank[srt] = torch.arange(n, dtype=torch.int32, device=device)
+        new_deg = deg[srt]
+        new_off = torch.zeros(n + 1, dtype=torch.int64, device=device)
+        torch.cumsum(new_deg, 0, out=new_off[1:])
+        relabel = (off, succ, perm, rank)      # window slices map onto themselves
+        off, succ, deg = new_off, torch.empty(m, dtype=torch.int32, device=device), new_deg
+        del srt
+    elif order == "window" and n > 0:
         rank = torch.empty_like(perm)
         rank[srt] = torch.arange(n, dtype=torch.int32, device=device)
         new_deg = deg[srt]
@@ -312,11 +409,12 @@ def build_schedule(offsets, successors, b: int, device, order: str = "auto", wor
         steady = lo + max(n_nonzero, n_heavy)
     else:
         light_lo, light_hi, steady = lo, hi, hi
-    return Schedule(n=n, m=m, b=b, order=order, perm=perm, rank=rank, offsets=off, succ=succ,
+    return Schedule(n=n, m=m, b=b, order=order, perm=perm, rank=rank, offsets=off, succ_buf=succ,
                     lo=lo, hi=hi, light_lo=light_lo, light_hi=light_hi,
                     light_hi_steady=steady, light_max_deg=light_max_deg, item_arcs=item_arcs,
                     heavy_nodes=heavy.to(torch.int32), item_first=item_first.to(torch.int32),
                     finish_order=finish_order, n_mega=n_mega,
                     item_node=item_node.to(torch.int32), item_beg=item_beg.contiguous(),
                     partial=partial, max_deg=max_deg,
-                    hot_rows=n if order == "degree" else 0)
+                    hot_rows=n if order == "degree" else 0, pending=pending,
+                    relabel=relabel, stream=s_main)

@@ -1,4 +1,6 @@
-"""Break down one end-to-end run (bench.py's e2e step) into phases."""
+"""Break down one end-to-end run (bench.py's e2e step) into phases.  The synchronize
+after initialize() waits for the whole streamed upload, so "init" + iteration 1 here
+overstate the pipelined run (bench.py's e2e has no sync there)."""
 import os
 import sys
 import time
