@@ -376,7 +376,10 @@ __device__ __forceinline__ bool finish_node(const Peers &peers, bool doit, int64
     // sum_j 2^-M[j] as exact fp64 partial sums (every M <= 31 here: at most 36 significant
     // bits, so any summation order gives the reference's sequential result), zero count by
     // SWAR, and an OR of all bytes to detect registers > 31 (sequential fallback).
-    double s4[4] = {0.0, 0.0, 0.0, 0.0};
+    // Integer form: 2^(31-M) for every byte by one wrapping funnel shift of 2^31 (the
+    // shift count's low 5 bits are M whenever M <= 31; larger registers take the
+    // sequential path below), summed in 64 bits (< 2^37), scaled once: exact.
+    uint64_t S = 0;
     uint32_t zeros = 0, big = 0;
 #pragma unroll
     for (int c = 0; c < Gm::CPL; c++) {
@@ -386,14 +389,14 @@ __device__ __forceinline__ bool finish_node(const Peers &peers, bool doit, int64
         const uint32_t w = ws[q];
         zeros += __popc(~(((w & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | w) & 0x80808080u);
         big |= w;
-#pragma unroll
-        for (int i = 0; i < 4; i++) {
-          const uint32_t m = (w >> (8 * i)) & 0xffu;
-          s4[i] = __dadd_rn(s4[i], __hiloint2double((int)(0x3FF00000u - (m << 20)), 0));
-        }
+        const uint32_t t0 = __funnelshift_r(0x80000000u, 0u, w);
+        const uint32_t t1 = __funnelshift_r(0x80000000u, 0u, w >> 8);
+        const uint32_t t2 = __funnelshift_r(0x80000000u, 0u, w >> 16);
+        const uint32_t t3 = __funnelshift_r(0x80000000u, 0u, w >> 24);
+        S += ((uint64_t)t0 + t1) + ((uint64_t)t2 + t3);
       }
     }
-    double s = __dadd_rn(__dadd_rn(s4[0], s4[1]), __dadd_rn(s4[2], s4[3]));
+    double s = __dmul_rn(__ull2double_rn(S), 0x1p-31);
 #pragma unroll
     for (int off = 1; off < Gm::G; off <<= 1) {   // xor partners stay inside the group
       s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, off));
