@@ -184,8 +184,11 @@ def _upload_slices(successors, off_host: np.ndarray, device, main, nslices: int,
         for r0, r1 in zip(rows[:-1].tolist(), rows[1:].tolist()):
             a0, a1 = int(off_host[r0]), int(off_host[r1])
             if a1 > a0:
-                dst[a0:a1].copy_(ht[a0:a1], non_blocking=True)
-            ev = torch.cuda.Event()
+                if ht.dtype == torch.int32:
+                    dst[a0:a1].copy_(ht[a0:a1], non_blocking=True)
+                else:                            # int64 ids (the reference's CsrGraph):
+                    dst[a0:a1].copy_(ht[a0:a1].to(device, non_blocking=True))  # narrow on
+            ev = torch.cuda.Event()                                             # the device
             ev.record(side)
             slices.append((r0, r1, ev))
     dst.record_stream(side)
@@ -287,7 +290,7 @@ def build_schedule(offsets, successors, b: int, device, order: str = "auto", wor
     slices = None
     if (world == 1 and STREAM_SLICES > 1 and not isinstance(successors, torch.Tensor)
             and not isinstance(offsets, torch.Tensor)
-            and np.asarray(successors).dtype == np.int32
+            and np.asarray(successors).dtype in (np.int32, np.int64)
             and np.asarray(successors).shape[0] >= STREAM_MIN_ARCS):
         off_host = np.asarray(offsets, dtype=np.int64)
         succ, slices = _upload_slices(successors, off_host, device, s_main, STREAM_SLICES,

@@ -84,8 +84,8 @@ def test_degree_order_waits_for_every_slice(weblike, monkeypatch):
 
 
 def test_reader_before_first_step_finishes_slices(weblike, monkeypatch):
-    """Anything that reads the CSR before iteration 1 (here the batched multi-run and a
-    checkpoint round trip) sees every slice uploaded and relabelled."""
+    """Anything that reads the CSR before iteration 1 (through Schedule.succ) sees every
+    slice uploaded and relabelled; the run then proceeds unsliced."""
     monkeypatch.setattr(sched_mod, "STREAM_SLICES", 4)
     monkeypatch.setattr(sched_mod, "STREAM_MIN_ARCS", 0)
     cfg = hb.HyperBallConfig(params=hb.CounterParams(b=8, seed=42), schedule="window")
@@ -104,5 +104,15 @@ def test_reader_before_first_step_finishes_slices(weblike, monkeypatch):
 def test_skip_off_streamed(weblike, monkeypatch):
     ref, _, _ = _run(weblike, 5, "window", 1, monkeypatch, skip=False)
     got, pend, _ = _run(weblike, 5, "window", 4, monkeypatch, skip=False)
+    assert pend > 1
+    _same(got, ref)
+
+
+def test_int64_ids_streamed(weblike, monkeypatch):
+    """The reference's CsrGraph carries int64 ids: streamed too, narrowed on the device."""
+    g64 = hb.CsrGraph(np.asarray(weblike.offsets, np.int64),
+                      np.asarray(weblike.successors, np.int64))
+    ref, _, _ = _run(weblike, 8, "window", 1, monkeypatch)
+    got, pend, _ = _run(g64, 8, "window", 5, monkeypatch)
     assert pend > 1
     _same(got, ref)
