@@ -24,6 +24,9 @@
  *                     multi-GPU exchange of changed counter rows (no reference
  *                     counterpart: the reference shares `cur` between threads,
  *                     engine.py:377-390)
+ *   hb_sample_flagged_arcs
+ *                     share of arcs with a changed source, sampled (picks the dense
+ *                     step; no reference counterpart)
  *   hb_relabel_csr / hb_relabel_csr_rows
  *                     graph.py:145-155 transpose's output consumed in schedule order
  *                     (internal relabelling; no reference counterpart)
@@ -180,6 +183,13 @@ int hb_relabel_csr(int64_t n, const int64_t *old_offsets, const int32_t *old_suc
 int hb_relabel_csr_rows(int64_t n, int64_t r0, int64_t r1, const int64_t *old_offsets,
                         const int32_t *old_succ, const int32_t *perm, const int32_t *rank,
                         const int64_t *new_offsets, int32_t *new_succ, void *stream);
+
+/* *out (device uint64) = how many of `samples` pseudo-random arcs (arc splitmix64(seed + i)
+ * mod m of succ, device int32 [m]) have their source flagged in bits (device uint32
+ * [ceil(n/32)]): an estimate of the share of arcs whose source changed, which decides
+ * whether the next step merges every source without the per-source test (engine.py). */
+int hb_sample_flagged_arcs(int64_t m, const int32_t *succ, const uint32_t *bits,
+                           int64_t samples, uint64_t seed, uint64_t *out, void *stream);
 
 /* Sort the ids of every CSR row ascending (schedule setup, after hb_relabel_csr): offsets
  * (device int64 [n+1]) describe the rows of ids (device int32 [m]); alt (device int32 [m])

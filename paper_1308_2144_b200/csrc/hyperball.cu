@@ -1438,6 +1438,29 @@ __global__ void k_count_src(int64_t m, const int32_t *__restrict__ succ,
   }
 }
 
+// Sampled share of arcs whose source is flagged in `bits`: thread i tests the source of
+// arc splitmix(seed + i) mod m; one atomic per block with the block's hit count.
+__global__ void k_sample_flagged(int64_t m, const int32_t *__restrict__ succ,
+                                 const uint32_t *__restrict__ bits, int64_t samples,
+                                 uint64_t seed, unsigned long long *__restrict__ out) {
+  uint32_t hits = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < samples;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = (int64_t)(mix64(seed + (uint64_t)i) % (uint64_t)m);
+    const int32_t v = __ldg(succ + k);
+    hits += (__ldg(bits + (v >> 5)) >> (v & 31)) & 1u;
+  }
+  hits = __reduce_add_sync(0xffffffffu, hits);
+  __shared__ uint32_t red[kThreads / 32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = hits;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); i++) t += red[i];
+    if (t) atomicAdd(out, (unsigned long long)t);
+  }
+}
+
 __global__ void k_scatter_fwd(int64_t n, const int64_t *__restrict__ off,
                               const int32_t *__restrict__ succ,
                               unsigned long long *__restrict__ cursor,
@@ -2210,6 +2233,19 @@ int hb_forward_csr(int64_t n, const int64_t *offsets, const int32_t *succ, int64
   k_scatter_fwd<<<grid_for_warps(n), kThreads, 0, s>>>(
       n, offsets, succ, reinterpret_cast<unsigned long long *>(cursor), fwd_dst);
   return check_launch("hb_forward_csr");
+}
+
+int hb_sample_flagged_arcs(int64_t m, const int32_t *succ, const uint32_t *bits,
+                           int64_t samples, uint64_t seed, uint64_t *out, void *stream) {
+  if (m < 0 || samples < 0 || !out || (m > 0 && samples > 0 && (!succ || !bits)))
+    return set_err_msg("hb_sample_flagged_arcs: bad arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(out, 0, sizeof(uint64_t), s);
+  if (e != cudaSuccess) return set_err("hb_sample_flagged_arcs memset", e);
+  if (m == 0 || samples == 0) return 0;
+  k_sample_flagged<<<grid_for_threads(samples), kThreads, 0, s>>>(
+      m, succ, bits, samples, seed, reinterpret_cast<unsigned long long *>(out));
+  return check_launch("k_sample_flagged");
 }
 
 int hb_gen_rmat_keys(int scale, int64_t m, uint64_t thr_a, uint64_t thr_ab, uint64_t thr_abc,

@@ -49,6 +49,13 @@ FRONTIER_AFTER = int(_os.environ.get("HB_FRONTIER_AFTER", "4"))
 # a step runs dense (no per-source change test) when at least this fraction of the counters
 # changed in the previous iteration
 DENSE_FRAC = float(_os.environ.get("HB_DENSE_FRAC", "0.95"))
+# ... or when the counters that changed are the sources of at least DENSE_ARC_FRAC of the
+# arcs (estimated on the device from FLAG_SAMPLES random arcs, hb_sample_flagged_arcs;
+# graphs of FLAG_MIN_ARCS arcs and more): on R-MAT a third of the nodes change but they
+# feed 99% of the arcs, and the per-source test then costs more than the merges it saves.
+DENSE_ARC_FRAC = float(_os.environ.get("HB_DENSE_ARC_FRAC", "0.7"))
+FLAG_MIN_ARCS = 1 << 26
+FLAG_SAMPLES = 1 << 16
 
 CHECKPOINT_MAGIC = b"HBCK"
 CHECKPOINT_VERSION = 1
@@ -333,6 +340,8 @@ class _Device:
         self.active = None
         self.last_nch = None
         self.slice_counts = None      # per-slice counters of a streamed iteration 1
+        self.flag_out = None          # device: arcs whose source changed (last step)
+        self.last_flagged = None
         early = None
         if seed_weights is not False:
             def early(perm):
@@ -362,6 +371,8 @@ class _Device:
         other.active = None
         other.last_nch = None
         other.slice_counts = None
+        other.flag_out = None
+        other.last_flagged = None
         other._sparse_run = 0
         return other
 
@@ -511,7 +522,7 @@ class _Device:
         return self.active.data_ptr()
 
     def union_step(self, t: int, dense: bool, sums: _DeviceSums | None, peers=None,
-                   clear_chg_now: bool = True) -> int:
+                   clear_chg_now: bool = True, flag_arcs: bool = False) -> int:
         """One hb_union_step.  peers: (n, host uint8** array, host uint32** array) of peer
         nxt / chg_now device addresses for the fused multi-GPU push (distributed.py)."""
         s = self.sched
@@ -556,8 +567,21 @@ class _Device:
         if len(parts) > 1:
             s.relabel = None
             self.counts.copy_(self.slice_counts[:len(parts)].sum(0))
+        flagged = None
+        if flag_arcs and s.m >= FLAG_MIN_ARCS and DENSE_ARC_FRAC < 1.0:
+            if self.flag_out is None:
+                self.flag_out = torch.zeros(1, dtype=torch.int64, device=self.device)
+            _lib.check(L.hb_sample_flagged_arcs(s.m, s.succ_buf.data_ptr(),
+                                                self.chg_now.data_ptr(), FLAG_SAMPLES, t,
+                                                self.flag_out.data_ptr(),
+                                                self.stream.cuda_stream),
+                       "hb_sample_flagged_arcs")
+            self.launches += 1
+            flagged = self.flag_out
         self.launches_at_last_step = self.launches
         nch, merged = (int(x) for x in self.counts.cpu())
+        self.last_flagged = (int(flagged.item()) / FLAG_SAMPLES if flagged is not None
+                             else None)
         self.last_nch = nch
         self.last_merged = merged
         self.merged_total += merged
@@ -663,7 +687,7 @@ class _ExactDevice(_Device):
         return None
 
     def union_step(self, t: int, dense: bool, sums: _DeviceSums | None, peers=None,
-                   clear_chg_now: bool = True) -> int:
+                   clear_chg_now: bool = True, flag_arcs: bool = False) -> int:
         if peers is not None:
             raise ValueError("the exact backend runs on one device")
         s = self.sched
@@ -869,9 +893,12 @@ def iterate(g, state: HyperBallState, observers: Iterable = ()) -> int:
     # Merging an unchanged source is a no-op, so when nearly every counter
     # changed last iteration the step skips the per-source bitmap tests (dense mode):
     # identical bits, less work per arc.
-    dense = (dev.prev_all or not state.config.skip_stable_nodes
+    skip = state.config.skip_stable_nodes
+    dense = (dev.prev_all or not skip
              or (dev.last_nch is not None and dev.last_nch >= DENSE_FRAC * dev.n))
-    nch = dev.union_step(t_next, dense, sums)
+    arc_dense = (not dense and getattr(dev, "last_flagged", None) is not None
+                 and dev.last_flagged >= DENSE_ARC_FRAC)
+    nch = dev.union_step(t_next, dense or arc_dense, sums, flag_arcs=skip)
     if generic:
         old_h, new_h = dev.to_host(old), dev.to_host(dev.est)
         old_h.setflags(write=False)
