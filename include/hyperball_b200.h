@@ -27,7 +27,7 @@
  *   hb_sample_flagged_arcs
  *                     share of arcs with a changed source, sampled (picks the dense
  *                     step; no reference counterpart)
- *   hb_relabel_csr / hb_relabel_csr_rows
+ *   hb_relabel_csr / hb_relabel_csr_rows / hb_relabel_csr_src_rows
  *                     graph.py:145-155 transpose's output consumed in schedule order
  *                     (internal relabelling; no reference counterpart)
  *   hb_sort_rows      graph.py:52-80 keeps successor lists sorted; this restores that
@@ -183,6 +183,12 @@ int hb_relabel_csr(int64_t n, const int64_t *old_offsets, const int32_t *old_suc
 int hb_relabel_csr_rows(int64_t n, int64_t r0, int64_t r1, const int64_t *old_offsets,
                         const int32_t *old_succ, const int32_t *perm, const int32_t *rank,
                         const int64_t *new_offsets, int32_t *new_succ, void *stream);
+
+/* hb_relabel_csr by OLD rows [o0, o1) (old row o becomes new row rank[o]): the degree
+ * relabel runs on every slice of the successor-id upload as soon as it has landed. */
+int hb_relabel_csr_src_rows(int64_t n, int64_t o0, int64_t o1, const int64_t *old_offsets,
+                            const int32_t *old_succ, const int32_t *rank,
+                            const int64_t *new_offsets, int32_t *new_succ, void *stream);
 
 /* *out (device uint64) = how many of `samples` pseudo-random arcs (arc splitmix64(seed + i)
  * mod m of succ, device int32 [m]) have their source flagged in bits (device uint32

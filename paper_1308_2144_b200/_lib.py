@@ -64,6 +64,7 @@ HB_SIGNATURES = {
     "hb_relabel_csr": (_int, [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "hb_relabel_csr_rows": (_int, [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "hb_sample_flagged_arcs": (_int, [_i64, _vp, _vp, _i64, _u64, _vp, _vp]),
+    "hb_relabel_csr_src_rows": (_int, [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "hb_sort_rows": (_int, [_i64, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "hb_gen_rmat_keys": (_int, [_int, _i64, _u64, _u64, _u64, _u64, _vp, _vp]),
     "hb_keys_to_csr": (_int, [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),

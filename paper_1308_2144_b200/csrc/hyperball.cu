@@ -1572,6 +1572,23 @@ __global__ void k_relabel(int64_t r0, int64_t r1, const int64_t *__restrict__ ol
   }
 }
 
+// Scatter form of k_relabel over OLD rows [o0, o1): old row o becomes new row rank[o].
+// Lets the degree relabel run on each slice of the upload as soon as it has landed.
+__global__ void k_relabel_src(int64_t o0, int64_t o1, const int64_t *__restrict__ old_off,
+                              const int32_t *__restrict__ old_succ,
+                              const int32_t *__restrict__ rank,
+                              const int64_t *__restrict__ new_off,
+                              int32_t *__restrict__ new_succ) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t o = o0 + warp; o < o1; o += nwarps) {
+    const int64_t b0 = __ldg(old_off + o), len = __ldg(old_off + o + 1) - b0;
+    const int64_t d0 = __ldg(new_off + __ldg(rank + o));
+    for (int64_t k = lane; k < len; k += 32) new_succ[d0 + k] = __ldg(rank + __ldg(old_succ + b0 + k));
+  }
+}
+
 __global__ void k_hash(int64_t n, const uint64_t *__restrict__ items,
                        const uint64_t *__restrict__ replicas, uint64_t seed,
                        uint64_t *__restrict__ out) {
@@ -2315,6 +2332,18 @@ int hb_relabel_csr_rows(int64_t n, int64_t r0, int64_t r1, const int64_t *old_of
   k_relabel<<<grid_for_warps(r1 - r0), kThreads, 0, (cudaStream_t)stream>>>(
       r0, r1, old_offsets, old_succ, perm, rank, new_offsets, new_succ);
   return check_launch("k_relabel");
+}
+
+int hb_relabel_csr_src_rows(int64_t n, int64_t o0, int64_t o1, const int64_t *old_offsets,
+                            const int32_t *old_succ, const int32_t *rank,
+                            const int64_t *new_offsets, int32_t *new_succ, void *stream) {
+  if (o0 < 0 || o1 > n || o0 > o1) return set_err_msg("hb_relabel_csr_src_rows: bad row range");
+  if (o1 == o0) return 0;
+  if (!old_offsets || !rank || !new_offsets)
+    return set_err_msg("hb_relabel_csr_src_rows: bad arguments");
+  k_relabel_src<<<grid_for_warps(o1 - o0), kThreads, 0, (cudaStream_t)stream>>>(
+      o0, o1, old_offsets, old_succ, rank, new_offsets, new_succ);
+  return check_launch("k_relabel_src");
 }
 
 int hb_hash_items(int64_t n, const uint64_t *items, const uint64_t *replicas, uint64_t seed,

@@ -326,10 +326,12 @@ def build_schedule(offsets, successors, b: int, device, order: str = "auto", wor
         on_order(perm)
     if ids_ready is not None:
         s_main.wait_event(ids_ready)
-    pending, relabel = [], None
+    pending, relabel, src_slices = [], None, None
     if slices is not None:
         if order in ("window", "identity") and n > 0:
             pending = slices                   # consumed by iteration 1, slice by slice
+        elif order == "degree" and n > 0:
+            src_slices = slices                # relabelled slice by slice as they land
         else:
             for _, _, ev in slices:
                 s_main.wait_event(ev)
@@ -364,9 +366,19 @@ def build_schedule(offsets, successors, b: int, device, order: str = "auto", wor
         torch.cumsum(new_deg, 0, out=new_off[1:])
         new_succ = torch.empty(m, dtype=torch.int32, device=device)
         s = s_main
-        _lib.check(L.hb_relabel_csr(n, off.data_ptr(), succ.data_ptr(), perm.data_ptr(),
-                                    rank.data_ptr(), new_off.data_ptr(), new_succ.data_ptr(),
-                                    s.cuda_stream), "hb_relabel_csr")
+        if src_slices is not None:
+            # scatter form by uploaded (old) rows: slice k is relabelled while slices
+            # k+1.. are still crossing PCIe; every new row is complete after the last one
+            for r0, r1, ev in src_slices:
+                s.wait_event(ev)
+                _lib.check(L.hb_relabel_csr_src_rows(
+                    n, r0, r1, off.data_ptr(), succ.data_ptr(), rank.data_ptr(),
+                    new_off.data_ptr(), new_succ.data_ptr(), s.cuda_stream),
+                    "hb_relabel_csr_src_rows")
+        else:
+            _lib.check(L.hb_relabel_csr(n, off.data_ptr(), succ.data_ptr(), perm.data_ptr(),
+                                        rank.data_ptr(), new_off.data_ptr(),
+                                        new_succ.data_ptr(), s.cuda_stream), "hb_relabel_csr")
         # optionally restore ascending ids inside every row (graph.py's normalisation), in
         # internal ids: a hub's consecutive arcs then read neighbouring register rows
         if SORT_ROWS:

@@ -76,10 +76,21 @@ def test_streamed_matches_oracle(weblike, monkeypatch):
         assert np.array_equal(got[k].view(np.uint64), want.view(np.uint64)), k
 
 
-def test_degree_order_waits_for_every_slice(weblike, monkeypatch):
+@pytest.mark.parametrize("slices", [2, 6])
+def test_degree_order_relabels_by_slice(weblike, slices, monkeypatch):
+    """Degree order: every slice is relabelled (scatter form) as it lands; iteration 1
+    starts after the last one."""
     ref, _, _ = _run(weblike, 7, "degree", 1, monkeypatch)
-    got, pend, _ = _run(weblike, 7, "degree", 6, monkeypatch)
-    assert pend == 0                               # relabel needs every id first
+    got, pend, _ = _run(weblike, 7, "degree", slices, monkeypatch)
+    assert pend == 0
+    _same(got, ref)
+
+
+def test_degree_order_rmat_streamed(monkeypatch):
+    """Skewed in-degree (heavy items) with the per-slice degree relabel."""
+    g = gen.rmat_t(13, 16 << 13, seed=3)
+    ref, _, _ = _run(g, 4, "degree", 1, monkeypatch)
+    got, _, _ = _run(g, 4, "degree", 5, monkeypatch)
     _same(got, ref)
 
 
