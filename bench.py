@@ -406,9 +406,9 @@ def run_b200(args):
         mean_dt = sum_dt / len(dts)
         e2e = {"value": merged_total * p / mean_dt, "unit": UNIT,
                "h2d_bytes_per_step": int(off_pin.numel() * 8 + suc_pin.numel() * 4),
-               # the outputs, the final estimates run() hands to on_converged, and the
-               # 16-byte changed/merged counters read after every iteration
-               "d2h_bytes_per_step": int(n * 8 * (len(outputs) + 1) + 16 * iters),
+               # the outputs and the 16-byte changed/merged counters read after every
+               # iteration (the fused accumulator's final estimates stay on the device)
+               "d2h_bytes_per_step": int(n * 8 * len(outputs) + 16 * iters),
                "seconds_per_run": mean_dt, "iterations": iters,
                "merged_arcs_per_run": merged_total,
                "what": "run(g, config, [CentralityAccumulator]) + finalize_{%s} from pinned "

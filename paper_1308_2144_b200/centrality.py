@@ -115,7 +115,9 @@ class CentralityAccumulator(BallObserver):
         if len(names) != len(set(names)):
             raise ValueError(f"duplicate discount names: {names}")
         self._discounted = {d.name: np.zeros(n, dtype=np.float64) for d in self.discounts}
-        self.coreach = np.zeros(n, dtype=np.float64)
+        self._coreach = np.zeros(n, dtype=np.float64)
+        self._coreach_fetch = None    # engine: downloads the final estimates on first read
+        self._coreach_version = 0     # bumped whenever coreach is replaced
         self.converged = False
         self._binding = None   # engine-side DeviceSums when fused
         self._fresh = True     # sums never touched: the device copy can start from zeros
@@ -160,6 +162,29 @@ class CentralityAccumulator(BallObserver):
         if self._binding is not None:
             self._binding.invalidate()
 
+    @property
+    def coreach(self) -> np.ndarray:
+        """Final ball sizes (centrality.py:137-139).  After a fused run it stays on the
+        device until first read (finalize_lin does not need the host copy)."""
+        if self._coreach_fetch is not None:
+            fetch, self._coreach_fetch = self._coreach_fetch, None
+            self._coreach = fetch()
+        return self._coreach
+
+    @coreach.setter
+    def coreach(self, value) -> None:
+        self._coreach = value
+        self._coreach_fetch = None
+        self._coreach_version += 1
+
+    def _converged_on_device(self, fetch) -> None:
+        """Engine hook for the fused accumulator: the final estimates are captured on the
+        device; `fetch()` returns the host copy the reference would have received."""
+        self._coreach, self._coreach_fetch = None, fetch
+        self._coreach_version += 1
+        self._binding.capture_coreach(self._coreach_version)
+        self.converged = True
+
     # BallObserver contract (host path: used when not fused)
     def on_step(self, t: int, old_estimates: np.ndarray, new_estimates: np.ndarray) -> None:
         diff = np.asarray(new_estimates, dtype=np.float64) - np.asarray(old_estimates,
@@ -171,7 +196,7 @@ class CentralityAccumulator(BallObserver):
         # the engine hands every observer a fresh read-only host copy: keep it as is
         self.coreach = final if not final.flags.writeable else final.copy()
         if self._binding is not None and not self._binding.stale:
-            self._binding.capture_coreach(self.coreach)
+            self._binding.capture_coreach(self._coreach_version)
         self.converged = True
 
     def accumulate(self, t: int, delta: np.ndarray) -> None:
@@ -213,7 +238,8 @@ def _on_device(acc, which: str):
     b = getattr(acc, "_binding", None)
     if b is None or b.stale:
         return None
-    if which == "lin" and (b.coreach_dev is None or b.coreach_host_id != id(acc.coreach)):
+    if which == "lin" and (b.coreach_dev is None
+                           or b.coreach_version != getattr(acc, "_coreach_version", None)):
         return None
     return b.finalize(which)
 

@@ -227,12 +227,19 @@ class _DeviceSums:
         return self.disc.data_ptr(), self.dev.n, k, ctypes.cast(scale, ctypes.c_void_p), div
 
     coreach_dev = None
-    coreach_host_id = None
+    coreach_version = None
 
-    def capture_coreach(self, host_final) -> None:
-        """on_converged: keep the final estimates on the device for finalize_lin."""
+    def capture_coreach(self, version) -> None:
+        """on_converged: keep the final estimates on the device for finalize_lin, tagged
+        with the accumulator's coreach version (a later reassignment invalidates it)."""
         self.coreach_dev = self.dev.est.clone()
-        self.coreach_host_id = id(host_final)
+        self.coreach_version = version
+
+    def fetch_coreach(self) -> np.ndarray:
+        """Host copy (original order, read-only) of the captured final estimates."""
+        out = self.dev.to_host(self.coreach_dev)
+        out.setflags(write=False)
+        return out
 
     _fin_cache = None   # (key, {name: host array}, {name: handed out once})
 
@@ -241,7 +248,7 @@ class _DeviceSums:
         original order and keeps them there); each is copied to the host (pinned) on its
         first request only, so a harmonic-only caller downloads n doubles, not 3n."""
         dev = self.dev
-        key = (dev.launches_at_last_step, self.coreach_host_id)
+        key = (dev.launches_at_last_step, self.coreach_version)
         if self._fin_cache is None or self._fin_cache[0] != key:
             n = dev.n
             with_lin = self.coreach_dev is not None
@@ -938,6 +945,15 @@ def resume(g, state: HyperBallState, observers: Iterable = ()) -> HyperBallState
                 raise ConvergenceError(state.t, nch)
     else:
         state.num_changed = 0
+    # The fused accumulator keeps the final estimates on the device (its coreach is
+    # downloaded on first read); any other observer gets the host copy as in the reference.
+    sums = state._sums
+    fused = (sums.acc if sums is not None and not sums.stale and not sums.foreign
+             and sums.dev is state._dev else None)
+    if fused is not None and any(o is fused for o in observers) and all(
+            o is fused for o in observers):
+        fused._converged_on_device(sums.fetch_coreach)
+        return state
     final = state.est
     final.setflags(write=False)
     for obs in observers:

@@ -196,3 +196,43 @@ class TestCheckpoint:
         assert back.t == full.t
         assert np.array_equal(back.register_matrix(), full.register_matrix())
         assert np.array_equal(back.est.view(np.uint64), full.est.view(np.uint64))
+
+
+class TestLazyCoreach:
+    """run() with only a fused accumulator keeps the final estimates on the device: the
+    accumulator's coreach is downloaded on first read and equals the state's estimates."""
+
+    def test_coreach_lazy_and_exact(self):
+        g = random_graph(4, 3000, 5.0)
+        acc = hb.CentralityAccumulator(g.n)
+        st = hb.run(g, cfg(b=8, seed=3), [acc])
+        assert acc.converged and acc._coreach_fetch is not None
+        lin = hb.finalize_lin(acc)                    # on the device, no host coreach
+        assert acc._coreach_fetch is not None
+        c = acc.coreach
+        assert acc._coreach_fetch is None and not c.flags.writeable
+        assert np.array_equal(c.view(np.uint64), st.est.view(np.uint64))
+        s = acc.sum_dist
+        want = np.divide(c * c, s, out=np.ones_like(s), where=s > 0)
+        assert np.array_equal(lin.view(np.uint64), want.view(np.uint64))
+
+    def test_reassigned_coreach_goes_host_path(self):
+        g = random_graph(5, 2000, 4.0)
+        acc = hb.CentralityAccumulator(g.n)
+        hb.run(g, cfg(b=6, seed=1), [acc])
+        acc.coreach = np.full(g.n, 2.0)
+        s = acc.sum_dist
+        want = np.divide(4.0, s, out=np.ones_like(s), where=s > 0)
+        assert np.array_equal(hb.finalize_lin(acc), want)
+
+    def test_extra_observer_gets_host_copy(self):
+        class Last(hb.BallObserver):
+            final = None
+
+            def on_converged(self, final_estimates):
+                self.final = final_estimates
+        g = random_graph(6, 2000, 4.0)
+        acc, last = hb.CentralityAccumulator(g.n), Last()
+        st = hb.run(g, cfg(b=6, seed=2), [acc, last])
+        assert last.final is not None and acc._coreach_fetch is None
+        assert np.array_equal(acc.coreach, st.est) and np.array_equal(last.final, st.est)
