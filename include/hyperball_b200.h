@@ -44,7 +44,7 @@
  *   hb_exact_seed / hb_exact_union_step
  *                     engine.py:194-206 _ExactBackend.seed / union_range
  *                     (-> _kernels.py:117-172 bitset_union_range, weighted_popcount_row)
- *   hb_forward_csr / hb_mark_active / hb_mark_pull
+ *   hb_forward_csr / hb_mark_active / hb_mark_pull / hb_mark_pull_filtered
  *                     frontier of a sparse iteration (no reference counterpart: the
  *                     reference scans every node's successor list, _kernels.py:82-87)
  *   hb_hash_items     hll.py:79-88 hash_items (device twin, used by tests)
@@ -281,6 +281,19 @@ int hb_mark_pull(int64_t n, const int64_t *offsets, const int32_t *succ,
                  const uint32_t *chg_prev, uint32_t *active, int64_t light_max_deg,
                  const int32_t *item_node, const int64_t *item_beg, int64_t n_items,
                  int64_t item_arcs, void *stream);
+
+/* hb_mark_pull with two speed-ups, same result.  heavy_lo < heavy_hi: the heavy rows are
+ * exactly the row range [heavy_lo, heavy_hi) (degree order), so their ids are streamed
+ * flat instead of item by item.  filter != NULL (nearly converged steps, a few thousand
+ * changed nodes): a 2^18-bit hash filter of the changed nodes is built there (device
+ * uint32 [hb_change_filter_words()]) and kept in shared memory by every block, so each
+ * streamed id is tested there and the change bitmap is read only on a filter hit. */
+int hb_mark_pull_filtered(int64_t n, const int64_t *offsets, const int32_t *succ,
+                          const uint32_t *chg_prev, uint32_t *active, int64_t light_max_deg,
+                          const int32_t *item_node, const int64_t *item_beg, int64_t n_items,
+                          int64_t item_arcs, int64_t heavy_lo, int64_t heavy_hi,
+                          uint32_t *filter, void *stream);
+int64_t hb_change_filter_words(void);
 
 /* GPU graph build.
  * hb_gen_rmat_keys: m R-MAT arcs (scale levels, 32-bit quadrant thresholds thr_a <= thr_ab

@@ -51,6 +51,9 @@ HB_SIGNATURES = {
     "hb_pack_registers": (_int, [_i64, _int, _int, _vp, _vp, _vp, _vp]),
     "hb_unpack_registers": (_int, [_i64, _int, _int, _vp, _vp, _vp, _vp]),
     "hb_mark_pull": (_int, [_i64, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _i64, _i64, _vp]),
+    "hb_mark_pull_filtered": (_int, [_i64, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _i64, _i64,
+                                     _i64, _i64, _vp, _vp]),
+    "hb_change_filter_words": (_i64, []),
     "hb_exact_seed": (_int, [_i64, _i64, _vp, _vp, _vp, _vp]),
     "hb_exact_union_step": (_int, [_i64, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp,
                                    _i64, _int, _vp, _vp, _i64, _int, _vp, _int, _vp, _vp,

@@ -1347,10 +1347,60 @@ __global__ void k_mark_active(int64_t n, const int64_t *__restrict__ fwd_off,
 // light_max_deg) are skipped here and marked by k_mark_items over the schedule's work
 // items, so every warp streams a bounded number of ids.  Every bitmap word is written by
 // one warp of k_mark_pull (k_mark_items, launched after it, only ORs bits in).
+// Change filter for the pull marking of nearly converged steps: a 2^18-bit hash bitmap of
+// the changed nodes (a few thousand at most), copied into shared memory by every block,
+// so the per-id test of a streamed successor id is a shared-memory lookup and the global
+// change bitmap is read only on a filter hit.
+constexpr int kFilterBits = 18;
+constexpr int kFilterWords = (1 << kFilterBits) / 32;
+__device__ __forceinline__ uint32_t filter_slot(int64_t v) {
+  return ((uint32_t)v * 0x9E3779B1u) >> (32 - kFilterBits);
+}
+__global__ void k_build_filter(int64_t n, const uint32_t *__restrict__ bits,
+                               uint32_t *__restrict__ filter) {
+  const int64_t words = (n + 31) >> 5;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < words;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t b = __ldg(bits + w);
+    while (b) {
+      const int i = __ffs(b) - 1;
+      b &= b - 1u;
+      const uint32_t h = filter_slot((w << 5) + i);
+      atomicOr(filter + (h >> 5), 1u << (h & 31));
+    }
+  }
+}
+template <bool FILT>
+struct ChangeTest {
+  const uint32_t *bits;
+  uint32_t *sf;   // shared filter (FILT)
+  __device__ __forceinline__ bool operator()(int64_t v) const {
+    if constexpr (FILT) {
+      const uint32_t h = filter_slot(v);
+      if (!((sf[h >> 5] >> (h & 31)) & 1u)) return false;
+    }
+    return test_bit(bits, v);
+  }
+};
+template <bool FILT>
+__device__ __forceinline__ ChangeTest<FILT> make_change_test(const uint32_t *bits,
+                                                             const uint32_t *filter) {
+  ChangeTest<FILT> t{bits, nullptr};
+  if constexpr (FILT) {
+    extern __shared__ uint32_t dyn_filter[];
+    for (int i = threadIdx.x; i < kFilterWords; i += blockDim.x) dyn_filter[i] = __ldg(filter + i);
+    __syncthreads();
+    t.sf = dyn_filter;
+  }
+  return t;
+}
+
+template <bool FILT>
 __global__ void k_mark_pull(int64_t n, const int64_t *__restrict__ offsets,
                             const int32_t *__restrict__ succ,
                             const uint32_t *__restrict__ chg_prev, uint32_t *__restrict__ active,
-                            int64_t light_max_deg) {
+                            int64_t light_max_deg, const uint32_t *__restrict__ filter) {
+  const auto changed = make_change_test<FILT>(chg_prev, filter);
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1360,7 +1410,7 @@ __global__ void k_mark_pull(int64_t n, const int64_t *__restrict__ offsets,
     const int64_t my_end = __ldg(offsets + (v + 1 < n ? v + 1 : n));
     const int64_t a0 = __shfl_sync(0xffffffffu, my_off, 0);
     const int64_t a1 = __shfl_sync(0xffffffffu, my_end, 31);
-    bool mark = v < n && test_bit(chg_prev, v);
+    bool mark = v < n && changed(v);
     const bool heavy = v < n && my_end - my_off > light_max_deg;
     const unsigned heavy_mask = __ballot_sync(0xffffffffu, heavy);
     if (heavy_mask == 0u && a1 - a0 <= 32 * 64) {
@@ -1374,7 +1424,7 @@ __global__ void k_mark_pull(int64_t n, const int64_t *__restrict__ offsets,
         }
         bool hit[IL];
 #pragma unroll
-        for (int j = 0; j < IL; j++) hit[j] = id[j] >= 0 && test_bit(chg_prev, id[j]);
+        for (int j = 0; j < IL; j++) hit[j] = id[j] >= 0 && changed(id[j]);
 #pragma unroll
         for (int j = 0; j < IL; j++) {
           unsigned bal = __ballot_sync(0xffffffffu, hit[j]);
@@ -1392,7 +1442,7 @@ __global__ void k_mark_pull(int64_t n, const int64_t *__restrict__ offsets,
         const int64_t b1 = __shfl_sync(0xffffffffu, my_end, r);
         if (((heavy_mask >> r) & 1u) || v0 + r >= n) continue;
         bool any = false;
-        for (int64_t k = b0 + lane; k < b1; k += 32) any |= test_bit(chg_prev, __ldg(succ + k));
+        for (int64_t k = b0 + lane; k < b1; k += 32) any |= changed(__ldg(succ + k));
         if (__any_sync(0xffffffffu, any)) mark |= lane == r;
       }
     }
@@ -1402,11 +1452,14 @@ __global__ void k_mark_pull(int64_t n, const int64_t *__restrict__ offsets,
 }
 
 // Heavy rows of the pull marking: one warp per work item (<= item_arcs ids of one node).
+template <bool FILT>
 __global__ void k_mark_items(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
                              const uint32_t *__restrict__ chg_prev,
                              const int32_t *__restrict__ item_node,
                              const int64_t *__restrict__ item_beg, int64_t n_items,
-                             int64_t item_arcs, uint32_t *__restrict__ active) {
+                             int64_t item_arcs, uint32_t *__restrict__ active,
+                             const uint32_t *__restrict__ filter) {
+  const auto changed = make_change_test<FILT>(chg_prev, filter);
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1416,9 +1469,55 @@ __global__ void k_mark_items(const int64_t *__restrict__ offsets, const int32_t 
     int64_t end = __ldg(offsets + v + 1);
     if (end > beg + item_arcs) end = beg + item_arcs;
     bool any = false;
-    for (int64_t k = beg + lane; k < end; k += 32) any |= test_bit(chg_prev, __ldg(succ + k));
+    constexpr int IL = 4;                 // independent id loads per lane in flight
+    for (int64_t kb = beg; kb < end; kb += 32 * IL) {
+      int32_t id[IL];
+#pragma unroll
+      for (int j = 0; j < IL; j++) {
+        const int64_t k = kb + j * 32 + lane;
+        id[j] = k < end ? ld_stream_id(succ + k) : -1;
+      }
+#pragma unroll
+      for (int j = 0; j < IL; j++) any |= id[j] >= 0 && changed(id[j]);
+    }
     if (__any_sync(0xffffffffu, any) && lane == 0 && !test_bit(active, v))
       atomicOr(active + (v >> 5), 1u << (v & 31));
+  }
+}
+
+// Heavy rows of the pull marking when they are one contiguous row range [h0, h1) (the
+// degree order's prefix): their ids [offsets[h0], offsets[h1]) are streamed flat, IL
+// loads per lane in flight, and a changed source marks its row, found by binary search
+// over the range's offsets (rare: only on hits).
+template <bool FILT>
+__global__ void k_mark_heavy_flat(const int64_t *__restrict__ offsets,
+                                  const int32_t *__restrict__ succ,
+                                  const uint32_t *__restrict__ chg_prev, int64_t h0, int64_t h1,
+                                  uint32_t *__restrict__ active,
+                                  const uint32_t *__restrict__ filter) {
+  const auto changed = make_change_test<FILT>(chg_prev, filter);
+  constexpr int IL = 8;
+  const int64_t a0 = __ldg(offsets + h0), a1 = __ldg(offsets + h1);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * IL;
+  for (int64_t kb = a0 + ((int64_t)blockIdx.x * blockDim.x) * IL; kb < a1; kb += stride) {
+    int32_t id[IL];
+#pragma unroll
+    for (int j = 0; j < IL; j++) {
+      const int64_t k = kb + (int64_t)j * blockDim.x + threadIdx.x;
+      id[j] = k < a1 ? ld_stream_id(succ + k) : -1;
+    }
+#pragma unroll
+    for (int j = 0; j < IL; j++) {
+      if (id[j] >= 0 && changed(id[j])) {
+        const int64_t k = kb + (int64_t)j * blockDim.x + threadIdx.x;
+        int64_t lo = h0, hi = h1;            // last row r with offsets[r] <= k
+        while (hi - lo > 1) {
+          const int64_t mid = (lo + hi) >> 1;
+          if (__ldg(offsets + mid) <= k) lo = mid; else hi = mid;
+        }
+        if (!test_bit(active, lo)) atomicOr(active + (lo >> 5), 1u << (lo & 31));
+      }
+    }
   }
 }
 
@@ -2203,6 +2302,52 @@ int hb_mark_active(int64_t n, const int64_t *fwd_offsets, const int32_t *fwd_suc
   return check_launch("k_mark_active");
 }
 
+static int mark_pull_impl(int64_t n, const int64_t *offsets, const int32_t *succ,
+                          const uint32_t *chg_prev, uint32_t *active, int64_t light_max_deg,
+                          const int32_t *item_node, const int64_t *item_beg, int64_t n_items,
+                          int64_t item_arcs, const uint32_t *filter, cudaStream_t s,
+                          int64_t h0 = -1, int64_t h1 = -1) {
+  const size_t smem = filter ? sizeof(uint32_t) * kFilterWords : 0;
+  if (filter) {
+    static bool attr = [] {
+      cudaFuncSetAttribute(k_mark_pull<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(sizeof(uint32_t) * kFilterWords));
+      cudaFuncSetAttribute(k_mark_items<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(sizeof(uint32_t) * kFilterWords));
+      cudaFuncSetAttribute(k_mark_heavy_flat<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(sizeof(uint32_t) * kFilterWords));
+      return true;
+    }();
+    (void)attr;
+    k_mark_pull<true><<<grid_for_warps((n + 31) / 32), kThreads, smem, s>>>(
+        n, offsets, succ, chg_prev, active, light_max_deg, filter);
+  } else {
+    k_mark_pull<false><<<grid_for_warps((n + 31) / 32), kThreads, 0, s>>>(
+        n, offsets, succ, chg_prev, active, light_max_deg, nullptr);
+  }
+  if (int e = check_launch("k_mark_pull")) return e;
+  if (n_items > 0 && h0 >= 0 && h1 > h0) {     // heavy rows contiguous: flat stream
+    const unsigned grid = (unsigned)num_sms() * 4;
+    if (filter)
+      k_mark_heavy_flat<true><<<grid, kThreads, smem, s>>>(offsets, succ, chg_prev, h0, h1,
+                                                           active, filter);
+    else
+      k_mark_heavy_flat<false><<<grid, kThreads, 0, s>>>(offsets, succ, chg_prev, h0, h1,
+                                                         active, nullptr);
+    return check_launch("k_mark_heavy_flat");
+  }
+  if (n_items > 0) {
+    if (filter)
+      k_mark_items<true><<<grid_for_warps(n_items), kThreads, smem, s>>>(
+          offsets, succ, chg_prev, item_node, item_beg, n_items, item_arcs, active, filter);
+    else
+      k_mark_items<false><<<grid_for_warps(n_items), kThreads, 0, s>>>(
+          offsets, succ, chg_prev, item_node, item_beg, n_items, item_arcs, active, nullptr);
+    return check_launch("k_mark_items");
+  }
+  return 0;
+}
+
 int hb_mark_pull(int64_t n, const int64_t *offsets, const int32_t *succ,
                  const uint32_t *chg_prev, uint32_t *active, int64_t light_max_deg,
                  const int32_t *item_node, const int64_t *item_beg, int64_t n_items,
@@ -2210,17 +2355,31 @@ int hb_mark_pull(int64_t n, const int64_t *offsets, const int32_t *succ,
   if (n <= 0) return 0;
   if (!offsets || !chg_prev || !active || (n_items > 0 && (!item_node || !item_beg)))
     return set_err_msg("hb_mark_pull: bad arguments");
-  cudaStream_t s = (cudaStream_t)stream;
-  k_mark_pull<<<grid_for_warps((n + 31) / 32), kThreads, 0, s>>>(n, offsets, succ, chg_prev,
-                                                                active, light_max_deg);
-  if (int e = check_launch("k_mark_pull")) return e;
-  if (n_items > 0) {
-    k_mark_items<<<grid_for_warps(n_items), kThreads, 0, s>>>(
-        offsets, succ, chg_prev, item_node, item_beg, n_items, item_arcs, active);
-    return check_launch("k_mark_items");
-  }
-  return 0;
+  return mark_pull_impl(n, offsets, succ, chg_prev, active, light_max_deg, item_node,
+                        item_beg, n_items, item_arcs, nullptr, (cudaStream_t)stream);
 }
+
+int hb_mark_pull_filtered(int64_t n, const int64_t *offsets, const int32_t *succ,
+                          const uint32_t *chg_prev, uint32_t *active, int64_t light_max_deg,
+                          const int32_t *item_node, const int64_t *item_beg, int64_t n_items,
+                          int64_t item_arcs, int64_t heavy_lo, int64_t heavy_hi,
+                          uint32_t *filter, void *stream) {
+  if (n <= 0) return 0;
+  if (!offsets || !chg_prev || !active || (n_items > 0 && (!item_node || !item_beg)) ||
+      (heavy_hi > heavy_lo && (heavy_lo < 0 || heavy_hi > n)))
+    return set_err_msg("hb_mark_pull_filtered: bad arguments");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (filter) {
+    cudaError_t e = cudaMemsetAsync(filter, 0, sizeof(uint32_t) * kFilterWords, s);
+    if (e != cudaSuccess) return set_err("hb_mark_pull_filtered memset", e);
+    k_build_filter<<<grid_for_threads((n + 31) / 32), kThreads, 0, s>>>(n, chg_prev, filter);
+    if (int er = check_launch("k_build_filter")) return er;
+  }
+  return mark_pull_impl(n, offsets, succ, chg_prev, active, light_max_deg, item_node,
+                        item_beg, n_items, item_arcs, filter, s, heavy_lo, heavy_hi);
+}
+
+int64_t hb_change_filter_words(void) { return kFilterWords; }
 
 int hb_forward_csr(int64_t n, const int64_t *offsets, const int32_t *succ, int64_t m,
                    int64_t *fwd_offsets, int64_t *cursor, int32_t *fwd_dst, void *temp,

@@ -56,6 +56,8 @@ DENSE_FRAC = float(_os.environ.get("HB_DENSE_FRAC", "0.95"))
 DENSE_ARC_FRAC = float(_os.environ.get("HB_DENSE_ARC_FRAC", "0.7"))
 FLAG_MIN_ARCS = 1 << 26
 FLAG_SAMPLES = 1 << 16
+# pull marking with a shared-memory filter of the changed nodes at or below this many
+FILTER_MAX_CHANGED = int(_os.environ.get("HB_FILTER_MAX_CHANGED", "8192"))
 
 CHECKPOINT_MAGIC = b"HBCK"
 CHECKPOINT_VERSION = 1
@@ -348,6 +350,7 @@ class _Device:
         self.last_nch = None
         self.slice_counts = None      # per-slice counters of a streamed iteration 1
         self.flag_out = None          # device: arcs whose source changed (last step)
+        self.change_filter = None     # device: hash filter of the changed nodes
         self.last_flagged = None
         early = None
         if seed_weights is not False:
@@ -513,11 +516,23 @@ class _Device:
         # successor lists) to build: only for long sparse tails, or once it exists;
         # before that, one streaming pass over the CSR of G^T marks the frontier
         if self.fwd is None and self._sparse_run < FRONTIER_AFTER:
-            _lib.check(_lib.hb().hb_mark_pull(
-                self.n, s.offsets.data_ptr(), s.succ.data_ptr(), self.chg_prev.data_ptr(),
-                self.active.data_ptr(), s.light_max_deg, s.item_node.data_ptr(),
-                s.item_beg.data_ptr(), s.n_items, s.item_arcs, self.stream.cuda_stream),
-                "hb_mark_pull")
+            L = _lib.hb()
+            args = (self.n, s.offsets.data_ptr(), s.succ.data_ptr(), self.chg_prev.data_ptr(),
+                    self.active.data_ptr(), s.light_max_deg, s.item_node.data_ptr(),
+                    s.item_beg.data_ptr(), s.n_items, s.item_arcs)
+            # degree order: the heavy rows are one range, streamed flat; nearly converged:
+            # the streamed ids are tested against a shared-memory hash filter of the few
+            # changed nodes (hb_mark_pull_filtered)
+            h0, h1 = (s.light_lo - s.n_heavy, s.light_lo) if s.order == "degree" else (0, 0)
+            filt = None
+            if self.last_nch <= FILTER_MAX_CHANGED:
+                if self.change_filter is None:
+                    self.change_filter = torch.empty(int(L.hb_change_filter_words()),
+                                                     dtype=torch.int32, device=self.device)
+                filt = self.change_filter.data_ptr()
+                self.launches += 1
+            _lib.check(L.hb_mark_pull_filtered(*args, h0, h1, filt, self.stream.cuda_stream),
+                       "hb_mark_pull_filtered")
             self.launches += 1 if s.n_items else 0
         else:
             off, dst = self._forward()

@@ -242,17 +242,19 @@ def test_run_multi_matches_independent_runs():
     assert bits_equal(mean, stack.mean(axis=0)) and bits_equal(std, stack.std(axis=0, ddof=1))
 
 
-@pytest.mark.parametrize("mode", ["forward", "pull", "off"])
+@pytest.mark.parametrize("mode", ["forward", "pull", "pull-filtered", "off"])
 @pytest.mark.parametrize("key", ["sparse2000_b4_s42_w5", "disc14_b4_s42_w5", "rmat12_b7_s42_w5",
                                  "islands400_b11_s3_w5", "config1_b6_s42_w5", "web14_b8_s42_w5"])
 def test_frontier_mode_matches_reference(key, mode, monkeypatch):
     """Sparse iterations visiting only chg_prev | out-neighbours(chg_prev) give the
     reference's bits; the frontier is used whenever fewer than n counters changed, marked
     from the forward graph (hb_mark_active, 'forward') or by the pull pass over G^T
-    (hb_mark_pull, 'pull'); 'off' never."""
+    (hb_mark_pull, 'pull'; with the shared-memory change filter, hb_mark_pull_filtered,
+    'pull-filtered'); 'off' never."""
     from paper_1308_2144_b200 import engine as E
     monkeypatch.setattr(E, "FRONTIER_DIV", 1)
     monkeypatch.setattr(E, "FRONTIER_AFTER", 0 if mode == "forward" else 10**9)
+    monkeypatch.setattr(E, "FILTER_MAX_CHANGED", 10**12 if mode == "pull-filtered" else -1)
     case = next(c for c in CASES if c["key"] == key)
     off, suc = golden_graph(case)
     g = hb.CsrGraph(off, suc)
@@ -274,8 +276,9 @@ def test_frontier_mode_matches_reference(key, mode, monkeypatch):
     assert bits_equal(hb.finalize_lin(acc), arrays[f"{key}/lin"])
     if mode == "forward":
         assert st._dev.fwd is not None
-    if mode == "pull":
+    if mode.startswith("pull"):
         assert st._dev.fwd is None and st._dev.active is not None
+        assert (st._dev.change_filter is not None) == (mode == "pull-filtered")
 
 
 @pytest.mark.parametrize("key", ["random300_b6_s42_w5", "rmat12_b7_s42_w5", "sparse2000_b4_s42_w5"])

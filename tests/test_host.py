@@ -77,6 +77,8 @@ def test_c_abi_rejects_bad_arguments():
         "hb_gather_changed", a1=5, a4=4)))
     assert "hb_relabel_csr_rows" in err(L.hb_relabel_csr_rows(*_abi_args(
         "hb_relabel_csr_rows", a0=5, a1=3, a2=6)))
+    assert "hb_mark_pull_filtered" in err(L.hb_mark_pull_filtered(*_abi_args(
+        "hb_mark_pull_filtered", a0=5)))
     assert "hb_relabel_csr_src_rows" in err(L.hb_relabel_csr_src_rows(*_abi_args(
         "hb_relabel_csr_src_rows", a0=5, a1=3, a2=6)))
     assert "hb_sample_flagged_arcs" in err(L.hb_sample_flagged_arcs(*_abi_args(
