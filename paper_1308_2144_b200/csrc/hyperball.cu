@@ -629,6 +629,10 @@ __device__ __forceinline__ void l2_prefetch(const void *p, int64_t bytes) {
                : "memory");
 }
 
+#ifndef HB_DENSE_COPY
+#define HB_DENSE_COPY 1
+#endif
+constexpr bool kDenseCopy = HB_DENSE_COPY != 0;   // dense batches skip the id compaction
 constexpr int kLookRounds = 4;    // L2 prefetch distance of the light kernel, in warp rounds
 // warp rounds per grid-stride chunk of the light kernel (resident warps x chunk nodes is
 // the id window the GPU sweeps): 16 for p >= 256, 4 below (measured on configs 3-5)
@@ -764,12 +768,20 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
     for (int it = 0; it < wtrips; it++) {
       const int64_t kb = beg + (int64_t)it * B::NB;
       int cnt = 0;
+      if (kDenseCopy && dense) {
+        // every source merged: the batch's valid ids are the prefix of its NB slots
 #pragma unroll
-      for (int j = 0; j < B::J; j++) {
-        const bool act = idr[j] >= 0 && (dense || test_bit(chg_prev, idr[j]));
-        const unsigned bal = (__ballot_sync(0xffffffffu, act) >> (grp * Gm::G)) & lowmask;
-        if (act) my_ids[cnt + __popc(bal & below)] = idr[j];
-        cnt += __popc(bal);
+        for (int j = 0; j < B::J; j++) my_ids[j * Gm::G + gl] = idr[j];
+        const int64_t left = end - kb;
+        cnt = left <= 0 ? 0 : (left < B::NB ? (int)left : B::NB);
+      } else {
+#pragma unroll
+        for (int j = 0; j < B::J; j++) {
+          const bool act = idr[j] >= 0 && (dense || test_bit(chg_prev, idr[j]));
+          const unsigned bal = (__ballot_sync(0xffffffffu, act) >> (grp * Gm::G)) & lowmask;
+          if (act) my_ids[cnt + __popc(bal & below)] = idr[j];
+          cnt += __popc(bal);
+        }
       }
 #pragma unroll
       for (int j = 0; j < B::J; j++) {                // next batch's ids, in flight meanwhile
@@ -879,12 +891,19 @@ k_heavy_partial(const int64_t *__restrict__ offsets, const int32_t *__restrict__
     }
     for (int64_t kb = beg; kb < end; kb += B::HEAVY_IDS) {
       int cnt = 0;
+      if (kDenseCopy && dense) {            // valid ids are the prefix of the batch
 #pragma unroll
-      for (int j = 0; j < B::HJ; j++) {
-        const bool act = idr[j] >= 0 && (dense || test_bit(chg_prev, idr[j]));
-        const unsigned bal = __ballot_sync(0xffffffffu, act);
-        if (act) wids[cnt + __popc(bal & below)] = idr[j];
-        cnt += __popc(bal);
+        for (int j = 0; j < B::HJ; j++) wids[j * 32 + lane] = idr[j];
+        const int64_t left = end - kb;
+        cnt = left < B::HEAVY_IDS ? (int)left : B::HEAVY_IDS;
+      } else {
+#pragma unroll
+        for (int j = 0; j < B::HJ; j++) {
+          const bool act = idr[j] >= 0 && (dense || test_bit(chg_prev, idr[j]));
+          const unsigned bal = __ballot_sync(0xffffffffu, act);
+          if (act) wids[cnt + __popc(bal & below)] = idr[j];
+          cnt += __popc(bal);
+        }
       }
 #pragma unroll
       for (int j = 0; j < B::HJ; j++) {
