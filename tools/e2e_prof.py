@@ -13,7 +13,11 @@ from paper_1308_2144_b200 import generators as gen  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "config4"
 cfgd = gen.CONFIGS[name]
-g = cfgd.build()
+if name in gen.DEVICE_BUILDERS:      # R-MAT: built on the device, copied to the host
+    g = cfgd.build_device(torch.device("cuda", 0)).to_host()
+    torch.cuda.empty_cache()
+else:
+    g = cfgd.build()
 n, m = g.n, g.m
 off_pin = torch.empty(n + 1, dtype=torch.int64, pin_memory=True)
 off_pin.numpy()[:] = g.offsets
