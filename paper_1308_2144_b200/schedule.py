@@ -163,6 +163,17 @@ STREAM_SLICES = int(os.environ.get("HB_STREAM_SLICES", "8"))
 STREAM_MIN_ARCS = 1 << 24
 
 
+def slice_rows(off_host: np.ndarray, nslices: int, align: int) -> np.ndarray:
+    """Row bounds [0 = r_0 < r_1 < ... = n] of up to `nslices` upload slices holding about
+    equal arc counts, every inner bound a multiple of `align` rows (the light kernel's
+    chunk window, so the window relabel maps each slice onto itself)."""
+    n = off_host.shape[0] - 1
+    m = int(off_host[-1])
+    targets = np.arange(1, nslices, dtype=np.int64) * m // nslices
+    rows = np.searchsorted(off_host, targets, side="left") // align * align
+    return np.unique(np.concatenate([[0], rows, [n]])).astype(np.int64)
+
+
 def _upload_slices(successors, off_host: np.ndarray, device, main, nslices: int, align: int):
     """int32 ids uploaded on the side stream in row slices aligned to `align` rows; returns
     the device tensor and [(r0, r1, event)]."""
@@ -176,9 +187,7 @@ def _upload_slices(successors, off_host: np.ndarray, device, main, nslices: int,
     with warnings.catch_warnings():
         warnings.simplefilter("ignore", UserWarning)
         ht = torch.from_numpy(np.ascontiguousarray(successors))
-    targets = np.arange(1, nslices, dtype=np.int64) * m // nslices
-    rows = np.searchsorted(off_host, targets, side="left") // align * align
-    rows = np.unique(np.concatenate([[0], rows, [n]]))
+    rows = slice_rows(off_host, nslices, align)
     slices = []
     with torch.cuda.stream(side):
         for r0, r1 in zip(rows[:-1].tolist(), rows[1:].tolist()):

@@ -4,6 +4,7 @@ and exports every symbol include/hyperball_b200.h declares (no compute without a
 import ctypes
 import hashlib
 import io
+import os
 import re
 
 import numpy as np
@@ -232,3 +233,43 @@ def test_multi_run_aggregate_semantics():
         hb.multi_run_aggregate([])
     with pytest.raises(ValueError):
         hb.multi_run_aggregate([np.zeros(2), np.zeros(3)])
+
+
+@pytest.mark.parametrize("nslices,align", [(8, 64), (3, 16), (16, 1)])
+def test_upload_slice_rows(nslices, align):
+    """Streamed-upload slices: cover [0, n], strictly increasing, inner bounds aligned to
+    the chunk window, arcs roughly balanced."""
+    from paper_1308_2144_b200.schedule import slice_rows
+    rng = np.random.default_rng(nslices)
+    deg = rng.zipf(2.1, 100_000).clip(max=10_000)
+    off = np.zeros(deg.size + 1, np.int64)
+    np.cumsum(deg, out=off[1:])
+    rows = slice_rows(off, nslices, align)
+    assert rows[0] == 0 and rows[-1] == deg.size and np.all(np.diff(rows) > 0)
+    assert np.all(rows[1:-1] % align == 0) and len(rows) <= nslices + 1
+    arcs = np.diff(off[rows])
+    assert arcs.max() <= off[-1] / nslices + deg.max() + align * deg.max()
+
+
+def test_bench_reference_arm_json(tmp_path):
+    """bench.py --impl reference (the CPU arm the driver runs) prints one JSON line with
+    the contract's keys; a non-zero rank prints nothing."""
+    import json
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, os.path.join(repo, "bench.py"), "--impl", "reference", "--config",
+           "config1", "--steps", "2", "--warmup", "3", "--ref-budget", "1"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=300, check=True).stdout
+    lines = [ln for ln in out.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "dtype", "config", "cpu_baseline", "e2e"):
+        assert k in d, k
+    assert d["impl"] == "reference" and d["value"] > 0 and d["steps"] == 2
+    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    env = dict(os.environ, RANK="1", WORLD_SIZE="2")
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 0 and not [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
