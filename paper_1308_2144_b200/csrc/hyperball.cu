@@ -633,11 +633,20 @@ __device__ __forceinline__ void l2_prefetch(const void *p, int64_t bytes) {
 #define HB_DENSE_COPY 1
 #endif
 constexpr bool kDenseCopy = HB_DENSE_COPY != 0;   // dense batches skip the id compaction
-constexpr int kLookRounds = 4;    // L2 prefetch distance of the light kernel, in warp rounds
+#ifndef HB_LOOK_ROUNDS
+#define HB_LOOK_ROUNDS 4
+#endif
+#ifndef HB_CHUNK_BIG
+#define HB_CHUNK_BIG 16
+#endif
+#ifndef HB_CHUNK_SMALL
+#define HB_CHUNK_SMALL 4
+#endif
+constexpr int kLookRounds = HB_LOOK_ROUNDS;   // L2 prefetch distance of the light kernel, in warp rounds
 // warp rounds per grid-stride chunk of the light kernel (resident warps x chunk nodes is
 // the id window the GPU sweeps): 16 for p >= 256, 4 below (measured on configs 3-5)
 template <int LOGP>
-__host__ __device__ constexpr int chunk_rounds() { return LOGP >= 8 ? 16 : 4; }
+__host__ __device__ constexpr int chunk_rounds() { return LOGP >= 8 ? HB_CHUNK_BIG : HB_CHUNK_SMALL; }
 
 // Light nodes (in-degree <= max_deg): one group of G lanes per node, NPW nodes per warp
 // round.  Each warp owns one contiguous node range, balanced over the grid by arcs +
