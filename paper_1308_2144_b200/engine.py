@@ -246,28 +246,29 @@ class _DeviceSums:
     _fin_cache = None   # (key, {name: host array}, {name: handed out once})
 
     def finalize(self, which: str) -> np.ndarray:
-        """closeness / harmonic / lin on the device (one hb_finalize computes all three in
-        original order and keeps them there); each is copied to the host (pinned) on its
-        first request only, so a harmonic-only caller downloads n doubles, not 3n."""
+        """closeness / harmonic / lin on the device, in original order, each computed
+        (hb_finalize with that output only) and copied to the host on its first request:
+        a harmonic-only caller reads one sum array and downloads n doubles, not 3n."""
         dev = self.dev
         key = (dev.launches_at_last_step, self.coreach_version)
         if self._fin_cache is None or self._fin_cache[0] != key:
+            self._fin_cache = (key, {}, {})
+        _, device_rows, host = self._fin_cache
+        if which == "lin" and self.coreach_dev is None:
+            return None
+        if which not in device_rows:
             n = dev.n
-            with_lin = self.coreach_dev is not None
-            out = torch.empty((3 if with_lin else 2, n), dtype=torch.float64, device=dev.device)
+            out = torch.empty(n, dtype=torch.float64, device=dev.device)
             rank = dev.sched.rank
+            ptr = {nm: (out.data_ptr() if nm == which else None)
+                   for nm in ("closeness", "harmonic", "lin")}
             _lib.check(_lib.hb().hb_finalize(
                 n, rank.data_ptr() if rank is not None else None, self.sum_dist.data_ptr(),
                 self.sum_recip.data_ptr(),
-                self.coreach_dev.data_ptr() if with_lin else None, out[0].data_ptr(),
-                out[1].data_ptr(), out[2].data_ptr() if with_lin else None,
-                dev.stream.cuda_stream), "hb_finalize")
+                self.coreach_dev.data_ptr() if which == "lin" else None, ptr["closeness"],
+                ptr["harmonic"], ptr["lin"], dev.stream.cuda_stream), "hb_finalize")
             dev.launches += 1
-            names = ["closeness", "harmonic", "lin"][:out.shape[0]]
-            self._fin_cache = (key, {nm: out[i] for i, nm in enumerate(names)}, {})
-        _, device_rows, host = self._fin_cache
-        if which not in device_rows:
-            return None
+            device_rows[which] = out
         if which in host:                  # the reference returns a fresh array per call
             return host[which].copy()
         host[which] = dev.to_host_raw(device_rows[which])
