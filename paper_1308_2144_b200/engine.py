@@ -919,8 +919,11 @@ def iterate(g, state: HyperBallState, observers: Iterable = ()) -> int:
     skip = state.config.skip_stable_nodes
     dense = (dev.prev_all or not skip
              or (dev.last_nch is not None and dev.last_nch >= DENSE_FRAC * dev.n))
+    # (wide rows make a redundant merge dearer than the per-source test it saves: the
+    # measured 0.7 is for p = 16; from p = 128 up the rule waits for 0.9)
+    arc_frac = DENSE_ARC_FRAC if state.config.params.p <= 64 else max(DENSE_ARC_FRAC, 0.9)
     arc_dense = (not dense and getattr(dev, "last_flagged", None) is not None
-                 and dev.last_flagged >= DENSE_ARC_FRAC)
+                 and dev.last_flagged >= arc_frac)
     nch = dev.union_step(t_next, dense or arc_dense, sums, flag_arcs=skip)
     if generic:
         old_h, new_h = dev.to_host(old), dev.to_host(dev.est)
