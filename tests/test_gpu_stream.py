@@ -127,3 +127,21 @@ def test_int64_ids_streamed(weblike, monkeypatch):
     got, pend, _ = _run(g64, 8, "window", 5, monkeypatch)
     assert pend > 1
     _same(got, ref)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_streamed_random_small_graphs(seed, monkeypatch):
+    """Corner cases of the slicing: tiny and ragged graphs (isolated nodes, empty slices,
+    n not a multiple of the window), every order and several widths."""
+    rng = np.random.default_rng(100 + seed)
+    n = int(rng.integers(50, 3000))
+    m = int(rng.integers(0, 8 * n))
+    src, dst = rng.integers(0, n, m), rng.integers(0, n, m)
+    if seed % 2:                                 # hub-heavy variant: heavy items
+        dst[: m // 3] = rng.integers(0, 4, m // 3)
+    g = gen.from_arcs_t(n, src, dst)
+    b = int(rng.choice([4, 6, 8]))
+    for schedule in ("window", "identity", "degree"):
+        ref, _, _ = _run(g, b, schedule, 1, monkeypatch)
+        got, _, _ = _run(g, b, schedule, int(rng.integers(2, 17)), monkeypatch)
+        _same(got, ref)
