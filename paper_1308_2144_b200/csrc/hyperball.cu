@@ -15,6 +15,8 @@
 //     the translation unit is also built with -fmad=false.
 //   * registers are < 128 (rho_max = 65 - b <= 61), so the 7-bit-safe SIMD byte max below
 //     is exact.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <type_traits>
 #include <algorithm>
@@ -577,6 +579,34 @@ constexpr int kThreads = 256;
 //          batch's ids are already in flight.
 //   heavy: the whole warp loads 32*J ids of one work item per batch, compacts them, and
 //          its NPW slots of G lanes take every NPW-th compacted id, U rows in flight each.
+// TMA row gather for the light kernel at p = 256 (HB_TMA_P256): 4 register rows per
+// cp.async.bulk.tensor...tile::gather4 into a per-warp shared buffer, completion on an
+// mbarrier; lanes read their chunks back with LDS.  No row-load registers, no address math.
+#ifndef HB_TMA_P256
+#define HB_TMA_P256 1
+#endif
+#ifndef HB_TMA_MINB
+#define HB_TMA_MINB 3                 // 80 registers without the loads in flight: 3 CTAs / SM
+#endif
+template <int LOGP, int LOGR, bool HINT>
+__host__ __device__ constexpr bool kTma() {
+  return HB_TMA_P256 && LOGP == 8 && LOGR == 0 && !HINT;
+}
+__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap *tm, int32_t r0,
+                                            int32_t r1, int32_t r2, int32_t r3, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst), "l"(tm), "r"(0), "r"(r0), "r"(r1),
+      "r"(r2), "r"(r3), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], %2; "
+                 "selp.u32 %0, 1, 0, p; }" : "=r"(done) : "r"(bar), "r"(phase) : "memory");
+}
+
 template <int LOGP>
 struct Batch {
   using Gm = Geo<LOGP>;
@@ -608,7 +638,7 @@ struct Batch {
 #endif
   static constexpr int LOADS = LOGP == 8 ? HB_LOADS_P256 : (LOGP == 6 ? HB_LOADS_P64 :
                                (LOGP <= 5 ? HB_LOADS_P16 : (LOGP == 7 ? HB_LOADS_P128 : 8)));
-  static constexpr int MINB = LOGP >= 10 ? 2 : (LOGP == 8 ? HB_MINB_P256 : (LOGP == 6 ? HB_MINB_P64 :
+  static constexpr int MINB = LOGP >= 10 ? 2 : (LOGP == 8 ? (HB_TMA_P256 ? HB_TMA_MINB : HB_MINB_P256) : (LOGP == 6 ? HB_MINB_P64 :
                               (LOGP == 7 ? HB_MINB_P128 : HB_MINB_P16)));
   static constexpr int U = Gm::CPL >= LOADS ? 1 : LOADS / Gm::CPL;  // rows in flight per lane
   static constexpr int NB = Gm::G > 8 ? Gm::G : 8;            // light: ids per group batch
@@ -662,7 +692,8 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
         double *__restrict__ est, double *__restrict__ sum_dist, double *__restrict__ sum_recip,
         EstConst ec, int64_t lo, int64_t hi, int64_t max_deg, int dense, double tf,
         unsigned long long *__restrict__ nch_out, unsigned long long *__restrict__ merged_out,
-        const uint32_t *__restrict__ active, Peers peers, RunArgs ra, int64_t hot_lim) {
+        const uint32_t *__restrict__ active, Peers peers, RunArgs ra, int64_t hot_lim,
+        const __grid_constant__ CUtensorMap tmap) {
   static_assert(LOGR == 0 || !PUSH, "batched runs are single-device");
   constexpr bool kHint = HINT;
   uint64_t pol = 0;
@@ -681,6 +712,19 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   uint32_t my_nch = 0, my_merged = 0;
+  uint32_t tma_buf = 0, tma_bar = 0, tma_phase = 0;
+  if constexpr (kTma<LOGP, LOGR, HINT>()) {
+    extern __shared__ __align__(1024) uint8_t tma_smem[];
+    __shared__ __align__(8) uint64_t tma_bars[kThreads / 32];
+    const int wl = threadIdx.x >> 5;
+    tma_buf = (uint32_t)__cvta_generic_to_shared(tma_smem) + wl * (Gm::NPW * B::U * Gm::P);
+    tma_bar = (uint32_t)__cvta_generic_to_shared(&tma_bars[wl]);
+    if (lane == 0) {
+      asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(tma_bar));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+  }
 
   // Node chunks of kChunkRounds warp rounds, dealt to warps grid-stride: at any moment the
   // resident warps sweep one contiguous window of the id space (L2 reuse of shared
@@ -800,6 +844,42 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
       __syncwarp();
       const int cmax = __reduce_max_sync(0xffffffffu, (unsigned)cnt);
       for (int i = 0; i < cmax; i += B::U) {
+        if constexpr (kTma<LOGP, LOGR, HINT>()) {
+          static_assert(B::U % 4 == 0 && Gm::NPW * B::U <= 32, "TMA gather layout");
+          constexpr int GPG = B::U / 4;              // gather4 issues per lane group
+          constexpr uint32_t kTx = Gm::NPW * B::U * Gm::P;
+          // lane q < NPW * GPG: group g = q / GPG loads rows [4h, 4h + 4), h = q % GPG, of
+          // its batch slots, padded with that group's own row (a no-op merge)
+          const int cg = __shfl_sync(0xffffffffu, cnt, ((lane / GPG) & (Gm::NPW - 1)) * Gm::G);
+          if (lane == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(tma_bar),
+                         "r"(kTx) : "memory");
+          __syncwarp();
+          if (lane < Gm::NPW * GPG) {
+            const int g = lane / GPG, h = lane % GPG;
+            const int64_t vg = base + g;
+            const int32_t fbg = (int32_t)(vg < ve ? vg : lo);
+            const int32_t *gids = &sids[threadIdx.x >> 5][g * B::NB];
+            int32_t r[4];
+#pragma unroll
+            for (int k = 0; k < 4; k++) r[k] = (i + 4 * h + k < cg) ? gids[i + 4 * h + k] : fbg;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            tma_gather4(tma_buf + (g * B::U + 4 * h) * Gm::P, &tmap, r[0], r[1], r[2], r[3],
+                        tma_bar);
+          }
+          mbar_wait(tma_bar, tma_phase);
+          tma_phase ^= 1u;
+          const uint4 *rows = reinterpret_cast<const uint4 *>(
+              __cvta_shared_to_generic(tma_buf + grp * B::U * Gm::P));
+#pragma unroll
+          for (int u = 0; u + 1 < B::U; u += 2)
+#pragma unroll
+            for (int c = 0; c < Gm::CPL; c++)
+              macc.add2(c, rows[u * Gm::CH + c * Gm::G + gl],
+                        rows[(u + 1) * Gm::CH + c * Gm::G + gl]);
+          __syncwarp();                          // every lane done before the next gather
+          continue;
+        }
         // from p = 64 up, slots past the group's count load the fallback row instead of
         // being predicated off: merging a row that is already part of the union changes
         // nothing, and the loads stay unconditional (no zero-fill, no per-slot predicates)
@@ -1873,6 +1953,31 @@ unsigned grid_for_warps(int64_t work_warps) {
 }
 unsigned grid_for_threads(int64_t work) { return grid_for_warps((work + 31) / 32); }
 
+// 2D tensor map over the register rows ([rows, p] bytes, one row per box) for the TMA
+// row gather; the driver entry point is resolved once through the runtime.
+int encode_row_map(CUtensorMap *tm, const uint8_t *base, int64_t rows, int p) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = [] {
+    PFN_cuTensorMapEncodeTiled_v12000 f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void **)&f, cudaEnableDefault, &q) !=
+            cudaSuccess || q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    cudaGetLastError();
+    return f;
+  }();
+  if (!enc) return set_err_msg("cuTensorMapEncodeTiled unavailable");
+  if (rows <= 0) return set_err_msg("TMA row map: no rows");
+  const cuuint64_t dims[2] = {(cuuint64_t)p, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)p};
+  const cuuint32_t box[2] = {(cuuint32_t)p, 1};
+  const cuuint32_t es[2] = {1, 1};
+  const CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t *>(base), dims,
+                         strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : set_err_msg("cuTensorMapEncodeTiled failed");
+}
+
 template <int LOGP, bool PUSH, int LOGR = 0>
 int union_step_impl(int64_t lo, int64_t hi, const int64_t *offsets, const int32_t *succ,
                     const uint8_t *cur, uint8_t *nxt, const uint32_t *chg_prev,
@@ -1883,8 +1988,26 @@ int union_step_impl(int64_t lo, int64_t hi, const int64_t *offsets, const int32_
                     const int32_t *item_node, const int64_t *item_beg, int64_t n_items,
                     int64_t item_arcs, uint8_t *partial, unsigned long long *nch,
                     unsigned long long *merged, int64_t hot_rows, const uint32_t *active,
-                    const Peers &peers, cudaStream_t s, RunArgs ra = RunArgs{nullptr, 0, 0}) {
+                    const Peers &peers, cudaStream_t s, RunArgs ra = RunArgs{nullptr, 0, 0},
+                    int64_t n_rows = 0) {
   using Gm = Geo<LOGP>;
+  CUtensorMap tmap;
+  memset(&tmap, 0, sizeof(tmap));
+  size_t tma_smem = 0;
+  if constexpr (kTma<LOGP, LOGR, false>()) {
+    if (int e = encode_row_map(&tmap, cur, n_rows, Gm::P)) return e;
+    tma_smem = (size_t)(kThreads / 32) * Geo<LOGP>::NPW * Batch<LOGP>::U * Gm::P;
+    static bool once = [] {
+      cudaFuncSetAttribute(k_light<LOGP, false, LOGR, false>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)((kThreads / 32) * Gm::NPW * Batch<LOGP>::U * Gm::P));
+      cudaFuncSetAttribute(k_light<LOGP, true, LOGR, false>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)((kThreads / 32) * Gm::NPW * Batch<LOGP>::U * Gm::P));
+      return true;
+    }();
+    (void)once;
+  }
   if (hot_rows > 0 && persist_window_on()) {
     cudaCtxResetPersistingL2Cache();    // lines of last iteration's buffer stop persisting
     set_hot_window(s, cur, (size_t)hot_rows * Gm::P);
@@ -1911,12 +2034,12 @@ int union_step_impl(int64_t lo, int64_t hi, const int64_t *offsets, const int32_
       if (hint)
         k_light<LOGP, PUSH, LOGR, true><<<grid_for_warps(warps), kThreads, 0, s>>>(
             offsets, succ, cur, nxt, chg_prev, chg_now, est, sum_dist, sum_recip, ec, lo, hi,
-            light_max_deg, dense, tf, nch, merged, active, peers, ra, hot_lim);
+            light_max_deg, dense, tf, nch, merged, active, peers, ra, hot_lim, tmap);
     }
     if (!hint)
-      k_light<LOGP, PUSH, LOGR, false><<<grid_for_warps(warps), kThreads, 0, s>>>(
+      k_light<LOGP, PUSH, LOGR, false><<<grid_for_warps(warps), kThreads, tma_smem, s>>>(
           offsets, succ, cur, nxt, chg_prev, chg_now, est, sum_dist, sum_recip, ec, lo, hi,
-          light_max_deg, dense, tf, nch, merged, active, peers, ra, hot_lim);
+          light_max_deg, dense, tf, nch, merged, active, peers, ra, hot_lim, tmap);
     if (int e = check_launch("k_light")) return e;
   }
   if (n_heavy > 0) {
@@ -2080,7 +2203,7 @@ int hb_union_step(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets,
                        finish_order, n_mega, item_node, item_beg, n_items, item_arcs, partial,
                        reinterpret_cast<unsigned long long *>(nch_out),
                        reinterpret_cast<unsigned long long *>(merged_out), hot_rows, active,
-                       peers, s)));
+                       peers, s, RunArgs{nullptr, 0, 0}, n)));
   }
   HB_DISPATCH(b, return (union_step_impl<LB, false>(
                      lo, hi, offsets, succ, cur, nxt, chg_prev, chg_now, est, sum_dist,
@@ -2088,7 +2211,7 @@ int hb_union_step(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets,
                      finish_order, n_mega, item_node, item_beg, n_items, item_arcs, partial,
                      reinterpret_cast<unsigned long long *>(nch_out),
                      reinterpret_cast<unsigned long long *>(merged_out), hot_rows, active, peers,
-                     s)));
+                     s, RunArgs{nullptr, 0, 0}, n)));
   return 0;
 }
 
