@@ -588,9 +588,15 @@ constexpr int kThreads = 256;
 #ifndef HB_TMA_MINB
 #define HB_TMA_MINB 3                 // 80 registers without the loads in flight: 3 CTAs / SM
 #endif
+#ifndef HB_TMA_P128
+#define HB_TMA_P128 0
+#endif
+#ifndef HB_TMA_MINB128
+#define HB_TMA_MINB128 4
+#endif
 template <int LOGP, int LOGR, bool HINT>
 __host__ __device__ constexpr bool kTma() {
-  return HB_TMA_P256 && LOGP == 8 && LOGR == 0 && !HINT;
+  return ((HB_TMA_P256 && LOGP == 8) || (HB_TMA_P128 && LOGP == 7)) && LOGR == 0 && !HINT;
 }
 __device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap *tm, int32_t r0,
                                             int32_t r1, int32_t r2, int32_t r3, uint32_t bar) {
@@ -639,7 +645,7 @@ struct Batch {
   static constexpr int LOADS = LOGP == 8 ? HB_LOADS_P256 : (LOGP == 6 ? HB_LOADS_P64 :
                                (LOGP <= 5 ? HB_LOADS_P16 : (LOGP == 7 ? HB_LOADS_P128 : 8)));
   static constexpr int MINB = LOGP >= 10 ? 2 : (LOGP == 8 ? (HB_TMA_P256 ? HB_TMA_MINB : HB_MINB_P256) : (LOGP == 6 ? HB_MINB_P64 :
-                              (LOGP == 7 ? HB_MINB_P128 : HB_MINB_P16)));
+                              (LOGP == 7 ? (HB_TMA_P128 ? HB_TMA_MINB128 : HB_MINB_P128) : HB_MINB_P16)));
   static constexpr int U = Gm::CPL >= LOADS ? 1 : LOADS / Gm::CPL;  // rows in flight per lane
   static constexpr int NB = Gm::G > 8 ? Gm::G : 8;            // light: ids per group batch
   static constexpr int J = NB / Gm::G;                        // light: ids loaded per lane
