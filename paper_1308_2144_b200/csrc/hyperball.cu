@@ -591,12 +591,19 @@ constexpr int kThreads = 256;
 #ifndef HB_TMA_P128
 #define HB_TMA_P128 0
 #endif
+#ifndef HB_TMA_P64
+#define HB_TMA_P64 0
+#endif
+#ifndef HB_TMA_MINB64
+#define HB_TMA_MINB64 4
+#endif
 #ifndef HB_TMA_MINB128
 #define HB_TMA_MINB128 4
 #endif
 template <int LOGP, int LOGR, bool HINT>
 __host__ __device__ constexpr bool kTma() {
-  return ((HB_TMA_P256 && LOGP == 8) || (HB_TMA_P128 && LOGP == 7)) && LOGR == 0 && !HINT;
+  return ((HB_TMA_P256 && LOGP == 8) || (HB_TMA_P128 && LOGP == 7) || (HB_TMA_P64 && LOGP == 6)) &&
+         LOGR == 0 && !HINT;
 }
 __device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap *tm, int32_t r0,
                                             int32_t r1, int32_t r2, int32_t r3, uint32_t bar) {
@@ -644,7 +651,7 @@ struct Batch {
 #endif
   static constexpr int LOADS = LOGP == 8 ? HB_LOADS_P256 : (LOGP == 6 ? HB_LOADS_P64 :
                                (LOGP <= 5 ? HB_LOADS_P16 : (LOGP == 7 ? HB_LOADS_P128 : 8)));
-  static constexpr int MINB = LOGP >= 10 ? 2 : (LOGP == 8 ? (HB_TMA_P256 ? HB_TMA_MINB : HB_MINB_P256) : (LOGP == 6 ? HB_MINB_P64 :
+  static constexpr int MINB = LOGP >= 10 ? 2 : (LOGP == 8 ? (HB_TMA_P256 ? HB_TMA_MINB : HB_MINB_P256) : (LOGP == 6 ? (HB_TMA_P64 ? HB_TMA_MINB64 : HB_MINB_P64) :
                               (LOGP == 7 ? (HB_TMA_P128 ? HB_TMA_MINB128 : HB_MINB_P128) : HB_MINB_P16)));
   static constexpr int U = Gm::CPL >= LOADS ? 1 : LOADS / Gm::CPL;  // rows in flight per lane
   static constexpr int NB = Gm::G > 8 ? Gm::G : 8;            // light: ids per group batch
@@ -851,7 +858,7 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
       const int cmax = __reduce_max_sync(0xffffffffu, (unsigned)cnt);
       for (int i = 0; i < cmax; i += B::U) {
         if constexpr (kTma<LOGP, LOGR, HINT>()) {
-          static_assert(B::U % 4 == 0 && Gm::NPW * B::U <= 32, "TMA gather layout");
+          static_assert(B::U % 4 == 0 && Gm::NPW * (B::U / 4) <= 32, "TMA gather layout");
           constexpr int GPG = B::U / 4;              // gather4 issues per lane group
           constexpr uint32_t kTx = Gm::NPW * B::U * Gm::P;
           // lane q < NPW * GPG: group g = q / GPG loads rows [4h, 4h + 4), h = q % GPG, of
