@@ -336,7 +336,7 @@ def build_schedule(offsets, successors, b: int, device, order: str = "auto", wor
         on_order(perm)
     if ids_ready is not None:
         s_main.wait_event(ids_ready)
-    pending, relabel, src_slices = [], None, None
+    pending, relabel, src_slices, late_relabel = [], None, None, None
     if slices is not None:
         if order in ("window", "identity") and n > 0:
             pending = slices                   # consumed by iteration 1, slice by slice
@@ -376,15 +376,25 @@ def build_schedule(offsets, successors, b: int, device, order: str = "auto", wor
         torch.cumsum(new_deg, 0, out=new_off[1:])
         new_succ = torch.empty(m, dtype=torch.int32, device=device)
         s = s_main
-        if src_slices is not None:
+        if src_slices is not None and not SORT_ROWS:
             # scatter form by uploaded (old) rows: slice k is relabelled while slices
-            # k+1.. are still crossing PCIe; every new row is complete after the last one
-            for r0, r1, ev in src_slices:
+            # k+1.. are still crossing PCIe; every new row is complete after the last one.
+            # Enqueued at the end, after the heavy-item setup below, whose host reads must
+            # not wait for the copy.
+            def late_relabel(off=off, succ=succ, rank=rank, new_off=new_off,
+                             new_succ=new_succ, s=s):
+                for r0, r1, ev in src_slices:
+                    s.wait_event(ev)
+                    _lib.check(L.hb_relabel_csr_src_rows(
+                        n, r0, r1, off.data_ptr(), succ.data_ptr(), rank.data_ptr(),
+                        new_off.data_ptr(), new_succ.data_ptr(), s.cuda_stream),
+                        "hb_relabel_csr_src_rows")
+        elif src_slices is not None:
+            for _, _, ev in src_slices:
                 s.wait_event(ev)
-                _lib.check(L.hb_relabel_csr_src_rows(
-                    n, r0, r1, off.data_ptr(), succ.data_ptr(), rank.data_ptr(),
-                    new_off.data_ptr(), new_succ.data_ptr(), s.cuda_stream),
-                    "hb_relabel_csr_src_rows")
+            _lib.check(L.hb_relabel_csr(n, off.data_ptr(), succ.data_ptr(), perm.data_ptr(),
+                                        rank.data_ptr(), new_off.data_ptr(),
+                                        new_succ.data_ptr(), s.cuda_stream), "hb_relabel_csr")
         else:
             _lib.check(L.hb_relabel_csr(n, off.data_ptr(), succ.data_ptr(), perm.data_ptr(),
                                         rank.data_ptr(), new_off.data_ptr(),
@@ -434,6 +444,8 @@ def build_schedule(offsets, successors, b: int, device, order: str = "auto", wor
         steady = lo + max(n_nonzero, n_heavy)
     else:
         light_lo, light_hi, steady = lo, hi, hi
+    if late_relabel is not None:
+        late_relabel()
     return Schedule(n=n, m=m, b=b, order=order, perm=perm, rank=rank, offsets=off, succ_buf=succ,
                     lo=lo, hi=hi, light_lo=light_lo, light_hi=light_hi,
                     light_hi_steady=steady, light_max_deg=light_max_deg, item_arcs=item_arcs,
