@@ -273,3 +273,19 @@ def test_bench_reference_arm_json(tmp_path):
     env = dict(os.environ, RANK="1", WORLD_SIZE="2")
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=env)
     assert r.returncode == 0 and not [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+
+
+def test_sm100a_sass_uses_tma_gather_and_3input_max():
+    """The built library is sm_100a code using the Blackwell features the design relies
+    on: TMA tile::gather4 for the p = 256 row gathers (with mbarrier completion) and the
+    3-input 16x2 integer max for the byte-wise union."""
+    import shutil
+    import subprocess
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(exe):
+        pytest.skip("cuobjdump not available")
+    out = subprocess.run([exe, "-sass", _lib.HB_LIB_PATH], capture_output=True, text=True,
+                         timeout=300).stdout
+    assert "sm_100a" in out or "SM100" in out.upper()
+    for op in ("UTMALDG.2D.GATHER4", "SYNCS.PHASECHK.TRANS64", "VIMNMX3.U16x2"):
+        assert op in out, op
