@@ -860,15 +860,18 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
         if constexpr (kTma<LOGP, LOGR, HINT>()) {
           static_assert(B::U % 4 == 0 && Gm::NPW * (B::U / 4) <= 32, "TMA gather layout");
           constexpr int GPG = B::U / 4;              // gather4 issues per lane group
-          constexpr uint32_t kTx = Gm::NPW * B::U * Gm::P;
           // lane q < NPW * GPG: group g = q / GPG loads rows [4h, 4h + 4), h = q % GPG, of
           // its batch slots, padded with that group's own row (a no-op merge)
           const int cg = __shfl_sync(0xffffffffu, cnt, ((lane / GPG) & (Gm::NPW - 1)) * Gm::G);
+          // only groups of 4 slots holding at least one id are fetched (a batch's last
+          // slots are often empty); their rows are not merged either
+          const bool issue = lane < Gm::NPW * GPG && 4 * (lane % GPG) < cg - i;
+          const uint32_t ngat = __popc(__ballot_sync(0xffffffffu, issue));
           if (lane == 0)
             asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(tma_bar),
-                         "r"(kTx) : "memory");
+                         "r"(ngat * 4 * Gm::P) : "memory");
           __syncwarp();
-          if (lane < Gm::NPW * GPG) {
+          if (issue) {
             const int g = lane / GPG, h = lane % GPG;
             const int64_t vg = base + g;
             const int32_t fbg = (int32_t)(vg < ve ? vg : lo);
@@ -885,11 +888,16 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
           const uint4 *rows = reinterpret_cast<const uint4 *>(
               __cvta_shared_to_generic(tma_buf + grp * B::U * Gm::P));
 #pragma unroll
-          for (int u = 0; u + 1 < B::U; u += 2)
+          for (int h = 0; h < GPG; h++) {
+            if (4 * h < cnt - i) {
 #pragma unroll
-            for (int c = 0; c < Gm::CPL; c++)
-              macc.add2(c, rows[u * Gm::CH + c * Gm::G + gl],
-                        rows[(u + 1) * Gm::CH + c * Gm::G + gl]);
+              for (int u = 4 * h; u < 4 * h + 4; u += 2)
+#pragma unroll
+                for (int c = 0; c < Gm::CPL; c++)
+                  macc.add2(c, rows[u * Gm::CH + c * Gm::G + gl],
+                            rows[(u + 1) * Gm::CH + c * Gm::G + gl]);
+            }
+          }
           __syncwarp();                          // every lane done before the next gather
           continue;
         }
