@@ -28,7 +28,8 @@ def sha(a):
 @pytest.mark.parametrize("world", [2, 3, 8])
 @pytest.mark.parametrize("schedule", ["identity", "degree", "window"])
 @pytest.mark.parametrize("key", ["random300_b6_s42_w5", "disc14_b4_s42_w5", "rmat12_b7_s42_w5",
-                                 "config1_b6_s42_w5", "sparse2000_b4_s42_w5"])
+                                 "config1_b6_s42_w5", "sparse2000_b4_s42_w5",
+                                 "web14_b8_s42_w5"])
 def test_simulated_ranks_match_reference(key, world, schedule, packed):
     case = CASES[key]
     off, suc = golden_graph(case)
