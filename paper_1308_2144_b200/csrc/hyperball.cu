@@ -1974,6 +1974,9 @@ unsigned grid_for_warps(int64_t work_warps) {
 }
 unsigned grid_for_threads(int64_t work) { return grid_for_warps((work + 31) / 32); }
 
+#ifndef HB_TMA_L2PROMO
+#define HB_TMA_L2PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+#endif
 // 2D tensor map over the register rows ([rows, p] bytes, one row per box) for the TMA
 // row gather; the driver entry point is resolved once through the runtime.
 int encode_row_map(CUtensorMap *tm, const uint8_t *base, int64_t rows, int p) {
@@ -1994,7 +1997,7 @@ int encode_row_map(CUtensorMap *tm, const uint8_t *base, int64_t rows, int p) {
   const cuuint32_t es[2] = {1, 1};
   const CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t *>(base), dims,
                          strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_SWIZZLE_NONE, (CUtensorMapL2promotion)HB_TMA_L2PROMO,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : set_err_msg("cuTensorMapEncodeTiled failed");
 }
