@@ -142,6 +142,61 @@ int hb_union_step(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets,
                   int n_peers, uint8_t *const *peer_nxt, uint32_t *const *peer_chg,
                   void *stream);
 
+/* The same step with its arguments in one struct (the form to bind from a non-Python
+ * host: fields are named, and later versions only append fields, so a caller built
+ * against this header keeps working -- struct_size tells the library which fields the
+ * caller knows).  Field meanings are those of hb_union_step above; struct_size must be
+ * sizeof(hb_step_args).  hb_union_step is a thin wrapper that fills this struct. */
+typedef struct hb_step_args {
+  uint64_t struct_size;
+  /* graph (internal ids) and the row range of this call */
+  int64_t n, lo, hi;
+  const int64_t *offsets;
+  const int32_t *succ;
+  /* counters, change flags, estimates */
+  const uint8_t *cur;
+  uint8_t *nxt;
+  const uint32_t *chg_prev;
+  uint32_t *chg_now;
+  double *est;
+  int32_t b, dense, clear_chg_now, n_disc;
+  int64_t t;
+  const double *lc_table;
+  double alpha_p2, lc_cut;
+  /* fused accumulator (each may be NULL) and discounted-gain sums */
+  double *sum_dist, *sum_recip;
+  double *disc;
+  int64_t disc_stride;
+  const double *disc_scale;
+  int32_t disc_div, n_peers;
+  /* heavy-node schedule */
+  int64_t light_max_deg;
+  const int32_t *heavy_nodes, *item_first;
+  int64_t n_heavy;
+  const int32_t *finish_order;
+  int64_t n_mega;
+  const int32_t *item_node;
+  const int64_t *item_beg;
+  int64_t n_items, item_arcs;
+  uint8_t *partial;
+  /* outputs and options */
+  uint64_t *nch_out, *merged_out;
+  int64_t hot_rows;
+  const uint32_t *active;
+  uint8_t *const *peer_nxt;
+  uint32_t *const *peer_chg;
+  void *stream;
+} hb_step_args;
+
+int hb_union_step_v2(const hb_step_args *args);
+uint64_t hb_step_args_size(void);   /* sizeof(hb_step_args) as built */
+
+/* L2 persistence (hot_rows above): on by default.  hb_set_l2_persist(0) stops the
+ * library from touching the persisting-L2 set-aside and the stream's access-policy
+ * window (for a host that manages them itself).  When on, the set-aside limit is raised
+ * to the library's size only if the current limit is smaller. */
+void hb_set_l2_persist(int enable);
+
 /* Finalizers (centrality.py:153-171) over device sums in internal order, written in
  * original order: out[o] uses internal row rank[o] (rank NULL = identity).
  *   closeness[o] = 1 / sum_dist where sum_dist > 0, else 0

@@ -43,6 +43,9 @@ HB_SIGNATURES = {
                              _vp, _i64, _vp, _dbl, _dbl, _int, _int, _i64, _vp, _vp, _i64,
                              _vp, _i64, _vp, _vp, _i64, _i64, _vp, _vp, _vp, _i64,
                              _vp, _i64, _int, _vp, _int, _vp, _int, _vp, _vp, _vp]),
+    "hb_union_step_v2": (_int, [_vp]),
+    "hb_set_l2_persist": (None, [_int]),
+    "hb_step_args_size": (_u64, []),
     "hb_union_step_runs": (_int, [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                   _vp, _vp, _i64, _i64, _vp, _dbl, _dbl, _int, _int, _int,
                                   _i64, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _i64, _i64, _vp,
@@ -77,6 +80,47 @@ HB_SIGNATURES = {
     "hb_light_npw": (_i64, [_int]),
     "hb_light_window": (_i64, [_int]),
 }
+
+class StepArgs(ctypes.Structure):
+    """``hb_step_args`` (include/hyperball_b200.h): hb_union_step_v2's named arguments."""
+
+    _fields_ = [
+        ("struct_size", ctypes.c_uint64),
+        ("n", _i64), ("lo", _i64), ("hi", _i64),
+        ("offsets", _vp), ("succ", _vp),
+        ("cur", _vp), ("nxt", _vp), ("chg_prev", _vp), ("chg_now", _vp), ("est", _vp),
+        ("b", ctypes.c_int32), ("dense", ctypes.c_int32), ("clear_chg_now", ctypes.c_int32),
+        ("n_disc", ctypes.c_int32),
+        ("t", _i64),
+        ("lc_table", _vp), ("alpha_p2", _dbl), ("lc_cut", _dbl),
+        ("sum_dist", _vp), ("sum_recip", _vp), ("disc", _vp), ("disc_stride", _i64),
+        ("disc_scale", _vp), ("disc_div", ctypes.c_int32), ("n_peers", ctypes.c_int32),
+        ("light_max_deg", _i64), ("heavy_nodes", _vp), ("item_first", _vp), ("n_heavy", _i64),
+        ("finish_order", _vp), ("n_mega", _i64), ("item_node", _vp), ("item_beg", _vp),
+        ("n_items", _i64), ("item_arcs", _i64), ("partial", _vp),
+        ("nch_out", _vp), ("merged_out", _vp), ("hot_rows", _i64), ("active", _vp),
+        ("peer_nxt", _vp), ("peer_chg", _vp), ("stream", _vp),
+    ]
+
+    def __init__(self, **kw):
+        super().__init__(struct_size=ctypes.sizeof(StepArgs))
+        for k, v in kw.items():
+            setattr(self, k, v)
+
+
+def schedule_args(s) -> dict:
+    """The heavy-node schedule fields of StepArgs from a schedule.Schedule."""
+    return dict(light_max_deg=s.light_max_deg, heavy_nodes=s.heavy_nodes.data_ptr(),
+                item_first=s.item_first.data_ptr(), n_heavy=s.n_heavy,
+                finish_order=s.finish_order.data_ptr(), n_mega=s.n_mega,
+                item_node=s.item_node.data_ptr(), item_beg=s.item_beg.data_ptr(),
+                n_items=s.n_items, item_arcs=s.item_arcs, partial=s.partial.data_ptr(),
+                hot_rows=s.hot_rows)
+
+
+def union_step(args: StepArgs, what: str = "hb_union_step_v2") -> None:
+    check(hb().hb_union_step_v2(ctypes.byref(args)), what)
+
 
 GRAPH_SIGNATURES = {
     "hbg_er": (_vp, [_i64, _dbl, _u64, _int]),

@@ -220,6 +220,12 @@ def fusable(obs, n: int) -> bool:
     """An accumulator whose per-iteration fold the union kernel can do (no discounts).
     Never touches the lazily-refreshed sums (that would force a device read-back)."""
     if isinstance(obs, CentralityAccumulator):
+        # a subclass that overrides a hook must see its calls: host path (the reference
+        # calls on_step / on_converged on every observer, engine.py:391-392,433-434)
+        cls = type(obs)
+        if any(getattr(cls, h) is not getattr(CentralityAccumulator, h)
+               for h in ("on_step", "on_converged", "accumulate")):
+            return False
         return (len(obs.discounts) <= MAX_FUSED_DISCOUNTS and obs.n == n
                 and all(hasattr(d, "device_factor") for d in obs.discounts))
     if type(obs).__name__ != "CentralityAccumulator":

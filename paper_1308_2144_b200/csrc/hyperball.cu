@@ -1894,27 +1894,76 @@ __global__ void k_count_bits(const uint32_t *__restrict__ bits, int64_t words,
 }
 
 // ------------------------------------------------------------------ launch helpers
+// Device-scoped state.  Every C-ABI entry point that launches work first makes the
+// stream's device current (DevGuard), so a host that drives several GPUs from one thread
+// may call it with any current device; everything cached below is kept per device
+// ordinal (SM count, L2 set-aside, opt-in shared-memory sizes).
+constexpr int kMaxDevices = 64;
+
+struct DevGuard {
+  int prev = -1, dev = -1;
+  explicit DevGuard(cudaStream_t s) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (cudaStreamGetDevice(s, &dev) != cudaSuccess) dev = prev;
+    if (dev >= 0 && dev != prev) cudaSetDevice(dev);
+    cudaGetLastError();
+  }
+  ~DevGuard() {
+    if (prev >= 0 && dev != prev) cudaSetDevice(prev);
+  }
+};
+
+int current_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) dev = 0;
+  return dev;
+}
+
+// Opt-in dynamic shared memory of `func` on the current device (once per device and
+// kernel; the return code is checked).
+int ensure_smem_attr(const void *func, int bytes, const char *what) {
+  static struct { const void *f; int dev; int bytes; } done[256];
+  static int n_done = 0;
+  const int dev = current_device();
+  for (int i = 0; i < n_done; i++)
+    if (done[i].f == func && done[i].dev == dev && done[i].bytes >= bytes) return 0;
+  cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return set_err(what, e);
+  if (n_done < 256) done[n_done++] = {func, dev, bytes};
+  return 0;
+}
+
 // Persisting-L2 window over the hot head of the register array.  In degree order the
 // internal ids sort nodes by in-degree, which on the R-MAT configs is also the read
 // frequency of a row (corr > 0.999): the first 3% of rows serve ~78% of all row reads
 // (config 5 at 1/16 scale).  Without help those rows are evicted by the streamed ids and
 // the cold rows; an access-policy window marks them persisting.  hot_rows == 0 disables.
-// HB_L2_PERSIST_MB overrides the set-aside size (0 = off).
+// HB_L2_PERSIST_MB overrides the set-aside size (0 = off); hb_set_l2_persist(0) turns the
+// whole mechanism off for a host application that manages the L2 set-aside itself.  The
+// set-aside limit is only ever raised (a larger limit the host set is kept).
+bool g_l2_persist = true;
+
 size_t persist_bytes() {
-  static size_t b = [] {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceProp prop;
-    if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) return (size_t)0;
-    size_t want = (size_t)32 << 20;   // measured best on config 5 (16-96 MB swept)
-    if (const char *e = getenv("HB_L2_PERSIST_MB")) want = (size_t)atoll(e) << 20;
-    if (want > (size_t)prop.persistingL2CacheMaxSize) want = prop.persistingL2CacheMaxSize;
-    if (want > (size_t)prop.accessPolicyMaxWindowSize) want = prop.accessPolicyMaxWindowSize;
-    if (want && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) != cudaSuccess) want = 0;
+  static size_t per_dev[kMaxDevices];
+  static bool done[kMaxDevices];
+  const int dev = current_device();
+  if (done[dev]) return per_dev[dev];
+  done[dev] = true;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) {
     cudaGetLastError();
-    return want;
-  }();
-  return b;
+    return per_dev[dev] = 0;
+  }
+  size_t want = (size_t)32 << 20;   // measured best on config 5 (16-96 MB swept)
+  if (const char *e = getenv("HB_L2_PERSIST_MB")) want = (size_t)atoll(e) << 20;
+  if (want > (size_t)prop.persistingL2CacheMaxSize) want = prop.persistingL2CacheMaxSize;
+  if (want > (size_t)prop.accessPolicyMaxWindowSize) want = prop.accessPolicyMaxWindowSize;
+  size_t have = 0;
+  if (cudaDeviceGetLimit(&have, cudaLimitPersistingL2CacheSize) != cudaSuccess) have = 0;
+  if (want && have < want && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) != cudaSuccess)
+    want = have;
+  cudaGetLastError();
+  return per_dev[dev] = want;
 }
 
 // Bytes of the evict_last head (HB_HINT_MB, default 64); HB_PERSIST_WINDOW=0 turns the
@@ -1932,7 +1981,7 @@ bool persist_window_on() {
     const char *e = getenv("HB_PERSIST_WINDOW");
     return !(e && atoi(e) == 0);
   }();
-  return on;
+  return on && g_l2_persist;
 }
 
 void set_hot_window(cudaStream_t s, const void *base, size_t hot_bytes) {
@@ -1951,16 +2000,17 @@ void set_hot_window(cudaStream_t s, const void *base, size_t hot_bytes) {
   cudaGetLastError();
 }
 
-int g_num_sms = 0;
 int num_sms() {
-  if (g_num_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
-        g_num_sms <= 0)
-      g_num_sms = 148;
+  static int per_dev[kMaxDevices];
+  const int dev = current_device();
+  if (per_dev[dev] == 0) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
+      v = 148;
+    cudaGetLastError();
+    per_dev[dev] = v;
   }
-  return g_num_sms;
+  return per_dev[dev];
 }
 // Grid for `work_warps` warps of work: enough CTAs to fill every SM several times over,
 // capped by the work; kernels grid-stride over the rest.
@@ -2021,18 +2071,11 @@ int union_step_impl(int64_t lo, int64_t hi, const int64_t *offsets, const int32_
   if constexpr (kTma<LOGP, LOGR, false>()) {
     if (int e = encode_row_map(&tmap, cur, n_rows, Gm::P)) return e;
     tma_smem = (size_t)(kThreads / 32) * Geo<LOGP>::NPW * Batch<LOGP>::U * Gm::P;
-    static bool once = [] {
-      cudaFuncSetAttribute(k_light<LOGP, false, LOGR, false>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)((kThreads / 32) * Gm::NPW * Batch<LOGP>::U * Gm::P));
-      cudaFuncSetAttribute(k_light<LOGP, true, LOGR, false>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)((kThreads / 32) * Gm::NPW * Batch<LOGP>::U * Gm::P));
-      return true;
-    }();
-    (void)once;
+    if (int e = ensure_smem_attr((const void *)k_light<LOGP, PUSH, LOGR, false>, (int)tma_smem,
+                                 "k_light smem attribute"))
+      return e;
   }
-  if (hot_rows > 0 && persist_window_on()) {
+  if (hot_rows > 0 && persist_window_on() && persist_bytes() > 0) {
     cudaCtxResetPersistingL2Cache();    // lines of last iteration's buffer stop persisting
     set_hot_window(s, cur, (size_t)hot_rows * Gm::P);
   }
@@ -2151,6 +2194,7 @@ int64_t hb_light_window(int b) {
 int hb_seed(uint8_t *regs, double *est, int64_t n, int b, int register_width, uint64_t seed,
             const int32_t *perm, const int64_t *weights, const double *lc_table,
             double alpha_p2, double lc_cut, void *stream) {
+  DevGuard dg_((cudaStream_t)stream);
   if (register_width < 1 || register_width > 8) return set_err_msg("hb_seed: bad register_width");
   if (n == 0) return 0;
   if (n < 0 || !regs || !est || !lc_table) return set_err_msg("hb_seed: bad arguments");
@@ -2164,6 +2208,7 @@ int hb_seed(uint8_t *regs, double *est, int64_t n, int b, int register_width, ui
 int hb_estimate_rows(const uint8_t *regs, int64_t lo, int64_t hi, int b,
                      const double *lc_table, double alpha_p2, double lc_cut, double *out,
                      void *stream) {
+  DevGuard dg_((cudaStream_t)stream);
   if (hi <= lo) return 0;
   if (lo < 0 || !regs || !lc_table || !out) return set_err_msg("hb_estimate_rows: bad arguments");
   cudaStream_t s = (cudaStream_t)stream;
@@ -2171,6 +2216,67 @@ int hb_estimate_rows(const uint8_t *regs, int64_t lo, int64_t hi, int b,
   HB_DISPATCH(b, (k_estimate_rows<LB><<<grid_for_threads(hi - lo), kThreads, 0, s>>>(
                      regs, lo, hi, ec, out)));
   return check_launch("k_estimate_rows");
+}
+
+int hb_union_step_v2(const hb_step_args *a) {
+  if (!a || a->struct_size < sizeof(hb_step_args))
+    return set_err_msg("hb_union_step_v2: null args or struct_size < sizeof(hb_step_args)");
+  DevGuard dg_((cudaStream_t)a->stream);
+  const int n_peers = a->n_peers, n_disc = a->n_disc;
+  const int64_t n = a->n, lo = a->lo, hi = a->hi, t = a->t;
+  if (n_peers < 0 || n_peers > kMaxPeers || (n_peers > 0 && (!a->peer_nxt || !a->peer_chg)))
+    return set_err_msg("hb_union_step: bad peer arguments (at most 7 peers)");
+  Peers peers;
+  memset(&peers, 0, sizeof(peers));
+  peers.n = n_peers;
+  for (int q = 0; q < n_peers; q++) {
+    peers.nxt[q] = a->peer_nxt[q];
+    peers.chg[q] = a->peer_chg[q];
+  }
+  if (n_disc < 0 || n_disc > kMaxDisc || (n_disc > 0 && (!a->disc || !a->disc_scale)))
+    return set_err_msg("hb_union_step: bad discount arguments (at most 8 fused)");
+  if (n < 0 || lo < 0 || hi > n || lo > hi || t < 1 || !a->nch_out)
+    return set_err_msg("hb_union_step: bad range / t / nch_out");
+  if (n > 0 && (!a->offsets || !a->cur || !a->nxt || !a->chg_prev || !a->chg_now || !a->est ||
+                !a->lc_table))
+    return set_err_msg("hb_union_step: null graph / register / flag / estimate array");
+  if ((a->n_items > 0 && (!a->item_node || !a->item_beg || !a->partial)) ||
+      (a->n_heavy > 0 && (!a->heavy_nodes || !a->item_first || !a->finish_order || !a->partial)) ||
+      a->n_mega < 0 || a->n_mega > a->n_heavy)
+    return set_err_msg("hb_union_step: heavy schedule arrays missing");
+  cudaStream_t s = (cudaStream_t)a->stream;
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(a->nch_out, 0, sizeof(uint64_t), s)) != cudaSuccess)
+    return set_err("hb_union_step memset nch", e);
+  if (a->merged_out && (e = cudaMemsetAsync(a->merged_out, 0, sizeof(uint64_t), s)) != cudaSuccess)
+    return set_err("hb_union_step memset merged", e);
+  if (a->clear_chg_now && n > 0) {
+    if ((e = cudaMemsetAsync(a->chg_now, 0, sizeof(uint32_t) * (size_t)((n + 31) / 32), s)) !=
+        cudaSuccess)
+      return set_err("hb_union_step memset chg_now", e);
+  }
+  if (n == 0) return 0;
+  EstConst ec{a->alpha_p2, a->lc_cut, a->lc_table, a->disc, a->disc_stride, n_disc, a->disc_div,
+              {0, 0, 0, 0, 0, 0, 0, 0}};
+  for (int k = 0; k < n_disc; k++) ec.disc_scale[k] = a->disc_scale[k];
+  const double tf = (double)t;
+  unsigned long long *nch = reinterpret_cast<unsigned long long *>(a->nch_out);
+  unsigned long long *merged = reinterpret_cast<unsigned long long *>(a->merged_out);
+  if (n_peers > 0) {
+    HB_DISPATCH(a->b, return (union_step_impl<LB, true>(
+                       lo, hi, a->offsets, a->succ, a->cur, a->nxt, a->chg_prev, a->chg_now,
+                       a->est, a->sum_dist, a->sum_recip, tf, ec, a->dense, a->light_max_deg,
+                       a->heavy_nodes, a->item_first, a->n_heavy, a->finish_order, a->n_mega,
+                       a->item_node, a->item_beg, a->n_items, a->item_arcs, a->partial, nch,
+                       merged, a->hot_rows, a->active, peers, s, RunArgs{nullptr, 0, 0}, n)));
+  }
+  HB_DISPATCH(a->b, return (union_step_impl<LB, false>(
+                     lo, hi, a->offsets, a->succ, a->cur, a->nxt, a->chg_prev, a->chg_now,
+                     a->est, a->sum_dist, a->sum_recip, tf, ec, a->dense, a->light_max_deg,
+                     a->heavy_nodes, a->item_first, a->n_heavy, a->finish_order, a->n_mega,
+                     a->item_node, a->item_beg, a->n_items, a->item_arcs, a->partial, nch,
+                     merged, a->hot_rows, a->active, peers, s, RunArgs{nullptr, 0, 0}, n)));
+  return 0;
 }
 
 int hb_union_step(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets,
@@ -2186,58 +2292,26 @@ int hb_union_step(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets,
                   int n_disc, const double *disc_scale, int disc_div, const uint32_t *active,
                   int n_peers, uint8_t *const *peer_nxt, uint32_t *const *peer_chg,
                   void *stream) {
-  if (n_peers < 0 || n_peers > kMaxPeers || (n_peers > 0 && (!peer_nxt || !peer_chg)))
-    return set_err_msg("hb_union_step: bad peer arguments (at most 7 peers)");
-  Peers peers;
-  memset(&peers, 0, sizeof(peers));
-  peers.n = n_peers;
-  for (int q = 0; q < n_peers; q++) {
-    peers.nxt[q] = peer_nxt[q];
-    peers.chg[q] = peer_chg[q];
-  }
-  if (n_disc < 0 || n_disc > kMaxDisc || (n_disc > 0 && (!disc || !disc_scale)))
-    return set_err_msg("hb_union_step: bad discount arguments (at most 8 fused)");
-  if (n < 0 || lo < 0 || hi > n || lo > hi || t < 1 || !nch_out)
-    return set_err_msg("hb_union_step: bad range / t / nch_out");
-  if (n > 0 && (!offsets || !cur || !nxt || !chg_prev || !chg_now || !est || !lc_table))
-    return set_err_msg("hb_union_step: null graph / register / flag / estimate array");
-  if ((n_items > 0 && (!item_node || !item_beg || !partial)) ||
-      (n_heavy > 0 && (!heavy_nodes || !item_first || !finish_order || !partial)) ||
-      n_mega < 0 || n_mega > n_heavy)
-    return set_err_msg("hb_union_step: heavy schedule arrays missing");
-  cudaStream_t s = (cudaStream_t)stream;
-  cudaError_t e;
-  if ((e = cudaMemsetAsync(nch_out, 0, sizeof(uint64_t), s)) != cudaSuccess)
-    return set_err("hb_union_step memset nch", e);
-  if (merged_out && (e = cudaMemsetAsync(merged_out, 0, sizeof(uint64_t), s)) != cudaSuccess)
-    return set_err("hb_union_step memset merged", e);
-  if (clear_chg_now && n > 0) {
-    if ((e = cudaMemsetAsync(chg_now, 0, sizeof(uint32_t) * (size_t)((n + 31) / 32), s)) !=
-        cudaSuccess)
-      return set_err("hb_union_step memset chg_now", e);
-  }
-  if (n == 0) return 0;
-  EstConst ec{alpha_p2, lc_cut, lc_table, disc, disc_stride, n_disc, disc_div, {0, 0, 0, 0, 0, 0, 0, 0}};
-  for (int k = 0; k < n_disc; k++) ec.disc_scale[k] = disc_scale[k];
-  const double tf = (double)t;
-  if (n_peers > 0) {
-    HB_DISPATCH(b, return (union_step_impl<LB, true>(
-                       lo, hi, offsets, succ, cur, nxt, chg_prev, chg_now, est, sum_dist,
-                       sum_recip, tf, ec, dense, light_max_deg, heavy_nodes, item_first, n_heavy,
-                       finish_order, n_mega, item_node, item_beg, n_items, item_arcs, partial,
-                       reinterpret_cast<unsigned long long *>(nch_out),
-                       reinterpret_cast<unsigned long long *>(merged_out), hot_rows, active,
-                       peers, s, RunArgs{nullptr, 0, 0}, n)));
-  }
-  HB_DISPATCH(b, return (union_step_impl<LB, false>(
-                     lo, hi, offsets, succ, cur, nxt, chg_prev, chg_now, est, sum_dist,
-                     sum_recip, tf, ec, dense, light_max_deg, heavy_nodes, item_first, n_heavy,
-                     finish_order, n_mega, item_node, item_beg, n_items, item_arcs, partial,
-                     reinterpret_cast<unsigned long long *>(nch_out),
-                     reinterpret_cast<unsigned long long *>(merged_out), hot_rows, active, peers,
-                     s, RunArgs{nullptr, 0, 0}, n)));
-  return 0;
+  hb_step_args a;
+  memset(&a, 0, sizeof(a));
+  a.struct_size = sizeof(a);
+  a.n = n; a.lo = lo; a.hi = hi; a.offsets = offsets; a.succ = succ;
+  a.cur = cur; a.nxt = nxt; a.chg_prev = chg_prev; a.chg_now = chg_now; a.est = est;
+  a.b = b; a.dense = dense; a.clear_chg_now = clear_chg_now; a.n_disc = n_disc; a.t = t;
+  a.lc_table = lc_table; a.alpha_p2 = alpha_p2; a.lc_cut = lc_cut;
+  a.sum_dist = sum_dist; a.sum_recip = sum_recip;
+  a.disc = disc; a.disc_stride = disc_stride; a.disc_scale = disc_scale; a.disc_div = disc_div;
+  a.n_peers = n_peers; a.light_max_deg = light_max_deg;
+  a.heavy_nodes = heavy_nodes; a.item_first = item_first; a.n_heavy = n_heavy;
+  a.finish_order = finish_order; a.n_mega = n_mega; a.item_node = item_node;
+  a.item_beg = item_beg; a.n_items = n_items; a.item_arcs = item_arcs; a.partial = partial;
+  a.nch_out = nch_out; a.merged_out = merged_out; a.hot_rows = hot_rows; a.active = active;
+  a.peer_nxt = peer_nxt; a.peer_chg = peer_chg; a.stream = stream;
+  return hb_union_step_v2(&a);
 }
+
+void hb_set_l2_persist(int enable) { g_l2_persist = enable != 0; }
+uint64_t hb_step_args_size(void) { return sizeof(hb_step_args); }
 
 int hb_union_step_runs(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets,
                        const int32_t *succ, const uint8_t *cur, uint8_t *nxt,
@@ -2252,6 +2326,7 @@ int hb_union_step_runs(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets
                        uint64_t *run_nch_out, int64_t hot_rows, double *disc,
                        int64_t disc_stride, int n_disc, const double *disc_scale, int disc_div,
                        const uint32_t *active, void *stream) {
+  DevGuard dg_((cudaStream_t)stream);
   const int wb = b + log2_runs;
   if (log2_runs < 1 || log2_runs > 4 || b < HB_MIN_B || wb > 8)
     return set_err_msg("hb_union_step_runs: need 2..16 runs and runs * p <= 256");
@@ -2307,6 +2382,7 @@ int hb_union_step_runs(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets
 
 int hb_pack_registers(int64_t n, int b, int width, const uint8_t *regs, const int32_t *order,
                       uint8_t *out, void *stream) {
+  DevGuard dg_((cudaStream_t)stream);
   if (n <= 0) return 0;
   if (b < HB_MIN_B || b > 16 || width < 1 || width > 8 || !regs || !out)
     return set_err_msg("hb_pack_registers: bad arguments");
@@ -2318,6 +2394,7 @@ int hb_pack_registers(int64_t n, int b, int width, const uint8_t *regs, const in
 
 int hb_unpack_registers(int64_t n, int b, int width, const uint8_t *packed, const int32_t *order,
                         uint8_t *regs, void *stream) {
+  DevGuard dg_((cudaStream_t)stream);
   if (n <= 0) return 0;
   if (b < HB_MIN_B || b > 16 || width < 1 || width > 8 || !packed || !regs)
     return set_err_msg("hb_unpack_registers: bad arguments");
@@ -2330,6 +2407,7 @@ int hb_unpack_registers(int64_t n, int b, int width, const uint8_t *packed, cons
 int hb_finalize(int64_t n, const int32_t *rank, const double *sum_dist, const double *sum_recip,
                 const double *coreach, double *closeness, double *harmonic, double *lin,
                 void *stream) {
+  DevGuard dg_((cudaStream_t)stream);
   if (n <= 0) return 0;
   if ((closeness || lin) && !sum_dist) return set_err_msg("hb_finalize: sum_dist required");
   if (harmonic && !sum_recip) return set_err_msg("hb_finalize: sum_recip required");
@@ -2344,6 +2422,7 @@ int hb_packed_row_bytes(int b) { return packed_row_bytes(1 << b); }
 int hb_gather_changed(int64_t lo, int64_t hi, const uint32_t *chg_bits, const uint8_t *rows,
                       int b, int packed, int32_t *ids_out, uint8_t *rows_out,
                       uint64_t *count_out, void *stream) {
+  DevGuard dg_((cudaStream_t)stream);
   cudaStream_t s = (cudaStream_t)stream;
   if (!count_out || lo < 0 || (hi > lo && (!chg_bits || !rows || !ids_out || !rows_out)) ||
       b < HB_MIN_B || b > HB_MAX_B)
@@ -2359,6 +2438,7 @@ int hb_gather_changed(int64_t lo, int64_t hi, const uint32_t *chg_bits, const ui
 
 int hb_scatter_rows(int64_t k, const int32_t *ids, const uint8_t *rows, int b, int packed,
                     uint8_t *dst, uint32_t *chg_bits, void *stream) {
+  DevGuard dg_((cudaStream_t)stream);
   if (k <= 0) return 0;
   if (!ids || !rows || !dst || !chg_bits || b < HB_MIN_B || b > HB_MAX_B)
     return set_err_msg("hb_scatter_rows: bad arguments");
@@ -2369,6 +2449,7 @@ int hb_scatter_rows(int64_t k, const int32_t *ids, const uint8_t *rows, int b, i
 
 int hb_refresh_rows(int64_t n, int64_t lo, int64_t hi, const uint32_t *bits, const uint8_t *src,
                     uint8_t *dst, int b, void *stream) {
+  DevGuard dg_((cudaStream_t)stream);
   if (n <= 0) return 0;
   if (!bits || !src || !dst || lo < 0 || hi > n || lo > hi || b < HB_MIN_B || b > HB_MAX_B)
     return set_err_msg("hb_refresh_rows: bad arguments");
@@ -2381,6 +2462,7 @@ int hb_sort_rows(int64_t n, const int64_t *offsets, int64_t n_batches,
                  const int64_t *host_batch_rows, const int64_t *host_batch_arcs, int32_t *ids,
                  int32_t *alt, void *temp, uint64_t *temp_bytes, int *result_in_alt,
                  void *stream) {
+  DevGuard dg_((cudaStream_t)stream);
   cudaStream_t s = (cudaStream_t)stream;
   if (!host_batch_rows || !host_batch_arcs || !temp_bytes || n_batches < 0)
     return set_err_msg("hb_sort_rows: batch arrays / temp_bytes");
@@ -2428,6 +2510,7 @@ int hb_sort_rows(int64_t n, const int64_t *offsets, int64_t n_batches,
 
 int hb_exact_seed(int64_t n, int64_t row_stride, uint8_t *bits, double *est,
                   const int64_t *weights, void *stream) {
+  DevGuard dg_((cudaStream_t)stream);
   if (n <= 0) return 0;
   if (row_stride % 16 || row_stride * 8 < n) return set_err_msg("hb_exact_seed: bad row_stride");
   cudaStream_t s = (cudaStream_t)stream;
@@ -2444,6 +2527,7 @@ int hb_exact_union_step(int64_t n, const int64_t *offsets, const int32_t *succ,
                         const int64_t *weights, double *disc, int64_t disc_stride, int n_disc,
                         const double *disc_scale, int disc_div, uint64_t *nch_out,
                         uint64_t *merged_out, void *stream) {
+  DevGuard dg_((cudaStream_t)stream);
   cudaStream_t s = (cudaStream_t)stream;
   if (n < 0 || t < 1 || !nch_out || row_stride % 16)
     return set_err_msg("hb_exact_union_step: bad arguments");
@@ -2466,6 +2550,7 @@ int hb_exact_union_step(int64_t n, const int64_t *offsets, const int32_t *succ,
 
 int hb_mark_active(int64_t n, const int64_t *fwd_offsets, const int32_t *fwd_succ,
                    const uint32_t *chg_prev, uint32_t *active, void *stream) {
+  DevGuard dg_((cudaStream_t)stream);
   cudaStream_t s = (cudaStream_t)stream;
   if (n <= 0) return 0;
   if (!fwd_offsets || !fwd_succ || !chg_prev || !active)
@@ -2484,16 +2569,11 @@ static int mark_pull_impl(int64_t n, const int64_t *offsets, const int32_t *succ
                           int64_t h0 = -1, int64_t h1 = -1) {
   const size_t smem = filter ? sizeof(uint32_t) * kFilterWords : 0;
   if (filter) {
-    static bool attr = [] {
-      cudaFuncSetAttribute(k_mark_pull<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)(sizeof(uint32_t) * kFilterWords));
-      cudaFuncSetAttribute(k_mark_items<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)(sizeof(uint32_t) * kFilterWords));
-      cudaFuncSetAttribute(k_mark_heavy_flat<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)(sizeof(uint32_t) * kFilterWords));
-      return true;
-    }();
-    (void)attr;
+    const int fb = (int)(sizeof(uint32_t) * kFilterWords);
+    if (int e = ensure_smem_attr((const void *)k_mark_pull<true>, fb, "k_mark_pull smem")) return e;
+    if (int e = ensure_smem_attr((const void *)k_mark_items<true>, fb, "k_mark_items smem")) return e;
+    if (int e = ensure_smem_attr((const void *)k_mark_heavy_flat<true>, fb, "k_mark_heavy_flat smem"))
+      return e;
     k_mark_pull<true><<<grid_for_warps((n + 31) / 32), kThreads, smem, s>>>(
         n, offsets, succ, chg_prev, active, light_max_deg, filter);
   } else {
@@ -2527,6 +2607,7 @@ int hb_mark_pull(int64_t n, const int64_t *offsets, const int32_t *succ,
                  const uint32_t *chg_prev, uint32_t *active, int64_t light_max_deg,
                  const int32_t *item_node, const int64_t *item_beg, int64_t n_items,
                  int64_t item_arcs, void *stream) {
+  DevGuard dg_((cudaStream_t)stream);
   if (n <= 0) return 0;
   if (!offsets || !chg_prev || !active || (n_items > 0 && (!item_node || !item_beg)))
     return set_err_msg("hb_mark_pull: bad arguments");
@@ -2539,6 +2620,7 @@ int hb_mark_pull_filtered(int64_t n, const int64_t *offsets, const int32_t *succ
                           const int32_t *item_node, const int64_t *item_beg, int64_t n_items,
                           int64_t item_arcs, int64_t heavy_lo, int64_t heavy_hi,
                           uint32_t *filter, void *stream) {
+  DevGuard dg_((cudaStream_t)stream);
   if (n <= 0) return 0;
   if (!offsets || !chg_prev || !active || (n_items > 0 && (!item_node || !item_beg)) ||
       (heavy_hi > heavy_lo && (heavy_lo < 0 || heavy_hi > n)))
@@ -2559,6 +2641,7 @@ int64_t hb_change_filter_words(void) { return kFilterWords; }
 int hb_forward_csr(int64_t n, const int64_t *offsets, const int32_t *succ, int64_t m,
                    int64_t *fwd_offsets, int64_t *cursor, int32_t *fwd_dst, void *temp,
                    uint64_t *temp_bytes, void *stream) {
+  DevGuard dg_((cudaStream_t)stream);
   cudaStream_t s = (cudaStream_t)stream;
   if (!temp_bytes) return set_err_msg("hb_forward_csr: temp_bytes");
   size_t need = 0;
@@ -2588,6 +2671,7 @@ int hb_forward_csr(int64_t n, const int64_t *offsets, const int32_t *succ, int64
 
 int hb_sample_flagged_arcs(int64_t m, const int32_t *succ, const uint32_t *bits,
                            int64_t samples, uint64_t seed, uint64_t *out, void *stream) {
+  DevGuard dg_((cudaStream_t)stream);
   if (m < 0 || samples < 0 || !out || (m > 0 && samples > 0 && (!succ || !bits)))
     return set_err_msg("hb_sample_flagged_arcs: bad arguments");
   cudaStream_t s = (cudaStream_t)stream;
@@ -2601,6 +2685,7 @@ int hb_sample_flagged_arcs(int64_t m, const int32_t *succ, const uint32_t *bits,
 
 int hb_gen_rmat_keys(int scale, int64_t m, uint64_t thr_a, uint64_t thr_ab, uint64_t thr_abc,
                      uint64_t seed, uint64_t *keys, void *stream) {
+  DevGuard dg_((cudaStream_t)stream);
   if (scale < 1 || scale > 31 || m < 0) return set_err_msg("hb_gen_rmat_keys: bad scale / m");
   if (m == 0) return 0;
   k_gen_rmat<<<grid_for_threads(m), kThreads, 0, (cudaStream_t)stream>>>(scale, m, thr_a, thr_ab,
@@ -2611,6 +2696,7 @@ int hb_gen_rmat_keys(int scale, int64_t m, uint64_t thr_a, uint64_t thr_ab, uint
 int hb_keys_to_csr(int64_t n, int64_t m, uint64_t *keys, uint64_t *alt, void *temp,
                    uint64_t *temp_bytes, int64_t *m_out, int64_t *offsets, int32_t *succ,
                    void *stream) {
+  DevGuard dg_((cudaStream_t)stream);
   cudaStream_t s = (cudaStream_t)stream;
   if (!temp_bytes) return set_err_msg("hb_keys_to_csr: temp_bytes");
   cub::DoubleBuffer<uint64_t> db(keys, alt);
@@ -2648,6 +2734,7 @@ int hb_keys_to_csr(int64_t n, int64_t m, uint64_t *keys, uint64_t *alt, void *te
 int hb_relabel_csr(int64_t n, const int64_t *old_offsets, const int32_t *old_succ,
                    const int32_t *perm, const int32_t *rank, const int64_t *new_offsets,
                    int32_t *new_succ, void *stream) {
+  DevGuard dg_((cudaStream_t)stream);
   if (n <= 0) return 0;
   if (!old_offsets || !perm || !rank || !new_offsets)   // succ arrays may be empty (NULL)
     return set_err_msg("hb_relabel_csr: bad arguments");
@@ -2659,6 +2746,7 @@ int hb_relabel_csr(int64_t n, const int64_t *old_offsets, const int32_t *old_suc
 int hb_relabel_csr_rows(int64_t n, int64_t r0, int64_t r1, const int64_t *old_offsets,
                         const int32_t *old_succ, const int32_t *perm, const int32_t *rank,
                         const int64_t *new_offsets, int32_t *new_succ, void *stream) {
+  DevGuard dg_((cudaStream_t)stream);
   if (r0 < 0 || r1 > n || r0 > r1) return set_err_msg("hb_relabel_csr_rows: bad row range");
   if (r1 == r0) return 0;
   if (!old_offsets || !perm || !rank || !new_offsets)
@@ -2671,6 +2759,7 @@ int hb_relabel_csr_rows(int64_t n, int64_t r0, int64_t r1, const int64_t *old_of
 int hb_relabel_csr_src_rows(int64_t n, int64_t o0, int64_t o1, const int64_t *old_offsets,
                             const int32_t *old_succ, const int32_t *rank,
                             const int64_t *new_offsets, int32_t *new_succ, void *stream) {
+  DevGuard dg_((cudaStream_t)stream);
   if (o0 < 0 || o1 > n || o0 > o1) return set_err_msg("hb_relabel_csr_src_rows: bad row range");
   if (o1 == o0) return 0;
   if (!old_offsets || !rank || !new_offsets)
@@ -2682,6 +2771,7 @@ int hb_relabel_csr_src_rows(int64_t n, int64_t o0, int64_t o1, const int64_t *ol
 
 int hb_hash_items(int64_t n, const uint64_t *items, const uint64_t *replicas, uint64_t seed,
                   uint64_t *out, void *stream) {
+  DevGuard dg_((cudaStream_t)stream);
   if (n <= 0) return 0;
   if (!items || !replicas || !out) return set_err_msg("hb_hash_items: bad arguments");
   k_hash<<<grid_for_threads(n), kThreads, 0, (cudaStream_t)stream>>>(n, items, replicas, seed,

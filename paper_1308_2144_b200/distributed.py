@@ -93,6 +93,58 @@ class TorchComm:
         return full
 
 
+class _RankSums:
+    """A rank's fused accumulator sums (full-length arrays, the owned slice is live)."""
+
+    def __init__(self, n: int, device, specs=()):
+        self.specs = list(specs)
+        self.sum_dist = torch.zeros(n, dtype=torch.float64, device=device)
+        self.sum_recip = torch.zeros(n, dtype=torch.float64, device=device)
+        self.disc = torch.zeros((len(self.specs), n), dtype=torch.float64, device=device)
+        self.n = n
+
+    def disc_args(self, t: int):
+        """(base ptr, stride, count, host scale array, divide mask) for hb_union_step."""
+        import ctypes
+        k = len(self.specs)
+        if k == 0:
+            return None, 0, 0, None, 0
+        scale = (ctypes.c_double * k)()
+        div = 0
+        for i, spec in enumerate(self.specs):
+            d, f = spec.device_factor(t)
+            scale[i] = f
+            div |= int(d) << i
+        self._scale_keepalive = scale
+        return self.disc.data_ptr(), self.n, k, ctypes.cast(scale, ctypes.c_void_p), div
+
+
+def _fill_accumulators(accs, host) -> None:
+    """Hand the gathered sums (original order) to the fused accumulators."""
+    for acc in accs:
+        if isinstance(acc, CentralityAccumulator):
+            acc._sum_dist, acc._sum_recip = host["sum_dist"].copy(), host["sum_recip"].copy()
+            acc._discounted = {spec.name: host["disc:" + spec.name].copy()
+                               for spec in acc.discounts}
+            acc._fresh = False
+        else:
+            acc.sum_dist, acc.sum_recip = host["sum_dist"].copy(), host["sum_recip"].copy()
+
+
+def _specs_of(accs):
+    """Discount specs of the (single) fused accumulator; several fused accumulators must
+    agree (they all receive the same sums)."""
+    specs = None
+    for acc in accs:
+        mine = [d.name for d in getattr(acc, "discounts", [])]
+        if specs is None:
+            specs = list(getattr(acc, "discounts", []))
+        elif [d.name for d in specs] != mine:
+            raise ValueError("fused accumulators of one distributed run must carry the same "
+                             "discounts")
+    return specs or []
+
+
 class CudaRankState:
     """One rank's device state: full register replica, owned range [lo, hi)."""
 
@@ -119,14 +171,12 @@ class CudaRankState:
         self.count = torch.zeros(1, dtype=torch.int64, device=dv)
         self.sums = None
 
-    def bind_sums(self, zeros: bool = True):
-        class _Sums:
-            pass
-        s = _Sums()
-        s.sum_dist = torch.zeros(self.n, dtype=torch.float64, device=self.dev.device)
-        s.sum_recip = torch.zeros(self.n, dtype=torch.float64, device=self.dev.device)
-        self.sums = s
-        return s
+    def bind_sums(self, specs=()):
+        """Device sums of the fused accumulator, including its discounted gains
+        (centrality.py:26-101,149-150; up to MAX_FUSED_DISCOUNTS, folded in the union
+        epilogue like on one GPU)."""
+        self.sums = _RankSums(self.n, self.dev.device, specs)
+        return self.sums
 
     def local_step(self, t: int, dense: bool) -> int:
         return self.dev.union_step(t, dense, self.sums)
@@ -170,6 +220,8 @@ class CudaRankState:
         if self.sums is not None:
             out["sum_dist"] = self.sums.sum_dist
             out["sum_recip"] = self.sums.sum_recip
+            for i, spec in enumerate(self.sums.specs):
+                out["disc:" + spec.name] = self.sums.disc[i]
         return out
 
     def to_original(self, x: torch.Tensor) -> np.ndarray:
@@ -237,7 +289,7 @@ def run_distributed(g, config: HyperBallConfig, observers: Iterable = (), group=
     observers = list(observers)
     accs = [o for o in observers if fusable(o, st.n)]
     if accs:
-        st.bind_sums()
+        st.bind_sums(_specs_of(accs))
     symm = None
     if (exchange == "push" and comm.world > 1 and isinstance(st, CudaRankState)
             and dist.get_backend(group) == "nccl" and st.n > 0):
@@ -274,12 +326,7 @@ def run_distributed(g, config: HyperBallConfig, observers: Iterable = (), group=
     res.merged_total = int(mt.item())
     final = host["est"]
     final.setflags(write=False)
-    for acc in accs:
-        if isinstance(acc, CentralityAccumulator):
-            acc._sum_dist, acc._sum_recip = host["sum_dist"].copy(), host["sum_recip"].copy()
-            acc._fresh = False
-        else:
-            acc.sum_dist, acc.sum_recip = host["sum_dist"].copy(), host["sum_recip"].copy()
+    _fill_accumulators(accs, host)
     for obs in observers:
         obs.on_converged(final)
     return res
@@ -348,8 +395,9 @@ def run_simulated(g, config: HyperBallConfig, world: int, observers: Iterable = 
     observers = list(observers)
     accs = [o for o in observers if fusable(o, states[0].n)]
     if accs:
+        specs = _specs_of(accs)
         for s in states:
-            s.bind_sums()
+            s.bind_sums(specs)
     t = 0
     nch = states[0].n
     if nch > 0:
@@ -392,10 +440,7 @@ def run_simulated(g, config: HyperBallConfig, world: int, observers: Iterable = 
                             sum(s.dev.launches for s in states))
     res.registers = [s.to_original(s.dev.cur) for s in states]
     final = full["est"]
-    for acc in accs:
-        if isinstance(acc, CentralityAccumulator):
-            acc._sum_dist, acc._sum_recip = full["sum_dist"].copy(), full["sum_recip"].copy()
-            acc._fresh = False
+    _fill_accumulators(accs, full)
     for obs in observers:
         obs.on_converged(final)
     return res

@@ -21,6 +21,7 @@ fallback: without a CUDA device or the built library every entry point raises.
 
 from __future__ import annotations
 
+import ctypes
 import io
 import math
 import weakref
@@ -574,18 +575,22 @@ class _Device:
             if ev is not None:
                 s.ready_slice(lo, hi, ev)
             cnt = self.counts if len(parts) == 1 else self.slice_counts[k]
-            _lib.check(L.hb_union_step(
-                self.n, lo, hi, s.offsets.data_ptr(), s.succ_buf.data_ptr(),
-                self.cur.data_ptr(), self.nxt.data_ptr(), self.chg_prev.data_ptr(),
-                self.chg_now.data_ptr(), int(clear_chg_now and k == 0), self.est.data_ptr(),
-                sd, sr, t, self.lc.data_ptr(),
-                self.alpha_p2, self.lc_cut, self.b, int(dense), s.light_max_deg,
-                s.heavy_nodes.data_ptr(), s.item_first.data_ptr(), s.n_heavy,
-                s.finish_order.data_ptr(), s.n_mega, s.item_node.data_ptr(),
-                s.item_beg.data_ptr(), s.n_items, s.item_arcs,
-                s.partial.data_ptr(), cnt.data_ptr(), cnt.data_ptr() + 8,
-                s.hot_rows, *dargs, active, n_peers, peer_nxt, peer_chg,
-                self.stream.cuda_stream), "hb_union_step")
+            disc, disc_stride, n_disc, disc_scale, disc_div = dargs
+            _lib.union_step(_lib.StepArgs(
+                n=self.n, lo=lo, hi=hi, offsets=s.offsets.data_ptr(),
+                succ=s.succ_buf.data_ptr(), cur=self.cur.data_ptr(), nxt=self.nxt.data_ptr(),
+                chg_prev=self.chg_prev.data_ptr(), chg_now=self.chg_now.data_ptr(),
+                est=self.est.data_ptr(), b=self.b, dense=int(dense),
+                clear_chg_now=int(clear_chg_now and k == 0), n_disc=n_disc, t=t,
+                lc_table=self.lc.data_ptr(), alpha_p2=self.alpha_p2, lc_cut=self.lc_cut,
+                sum_dist=sd, sum_recip=sr, disc=disc, disc_stride=disc_stride,
+                disc_scale=disc_scale, disc_div=disc_div, n_peers=n_peers,
+                nch_out=cnt.data_ptr(), merged_out=cnt.data_ptr() + 8, active=active,
+                peer_nxt=ctypes.cast(peer_nxt, ctypes.c_void_p) if peer_nxt is not None
+                else None,
+                peer_chg=ctypes.cast(peer_chg, ctypes.c_void_p) if peer_chg is not None
+                else None,
+                stream=self.stream.cuda_stream, **_lib.schedule_args(s)))
             self.launches += (hi > lo) + (s.n_items > 0) + (s.n_heavy > 0)
         if len(parts) > 1:
             s.relabel = None

@@ -202,6 +202,24 @@ def run_batched(g, config: HyperBallConfig, seeds, observers, discounts=()):
     need_old = any(generic)
     done = [False] * R
     t_run = [0] * R
+
+    def _finish(r):
+        # hand run r an ordinary single-run state: its device arrays are sliced out of the
+        # batch (internal order of the batch schedule); the single-run schedule is only
+        # built if the state is iterated again (graph_key None -> _Device.bind_graph)
+        view = bt.cur.view(n, R, bt.p)          # bt.cur: the buffer of the latest step
+        dev = _parked_device(bt, cfgs[r], view[:, r].contiguous(), bt.est[r].clone())
+        st = HyperBallState(cfgs[r], n, dev)
+        st.t, st.num_changed = t_run[r], 0
+        if fused[r] is not None:
+            _bind_batch_sums(st, fused[r], bt.sum_dist[r], bt.sum_recip[r], bt.disc[r],
+                             bt.specs)
+        final = st.est
+        final.setflags(write=False)
+        for obs in observers[r]:
+            obs.on_converged(final)
+        return st
+
     t = 0
     while True:
         t += 1
@@ -225,31 +243,22 @@ def run_batched(g, config: HyperBallConfig, seeds, observers, discounts=()):
             if per_run[r] == 0:
                 done[r], t_run[r] = True, t
             elif config.max_iterations is not None and t >= config.max_iterations:
+                # The reference runs the seeds one after another (cli.py:222-254): every
+                # earlier run has converged (a non-converged earlier run would have raised
+                # first, at a lower r), written its progress lines and received
+                # on_converged before run r raises; later runs never start.
+                if config.progress is not None:
+                    for q in range(r + 1):
+                        config.progress.write("".join(lines[q]))
+                for q in range(r):
+                    _finish(q)
                 raise ConvergenceError(t, per_run[r])
         if all(done):
             break
     if config.progress is not None:
         for r in range(R):
             config.progress.write("".join(lines[r]))
-    # hand every run an ordinary single-run state: its device arrays are sliced out of the
-    # batch (internal order of the batch schedule); the single-run schedule is only built
-    # if the state is iterated again (graph_key None -> _Device.bind_graph relabels)
-    states = []
-    p = bt.p
-    view = bt.cur.view(n, R, p)
-    for r in range(R):
-        dev = _parked_device(bt, cfgs[r], view[:, r].contiguous(), bt.est[r].clone())
-        st = HyperBallState(cfgs[r], n, dev)
-        st.t, st.num_changed = t_run[r], 0
-        if fused[r] is not None:
-            _bind_batch_sums(st, fused[r], bt.sum_dist[r], bt.sum_recip[r], bt.disc[r],
-                             bt.specs)
-        final = st.est
-        final.setflags(write=False)
-        for obs in observers[r]:
-            obs.on_converged(final)
-        states.append(st)
-    return states
+    return [_finish(r) for r in range(R)]
 
 
 def _parked_device(bt: _Batch, cfg: HyperBallConfig, cur: torch.Tensor,

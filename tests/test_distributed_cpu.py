@@ -40,7 +40,8 @@ class OracleRankState:
         self.sum_recip = np.zeros(self.n)
         self.sums = None
 
-    def bind_sums(self):
+    def bind_sums(self, specs=()):
+        assert not specs, "the CPU twin folds no discounts"
         self.sums = True
 
     def local_step(self, t, dense):

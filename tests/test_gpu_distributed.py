@@ -166,3 +166,31 @@ def test_always_dense_steps(key, world, monkeypatch):
     assert res.t == case["t"]
     for regs in res.registers:
         assert sha(regs) == case["reg_digests"][-1]
+
+
+DISC_KEYS = [c["key"] for c in golden_cases() if c.get("discounts")]
+
+
+@pytest.mark.parametrize("exchange", ["allgather", "push"])
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("key", DISC_KEYS)
+def test_simulated_ranks_fused_discounts(key, world, exchange):
+    """Discounted gains (centrality.py:26-101,149-150) folded in every rank's union
+    epilogue and gathered back: bit-identical to the reference's host accumulation."""
+    case = CASES[key]
+    off, suc = golden_graph(case)
+    g = hb.CsrGraph(off, suc)
+    specs = [hb.DiscountSpec.preset(name) if tab is None
+             else hb.DiscountSpec.from_table(tab[0], tab[1], name="table")
+             for name, tab in case["discounts"]]
+    acc = hb.CentralityAccumulator(g.n, specs)
+    cfg = hb.HyperBallConfig(params=hb.CounterParams(b=case["b"], seed=int(case["seed"])))
+    res = run_simulated(g, cfg, world, [acc], exchange=exchange)
+    assert res.t == case["t"]
+    _, arrays = golden()
+    for spec in specs:
+        got = hb.finalize_discounted(acc, spec.name)
+        want = arrays[f"{key}/disc_{spec.name}"]
+        assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), spec.name
+    assert np.array_equal(hb.finalize_harmonic(acc).view(np.uint64),
+                          arrays[f"{key}/harmonic"].view(np.uint64))

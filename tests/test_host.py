@@ -33,6 +33,19 @@ def test_library_exports_every_header_symbol():
     assert set(syms) == set(_lib.HB_SIGNATURES), "ctypes table out of sync with header"
 
 
+def test_step_args_struct_layout():
+    """ctypes' StepArgs and the library's hb_step_args agree (size and the struct_size
+    check of hb_union_step_v2)."""
+    L = _lib.hb()
+    assert L.hb_step_args_size() == ctypes.sizeof(_lib.StepArgs)
+    a = _lib.StepArgs(n=10, hi=10, t=1, b=4, nch_out=8)
+    assert L.hb_union_step_v2(ctypes.byref(a)) == -1
+    assert "null" in L.hb_last_error().decode()
+    a.struct_size = 8
+    assert L.hb_union_step_v2(ctypes.byref(a)) == -1
+    assert "struct_size" in L.hb_last_error().decode()
+
+
 def test_library_metadata_calls():
     L = _lib.hb()
     assert b"sm_100a" in L.hb_version()
