@@ -122,6 +122,19 @@ def build_graph(config_name: str):
     return g
 
 
+def mapped_repo_libs():
+    """In-tree shared libraries mapped by this process (evidence of which native code ran:
+    the reference arm maps only oracle/liborc.so, the B200 arm the kernel library)."""
+    try:
+        with open("/proc/self/maps") as fh:
+            paths = {ln.split()[-1] for ln in fh if ln.rstrip().endswith(".so")}
+    except OSError:
+        return None
+    root = os.path.realpath(REPO)
+    return sorted(os.path.relpath(p_, root) for p_ in paths
+                  if os.path.realpath(p_).startswith(root + os.sep))
+
+
 def alg_bytes(n: int, m: int, p: int) -> int:
     """Algorithmic bytes of one dense step: source rows + CSR + counter writes."""
     return m * p + 8 * (n + 1) + 4 * m + n * p
@@ -131,8 +144,10 @@ def alg_bytes(n: int, m: int, p: int) -> int:
 
 def cpu_dense_sample(g, b: int, seed: int, budget_s: float, threads: int, repeats: int = 1,
                      rotate: bool = False):
-    """Time the oracle's dense union pass (hll_union_range restated, pthreads) on node
-    ranges holding about `budget_s` seconds of work.  Returns a list of (arcs, seconds)."""
+    """Time the oracle's dense step on node ranges holding about `budget_s` seconds of
+    work: the union pass (hll_union_range restated, arc-balanced pthread ranges as
+    engine.py:351-390) plus the accumulator fold of the same nodes (centrality.py:132-150,
+    one thread like the reference's numpy observer).  Returns a list of (arcs, seconds)."""
     import ctypes
 
     import oracle as orc
@@ -146,13 +161,19 @@ def cpu_dense_sample(g, b: int, seed: int, budget_s: float, threads: int, repeat
     chg_prev = np.ones(n, np.uint8)
     chg_now = np.zeros(n, np.uint8)
     new_est = np.zeros(n, np.float64)
+    sum_dist = np.zeros(n, np.float64)
+    sum_recip = np.zeros(n, np.float64)
     P = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    Pd = lambda a, k: ctypes.c_void_p(a.ctypes.data + 8 * k)  # noqa: E731
 
     def run_range(lo, hi):
-        # arc-balanced sub-ranges over `threads` pthreads, like engine.py:351-390
+        # arc-balanced sub-ranges over `threads` pthreads, like engine.py:351-390, then
+        # the accumulate of the same rows (t = 1)
         t0 = time.perf_counter()
         L.orc_iterate_range_mt(lo, hi, P(off), P(suc), P(cur), P(nxt), P(chg_prev),
                                P(chg_now), P(est), P(new_est), b, 1, threads)
+        L.orc_accumulate(hi - lo, 1, Pd(est, lo), Pd(new_est, lo), Pd(sum_dist, lo),
+                         Pd(sum_recip, lo))
         return int(off[hi] - off[lo]), time.perf_counter() - t0
 
     # calibrate on ~1/64 of the arcs
@@ -180,10 +201,29 @@ def _local_sub_csr_note():
             "full register array")
 
 
+def bench_config(cfgd, n: int, m: int, world: int = 1, exchange: str = "push") -> dict:
+    """The workload description both arms print (identical, so the driver can pair them)."""
+    p = 1 << cfgd.log2m
+    return {"workload": f"{cfgd.name}: {cfgd.description}", "n": n, "m": m,
+            "log2m": cfgd.log2m, "register_width": 5, "hash_seed": cfgd.hash_seed,
+            "step": "one dense iteration (all sources changed): union + estimate + "
+                    "accumulate for %s" % "/".join(cfgd.outputs),
+            "l2": ("inputs larger than L2 (%.2f GB of registers + %.2f GB of CSR), no flush"
+                   if n * p > 126e6 else
+                   "registers (%.2f GB) + CSR (%.2f GB) partly L2-resident, no flush: a "
+                   "small-graph line") % (n * p / 1e9, (8 * (n + 1) + 4 * m) / 1e9),
+            "parallelism": (f"node-partition x{world}, {exchange} exchange"
+                            if world > 1 else "single GPU")}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    from paper_1308_2144_b200 import _lib
+    # the graph is built by the oracle library's copy of the builders: this process maps
+    # no product library (only oracle/liborc.so)
+    _lib.use_graph_library(os.path.join(REPO, "oracle", "liborc.so"))
     from paper_1308_2144_b200 import generators as gen
     cfg = gen.CONFIGS[args.config]
     g = build_graph(args.config)
@@ -200,26 +240,164 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000.0 * secs / len(timed), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": f"{args.config}: {cfg.description}", "n": g.n, "m": g.m,
-                   "log2m": cfg.log2m, "hash_seed": cfg.hash_seed,
-                   "step": "dense union pass (hll_union_range restated in C) over a "
-                           "contiguous destination range of ~%.1f s of work" % per_step},
+        "config": bench_config(cfg, g.n, g.m, args.gpus, args.exchange),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{len(timed)} dense-pass samples, {arcs} arcs total; "
-                                   + _local_sub_csr_note()},
+                         "sample": f"{len(timed)} dense-step samples (union pass of "
+                                   f"hll_union_range restated in C on {threads} pthreads + "
+                                   f"the accumulate of the same rows), ~{per_step:.1f} s each, "
+                                   f"{arcs} arcs total; " + _local_sub_csr_note()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "mapped_repo_libs": mapped_repo_libs(),
     }
     print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------------------ GPU arm
 
-def run_b200(args):
+def load_traffic(config: str):
+    """ncu DRAM bytes (read + write) per dense step of `config`, from the committed
+    profile summary (profiles/ncu_traffic.json), or None."""
+    tpath = os.path.join(REPO, "profiles", "ncu_traffic.json")
+    try:
+        return json.load(open(tpath)).get(config)
+    except Exception:
+        return None
+
+
+def dense_steps(g, cfgd, local: int, steps: int, warmup: int, schedule: str = "auto",
+                world: int = 1, rank: int = 0, exchange: str = "push", clocks: bool = False):
+    """Device-resident dense iterations of config `cfgd` on graph `g`: `warmup` untimed,
+    then `steps` timed with CUDA events on the launching stream (barrier +
+    synchronize on both sides; max over ranks).  Returns a dict of the measurements."""
     import torch
     import torch.distributed as dist
 
     import paper_1308_2144_b200 as hb
     from paper_1308_2144_b200 import _lib
+
+    b, seed = cfgd.log2m, cfgd.hash_seed
+    p = 1 << b
+    n, m = g.n, g.m
+    params = hb.CounterParams(b=b, seed=seed)
+    cfg = hb.HyperBallConfig(params=params, device=local, schedule=schedule)
+    acc = hb.CentralityAccumulator(n)
+    rs = st = symm = comm = None
+    if world > 1:
+        from paper_1308_2144_b200.distributed import CudaRankState, TorchComm
+        comm = TorchComm()
+        rs = CudaRankState(g, cfg, world, rank)
+        sums = rs.bind_sums()
+        dev = rs.dev
+        if exchange == "push":
+            from paper_1308_2144_b200.distributed import setup_push
+            symm = setup_push(rs)
+    else:
+        from paper_1308_2144_b200.engine import _bind_sums
+        st = hb.initialize(g, cfg)
+        dev = st._dev
+        sums = _bind_sums(st, acc)
+    s = dev.sched
+    stream = dev.stream
+    outputs = tuple(cfgd.outputs)
+    need_dist = "closeness" in outputs or "lin" in outputs
+
+    def step(ev0=None, ev1=None):
+        """One dense iteration: union kernels (+ exchange of changed rows when N > 1: fused
+        into the union epilogue with --exchange push, else pack / all-gather / scatter)."""
+        from paper_1308_2144_b200.distributed import _ptr_array
+        import ctypes
+        npeer, pn, pc, clear = 0, None, None, 1
+        if symm is not None:
+            pnl, pcl = symm.peer_pointers(dev)
+            npeer, pn, pc, clear = len(pnl), _ptr_array(pnl), _ptr_array(pcl), 0
+        if ev0 is not None:
+            ev0.record(stream)
+        _lib.union_step(_lib.StepArgs(
+            n=n, lo=s.light_lo, hi=s.light_hi if dev.full_pass else s.light_hi_steady,
+            offsets=s.offsets.data_ptr(), succ=s.succ.data_ptr(), cur=dev.cur.data_ptr(),
+            nxt=dev.nxt.data_ptr(), chg_prev=dev.chg_prev.data_ptr(),
+            chg_now=dev.chg_now.data_ptr(), est=dev.est.data_ptr(), b=b, dense=1,
+            clear_chg_now=clear, t=1, lc_table=dev.lc.data_ptr(), alpha_p2=dev.alpha_p2,
+            lc_cut=dev.lc_cut, sum_dist=sums.sum_dist.data_ptr() if need_dist else None,
+            sum_recip=sums.sum_recip.data_ptr(), n_peers=npeer,
+            peer_nxt=ctypes.cast(pn, ctypes.c_void_p) if pn is not None else None,
+            peer_chg=ctypes.cast(pc, ctypes.c_void_p) if pc is not None else None,
+            nch_out=dev.counts.data_ptr(), merged_out=dev.counts.data_ptr() + 8,
+            stream=stream.cuda_stream, **_lib.schedule_args(s)))
+        if ev1 is not None:
+            ev1.record(stream)
+        nch, merged = (int(x) for x in dev.counts.cpu())   # the per-iteration termination read
+        if symm is not None:
+            # the all-reduce of the changed count is the barrier after which every peer's
+            # pushed rows are visible; chg_prev stays all-ones so each step is iteration 1
+            tot = torch.tensor([nch], dtype=torch.int64, device=dev.device)
+            dist.all_reduce(tot)
+        elif rs is not None:
+            rs.refresh_unowned()
+            ids, rows, k = rs.gather_changed()
+            _, parts = comm.exchange(ids, rows, k)
+            for ids_q, rows_q in parts:
+                rs.apply_remote(ids_q, rows_q)
+        return nch, merged
+
+    launches_per_step = (s.light_hi > s.light_lo) + (s.n_items > 0) + (s.n_heavy > 0) + (
+        s.n_mega > 0 and s.n_heavy > s.n_mega)
+    if world > 1 and symm is None:
+        launches_per_step += 2 + (world - 1)   # refresh, gather, one scatter per peer
+    for _ in range(warmup):
+        step()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(steps)]
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    merged_check = None
+    clk = ClockSampler(local) if clocks else None
+    if clk is not None:
+        clk.__enter__()
+    t_start.record(stream)
+    for i in range(steps):
+        nch, merged = step(*evs[i])
+        merged_check = merged
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    if clk is not None:
+        clk.__exit__(None, None, None)
+    if world > 1:
+        dist.barrier()
+    total_ms = t_start.elapsed_time(t_end)
+    kernel_ms = [a.elapsed_time(b_) for a, b_ in evs]
+    if world > 1:
+        tt = torch.tensor([total_ms, sum(kernel_ms)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms, ksum = tt.tolist()
+        mt = torch.tensor([merged_check], dtype=torch.int64, device="cuda")
+        dist.all_reduce(mt)
+        merged_check = int(mt.item())
+    else:
+        ksum = sum(kernel_ms)
+    assert merged_check == m, (merged_check, m)   # a dense step merges every arc
+    ms_per_step = total_ms / steps
+    k_ms = ksum / steps
+    peak, peak_src = measured_peak()
+    B = alg_bytes(n, m, p)
+    achieved = B / world / (k_ms / 1000.0) / 1e9    # per GPU: its share of B / its kernel time
+    out = {"ms_per_step": ms_per_step, "kernel_ms": k_ms, "value": m * p / (ms_per_step / 1e3),
+           "alg_bytes": B, "achieved": achieved, "peak": peak, "peak_src": peak_src,
+           "frac": achieved / peak, "launches_per_step": launches_per_step,
+           "schedule": s.order, "heavy_nodes": s.n_heavy, "items": s.n_items,
+           "clocks": clk.summary() if clk is not None else None}
+    del st, rs, dev, sums, acc, symm
+    return out
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1308_2144_b200 as hb
     from paper_1308_2144_b200 import generators as gen
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -245,134 +423,15 @@ def run_b200(args):
             host_graph = g.to_host() if hasattr(g, "to_host") else g
         return host_graph
     params = hb.CounterParams(b=b, seed=seed)
+    outputs = tuple(cfgd.outputs)
 
     # ---------------------------------------------------------------- device-resident step
-    cfg = hb.HyperBallConfig(params=params, device=local, schedule=args.schedule)
-    acc = hb.CentralityAccumulator(n)
-    rs = comm = st = symm = None
-    if world > 1:
-        from paper_1308_2144_b200.distributed import CudaRankState, TorchComm
-        comm = TorchComm()
-        rs = CudaRankState(g, cfg, world, rank)
-        sums = rs.bind_sums()
-        dev = rs.dev
-        symm = None
-        if args.exchange == "push":
-            from paper_1308_2144_b200.distributed import _ptr_array, setup_push
-            symm = setup_push(rs)
-    else:
-        from paper_1308_2144_b200.engine import _bind_sums
-        st = hb.initialize(g, cfg)
-        dev = st._dev
-        sums = _bind_sums(st, acc)
-    s = dev.sched
-    stream = dev.stream
-    L = _lib.hb()
-    # the config's outputs (BASELINE: config 5 is harmonic only): closeness and Lin need
-    # sum_dist, harmonic needs sum_recip
-    outputs = tuple(cfgd.outputs)
-    need_dist = "closeness" in outputs or "lin" in outputs
-
-    def step(ev0=None, ev1=None):
-        """One dense iteration: union kernels (+ exchange of changed rows when N > 1: fused
-        into the union epilogue with --exchange push, else pack / all-gather / scatter)."""
-        npeer, pn, pc, clear = 0, None, None, 1
-        if symm is not None:
-            pnl, pcl = symm.peer_pointers(dev)
-            npeer, pn, pc, clear = len(pnl), _ptr_array(pnl), _ptr_array(pcl), 0
-        if ev0 is not None:
-            ev0.record(stream)
-        _lib.check(L.hb_union_step(
-            n, s.light_lo, s.light_hi if dev.full_pass else s.light_hi_steady,
-            s.offsets.data_ptr(), s.succ.data_ptr(),
-            dev.cur.data_ptr(), dev.nxt.data_ptr(), dev.chg_prev.data_ptr(),
-            dev.chg_now.data_ptr(), clear, dev.est.data_ptr(),
-            sums.sum_dist.data_ptr() if need_dist else None,
-            sums.sum_recip.data_ptr(), 1, dev.lc.data_ptr(), dev.alpha_p2, dev.lc_cut, b, 1,
-            s.light_max_deg, s.heavy_nodes.data_ptr(), s.item_first.data_ptr(), s.n_heavy,
-            s.finish_order.data_ptr(), s.n_mega, s.item_node.data_ptr(), s.item_beg.data_ptr(), s.n_items, s.item_arcs,
-            s.partial.data_ptr(), dev.counts.data_ptr(), dev.counts.data_ptr() + 8,
-            s.hot_rows, None, 0, 0, None, 0, None, npeer, pn, pc, stream.cuda_stream),
-            "hb_union_step")
-        if ev1 is not None:
-            ev1.record(stream)
-        nch, merged = (int(x) for x in dev.counts.cpu())   # the per-iteration termination read
-        if symm is not None:
-            # the all-reduce of the changed count is the barrier after which every peer's
-            # pushed rows are visible; chg_prev stays all-ones so each step is iteration 1
-            tot = torch.tensor([nch], dtype=torch.int64, device=dev.device)
-            dist.all_reduce(tot)
-        elif rs is not None:
-            rs.refresh_unowned()
-            ids, rows, k = rs.gather_changed()
-            _, parts = comm.exchange(ids, rows, k)
-            for ids_q, rows_q in parts:
-                rs.apply_remote(ids_q, rows_q)
-        return nch, merged
-
-    launches_per_step = (s.light_hi > s.light_lo) + (s.n_items > 0) + (s.n_heavy > 0)
-    if world > 1 and symm is None:
-        launches_per_step += 2 + (world - 1)   # refresh, gather, one scatter per peer
-    for _ in range(args.warmup):
-        step()
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
-    t_start = torch.cuda.Event(enable_timing=True)
-    t_end = torch.cuda.Event(enable_timing=True)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    merged_check = None
-    with ClockSampler(local) as clk:
-        t_start.record(stream)
-        for i in range(args.steps):
-            nch, merged = step(*evs[i])
-            merged_check = merged
-        t_end.record(stream)
-        torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    total_ms = t_start.elapsed_time(t_end)
-    kernel_ms = [a.elapsed_time(b_) for a, b_ in evs]
-    if world > 1:
-        tt = torch.tensor([total_ms, sum(kernel_ms)], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        total_ms, ksum = tt.tolist()
-    else:
-        ksum = sum(kernel_ms)
-    ms_per_step = total_ms / args.steps
-    k_ms = ksum / args.steps
-    if world > 1:
-        mt = torch.tensor([merged_check], dtype=torch.int64, device="cuda")
-        dist.all_reduce(mt)
-        merged_check = int(mt.item())
-    assert merged_check == m, (merged_check, m)   # dense step merges every arc
-    value = m * p / (ms_per_step / 1000.0)
-    peak, peak_src = measured_peak()
-    B = alg_bytes(n, m, p)
-    achieved = B / world / (k_ms / 1000.0) / 1e9    # per GPU: its share of B / its kernel time
-    traffic = None
-    tpath = os.path.join(REPO, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get(args.config)
-        except Exception:
-            traffic = None
-    clocks = clk.summary()
+    d = dense_steps(g, cfgd, local, args.steps, args.warmup, args.schedule, world, rank,
+                    args.exchange, clocks=True)
+    torch.cuda.empty_cache()
 
     # ---------------------------------------------------------------- whole run + e2e
-    e2e = None
-    whole = None
-    if not args.no_e2e:
-        # pinned host copies of the graph: the user-side buffers of the e2e call
-        off_pin = torch.empty(n + 1, dtype=torch.int64, pin_memory=True)
-        suc_pin = torch.empty(m, dtype=torch.int32, pin_memory=True)
-        hg = host_g()
-        off_pin.numpy()[:] = hg.offsets
-        suc_pin.numpy()[:] = hg.successors
-        gp = hb.CsrGraph(off_pin.numpy(), suc_pin.numpy())
-        del st, rs, dev, sums, acc
-        torch.cuda.empty_cache()
+    def e2e_run(gp, what, h2d):
         runs = []
         for i in range(args.e2e_warmup + args.e2e_steps):
             if world > 1:
@@ -394,7 +453,6 @@ def run_b200(args):
             del st2, acc2, fins
             if i >= args.e2e_warmup:
                 runs.append((dt, merged_total, iters))
-        dt = max(r[0] for r in runs) if runs else float("nan")
         dts = [r[0] for r in runs]
         merged_total, iters = runs[-1][1], runs[-1][2]
         if world > 1:
@@ -404,18 +462,77 @@ def run_b200(args):
         else:
             sum_dt = sum(dts)
         mean_dt = sum_dt / len(dts)
-        e2e = {"value": merged_total * p / mean_dt, "unit": UNIT,
-               "h2d_bytes_per_step": int(off_pin.numel() * 8 + suc_pin.numel() * 4),
-               # the outputs and the 16-byte changed/merged counters read after every
-               # iteration (the fused accumulator's final estimates stay on the device)
-               "d2h_bytes_per_step": int(n * 8 * len(outputs) + 16 * iters),
-               "seconds_per_run": mean_dt, "iterations": iters,
-               "merged_arcs_per_run": merged_total,
-               "what": "run(g, config, [CentralityAccumulator]) + finalize_{%s} from pinned "
-                       "host CSR; graph upload, schedule, seed, all iterations to convergence "
-                       "and result download timed" % ",".join(outputs)}
-        whole = {"iterations": iters, "merged_arcs": merged_total,
-                 "dense_equivalent_arcs": m * iters}
+        return {"value": merged_total * p / mean_dt, "unit": UNIT,
+                "h2d_bytes_per_step": int(h2d),
+                # the outputs and the 16-byte changed/merged counters read after every
+                # iteration (the fused accumulator's final estimates stay on the device)
+                "d2h_bytes_per_step": int(n * 8 * len(outputs) + 16 * iters),
+                "seconds_per_run": mean_dt, "iterations": iters,
+                "merged_arcs_per_run": merged_total,
+                "what": "run(g, config, [CentralityAccumulator]) + finalize_{%s} from %s; "
+                        "graph upload, schedule, seed, all iterations to convergence and "
+                        "result download timed" % (",".join(outputs), what)}
+
+    e2e = whole = e2e_ref_graph = None
+    if not args.no_e2e:
+        # pinned host copies of the graph: the user-side buffers of the e2e call
+        off_pin = torch.empty(n + 1, dtype=torch.int64, pin_memory=True)
+        suc_pin = torch.empty(m, dtype=torch.int32, pin_memory=True)
+        hg = host_g()
+        off_pin.numpy()[:] = hg.offsets
+        suc_pin.numpy()[:] = hg.successors
+        gp = hb.CsrGraph(off_pin.numpy(), suc_pin.numpy())
+        e2e = e2e_run(gp, "pinned host CSR (int64 offsets, int32 ids)",
+                      off_pin.numel() * 8 + suc_pin.numel() * 4)
+        whole = {"iterations": e2e["iterations"], "merged_arcs": e2e["merged_arcs_per_run"],
+                 "dense_equivalent_arcs": m * e2e["iterations"]}
+        del gp, off_pin, suc_pin
+        if not args.no_e2e_int64:
+            # the reference's own input type: CsrGraph (graph.py:29-50) holds pageable int64
+            # offsets and successors
+            off64 = np.ascontiguousarray(hg.offsets, dtype=np.int64)
+            suc64 = np.ascontiguousarray(hg.successors, dtype=np.int64)
+            g64 = hb.CsrGraph(off64, suc64)
+            e2e_ref_graph = e2e_run(g64, "the reference's CsrGraph layout (pageable int64 "
+                                         "offsets and successors)",
+                                    off64.nbytes + suc64.nbytes)
+            del g64, off64, suc64
+        torch.cuda.empty_cache()
+
+    # ---------------------------------------------------------------- other configs
+    per_config = None
+    if rank == 0 and world == 1 and not args.no_per_config:
+        per_config = {}
+        if not args.no_cpu_baseline:
+            host_g()                       # keep the host copy for the CPU baseline below
+        g = None                           # a device-built graph frees its HBM here
+        torch.cuda.empty_cache()
+        for name in [c for c in args.per_config.split(",") if c and c != args.config]:
+            try:
+                cd = gen.CONFIGS[name]
+                t0 = time.perf_counter()
+                gq = cd.build_device(torch.device("cuda", local))
+                torch.cuda.synchronize()
+                log(f"[bench] per-config {name}: n={gq.n} m={gq.m} built in "
+                    f"{time.perf_counter() - t0:.1f}s")
+                r = dense_steps(gq, cd, local, args.per_config_steps, 3)
+                pq = 1 << cd.log2m
+                per_config[name] = {
+                    "workload": f"{name}: {cd.description}", "n": gq.n, "m": gq.m,
+                    "log2m": cd.log2m, "dense_ms": r["ms_per_step"],
+                    "kernel_ms": r["kernel_ms"], "value": r["value"], "unit": UNIT,
+                    "roofline": {"bound": "hbm", "achieved": r["achieved"], "peak": r["peak"],
+                                 "unit": "GB/s", "frac": r["frac"],
+                                 "algorithmic_bytes_per_launch": r["alg_bytes"],
+                                 "traffic": load_traffic(name)},
+                    "schedule": r["schedule"], "steps": args.per_config_steps}
+                del gq, r
+                torch.cuda.empty_cache()
+                log(f"[bench] per-config {name}: {per_config[name]['dense_ms']:.3f} ms, "
+                    f"frac {per_config[name]['roofline']['frac']:.3f}")
+            except Exception as exc:   # one config failing must not lose the headline line
+                per_config[name] = {"error": repr(exc)[:300]}
+                torch.cuda.empty_cache()
 
     # ---------------------------------------------------------------- CPU baseline
     cpu = None
@@ -424,38 +541,33 @@ def run_b200(args):
         samples, _ = cpu_dense_sample(host_g(), b, seed, args.cpu_budget, threads, repeats=1)
         arcs, secs = samples[0]
         cpu = {"value": arcs * p / secs, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"one dense union pass (oracle/hb_oracle.c, {threads} pthreads) over "
-                         f"destination nodes holding {arcs} of {m} arcs ({secs:.1f} s)"}
+               "sample": f"one dense step (oracle/hb_oracle.c union pass on {threads} pthreads "
+                         f"+ accumulate) over destination nodes holding {arcs} of {m} arcs "
+                         f"({secs:.1f} s)"}
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "metric": METRIC, "value": d["value"], "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": d["ms_per_step"],
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "u8", "data": "synthetic",
-            "config": {"workload": f"{args.config}: {cfgd.description}", "n": n, "m": m,
-                       "log2m": b, "register_width": 5, "hash_seed": seed,
-                       "schedule": s.order, "heavy_nodes": s.n_heavy, "items": s.n_items,
-                       "step": "one dense iteration (all sources changed): union + estimate + "
-                               "fused accumulate for %s" % "/".join(outputs),
-                       "l2": ("inputs larger than L2 (%.2f GB of registers + %.2f GB of CSR), "
-                              "no flush" if n * p > 126e6 else
-                              "registers (%.2f GB) + CSR (%.2f GB) partly L2-resident, no "
-                              "flush: a small-graph line") % (n * p / 1e9,
-                                                             (8 * (n + 1) + 4 * m) / 1e9),
-                       "parallelism": (f"node-partition x{world}, {args.exchange} exchange"
-                                       if world > 1 else "single GPU")},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "algorithmic_bytes_per_launch": B, "kernel_ms": k_ms,
-                         "peak_source": peak_src,
+            "config": bench_config(cfgd, n, m, world, args.exchange),
+            "schedule": {"order": d["schedule"], "heavy_nodes": d["heavy_nodes"],
+                         "items": d["items"]},
+            "roofline": {"bound": "hbm", "achieved": d["achieved"], "peak": d["peak"],
+                         "unit": "GB/s", "frac": d["frac"], "traffic": load_traffic(args.config),
+                         "algorithmic_bytes_per_launch": d["alg_bytes"],
+                         "kernel_ms": d["kernel_ms"], "peak_source": d["peak_src"],
                          "kernels": "hb_union_step (light%s)" % (
-                             " + heavy items + finish" if s.n_items else "")},
+                             " + heavy items + finish" if d["items"] else "")},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "e2e_reference_graph": e2e_ref_graph,
             "whole_run": whole,
-            "clocks": clocks,
-            "gpu_launches": launches_per_step * args.steps,
+            "per_config": per_config,
+            "clocks": d["clocks"],
+            "gpu_launches": d["launches_per_step"] * args.steps,
+            "mapped_repo_libs": mapped_repo_libs(),
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -475,6 +587,12 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-warmup", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-e2e-int64", action="store_true",
+                    help="skip the second e2e from the reference's int64 CsrGraph")
+    ap.add_argument("--per-config", default="config2,config3,config5",
+                    help="other configs whose dense step is measured into per_config")
+    ap.add_argument("--per-config-steps", type=int, default=10)
+    ap.add_argument("--no-per-config", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0,
                     help="seconds of CPU work in the cpu_baseline sample")

@@ -169,11 +169,14 @@ class OracleResult:
 
 def run_oracle(offsets, succ, b: int, seed: int = 0, width: int = 5, workers: int = 1,
                skip: bool = True, max_iterations: int | None = None, weights=None,
-               record: bool = True, keep_snapshots: bool = False) -> OracleResult:
+               record: bool = True, keep_snapshots: bool = False,
+               reg_digest=None) -> OracleResult:
     """engine.run(g, HyperBallConfig(CounterParams(b, width, seed)), [CentralityAccumulator])
     restated: initialize (engine.py:330-348), iterate until no counter changes
     (engine.py:413-435), accumulate per iteration (centrality.py:132-150), finalize
-    (centrality.py:153-171).  Index 0 of the digest lists is the seeded state."""
+    (centrality.py:153-171).  Index 0 of the digest lists is the seeded state.
+    reg_digest: digest function of the register matrix (default: sha256 of the bytes)."""
+    rdig = reg_digest or sha
     offsets = _c(offsets, np.int64)
     succ = _c(succ, np.int64)
     n = offsets.shape[0] - 1
@@ -183,7 +186,7 @@ def run_oracle(offsets, succ, b: int, seed: int = 0, width: int = 5, workers: in
     sum_recip = np.zeros(n, np.float64)
     res = OracleResult(0, cur, est, sum_dist, sum_recip, None, None, None, None)
     if record:
-        res.reg_digests.append(sha(cur))
+        res.reg_digests.append(rdig(cur))
         res.est_digests.append(sha(est))
     if keep_snapshots:
         res.snapshots.append((cur.copy(), est.copy(), chg_prev.copy()))
@@ -197,7 +200,7 @@ def run_oracle(offsets, succ, b: int, seed: int = 0, width: int = 5, workers: in
             cur, est, chg_prev = nxt, new_est, chg_now
             res.nch.append(nch)
             if record:
-                res.reg_digests.append(sha(cur))
+                res.reg_digests.append(rdig(cur))
                 res.est_digests.append(sha(est))
             if keep_snapshots:
                 res.snapshots.append((cur.copy(), est.copy(), chg_prev.copy()))
@@ -271,7 +274,7 @@ def run_exact_oracle(offsets, succ, weights=None, skip: bool = True,
             cur, est, chg_prev = nxt, new_est, chg_now
             res.nch.append(nch)
             if record:
-                res.reg_digests.append(sha(cur))
+                res.reg_digests.append(rdig(cur))
                 res.est_digests.append(sha(est))
             if nch == 0:
                 break

@@ -163,6 +163,17 @@ def hb():
     return _hb
 
 
+def use_graph_library(path: str) -> None:
+    """Bind the synthetic-graph builders (hbg_*) from another library exporting them --
+    bench.py's CPU reference arm uses the oracle's copy, so that process maps no product
+    library.  Must be called before the first graphlib()."""
+    global GRAPH_LIB_PATH, _graph
+    with _lock:
+        if _graph is not None and GRAPH_LIB_PATH != path:
+            raise RuntimeError("graph library already bound")
+        GRAPH_LIB_PATH = path
+
+
 def graphlib():
     global _graph
     if _graph is None:

@@ -283,6 +283,13 @@ def test_bench_reference_arm_json(tmp_path):
     assert d["impl"] == "reference" and d["value"] > 0 and d["steps"] == 2
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    # no product library in the reference arm; its config dict is the one the B200 arm
+    # prints for the same workload
+    assert d["mapped_repo_libs"] == ["oracle/liborc.so"], d["mapped_repo_libs"]
+    sys.path.insert(0, repo)
+    import bench
+    g = gen.BUILDERS["config1"]()
+    assert d["config"] == bench.bench_config(gen.CONFIGS["config1"], g.n, g.m)
     env = dict(os.environ, RANK="1", WORLD_SIZE="2")
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=env)
     assert r.returncode == 0 and not [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
@@ -302,3 +309,27 @@ def test_sm100a_sass_uses_tma_gather_and_3input_max():
     assert "sm_100a" in out or "SM100" in out.upper()
     for op in ("UTMALDG.2D.GATHER4", "SYNCS.PHASECHK.TRANS64", "VIMNMX3.U16x2"):
         assert op in out, op
+
+
+def test_oracle_carries_identical_graph_builders():
+    """bench.py's reference arm builds its graph with the oracle library's copy of the
+    builders (no product .so in that process): same bytes as libhbgraph.so."""
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys, os; sys.path.insert(0, %r)\n"
+        "from paper_1308_2144_b200 import _lib\n"
+        "_lib.use_graph_library(os.path.join(%r, 'oracle', 'liborc.so'))\n"
+        "from paper_1308_2144_b200 import generators as gen\n"
+        "print(gen.graph_digest(gen.BUILDERS['config1']()))\n"
+        "print(gen.graph_digest(gen.weblike_t(1 << 14, seed=3)))\n"
+        "print(gen.graph_digest(gen.disconnected_t(1 << 14, 1 << 13, 0.1, 6.0, seed=2)))\n"
+        "print(open('/proc/self/maps').read().count('libhbgraph'))\n"
+    ) % (repo, repo)
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                         check=True).stdout.split()
+    assert out[3] == "0"
+    assert out[0] == gen.graph_digest(gen.BUILDERS["config1"]())
+    assert out[1] == gen.graph_digest(gen.weblike_t(1 << 14, seed=3))
+    assert out[2] == gen.graph_digest(gen.disconnected_t(1 << 14, 1 << 13, 0.1, 6.0, seed=2))

@@ -103,3 +103,33 @@ def test_exact_oracle_skip_equals_naive():
     a = orc.run_exact_oracle(off, suc, skip=True)
     b = orc.run_exact_oracle(off, suc, skip=False)
     assert a.reg_digests == b.reg_digests and a.est_digests == b.est_digests
+
+
+@pytest.mark.parametrize("name", ["config1", "config2", "config3"])
+def test_oracle_matches_reference_at_full_size(name):
+    """The oracle against the reference's own full-size runs (tests/golden/fullsize.json,
+    tests/golden/make_fullsize.py): registers and estimates after every iteration,
+    changed counts, t and the finalizers, on BASELINE.json's configs 1-3 (config 4 is
+    pinned on the GPU box, where the device run is compared with the same fixture)."""
+    import json
+    import os
+    import sys
+
+    from conftest import GOLDEN_DIR
+    sys.path.insert(0, GOLDEN_DIR)
+    from digest import reg_digest
+    from paper_1308_2144_b200 import generators as gen
+
+    want = json.load(open(os.path.join(GOLDEN_DIR, "fullsize.json")))[name]
+    cfgd = gen.CONFIGS[name]
+    g = cfgd.build()
+    assert gen.graph_digest(g) == want["graph_digest"]
+    res = orc.run_oracle(np.asarray(g.offsets, np.int64), np.asarray(g.successors, np.int64),
+                         cfgd.log2m, cfgd.hash_seed, 5, workers=os.cpu_count() or 1,
+                         reg_digest=reg_digest)
+    assert res.t == want["t"]
+    assert res.nch == want["nch"]
+    assert res.reg_digests == want["reg_digests"]
+    assert res.est_digests == want["est_digests"]
+    for nm in ("closeness", "harmonic", "lin"):
+        assert hashlib.sha256(getattr(res, nm).tobytes()).hexdigest() == want[nm], nm
