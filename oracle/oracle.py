@@ -274,7 +274,7 @@ def run_exact_oracle(offsets, succ, weights=None, skip: bool = True,
             cur, est, chg_prev = nxt, new_est, chg_now
             res.nch.append(nch)
             if record:
-                res.reg_digests.append(rdig(cur))
+                res.reg_digests.append(sha(cur))
                 res.est_digests.append(sha(est))
             if nch == 0:
                 break
