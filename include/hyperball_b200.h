@@ -32,9 +32,10 @@
  *                     (internal relabelling; no reference counterpart)
  *   hb_sort_rows      graph.py:52-80 keeps successor lists sorted; this restores that
  *                     order after the internal relabelling
- *   hb_gen_rmat_keys / hb_keys_to_csr
+ *   hb_gen_rmat_keys / hb_gen_degrees / hb_gen_blocks / hb_gen_arc_keys / hb_keys_to_csr
  *                     graph.py:52-80 (from_edges: sort, dedup, CSR) + 145-155 (transpose),
- *                     for the synthetic R-MAT configs, on the device
+ *                     for the synthetic configs, on the device
+ *   hb_transpose_csr  graph.py:145-155 transpose, on the device
  *   hb_pack_registers / hb_unpack_registers
  *                     hll.py:145-177 (CounterArray packing, to_blob / from_blob body),
  *                     for counters(), save() and load_state() (engine.py:254-327)
@@ -365,6 +366,36 @@ int hb_gen_rmat_keys(int scale, int64_t m, uint64_t thr_a, uint64_t thr_ab, uint
 int hb_keys_to_csr(int64_t n, int64_t m, uint64_t *keys, uint64_t *alt, void *temp,
                    uint64_t *temp_bytes, int64_t *m_out, int64_t *offsets, int32_t *succ,
                    void *stream);
+
+/* Device builders of the other synthetic configs (bit-identical to libhbgraph.so's hbg_er /
+ * hbg_disconnected / hbg_weblike): kind 1 = ER, 3 = disconnected, 4 = web-like.
+ * hb_gen_degrees: deg[u] (device int64 [n]) = out-degree of source u, drawn from the host
+ *   built CDF table (device fp64 [cdf_len]: Poisson CDF for kinds 1 / 3, Zipf CDF on
+ *   {kmin..} for kind 4 -- the same tables graphgen.c builds).
+ * hb_gen_blocks: the disconnected config's blocks: the giant block [0, giant), then
+ *   Geometric(geo_p) sized blocks; lo / hi (device int64 [n]) receive each node's block
+ *   bounds.  size / start: device int64 scratch [n - giant]; temp == NULL queries
+ *   *temp_bytes.
+ * hb_gen_arc_keys: the arcs of every source u at offsets[u]..offsets[u+1] (device int64
+ *   [n+1], exclusive prefix sum of the degrees) as transpose keys (dst << 32 | src),
+ *   self-loops as ~0; feed them to hb_keys_to_csr. */
+int hb_gen_degrees(int kind, int64_t n, uint64_t seed, const double *cdf, int64_t cdf_len,
+                   int64_t kmin, int64_t *deg, void *stream);
+int hb_gen_blocks(int64_t n, int64_t giant, double geo_p, uint64_t seed, int64_t *size,
+                  int64_t *start, int64_t *lo, int64_t *hi, void *temp, uint64_t *temp_bytes,
+                  void *stream);
+int hb_gen_arc_keys(int kind, int64_t n, uint64_t seed, const int64_t *offsets,
+                    const int64_t *block_lo, const int64_t *block_hi, double p_local,
+                    int64_t window, uint64_t *keys, void *stream);
+
+/* Transpose of a CSR on the device (graph.py:145-155 transpose: every arc reversed,
+ * duplicates and self-loops kept, each new row listing its sources in ascending order --
+ * the reference's stable argsort by target).  offsets / succ: device int64 [n+1] /
+ * int32 [m]; keys, alt: device uint64 [m] scratch; out_offsets / out_succ: device int64
+ * [n+1] / int32 [m].  temp == NULL queries *temp_bytes. */
+int hb_transpose_csr(int64_t n, int64_t m, const int64_t *offsets, const int32_t *succ,
+                     uint64_t *keys, uint64_t *alt, void *temp, uint64_t *temp_bytes,
+                     int64_t *out_offsets, int32_t *out_succ, void *stream);
 
 /* out[i] = hash_items(items[i], replicas[i], seed) (hll.py:79-88), device arrays. */
 int hb_hash_items(int64_t n, const uint64_t *items, const uint64_t *replicas, uint64_t seed,

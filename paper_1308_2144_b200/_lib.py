@@ -75,6 +75,10 @@ HB_SIGNATURES = {
     "hb_gen_rmat_keys": (_int, [_int, _i64, _u64, _u64, _u64, _u64, _vp, _vp]),
     "hb_keys_to_csr": (_int, [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "hb_hash_items": (_int, [_i64, _vp, _vp, _u64, _vp, _vp]),
+    "hb_gen_degrees": (_int, [_int, _i64, _u64, _vp, _i64, _i64, _vp, _vp]),
+    "hb_gen_blocks": (_int, [_i64, _i64, _dbl, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "hb_gen_arc_keys": (_int, [_int, _i64, _u64, _vp, _vp, _vp, _dbl, _i64, _vp, _vp]),
+    "hb_transpose_csr": (_int, [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "hb_item_arcs": (_i64, [_int]),
     "hb_light_max_deg": (_i64, [_int]),
     "hb_light_npw": (_i64, [_int]),
@@ -128,6 +132,8 @@ GRAPH_SIGNATURES = {
     "hbg_disconnected": (_vp, [_i64, _i64, _dbl, _dbl, _u64, _int]),
     "hbg_weblike": (_vp, [_i64, _dbl, _i64, _i64, _dbl, _i64, _u64, _int]),
     "hbg_from_arcs": (_vp, [_i64, _i64, _vp, _vp, _int]),
+    "hbg_poisson_cdf": (_int, [_dbl, _vp]),
+    "hbg_zipf_cdf": (None, [_dbl, _i64, _i64, _vp]),
     "hbg_n": (_i64, [_vp]),
     "hbg_m": (_i64, [_vp]),
     "hbg_copy": (None, [_vp, _vp, _vp]),

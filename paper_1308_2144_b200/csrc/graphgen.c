@@ -403,6 +403,22 @@ void *hbg_from_arcs(int64_t n, int64_t M, const uint32_t *src, const uint32_t *d
     return transpose_build(n, M, src, dst, threads);
 }
 
+/* The CDF tables the degree draws use (for the device builders, which must draw
+ * bit-identical degrees: hb_gen_degrees).  hbg_poisson_cdf writes up to 256 entries and
+ * returns the count (the last one is the 2.0 sentinel); hbg_zipf_cdf writes kmax-kmin+1. */
+int hbg_poisson_cdf(double lam, double *out) {
+    poisson_tab t;
+    poisson_init(&t, lam);
+    memcpy(out, t.cdf, sizeof(double) * (size_t)(t.kmax + 1));
+    return t.kmax + 1;
+}
+void hbg_zipf_cdf(double alpha, int64_t kmin, int64_t kmax, double *out) {
+    zipf_tab z;
+    zipf_init(&z, alpha, kmin, kmax);
+    memcpy(out, z.cdf, sizeof(double) * (size_t)(kmax - kmin + 1));
+    free(z.cdf);
+}
+
 int64_t hbg_n(void *h) { return ((hbg_graph *)h)->n; }
 int64_t hbg_m(void *h) { return ((hbg_graph *)h)->m; }
 void hbg_copy(void *h, int64_t *offsets, int32_t *succ) {

@@ -183,6 +183,26 @@ __device__ __forceinline__ uint4 ld_chunk(const uint4 *__restrict__ cur4, int32_
                                           uint32_t k) {
   return __ldg(cur4 + ((uint32_t)w * ch + k));
 }
+// Small rows (p <= 2^HB_L2_64B_MAX_LOGP bytes): the L2 fetches 64 bytes instead of its
+// default 128 on a miss (`.L2::64B`, SASS LDG...LTC64B).  A random 16-byte row that misses
+// L2 otherwise pulls a whole 128-byte line from HBM (profiles/r1c_l2_gather_probe.md);
+// tools/pb_probe.cu measured 68.6 instead of 136.8 GB of DRAM reads for 2^30 random
+// 16-byte rows, same time; config 5 32.85 -> 32.4 ms, p = 64 (config 3) slightly slower.
+#ifndef HB_L2_64B_MAX_LOGP
+#define HB_L2_64B_MAX_LOGP 5
+#endif
+__device__ __forceinline__ uint4 ld_nc_64b(const uint4 *p) {
+  uint4 r;
+  asm("ld.global.nc.L2::64B.v4.u32 {%0, %1, %2, %3}, [%4];"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+template <int LOGP>
+__device__ __forceinline__ uint4 ld_row_chunk(const uint4 *__restrict__ cur4, int32_t w,
+                                              uint32_t ch, uint32_t k) {
+  if constexpr (LOGP <= HB_L2_64B_MAX_LOGP) return ld_nc_64b(cur4 + ((uint32_t)w * ch + k));
+  else return ld_chunk(cur4, w, ch, k);
+}
 
 // L2 eviction priorities for the DRAM-bound small-p kernels (p <= 32, degree order): one
 // uniform range policy over cur -- rows in the hot head (the most-read rows, first
@@ -210,6 +230,20 @@ __device__ __forceinline__ uint64_t range_policy(const void *base, uint32_t hot,
 __device__ __forceinline__ uint4 ld_chunk_hint(const uint4 *__restrict__ cur4, int32_t w,
                                                uint32_t ch, uint32_t k, uint64_t pol) {
   return ld_pol(cur4 + ((uint32_t)w * ch + k), pol);
+}
+__device__ __forceinline__ uint4 ld_pol_64b(const uint4 *p, uint64_t pol) {
+  uint4 r;
+  asm("ld.global.nc.L2::cache_hint.L2::64B.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "l"(p), "l"(pol));
+  return r;
+}
+template <int LOGP>
+__device__ __forceinline__ uint4 ld_row_chunk_hint(const uint4 *__restrict__ cur4, int32_t w,
+                                                   uint32_t ch, uint32_t k, uint64_t pol) {
+  if constexpr (LOGP <= HB_L2_64B_MAX_LOGP)
+    return ld_pol_64b(cur4 + ((uint32_t)w * ch + k), pol);
+  else return ld_chunk_hint(cur4, w, ch, k, pol);
 }
 
 __device__ __forceinline__ uint4 ldg4(const uint8_t *p) {
@@ -912,8 +946,8 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
 #pragma unroll
           for (int c = 0; c < Gm::CPL; c++)
             r[u][c] = (LOGP >= HB_PAD_MIN_LOGP || ok)
-                          ? (kHint ? ld_chunk_hint(cur4, w, Gm::CH, c * Gm::G + gl, pol)
-                                   : ld_chunk(cur4, w, Gm::CH, c * Gm::G + gl))
+                          ? (kHint ? ld_row_chunk_hint<LOGP>(cur4, w, Gm::CH, c * Gm::G + gl, pol)
+                                   : ld_row_chunk<LOGP>(cur4, w, Gm::CH, c * Gm::G + gl))
                           : make_uint4(0, 0, 0, 0);
         }
         // sequential accumulate: a pairwise tree (shorter chains) measured 20% slower on
@@ -1033,8 +1067,8 @@ k_heavy_partial(const int64_t *__restrict__ offsets, const int32_t *__restrict__
 #pragma unroll
           for (int c = 0; c < Gm::CPL; c++)
             r[u][c] = (LOGP >= HB_PAD_MIN_LOGP || ok)
-                          ? (kHint ? ld_chunk_hint(cur4, w, Gm::CH, c * Gm::G + gl, pol)
-                                   : ld_chunk(cur4, w, Gm::CH, c * Gm::G + gl))
+                          ? (kHint ? ld_row_chunk_hint<LOGP>(cur4, w, Gm::CH, c * Gm::G + gl, pol)
+                                   : ld_row_chunk<LOGP>(cur4, w, Gm::CH, c * Gm::G + gl))
                           : make_uint4(0, 0, 0, 0);
         }
 #pragma unroll
@@ -1753,6 +1787,120 @@ __global__ void k_keys_to_csr(int64_t n, int64_t mu, const uint64_t *__restrict_
     const int64_t prev = k > 0 ? (int64_t)(__ldg(keys + k - 1) >> 32) : -1;
     for (int64_t v = prev + 1; v <= d; v++) offsets[v] = k;
     if (k < mu) succ[k] = (int32_t)(__ldg(keys + k) & 0xffffffffull);
+  }
+}
+
+// Out-degree laws and arc targets of the other synthetic configs, bit-identical to
+// graphgen.c's out_degree / fill_fn (same counter-based draws, same double arithmetic:
+// u01 is exact, the Poisson / Zipf CDF tables are built on the host by the same C code
+// and uploaded, `below` is the 64x64 -> high-64 product).
+enum { GG_ER = 1, GG_DISC = 3, GG_WEB = 4 };
+__device__ __forceinline__ double gg_u01(uint64_t x) { return (double)(x >> 11) * 0x1.0p-53; }
+__device__ __forceinline__ uint64_t gg_below(uint64_t x, uint64_t n) { return __umul64hi(x, n); }
+
+__global__ void k_gen_degree(int kind, int64_t n, uint64_t seed, const double *__restrict__ cdf,
+                             int64_t cdf_len, int64_t kmin, int64_t *__restrict__ deg) {
+  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    const double x = gg_u01(gg_rng3(seed, 1, (uint64_t)u, 0));
+    int64_t k;
+    if (kind == GG_WEB) {                 // zipf_draw: first i with x < cdf[i]
+      int64_t lo = 0, hi = cdf_len - 1;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) / 2;
+        if (x < __ldg(cdf + mid)) hi = mid; else lo = mid + 1;
+      }
+      k = kmin + lo;
+    } else {                              // poisson_draw: linear scan of the CDF
+      k = 0;
+      while (x >= __ldg(cdf + k)) k++;
+    }
+    deg[u] = k;
+  }
+}
+
+// Geometric(p) block sizes of the disconnected config: block b has size = number of
+// trials up to the first success of rng3(seed, 5, b, trial) < p (graphgen.c generate()).
+__global__ void k_gen_block_sizes(int64_t nblocks, uint64_t seed, double geo_p,
+                                  int64_t *__restrict__ size) {
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nblocks;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    int64_t k = 1;
+    while (gg_u01(gg_rng3(seed, 5, (uint64_t)b, (uint64_t)k)) >= geo_p) k++;
+    size[b] = k;
+  }
+}
+// Block bounds per node: block b covers [giant + start[b], giant + start[b] + size[b]) cut
+// at n (start = exclusive prefix sum of the sizes); the giant block is [0, giant).
+__global__ void k_gen_block_bounds(int64_t n, int64_t giant, int64_t nblocks,
+                                   const int64_t *__restrict__ start,
+                                   const int64_t *__restrict__ size, int64_t *__restrict__ lo,
+                                   int64_t *__restrict__ hi) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < giant;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    lo[v] = 0;
+    hi[v] = giant;
+  }
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nblocks;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p0 = giant + __ldg(start + b);
+    if (p0 >= n) continue;
+    int64_t p1 = p0 + __ldg(size + b);
+    if (p1 > n) p1 = n;
+    for (int64_t v = p0; v < p1; v++) {
+      lo[v] = p0;
+      hi[v] = p1;
+    }
+  }
+}
+
+// Arcs of source u at positions off[u]..off[u+1] as transpose keys (dst << 32 | src);
+// self-loops become the sentinel ~0 (dropped by hb_keys_to_csr).  Warp per source.
+__global__ void k_gen_arcs(int kind, int64_t n, uint64_t seed, const int64_t *__restrict__ off,
+                           const int64_t *__restrict__ blo, const int64_t *__restrict__ bhi,
+                           double p_local, int64_t window, uint64_t *__restrict__ keys) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t u = warp; u < n; u += nwarps) {
+    const int64_t base = __ldg(off + u), k = __ldg(off + u + 1) - base;
+    for (int64_t j = lane; j < k; j += 32) {
+      const uint64_t r = gg_rng3(seed, 2, (uint64_t)u, (uint64_t)j);
+      int64_t v;
+      if (kind == GG_ER) {
+        v = (int64_t)gg_below(r, (uint64_t)(n - 1));
+        if (v >= u) v++;
+      } else if (kind == GG_DISC) {
+        const int64_t a = __ldg(blo + u), b = __ldg(bhi + u);
+        v = a + (int64_t)gg_below(r, (uint64_t)(b - a));
+      } else {
+        const uint64_t r2 = gg_rng3(seed, 3, (uint64_t)u, (uint64_t)j);
+        if (gg_u01(r) < p_local) {
+          const int64_t o = 1 + (int64_t)gg_below(r2 >> 1, (uint64_t)window);
+          v = (r2 & 1) ? u + o : u - o;
+          v %= n;
+          if (v < 0) v += n;
+        } else {
+          v = (int64_t)gg_below(r2, (uint64_t)n);
+        }
+      }
+      keys[base + j] = (v == u) ? ~0ull : (((uint64_t)v << 32) | (uint64_t)u);
+    }
+  }
+}
+
+// Keys of the transpose of a CSR (forward graph G): arc (u -> v) becomes (v << 32 | u).
+// Warp per row.  Sorting these keys gives the reference's transpose order exactly
+// (graph.py:145-155: stable argsort by target of arcs listed by ascending source).
+__global__ void k_transpose_keys(int64_t n, const int64_t *__restrict__ off,
+                                 const int32_t *__restrict__ succ, uint64_t *__restrict__ keys) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t u = warp; u < n; u += nwarps) {
+    const int64_t b0 = __ldg(off + u), b1 = __ldg(off + u + 1);
+    for (int64_t k = b0 + lane; k < b1; k += 32)
+      keys[k] = ((uint64_t)(uint32_t)__ldg(succ + k) << 32) | (uint64_t)u;
   }
 }
 
@@ -2728,6 +2876,90 @@ int hb_keys_to_csr(int64_t n, int64_t m, uint64_t *keys, uint64_t *alt, void *te
   if (e != cudaSuccess) return set_err("hb_keys_to_csr count", e);
   k_keys_to_csr<<<grid_for_threads(mu + 1), kThreads, 0, s>>>(n, mu, other, offsets, succ);
   *m_out = mu;
+  return check_launch("k_keys_to_csr");
+}
+
+int hb_gen_degrees(int kind, int64_t n, uint64_t seed, const double *cdf, int64_t cdf_len,
+                   int64_t kmin, int64_t *deg, void *stream) {
+  DevGuard dg_((cudaStream_t)stream);
+  if (n <= 0) return 0;
+  if ((kind != GG_ER && kind != GG_DISC && kind != GG_WEB) || !cdf || cdf_len < 1 || !deg)
+    return set_err_msg("hb_gen_degrees: bad arguments");
+  k_gen_degree<<<grid_for_threads(n), kThreads, 0, (cudaStream_t)stream>>>(kind, n, seed, cdf,
+                                                                           cdf_len, kmin, deg);
+  return check_launch("k_gen_degree");
+}
+
+int hb_gen_blocks(int64_t n, int64_t giant, double geo_p, uint64_t seed, int64_t *size,
+                  int64_t *start, int64_t *lo, int64_t *hi, void *temp, uint64_t *temp_bytes,
+                  void *stream) {
+  DevGuard dg_((cudaStream_t)stream);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!temp_bytes) return set_err_msg("hb_gen_blocks: temp_bytes");
+  const int64_t nb = n > giant ? n - giant : 0;
+  size_t need = 0;
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, need, size, start, nb > 0 ? nb : 1, s);
+  if (e != cudaSuccess) return set_err("hb_gen_blocks scan size", e);
+  if (!temp) {
+    *temp_bytes = need;
+    return 0;
+  }
+  if (n <= 0) return 0;
+  if (!lo || !hi || giant < 0 || !(geo_p > 0.0) || (nb > 0 && (!size || !start)))
+    return set_err_msg("hb_gen_blocks: bad arguments");
+  if (nb > 0) {
+    k_gen_block_sizes<<<grid_for_threads(nb), kThreads, 0, s>>>(nb, seed, geo_p, size);
+    size_t bytes = *temp_bytes;
+    e = cub::DeviceScan::ExclusiveSum(temp, bytes, size, start, nb, s);
+    if (e != cudaSuccess) return set_err("hb_gen_blocks scan", e);
+  }
+  const int64_t g = giant < n ? giant : n;
+  k_gen_block_bounds<<<grid_for_threads(nb > g ? nb : g), kThreads, 0, s>>>(n, g, nb, start,
+                                                                             size, lo, hi);
+  return check_launch("k_gen_block_bounds");
+}
+
+int hb_gen_arc_keys(int kind, int64_t n, uint64_t seed, const int64_t *offsets,
+                    const int64_t *block_lo, const int64_t *block_hi, double p_local,
+                    int64_t window, uint64_t *keys, void *stream) {
+  DevGuard dg_((cudaStream_t)stream);
+  if (n <= 0) return 0;
+  if ((kind != GG_ER && kind != GG_DISC && kind != GG_WEB) || !offsets || !keys ||
+      (kind == GG_DISC && (!block_lo || !block_hi)) || (kind == GG_WEB && window < 1))
+    return set_err_msg("hb_gen_arc_keys: bad arguments");
+  k_gen_arcs<<<grid_for_warps(n), kThreads, 0, (cudaStream_t)stream>>>(
+      kind, n, seed, offsets, block_lo, block_hi, p_local, window, keys);
+  return check_launch("k_gen_arcs");
+}
+
+int hb_transpose_csr(int64_t n, int64_t m, const int64_t *offsets, const int32_t *succ,
+                     uint64_t *keys, uint64_t *alt, void *temp, uint64_t *temp_bytes,
+                     int64_t *out_offsets, int32_t *out_succ, void *stream) {
+  DevGuard dg_((cudaStream_t)stream);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!temp_bytes || n < 0 || m < 0) return set_err_msg("hb_transpose_csr: bad arguments");
+  int bits = 1;
+  while (bits < 32 && ((int64_t)1 << bits) < n) bits++;
+  cub::DoubleBuffer<uint64_t> db(keys, alt);
+  size_t need = 0;
+  cudaError_t e = cub::DeviceRadixSort::SortKeys(nullptr, need, db, m > 0 ? m : 1, 0, 32 + bits, s);
+  if (e != cudaSuccess) return set_err("hb_transpose_csr sort size", e);
+  if (!temp) {
+    *temp_bytes = need;
+    return 0;
+  }
+  if (!out_offsets || (m > 0 && (!offsets || !succ || !keys || !alt || !out_succ)))
+    return set_err_msg("hb_transpose_csr: bad arguments");
+  if (m == 0) {
+    e = cudaMemsetAsync(out_offsets, 0, sizeof(int64_t) * (size_t)(n + 1), s);
+    return e == cudaSuccess ? 0 : set_err("hb_transpose_csr memset", e);
+  }
+  k_transpose_keys<<<grid_for_warps(n), kThreads, 0, s>>>(n, offsets, succ, keys);
+  size_t bytes = *temp_bytes;
+  e = cub::DeviceRadixSort::SortKeys(temp, bytes, db, m, 0, 32 + bits, s);
+  if (e != cudaSuccess) return set_err("hb_transpose_csr sort", e);
+  k_keys_to_csr<<<grid_for_threads(m + 1), kThreads, 0, s>>>(n, m, db.Current(), out_offsets,
+                                                             out_succ);
   return check_launch("k_keys_to_csr");
 }
 

@@ -54,6 +54,39 @@ def rmat_t(scale: int, arcs: int, seed: int, abc=RMAT_ABC, threads: int | None =
     return _collect(graphlib().hbg_rmat(scale, arcs, a, b, c, seed, _threads(threads)))
 
 
+def _keys_to_device_csr(n: int, keys, dev):
+    """hb_keys_to_csr on transpose keys (dst << 32 | src, self-loops ~0): sort, dedup,
+    CSR -- graph.py:52-80's normalisation on the device.  Consumes `keys`."""
+    import torch
+
+    from ._lib import check, hb
+    from .graph import DeviceCsrGraph
+    L = hb()
+    stream = torch.cuda.current_stream(dev)
+    m = keys.numel()
+    with torch.cuda.device(dev):
+        alt = torch.empty(m, dtype=torch.int64, device=dev)
+        tb = ctypes.c_uint64(0)
+        mo = ctypes.c_int64(0)
+        check(L.hb_keys_to_csr(n, m, keys.data_ptr(), alt.data_ptr(), None, ctypes.byref(tb),
+                               ctypes.byref(mo), None, None, stream.cuda_stream), "size")
+        temp = torch.empty(max(int(tb.value), 1), dtype=torch.uint8, device=dev)
+        offsets = torch.empty(n + 1, dtype=torch.int64, device=dev)
+        succ = torch.empty(max(m, 1), dtype=torch.int32, device=dev)
+        check(L.hb_keys_to_csr(n, m, keys.data_ptr(), alt.data_ptr(), temp.data_ptr(),
+                               ctypes.byref(tb), ctypes.byref(mo), offsets.data_ptr(),
+                               succ.data_ptr(), stream.cuda_stream), "hb_keys_to_csr")
+        del alt, temp
+        succ = succ[:mo.value].clone()
+    return DeviceCsrGraph(offsets, succ)
+
+
+def _device(device):
+    import torch
+    return torch.device(device) if device is not None else torch.device(
+        "cuda", torch.cuda.current_device())
+
+
 def rmat_t_device(scale: int, arcs: int, seed: int, abc=RMAT_ABC, device=None):
     """rmat_t built on the GPU (hb_gen_rmat_keys + hb_keys_to_csr): the same bytes as the
     host builder (tests pin the digest), as a DeviceCsrGraph.  Peak device memory is about
@@ -61,33 +94,106 @@ def rmat_t_device(scale: int, arcs: int, seed: int, abc=RMAT_ABC, device=None):
     import torch
 
     from ._lib import check, hb
-    from .graph import DeviceCsrGraph
-
-    dev = torch.device(device) if device is not None else torch.device(
-        "cuda", torch.cuda.current_device())
+    dev = _device(device)
     a, b, c = abc
     thr = [int(a * 4294967296.0), int((a + b) * 4294967296.0), int((a + b + c) * 4294967296.0)]
     n = 1 << scale
-    L = hb()
     stream = torch.cuda.current_stream(dev)
     with torch.cuda.device(dev):
         keys = torch.empty(arcs, dtype=torch.int64, device=dev)
-        alt = torch.empty(arcs, dtype=torch.int64, device=dev)
-        check(L.hb_gen_rmat_keys(scale, arcs, thr[0], thr[1], thr[2], seed, keys.data_ptr(),
-                                 stream.cuda_stream), "hb_gen_rmat_keys")
+        check(hb().hb_gen_rmat_keys(scale, arcs, thr[0], thr[1], thr[2], seed, keys.data_ptr(),
+                                    stream.cuda_stream), "hb_gen_rmat_keys")
+    return _keys_to_device_csr(n, keys, dev)
+
+
+_GG_ER, _GG_DISC, _GG_WEB = 1, 3, 4
+
+
+def _degree_law_device(kind: int, n: int, seed: int, dev, mean: float = 0.0,
+                       alpha: float = 0.0, kmin: int = 0, kmax: int = 0):
+    """Per-source out-degrees drawn on the device from graphgen.c's own CDF tables, and
+    their exclusive prefix sum (int64 [n+1])."""
+    import torch
+
+    from ._lib import check, hb
+    G = graphlib()
+    if kind == _GG_WEB:
+        tab = np.empty(kmax - kmin + 1, dtype=np.float64)
+        G.hbg_zipf_cdf(float(alpha), kmin, kmax, tab.ctypes.data_as(ctypes.c_void_p))
+    else:
+        tab = np.empty(256, dtype=np.float64)
+        tab = tab[:G.hbg_poisson_cdf(float(mean), tab.ctypes.data_as(ctypes.c_void_p))].copy()
+    stream = torch.cuda.current_stream(dev)
+    cdf = torch.from_numpy(tab).to(dev)
+    deg = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    check(hb().hb_gen_degrees(kind, n, seed, cdf.data_ptr(), tab.size, kmin, deg.data_ptr(),
+                              stream.cuda_stream), "hb_gen_degrees")
+    deg[n] = 0
+    off = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+    torch.cumsum(deg[:n], 0, out=off[1:])
+    return off
+
+
+def _arcs_device(kind, n, seed, off, dev, blo=None, bhi=None, p_local=0.0, window=1):
+    import torch
+
+    from ._lib import check, hb
+    m = int(off[-1].item())
+    stream = torch.cuda.current_stream(dev)
+    keys = torch.empty(max(m, 1), dtype=torch.int64, device=dev)[:m]
+    check(hb().hb_gen_arc_keys(kind, n, seed, off.data_ptr(),
+                               blo.data_ptr() if blo is not None else None,
+                               bhi.data_ptr() if bhi is not None else None, float(p_local),
+                               int(window), keys.data_ptr(), stream.cuda_stream),
+          "hb_gen_arc_keys")
+    return _keys_to_device_csr(n, keys, dev)
+
+
+def erdos_renyi_t_device(n: int, mean_degree: float, seed: int, device=None):
+    """erdos_renyi_t built on the GPU (same bytes as the host builder)."""
+    import torch
+    dev = _device(device)
+    with torch.cuda.device(dev):
+        off = _degree_law_device(_GG_ER, n, seed, dev, mean=mean_degree)
+        return _arcs_device(_GG_ER, n, seed, off, dev)
+
+
+def disconnected_t_device(n: int, giant: int, geo_p: float, mean_degree: float, seed: int,
+                          device=None):
+    """disconnected_t built on the GPU (same bytes as the host builder): block sizes drawn
+    for every possible block in parallel, prefix-summed into block bounds."""
+    import torch
+
+    from ._lib import check, hb
+    dev = _device(device)
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream(dev)
+        nb = max(n - giant, 0)
+        size = torch.empty(max(nb, 1), dtype=torch.int64, device=dev)
+        start = torch.empty(max(nb, 1), dtype=torch.int64, device=dev)
+        blo = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+        bhi = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
         tb = ctypes.c_uint64(0)
-        mo = ctypes.c_int64(0)
-        check(L.hb_keys_to_csr(n, arcs, keys.data_ptr(), alt.data_ptr(), None, ctypes.byref(tb),
-                               ctypes.byref(mo), None, None, stream.cuda_stream), "size")
-        temp = torch.empty(int(tb.value), dtype=torch.uint8, device=dev)
-        offsets = torch.empty(n + 1, dtype=torch.int64, device=dev)
-        succ = torch.empty(arcs, dtype=torch.int32, device=dev)
-        check(L.hb_keys_to_csr(n, arcs, keys.data_ptr(), alt.data_ptr(), temp.data_ptr(),
-                               ctypes.byref(tb), ctypes.byref(mo), offsets.data_ptr(),
-                               succ.data_ptr(), stream.cuda_stream), "hb_keys_to_csr")
-        del keys, alt, temp
-        succ = succ[:mo.value].clone()
-    return DeviceCsrGraph(offsets, succ)
+        check(hb().hb_gen_blocks(n, giant, float(geo_p), seed, size.data_ptr(), start.data_ptr(),
+                                 blo.data_ptr(), bhi.data_ptr(), None, ctypes.byref(tb),
+                                 stream.cuda_stream), "hb_gen_blocks(size)")
+        temp = torch.empty(max(int(tb.value), 1), dtype=torch.uint8, device=dev)
+        check(hb().hb_gen_blocks(n, giant, float(geo_p), seed, size.data_ptr(), start.data_ptr(),
+                                 blo.data_ptr(), bhi.data_ptr(), temp.data_ptr(),
+                                 ctypes.byref(tb), stream.cuda_stream), "hb_gen_blocks")
+        del size, start, temp
+        off = _degree_law_device(_GG_DISC, n, seed, dev, mean=mean_degree)
+        return _arcs_device(_GG_DISC, n, seed, off, dev, blo, bhi)
+
+
+def weblike_t_device(n: int, seed: int, alpha: float = 2.1, kmin: int = 3, kmax: int = 10_000,
+                     p_local: float = 0.8, window: int = 1024, device=None):
+    """weblike_t built on the GPU (same bytes as the host builder)."""
+    import torch
+    dev = _device(device)
+    with torch.cuda.device(dev):
+        off = _degree_law_device(_GG_WEB, n, seed, dev, alpha=alpha, kmin=kmin, kmax=kmax)
+        return _arcs_device(_GG_WEB, n, seed, off, dev, p_local=p_local, window=window)
 
 
 def disconnected_t(n: int, giant: int, geo_p: float, mean_degree: float, seed: int,
@@ -127,8 +233,8 @@ class BenchConfig:
         return BUILDERS[self.name](threads)
 
     def build_device(self, device=None):
-        """GPU-built graph where a device builder exists (R-MAT configs), else the host
-        graph (the engine uploads it)."""
+        """The graph built on the GPU (every config has a device builder producing the
+        host builder's bytes), as a DeviceCsrGraph."""
         if self.name in DEVICE_BUILDERS:
             return DEVICE_BUILDERS[self.name](device)
         return self.build()
@@ -145,6 +251,10 @@ BUILDERS = {
 }
 
 DEVICE_BUILDERS = {
+    "config1": lambda dev=None: erdos_renyi_t_device(10_000, 8.0, seed=0, device=dev),
+    "config3": lambda dev=None: disconnected_t_device(1 << 22, 1 << 21, 0.1, 6.0, seed=2,
+                                                      device=dev),
+    "config4": lambda dev=None: weblike_t_device(1 << 24, seed=3, device=dev),
     "config2": lambda dev=None: rmat_t_device(20, 16 << 20, seed=1, device=dev),
     "config5": lambda dev=None: rmat_t_device(28, 1 << 32, seed=4, device=dev),
     "config5s": lambda dev=None: rmat_t_device(24, 1 << 28, seed=4, device=dev),

@@ -111,8 +111,53 @@ class DeviceCsrGraph:
         return f"DeviceCsrGraph(n={self.n}, m={self.m}, device={self.offsets.device})"
 
 
+def transpose_device(g, device=None) -> DeviceCsrGraph:
+    """transpose (graph.py:145-155) on the GPU: every arc reversed, duplicates and
+    self-loops kept, each new row listing its sources in ascending order -- the
+    reference's stable argsort by target, as one radix sort of (target << 32 | source)
+    keys (hb_transpose_csr).  Accepts a host or device CSR; returns a DeviceCsrGraph."""
+    import ctypes
+
+    import torch
+
+    from ._lib import check, hb
+    if isinstance(g.offsets, torch.Tensor) and g.offsets.is_cuda:
+        dev = g.offsets.device
+    else:
+        dev = torch.device(device) if device is not None else torch.device(
+            "cuda", torch.cuda.current_device())
+    with torch.cuda.device(dev):
+        def up(a, dt):
+            if isinstance(a, torch.Tensor):
+                return a.to(device=dev, dtype=dt).contiguous()
+            return torch.from_numpy(np.ascontiguousarray(a)).to(dev).to(dt)
+        off = up(g.offsets, torch.int64)
+        suc = up(g.successors, torch.int32)
+        n, m = off.numel() - 1, suc.numel()
+        stream = torch.cuda.current_stream(dev)
+        keys = torch.empty(max(m, 1), dtype=torch.int64, device=dev)
+        alt = torch.empty(max(m, 1), dtype=torch.int64, device=dev)
+        tb = ctypes.c_uint64(0)
+        L = hb()
+        check(L.hb_transpose_csr(n, m, off.data_ptr(), suc.data_ptr(), keys.data_ptr(),
+                                 alt.data_ptr(), None, ctypes.byref(tb), None, None,
+                                 stream.cuda_stream), "hb_transpose_csr(size)")
+        temp = torch.empty(max(int(tb.value), 1), dtype=torch.uint8, device=dev)
+        out_off = torch.empty(n + 1, dtype=torch.int64, device=dev)
+        out_suc = torch.empty(max(m, 1), dtype=torch.int32, device=dev)
+        check(L.hb_transpose_csr(n, m, off.data_ptr(), suc.data_ptr(), keys.data_ptr(),
+                                 alt.data_ptr(), temp.data_ptr(), ctypes.byref(tb),
+                                 out_off.data_ptr(), out_suc.data_ptr(), stream.cuda_stream),
+              "hb_transpose_csr")
+        del keys, alt, temp
+    return DeviceCsrGraph(out_off, out_suc[:m])
+
+
 def transpose(g) -> CsrGraph:
-    """Reverse every arc; the result is normalised (sorted rows)."""
+    """Reverse every arc; the result is normalised (sorted rows).  A DeviceCsrGraph is
+    transposed on its device (transpose_device)."""
+    if isinstance(g, DeviceCsrGraph):
+        return transpose_device(g)
     n = int(np.asarray(g.offsets).size - 1)
     deg = np.diff(np.asarray(g.offsets, dtype=np.int64))
     src = np.repeat(np.arange(n, dtype=np.int64), deg)

@@ -333,3 +333,35 @@ def test_oracle_carries_identical_graph_builders():
     assert out[0] == gen.graph_digest(gen.BUILDERS["config1"]())
     assert out[1] == gen.graph_digest(gen.weblike_t(1 << 14, seed=3))
     assert out[2] == gen.graph_digest(gen.disconnected_t(1 << 14, 1 << 13, 0.1, 6.0, seed=2))
+
+
+def _tgold():
+    z = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden",
+                             "transpose.npz"))
+    return z, [str(x) for x in z["names"]]
+
+
+def test_transpose_matches_reference_fixtures():
+    """graph.transpose (host) == the reference's transpose (graph.py:145-155) on forward
+    graphs with duplicate arcs, self-loops and empty rows (tests/golden/transpose.npz)."""
+    z, names = _tgold()
+    for nm in names:
+        g = hb.CsrGraph(z[f"{nm}/offsets"], z[f"{nm}/successors"])
+        t = hb.transpose(g)
+        assert np.array_equal(np.asarray(t.offsets, np.int64), z[f"{nm}/t_offsets"]), nm
+        assert np.array_equal(np.asarray(t.successors, np.int64), z[f"{nm}/t_successors"]), nm
+
+
+def test_arc_list_builder_matches_reference_from_edges():
+    """generators.from_arcs_t (graphgen.c: transpose + normalise an arc list, self-loops
+    dropped) == the reference's transpose(from_edges(...)) of the self-loop-free arcs."""
+    z, names = _tgold()
+    for nm in names:
+        if f"{nm}/arcs_src" not in z:
+            continue
+        src, dst = z[f"{nm}/arcs_src"], z[f"{nm}/arcs_dst"]
+        n = int(z[f"{nm}/from_edges_offsets"].size - 1)
+        g = gen.from_arcs_t(n, src, dst)
+        assert np.array_equal(np.asarray(g.offsets, np.int64), z[f"{nm}/noloop_t_offsets"]), nm
+        assert np.array_equal(np.asarray(g.successors, np.int64),
+                              z[f"{nm}/noloop_t_successors"]), nm

@@ -45,6 +45,40 @@ __global__ void k_gather(const uint4 *__restrict__ src, uint4 *__restrict__ dst,
     dst[i] = __ldg(src + bij(i, n - 1));
 }
 
+// random gather with different load flavours (mode: 0 ld.global.nc, 1 ld.global.cs,
+// 2 ld.global.lu, 3 ld.global.cv, 4 ld.global.nc.L2::cache_hint evict_first,
+// 5 ld.global.nc.L1::no_allocate.L2::64B (prefetch-size hint), 6 ld.volatile.global,
+// 7 two 8-byte loads)
+template <int MODE>
+__device__ __forceinline__ uint4 ldm(const uint4 *p, uint64_t pol) {
+  uint4 r;
+  if (MODE == 0) asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  if (MODE == 1) asm volatile("ld.global.cs.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  if (MODE == 2) asm volatile("ld.global.lu.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  if (MODE == 3) asm volatile("ld.global.cv.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  if (MODE == 4) asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(pol));
+  if (MODE == 5) asm volatile("ld.global.nc.L1::no_allocate.L2::64B.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  if (MODE == 6) asm volatile("ld.global.nc.L2::64B.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  if (MODE == 7) asm volatile("ld.global.L2::64B.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  if (MODE == 8) asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  if (MODE == 9) asm volatile("ld.global.nc.L2::128B.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  if (MODE == 10) asm volatile("ld.global.nc.L2::cache_hint.L2::64B.v4.u32 {%0,%1,%2,%3}, [%4], %5;" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(pol));
+  if (MODE == 11) asm volatile("ld.global.L1::evict_first.L2::64B.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+template <int MODE>
+__global__ void k_gather_m(const uint4 *__restrict__ src, uint4 *__restrict__ dst, uint64_t n) {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  uint32_t acc = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint4 r = ldm<MODE>(src + bij(i, n - 1), pol);
+    acc ^= r.x ^ r.y ^ r.z ^ r.w;
+  }
+  if (acc == 0x1234567u) dst[0].x = acc;
+}
+
 int main(int argc, char **argv) {
   const int lg = argc > 1 ? atoi(argv[1]) : 30;
   const int lrb = argc > 2 ? atoi(argv[2]) : 12;
@@ -61,7 +95,7 @@ int main(int argc, char **argv) {
   cudaEventCreate(&e1);
   const int grid = 148 * 8, th = 256;
   const char *names[4] = {"seq", "scatter", "binned", "gather"};
-  for (int mode = 0; mode < 4; mode++) {
+  for (int mode = (argc > 3 ? 4 : 0); mode < 4; mode++) {
     for (int rep = 0; rep < 3; rep++) {
       cudaEventRecord(e0);
       if (mode == 0) k_seq<<<grid, th>>>(a, b, n);
@@ -76,6 +110,32 @@ int main(int argc, char **argv) {
         printf("%-8s records 2^%d (%.1f GB each way), bin 2^%d: %.3f ms, %.1f G records/s, "
                "%.0f GB/s (read+write)\n", names[mode], lg, n * 16 / 1e9, lrb, ms,
                n / (ms * 1e-3) / 1e9, 2.0 * n * 16 / (ms * 1e-3) / 1e9);
+    }
+  }
+  for (int mode = 0; mode < 12; mode++) {
+    if (mode >= 1 && mode <= 4) continue;
+    for (int rep = 0; rep < 2; rep++) {
+      cudaEventRecord(e0);
+      switch (mode) {
+        case 0: k_gather_m<0><<<grid, th>>>(a, b, n); break;
+        case 1: k_gather_m<1><<<grid, th>>>(a, b, n); break;
+        case 2: k_gather_m<2><<<grid, th>>>(a, b, n); break;
+        case 3: k_gather_m<3><<<grid, th>>>(a, b, n); break;
+        case 4: k_gather_m<4><<<grid, th>>>(a, b, n); break;
+        case 5: k_gather_m<5><<<grid, th>>>(a, b, n); break;
+        case 6: k_gather_m<6><<<grid, th>>>(a, b, n); break;
+        case 7: k_gather_m<7><<<grid, th>>>(a, b, n); break;
+        case 8: k_gather_m<8><<<grid, th>>>(a, b, n); break;
+        case 9: k_gather_m<9><<<grid, th>>>(a, b, n); break;
+        case 10: k_gather_m<10><<<grid, th>>>(a, b, n); break;
+        case 11: k_gather_m<11><<<grid, th>>>(a, b, n); break;
+      }
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (rep == 1)
+        printf("gather-only mode %d: %.3f ms, %.1f G rows/s\n", mode, ms, n / (ms * 1e-3) / 1e9);
     }
   }
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
