@@ -314,7 +314,7 @@ def dense_steps(g, cfgd, local: int, steps: int, warmup: int, schedule: str = "a
             ev0.record(stream)
         _lib.union_step(_lib.StepArgs(
             n=n, lo=s.light_lo, hi=s.light_hi if dev.full_pass else s.light_hi_steady,
-            offsets=s.offsets.data_ptr(), succ=s.succ.data_ptr(), cur=dev.cur.data_ptr(),
+            offsets=s.offsets_ptr(), succ=s.succ.data_ptr(), cur=dev.cur.data_ptr(),
             nxt=dev.nxt.data_ptr(), chg_prev=dev.chg_prev.data_ptr(),
             chg_now=dev.chg_now.data_ptr(), est=dev.est.data_ptr(), b=b, dense=1,
             clear_chg_now=clear, t=1, lc_table=dev.lc.data_ptr(), alpha_p2=dev.alpha_p2,

@@ -397,6 +397,10 @@ int hb_transpose_csr(int64_t n, int64_t m, const int64_t *offsets, const int32_t
                      uint64_t *keys, uint64_t *alt, void *temp, uint64_t *temp_bytes,
                      int64_t *out_offsets, int32_t *out_succ, void *stream);
 
+/* out[k] = rank[ids[k]] for k < m (device int32 arrays; out may alias ids): a rank-local
+ * CSR's ids relabelled into the internal order (multi-GPU). */
+int hb_map_ids(int64_t m, const int32_t *ids, const int32_t *rank, int32_t *out, void *stream);
+
 /* out[i] = hash_items(items[i], replicas[i], seed) (hll.py:79-88), device arrays. */
 int hb_hash_items(int64_t n, const uint64_t *items, const uint64_t *replicas, uint64_t seed,
                   uint64_t *out, void *stream);

@@ -75,6 +75,7 @@ HB_SIGNATURES = {
     "hb_gen_rmat_keys": (_int, [_int, _i64, _u64, _u64, _u64, _u64, _vp, _vp]),
     "hb_keys_to_csr": (_int, [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "hb_hash_items": (_int, [_i64, _vp, _vp, _u64, _vp, _vp]),
+    "hb_map_ids": (_int, [_i64, _vp, _vp, _vp, _vp]),
     "hb_gen_degrees": (_int, [_int, _i64, _u64, _vp, _i64, _i64, _vp, _vp]),
     "hb_gen_blocks": (_int, [_i64, _i64, _dbl, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "hb_gen_arc_keys": (_int, [_int, _i64, _u64, _vp, _vp, _vp, _dbl, _i64, _vp, _vp]),
@@ -134,6 +135,7 @@ GRAPH_SIGNATURES = {
     "hbg_from_arcs": (_vp, [_i64, _i64, _vp, _vp, _int]),
     "hbg_poisson_cdf": (_int, [_dbl, _vp]),
     "hbg_zipf_cdf": (None, [_dbl, _i64, _i64, _vp]),
+    "hbg_gather_rows": (_i64, [_vp, _vp, _int, _vp, _i64, _vp, _vp, _int]),
     "hbg_n": (_i64, [_vp]),
     "hbg_m": (_i64, [_vp]),
     "hbg_copy": (None, [_vp, _vp, _vp]),

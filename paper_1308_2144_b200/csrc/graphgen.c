@@ -419,6 +419,50 @@ void hbg_zipf_cdf(double alpha, int64_t kmin, int64_t kmax, double *out) {
     free(z.cdf);
 }
 
+/* Rank-local CSR for multi-GPU runs: rows[i] (old row ids, int32
+ * [nrows]) of a host CSR (offsets int64 [n+1], successors int32 or int64 by
+ * succ_bytes = 4 / 8) packed into out_off (int64 [nrows+1], local positions) and out
+ * (int32, narrowed ids), so each rank uploads only the ~m/W ids of the rows it owns. */
+typedef struct {
+    const int64_t *off;
+    const void *succ;
+    int succ_bytes;
+    const int32_t *rows;
+    const int64_t *out_off;
+    int32_t *out;
+} gather_ctx;
+
+static void gather_fn(void *ctx, int64_t lo, int64_t hi, int tid) {
+    (void)tid;
+    gather_ctx *c = (gather_ctx *)ctx;
+    for (int64_t i = lo; i < hi; i++) {
+        const int64_t r = c->rows[i], b = c->off[r], len = c->off[r + 1] - b;
+        int32_t *dst = c->out + c->out_off[i];
+        if (c->succ_bytes == 4) {
+            memcpy(dst, (const int32_t *)c->succ + b, sizeof(int32_t) * (size_t)len);
+        } else {
+            const int64_t *src = (const int64_t *)c->succ + b;
+            for (int64_t k = 0; k < len; k++) dst[k] = (int32_t)src[k];
+        }
+    }
+}
+
+int64_t hbg_gather_rows(const int64_t *off, const void *succ, int succ_bytes,
+                        const int32_t *rows, int64_t nrows, int64_t *out_off, int32_t *out,
+                        int threads) {
+    if (threads <= 0) threads = nthreads_default();
+    int64_t acc = 0;
+    for (int64_t i = 0; i < nrows; i++) {
+        out_off[i] = acc;
+        acc += off[rows[i] + 1] - off[rows[i]];
+    }
+    out_off[nrows] = acc;
+    if (out == NULL) return acc;            /* size query */
+    gather_ctx c = {off, succ, succ_bytes, rows, out_off, out};
+    parallel_for(nrows, threads, gather_fn, &c);
+    return acc;
+}
+
 int64_t hbg_n(void *h) { return ((hbg_graph *)h)->n; }
 int64_t hbg_m(void *h) { return ((hbg_graph *)h)->m; }
 void hbg_copy(void *h, int64_t *offsets, int32_t *succ) {

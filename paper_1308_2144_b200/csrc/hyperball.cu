@@ -1965,6 +1965,13 @@ __global__ void k_relabel_src(int64_t o0, int64_t o1, const int64_t *__restrict_
   }
 }
 
+__global__ void k_map_ids(int64_t m, const int32_t *ids, const int32_t *__restrict__ rank,
+                          int32_t *out) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m;
+       k += (int64_t)gridDim.x * blockDim.x)
+    out[k] = __ldg(rank + ids[k]);
+}
+
 __global__ void k_hash(int64_t n, const uint64_t *__restrict__ items,
                        const uint64_t *__restrict__ replicas, uint64_t seed,
                        uint64_t *__restrict__ out) {
@@ -2999,6 +3006,14 @@ int hb_relabel_csr_src_rows(int64_t n, int64_t o0, int64_t o1, const int64_t *ol
   k_relabel_src<<<grid_for_warps(o1 - o0), kThreads, 0, (cudaStream_t)stream>>>(
       o0, o1, old_offsets, old_succ, rank, new_offsets, new_succ);
   return check_launch("k_relabel_src");
+}
+
+int hb_map_ids(int64_t m, const int32_t *ids, const int32_t *rank, int32_t *out, void *stream) {
+  DevGuard dg_((cudaStream_t)stream);
+  if (m <= 0) return 0;
+  if (!ids || !rank || !out) return set_err_msg("hb_map_ids: bad arguments");
+  k_map_ids<<<grid_for_threads(m), kThreads, 0, (cudaStream_t)stream>>>(m, ids, rank, out);
+  return check_launch("k_map_ids");
 }
 
 int hb_hash_items(int64_t n, const uint64_t *items, const uint64_t *replicas, uint64_t seed,

@@ -359,6 +359,8 @@ class _Device:
             def early(perm):
                 self._launch_seed(seed_weights, perm)
         self._build_graph(g, on_order=early)
+        if self.sched.local:
+            self.frontier = False        # frontier marking scans every row's ids
         if early is not None:
             self._after_seed()
 
@@ -577,7 +579,7 @@ class _Device:
             cnt = self.counts if len(parts) == 1 else self.slice_counts[k]
             disc, disc_stride, n_disc, disc_scale, disc_div = dargs
             _lib.union_step(_lib.StepArgs(
-                n=self.n, lo=lo, hi=hi, offsets=s.offsets.data_ptr(),
+                n=self.n, lo=lo, hi=hi, offsets=s.offsets_ptr(),
                 succ=s.succ_buf.data_ptr(), cur=self.cur.data_ptr(), nxt=self.nxt.data_ptr(),
                 chg_prev=self.chg_prev.data_ptr(), chg_now=self.chg_now.data_ptr(),
                 est=self.est.data_ptr(), b=self.b, dense=int(dense),

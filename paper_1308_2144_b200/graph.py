@@ -15,6 +15,7 @@ can be exchanged with the reference CLI.
 from __future__ import annotations
 
 import struct
+import warnings
 from pathlib import Path
 
 import numpy as np
@@ -130,7 +131,9 @@ def transpose_device(g, device=None) -> DeviceCsrGraph:
         def up(a, dt):
             if isinstance(a, torch.Tensor):
                 return a.to(device=dev, dtype=dt).contiguous()
-            return torch.from_numpy(np.ascontiguousarray(a)).to(dev).to(dt)
+            with warnings.catch_warnings():      # read-only host arrays are only copied
+                warnings.simplefilter("ignore", UserWarning)
+                return torch.from_numpy(np.ascontiguousarray(a)).to(dev).to(dt)
         off = up(g.offsets, torch.int64)
         suc = up(g.successors, torch.int32)
         n, m = off.numel() - 1, suc.numel()

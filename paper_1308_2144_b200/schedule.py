@@ -62,6 +62,16 @@ class Schedule:
     pending: list = field(default_factory=list)
     relabel: tuple | None = None
     stream: object = None
+    # Rank-local CSR (multi-GPU): `offsets` / `succ_buf` hold only the rows [lo, hi) this
+    # rank owns (offsets[i] is the local position of row lo + i); kernels index offsets by
+    # global internal id through offsets_ptr() (base shifted by lo rows), which is valid
+    # for every id they touch (the owned rows).  Passes over every row (frontier marking,
+    # forward graph) are not available on a local CSR.
+    row_base: int = 0
+    local: bool = False
+
+    def offsets_ptr(self) -> int:
+        return self.offsets.data_ptr() - 8 * self.row_base
 
     @property
     def succ(self) -> torch.Tensor:
@@ -215,6 +225,10 @@ def _as_device(a, dtype, device) -> torch.Tensor:
     return t.to(device=device, non_blocking=True).to(dtype)
 
 
+# multi-GPU ranks hold only their own rows' successor ids (build_rank_local);
+# HB_RANK_LOCAL=0 uploads the whole CSR to every rank (round-1 behaviour)
+RANK_LOCAL = bool(int(os.environ.get("HB_RANK_LOCAL", "1")))
+
 WINDOW_MIN_NODES = 1 << 23
 # Re-sorting the rows after the degree relabel (hb_sort_rows) makes a hub's consecutive
 # arcs read neighbouring register rows: 1-4% off a dense iteration (config 5s 1.80 ->
@@ -285,6 +299,135 @@ def partition_bounds(n: int, world: int):
     return bounds
 
 
+def _deal_order(deg: torch.Tensor, order: str, b: int, bounds, max_deg: int, world: int):
+    """Internal order (perm: internal id -> old row) of the schedule, or None (identity)."""
+    n = deg.numel()
+    if order == "window" and n > 0:
+        return window_order(deg, b, bounds, max_deg)
+    if order == "degree" and n > 0:
+        srt = torch.sort(deg, descending=True, stable=True).indices
+        if world > 1:
+            # deal the degree ranking round-robin: rank r gets ranks r, r+W, r+2W, ...
+            # (bounds[r+1]-bounds[r] of them), each slice still in descending degree.
+            srt = torch.cat([srt[r::world] for r in range(world)])
+        return srt
+    return None
+
+
+def _heavy_items(deg_loc: torch.Tensor, off_loc: torch.Tensor, lo: int, light_max_deg: int,
+                 item_arcs: int, device):
+    """Heavy nodes of rows [lo, lo + len(deg_loc)) (global internal ids) and their work
+    items; off_loc[i] is the (local or global) position of row lo + i."""
+    heavy_l = torch.nonzero(deg_loc > light_max_deg).squeeze(1)
+    heavy = heavy_l + lo
+    cnt = (deg_loc[heavy_l] + item_arcs - 1) // item_arcs
+    item_first = torch.zeros(heavy.numel() + 1, dtype=torch.int64, device=device)
+    if heavy.numel():
+        torch.cumsum(cnt, 0, out=item_first[1:])
+    n_items = int(item_first[-1].item())
+    owner = torch.repeat_interleave(torch.arange(heavy.numel(), device=device), cnt)
+    item_node = heavy[owner]
+    item_beg = (off_loc[heavy_l[owner]]
+                + (torch.arange(n_items, device=device) - item_first[owner]) * item_arcs)
+    mega = cnt > MEGA_ITEMS
+    finish_order = torch.cat([torch.nonzero(mega).squeeze(1),
+                              torch.nonzero(~mega).squeeze(1)]).to(torch.int32)
+    return heavy, item_first, n_items, item_node, item_beg, finish_order, int(mega.sum().item())
+
+
+def build_rank_local(offsets, successors, b: int, device, order: str, world: int,
+                     rank_id: int, s_main, on_order=None) -> Schedule:
+    """Schedule of one rank of a multi-GPU run with a RANK-LOCAL CSR: the full offsets are
+    uploaded (the node order needs every in-degree), but only the successor ids of the
+    rows this rank owns -- ~m/W of them -- cross PCIe (gathered on the host by
+    hbg_gather_rows into pinned memory), or, for a graph already on the device, are
+    gathered there.  Ids are relabelled into the internal order (hashes still use the
+    original ids, so registers are bit-identical)."""
+    L = _lib.hb()
+    off = _as_device(offsets, torch.int64, device)
+    n = off.numel() - 1
+    bounds = partition_bounds(n, world)
+    lo, hi = bounds[rank_id], bounds[rank_id + 1]
+    light_max_deg = int(L.hb_light_max_deg(b))
+    item_arcs = int(L.hb_item_arcs(b))
+    deg = off[1:] - off[:-1]
+    max_deg = int(deg.max().item()) if n else 0
+    if order == "auto":
+        order = choose_order(max_deg, light_max_deg, n)
+    if order not in ("identity", "degree", "window"):
+        raise ValueError(f"unknown schedule order {order!r}")
+    srt = _deal_order(deg, order, b, bounds, max_deg, world)
+    perm = rank = None
+    if srt is not None:
+        perm = srt.to(torch.int32)
+        rank = torch.empty_like(perm)
+        rank[srt] = torch.arange(n, dtype=torch.int32, device=device)
+    if on_order is not None:
+        on_order(perm)
+    rows = perm[lo:hi] if perm is not None else torch.arange(lo, hi, dtype=torch.int32,
+                                                             device=device)
+    nloc = hi - lo
+    deg_loc = deg[rows.long()] if nloc else deg[:0]
+    off_loc = torch.zeros(nloc + 1, dtype=torch.int64, device=device)
+    if nloc:
+        torch.cumsum(deg_loc, 0, out=off_loc[1:])
+    mloc = int(off_loc[-1].item())
+    succ = torch.empty(max(mloc, 1), dtype=torch.int32, device=device)
+    if isinstance(successors, torch.Tensor) and successors.is_cuda:
+        full = successors.to(torch.int32) if successors.dtype != torch.int32 else successors
+        ident = torch.arange(n, dtype=torch.int32, device=device) if perm is None else None
+        if nloc:
+            # k_relabel over new rows [lo, hi): new row i = old row perm[i], ids mapped
+            # through rank, written at off_loc[i - lo] (offsets base shifted by lo rows)
+            _lib.check(L.hb_relabel_csr_rows(
+                n, lo, hi, off.data_ptr(), full.data_ptr(),
+                (perm if perm is not None else ident).data_ptr(),
+                (rank if rank is not None else ident).data_ptr(),
+                off_loc.data_ptr() - 8 * lo, succ.data_ptr(), s_main.cuda_stream),
+                "hb_relabel_csr_rows")
+    else:
+        hs = np.asarray(successors)
+        if hs.dtype not in (np.int32, np.int64):
+            hs = hs.astype(np.int64)
+        hs = np.ascontiguousarray(hs)
+        ho = np.ascontiguousarray(np.asarray(offsets, dtype=np.int64))
+        rows_h = np.ascontiguousarray(rows.cpu().numpy().astype(np.int32))
+        pin_off = torch.empty(nloc + 1, dtype=torch.int64, pin_memory=True)
+        pin_ids = torch.empty(max(mloc, 1), dtype=torch.int32, pin_memory=True)
+        G = _lib.graphlib()
+        import ctypes
+        vp = ctypes.c_void_p
+        got = G.hbg_gather_rows(vp(ho.ctypes.data), vp(hs.ctypes.data), hs.itemsize,
+                                vp(rows_h.ctypes.data), nloc, vp(pin_off.data_ptr()),
+                                vp(pin_ids.data_ptr()), 0)
+        assert got == mloc, (got, mloc)
+        succ[:mloc].copy_(pin_ids[:mloc], non_blocking=True)
+        if rank is not None and mloc:
+            _lib.check(L.hb_map_ids(mloc, succ.data_ptr(), rank.data_ptr(), succ.data_ptr(),
+                                    s_main.cuda_stream), "hb_map_ids")
+        s_main.synchronize()                      # the pinned staging buffers die here
+    heavy, item_first, n_items, item_node, item_beg, finish_order, n_mega = _heavy_items(
+        deg_loc, off_loc, lo, light_max_deg, item_arcs, device)
+    p = 1 << b
+    partial = torch.empty((max(n_items, 1), p), dtype=torch.uint8, device=device)
+    if order == "degree":
+        n_heavy = int(heavy.numel())
+        n_nonzero = int((deg_loc > 0).sum().item())
+        light_lo, light_hi = lo + n_heavy, hi
+        steady = lo + max(n_nonzero, n_heavy)
+    else:
+        light_lo, light_hi, steady = lo, hi, hi
+    return Schedule(n=n, m=mloc, b=b, order=order, perm=perm, rank=rank, offsets=off_loc,
+                    succ_buf=succ[:mloc], lo=lo, hi=hi, light_lo=light_lo, light_hi=light_hi,
+                    light_hi_steady=steady, light_max_deg=light_max_deg, item_arcs=item_arcs,
+                    heavy_nodes=heavy.to(torch.int32), item_first=item_first.to(torch.int32),
+                    finish_order=finish_order, n_mega=n_mega,
+                    item_node=item_node.to(torch.int32), item_beg=item_beg.contiguous(),
+                    partial=partial, max_deg=max_deg,
+                    hot_rows=n if order == "degree" else 0, stream=s_main, row_base=lo,
+                    local=True)
+
+
 def build_schedule(offsets, successors, b: int, device, order: str = "auto", world: int = 1,
                    rank_id: int = 0, stream=None, on_order=None) -> Schedule:
     """Upload the CSR of G^T, relabel it into schedule order and split the heavy nodes of
@@ -296,6 +439,9 @@ def build_schedule(offsets, successors, b: int, device, order: str = "auto", wor
     overlaps the rest of the upload (the engine seeds the counters there)."""
     L = _lib.hb()
     s_main = stream if stream is not None else torch.cuda.current_stream(device)
+    if world > 1 and RANK_LOCAL:
+        return build_rank_local(offsets, successors, b, device, order, world, rank_id,
+                                s_main, on_order)
     off = _as_device(offsets, torch.int64, device)
     slices = None
     if (world == 1 and STREAM_SLICES > 1 and not isinstance(successors, torch.Tensor)

@@ -194,3 +194,50 @@ def test_simulated_ranks_fused_discounts(key, world, exchange):
         assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), spec.name
     assert np.array_equal(hb.finalize_harmonic(acc).view(np.uint64),
                           arrays[f"{key}/harmonic"].view(np.uint64))
+
+
+@pytest.mark.parametrize("on_device", [False, True])
+@pytest.mark.parametrize("schedule", ["identity", "degree", "window"])
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_rank_local_csr(world, schedule, on_device):
+    """Every rank holds only the successor ids of the rows it owns (~m/W, uploaded or
+    gathered alone), ids in the internal order; the union over ranks is the graph, and the
+    simulated-rank run stays bit-identical to the reference."""
+    import torch
+    from paper_1308_2144_b200.distributed import CudaRankState
+    from paper_1308_2144_b200.schedule import partition_bounds
+    case = CASES["rmat12_b7_s42_w5"]
+    off, suc = golden_graph(case)
+    g = (hb.DeviceCsrGraph(torch.from_numpy(off).cuda(),
+                           torch.from_numpy(suc.astype(np.int32)).cuda())
+         if on_device else hb.CsrGraph(off, suc))
+    cfg = hb.HyperBallConfig(params=hb.CounterParams(b=case["b"], seed=int(case["seed"])),
+                             schedule=schedule)
+    states = [CudaRankState(g, cfg, world, r) for r in range(world)]
+    bounds = partition_bounds(g.n, world)
+    deg = np.diff(off)
+    total = 0
+    for r, st in enumerate(states):
+        s = st.dev.sched
+        assert s.local and s.row_base == bounds[r] and s.lo == bounds[r]
+        assert s.offsets.numel() == bounds[r + 1] - bounds[r] + 1
+        perm = (s.perm.cpu().numpy() if s.perm is not None
+                else np.arange(g.n, dtype=np.int32))
+        rank = np.empty(g.n, np.int64)
+        rank[perm] = np.arange(g.n)
+        mine = perm[bounds[r]:bounds[r + 1]]
+        assert s.m == int(deg[mine].sum())                  # only this rank's arcs
+        lo_off = s.offsets.cpu().numpy()
+        ids = s.succ.cpu().numpy()
+        for i in range(0, mine.size, max(1, mine.size // 50)):
+            row = np.sort(ids[lo_off[i]:lo_off[i + 1]])
+            want = np.sort(rank[suc[off[mine[i]]:off[mine[i] + 1]]])
+            assert np.array_equal(row, want)
+        total += s.m
+    assert total == int(off[-1])
+    del states
+    acc = hb.CentralityAccumulator(g.n)
+    res = run_simulated(g, cfg, world, [acc])
+    assert res.t == case["t"]
+    for regs in res.registers:
+        assert sha(regs) == case["reg_digests"][-1]
