@@ -62,10 +62,10 @@ class Schedule:
     pending: list = field(default_factory=list)
     relabel: tuple | None = None
     stream: object = None
-    # Rank-local CSR (multi-GPU): `offsets` / `succ_buf` hold only the rows [lo, hi) this
-    # rank owns (offsets[i] is the local position of row lo + i); kernels index offsets by
-    # global internal id through offsets_ptr() (base shifted by lo rows), which is valid
-    # for every id they touch (the owned rows).  Passes over every row (frontier marking,
+    # Rank-local CSR (multi-GPU): `offsets` / `succ_buf` hold only the rows this rank owns
+    # (offsets[i] is the local position of row row_base + i; rows row_base..lo-1 are
+    # empty padding); kernels index offsets by global internal id through offsets_ptr()
+    # (base shifted by row_base rows), valid for every id they touch.  Passes over every row (frontier marking,
     # forward graph) are not available on a local CSR.
     row_base: int = 0
     local: bool = False
@@ -368,7 +368,13 @@ def build_rank_local(offsets, successors, b: int, device, order: str, world: int
                                                              device=device)
     nloc = hi - lo
     deg_loc = deg[rows.long()] if nloc else deg[:0]
-    off_loc = torch.zeros(nloc + 1, dtype=torch.int64, device=device)
+    # offsets of rows [base, hi], base = lo rounded down to 64 rows: the light kernel
+    # aligns its warp rounds (and its L2 prefetch of the offsets) below lo; those leading
+    # rows are empty here and never valid there
+    base = (lo // 64) * 64
+    pad = lo - base
+    off_pad = torch.zeros(pad + nloc + 1, dtype=torch.int64, device=device)
+    off_loc = off_pad[pad:]
     if nloc:
         torch.cumsum(deg_loc, 0, out=off_loc[1:])
     mloc = int(off_loc[-1].item())
@@ -417,14 +423,14 @@ def build_rank_local(offsets, successors, b: int, device, order: str, world: int
         steady = lo + max(n_nonzero, n_heavy)
     else:
         light_lo, light_hi, steady = lo, hi, hi
-    return Schedule(n=n, m=mloc, b=b, order=order, perm=perm, rank=rank, offsets=off_loc,
+    return Schedule(n=n, m=mloc, b=b, order=order, perm=perm, rank=rank, offsets=off_pad,
                     succ_buf=succ[:mloc], lo=lo, hi=hi, light_lo=light_lo, light_hi=light_hi,
                     light_hi_steady=steady, light_max_deg=light_max_deg, item_arcs=item_arcs,
                     heavy_nodes=heavy.to(torch.int32), item_first=item_first.to(torch.int32),
                     finish_order=finish_order, n_mega=n_mega,
                     item_node=item_node.to(torch.int32), item_beg=item_beg.contiguous(),
                     partial=partial, max_deg=max_deg,
-                    hot_rows=n if order == "degree" else 0, stream=s_main, row_base=lo,
+                    hot_rows=n if order == "degree" else 0, stream=s_main, row_base=base,
                     local=True)
 
 
