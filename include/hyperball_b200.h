@@ -187,6 +187,9 @@ typedef struct hb_step_args {
   uint8_t *const *peer_nxt;
   uint32_t *const *peer_chg;
   void *stream;
+  /* bounds for the checked build (libhyperball_b200_checked.so; ignored otherwise):
+   * addressable register rows (0 = n) and successor ids in succ (0 = unchecked) */
+  int64_t check_rows, check_m;
 } hb_step_args;
 
 int hb_union_step_v2(const hb_step_args *args);

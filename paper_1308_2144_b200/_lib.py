@@ -105,6 +105,7 @@ class StepArgs(ctypes.Structure):
         ("n_items", _i64), ("item_arcs", _i64), ("partial", _vp),
         ("nch_out", _vp), ("merged_out", _vp), ("hot_rows", _i64), ("active", _vp),
         ("peer_nxt", _vp), ("peer_chg", _vp), ("stream", _vp),
+        ("check_rows", _i64), ("check_m", _i64),
     ]
 
     def __init__(self, **kw):
@@ -120,7 +121,7 @@ def schedule_args(s) -> dict:
                 finish_order=s.finish_order.data_ptr(), n_mega=s.n_mega,
                 item_node=s.item_node.data_ptr(), item_beg=s.item_beg.data_ptr(),
                 n_items=s.n_items, item_arcs=s.item_arcs, partial=s.partial.data_ptr(),
-                hot_rows=s.hot_rows)
+                hot_rows=s.hot_rows, check_m=int(s.succ_buf.numel()))
 
 
 def union_step(args: StepArgs, what: str = "hb_union_step_v2") -> None:

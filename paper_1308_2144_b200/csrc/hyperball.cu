@@ -52,6 +52,32 @@ int check_launch(const char *what) {
   return 0;
 }
 
+// ------------------------------------------------------------------ checked build
+// HB_CHECKED=1 (make checked -> libhyperball_b200_checked.so) compiles bounds checks into
+// the union kernels: every successor id, CSR position, row index, shared-memory slot and
+// work-item index is tested against the sizes of the step (set per call), and a violation
+// prints the site and traps.  compute-sanitizer is not available on the GPU pool, so this
+// build -- run over tools/sanitize_workload.py -- is the out-of-bounds evidence
+// (profiles/r2_checked_build.md).
+struct CheckDims {
+  int64_t rows;    // register rows addressable (cur / nxt)
+  int64_t m;       // successor ids in succ
+  int64_t items;   // heavy work items (partial rows)
+};
+#ifdef HB_CHECKED
+__device__ CheckDims g_chk;
+#define HB_CHK(cond, what)                                                                   \
+  do {                                                                                      \
+    if (g_chk.rows > 0 && !(cond)) {                                                        \
+      printf("HB_CHECKED violation: %s (%s:%d) block %d thread %d\n", what, __FILE__,       \
+             __LINE__, (int)blockIdx.x, (int)threadIdx.x);                                  \
+      __trap();                                                                             \
+    }                                                                                       \
+  } while (0)
+#else
+#define HB_CHK(cond, what) do { } while (0)
+#endif
+
 // ------------------------------------------------------------------ row geometry
 template <int LOGP>
 struct Geo {
@@ -828,6 +854,8 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
     if (valid) {
       beg = __ldg(offsets + v);
       end = __ldg(offsets + v + 1);
+      HB_CHK(v >= 0 && v < g_chk.rows && 0 <= beg && beg <= end && end <= g_chk.m,
+             "k_light row / offsets");
       if (end - beg > max_deg) {               // heavy: handled by the item path
         valid = false;
         end = beg;
@@ -859,7 +887,9 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
     for (int j = 0; j < B::J; j++) {
       const int64_t k = beg + j * Gm::G + gl;
       idr[j] = (k < end) ? __ldg(succ + k) : -1;
+      HB_CHK(idr[j] < g_chk.rows, "k_light successor id");
     }
+    HB_CHK(fb >= 0 && fb < g_chk.rows, "k_light fallback row");
     // batches of NB ids per group; the loop runs the warp's longest node so that every
     // ballot / shuffle below is full-warp (no per-group serialisation)
     const int trips = (int)((end - beg + B::NB - 1) / B::NB);
@@ -879,6 +909,7 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
         for (int j = 0; j < B::J; j++) {
           const bool act = idr[j] >= 0 && (dense || test_bit(chg_prev, idr[j]));
           const unsigned bal = (__ballot_sync(0xffffffffu, act) >> (grp * Gm::G)) & lowmask;
+          HB_CHK(!act || cnt + __popc(bal & below) < B::NB, "k_light shared id slot");
           if (act) my_ids[cnt + __popc(bal & below)] = idr[j];
           cnt += __popc(bal);
         }
@@ -887,6 +918,7 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
       for (int j = 0; j < B::J; j++) {                // next batch's ids, in flight meanwhile
         const int64_t k = kb + B::NB + j * Gm::G + gl;
         idr[j] = (k < end) ? __ldg(succ + k) : -1;
+        HB_CHK(idr[j] < g_chk.rows, "k_light successor id (next batch)");
       }
       __syncwarp();
       const int cmax = __reduce_max_sync(0xffffffffu, (unsigned)cnt);
@@ -913,6 +945,9 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
             int32_t r[4];
 #pragma unroll
             for (int k = 0; k < 4; k++) r[k] = (i + 4 * h + k < cg) ? gids[i + 4 * h + k] : fbg;
+#pragma unroll
+            for (int k = 0; k < 4; k++) HB_CHK(r[k] >= 0 && r[k] < g_chk.rows, "k_light TMA row");
+            HB_CHK(cg <= B::NB && (g * B::U + 4 * h + 4) <= Gm::NPW * B::U, "k_light TMA slot");
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             tma_gather4(tma_buf + (g * B::U + 4 * h) * Gm::P, &tmap, r[0], r[1], r[2], r[3],
                         tma_bar);
@@ -942,7 +977,9 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
 #pragma unroll
         for (int u = 0; u < B::U; u++) {
           const bool ok = i + u < cnt;
+          HB_CHK(!ok || i + u < B::NB, "k_light shared id read");
           const int32_t w = ok ? my_ids[i + u] : fb;
+          HB_CHK(w >= 0 && w < g_chk.rows, "k_light source row");
 #pragma unroll
           for (int c = 0; c < Gm::CPL; c++)
             r[u][c] = (LOGP >= HB_PAD_MIN_LOGP || ok)
@@ -1020,10 +1057,12 @@ k_heavy_partial(const int64_t *__restrict__ offsets, const int32_t *__restrict__
   uint32_t my_merged = 0;
   for (int64_t it = warp; it < n_items; it += nwarps) {
     const int64_t v = __ldg(item_node + it);
+    HB_CHK(it < g_chk.items && v >= 0 && v < g_chk.rows, "k_heavy_partial item / node");
     if (active && !test_bit(active, v)) continue;   // warp-uniform: one node per item
     const int64_t beg = __ldg(item_beg + it);
     int64_t end = __ldg(offsets + v + 1);
     if (end > beg + item_arcs) end = beg + item_arcs;
+    HB_CHK(0 <= beg && beg <= end && end <= g_chk.m, "k_heavy_partial arc range");
     uint4 acc[Gm::CPL];
     RowAcc<LOGP> macc;
     macc.init();
@@ -1032,6 +1071,7 @@ k_heavy_partial(const int64_t *__restrict__ offsets, const int32_t *__restrict__
     for (int j = 0; j < B::HJ; j++) {
       const int64_t k = beg + j * 32 + lane;
       idr[j] = (k < end) ? ld_stream_id(succ + k) : -1;
+      HB_CHK(idr[j] < g_chk.rows, "k_heavy_partial successor id");
     }
     for (int64_t kb = beg; kb < end; kb += B::HEAVY_IDS) {
       int cnt = 0;
@@ -1063,7 +1103,9 @@ k_heavy_partial(const int64_t *__restrict__ offsets, const int32_t *__restrict__
         for (int u = 0; u < B::U; u++) {
           const int e = i + u * Gm::NPW;
           const bool ok = e < cnt;
+          HB_CHK(!ok || e < B::HEAVY_IDS, "k_heavy_partial shared id read");
           const int32_t w = wids[ok ? e : 0];
+          HB_CHK(w >= 0 && w < g_chk.rows, "k_heavy_partial source row");
 #pragma unroll
           for (int c = 0; c < Gm::CPL; c++)
             r[u][c] = (LOGP >= HB_PAD_MIN_LOGP || ok)
@@ -1129,6 +1171,8 @@ k_heavy_finish(const int32_t *__restrict__ heavy_nodes, const int32_t *__restric
     const int64_t j = valid ? __ldg(order + e) : 0;
     const int64_t v = valid ? __ldg(heavy_nodes + j) : 0;
     const int i0 = valid ? __ldg(item_first + j) : 0, i1 = valid ? __ldg(item_first + j + 1) : 0;
+    HB_CHK(!valid || (v >= 0 && v < g_chk.rows && 0 <= i0 && i0 <= i1 && i1 <= g_chk.items),
+           "k_heavy_finish node / items");
     const int first = mega ? i0 + grp : i0, stride = mega ? Gm::NPW : 1;
     uint4 acc[Gm::CPL];
 #pragma unroll
@@ -2411,6 +2455,17 @@ int hb_union_step_v2(const hb_step_args *a) {
       return set_err("hb_union_step memset chg_now", e);
   }
   if (n == 0) return 0;
+#ifdef HB_CHECKED
+  {
+    int64_t m_arcs = 0;           // the graph's id count: offsets[n] is not known here, so the
+    if (a->check_m > 0) m_arcs = a->check_m;   // caller passes it (0 = unchecked ids range)
+    else m_arcs = INT64_MAX;
+    const CheckDims d{a->check_rows > 0 ? a->check_rows : n, m_arcs, a->n_items};
+    if ((e = cudaMemcpyToSymbolAsync(g_chk, &d, sizeof(d), 0, cudaMemcpyHostToDevice, s)) !=
+        cudaSuccess)
+      return set_err("hb_union_step checked dims", e);
+  }
+#endif
   EstConst ec{a->alpha_p2, a->lc_cut, a->lc_table, a->disc, a->disc_stride, n_disc, a->disc_div,
               {0, 0, 0, 0, 0, 0, 0, 0}};
   for (int k = 0; k < n_disc; k++) ec.disc_scale[k] = a->disc_scale[k];
