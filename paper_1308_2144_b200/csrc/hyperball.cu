@@ -77,6 +77,16 @@ __device__ CheckDims g_chk;
 #else
 #define HB_CHK(cond, what) do { } while (0)
 #endif
+int set_check_dims(int64_t rows, int64_t m, int64_t items, cudaStream_t s) {
+#ifdef HB_CHECKED
+  const CheckDims d{rows, m, items};
+  cudaError_t e = cudaMemcpyToSymbolAsync(g_chk, &d, sizeof(d), 0, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return set_err("checked build: dims", e);
+#else
+  (void)rows; (void)m; (void)items; (void)s;
+#endif
+  return 0;
+}
 
 // ------------------------------------------------------------------ row geometry
 template <int LOGP>
@@ -2455,17 +2465,11 @@ int hb_union_step_v2(const hb_step_args *a) {
       return set_err("hb_union_step memset chg_now", e);
   }
   if (n == 0) return 0;
-#ifdef HB_CHECKED
-  {
-    int64_t m_arcs = 0;           // the graph's id count: offsets[n] is not known here, so the
-    if (a->check_m > 0) m_arcs = a->check_m;   // caller passes it (0 = unchecked ids range)
-    else m_arcs = INT64_MAX;
-    const CheckDims d{a->check_rows > 0 ? a->check_rows : n, m_arcs, a->n_items};
-    if ((e = cudaMemcpyToSymbolAsync(g_chk, &d, sizeof(d), 0, cudaMemcpyHostToDevice, s)) !=
-        cudaSuccess)
-      return set_err("hb_union_step checked dims", e);
-  }
-#endif
+  // checked build: the sizes the kernels' bounds checks use (the graph's id count is not
+  // known here -- offsets live on the device -- so the caller passes it; 0 = unchecked)
+  if (int er = set_check_dims(a->check_rows > 0 ? a->check_rows : n,
+                              a->check_m > 0 ? a->check_m : INT64_MAX, a->n_items, s))
+    return er;
   EstConst ec{a->alpha_p2, a->lc_cut, a->lc_table, a->disc, a->disc_stride, n_disc, a->disc_div,
               {0, 0, 0, 0, 0, 0, 0, 0}};
   for (int k = 0; k < n_disc; k++) ec.disc_scale[k] = a->disc_scale[k];
@@ -2569,6 +2573,7 @@ int hb_union_step_runs(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets
   memset(&peers, 0, sizeof(peers));
   const RunArgs ra{chg_runs, words, run_stride};
   const double tf = (double)t;
+  if (int er = set_check_dims(n, INT64_MAX, n_items, s)) return er;
   int rc = 0;
 #define HB_RUNS_CASE(WB, LR)                                                                   \
   if (wb == WB && log2_runs == LR)                                                             \

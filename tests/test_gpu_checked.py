@@ -29,7 +29,9 @@ def _run(args, timeout=900):
 
 def test_sanitize_workload_clean_under_checked_build():
     r = _run([os.path.join(REPO, "tools", "sanitize_workload.py")])
-    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+    progress = [ln for ln in r.stdout.splitlines() if "HB_CHECKED" not in ln]
+    violations = [ln for ln in r.stdout.splitlines() if "HB_CHECKED" in ln]
+    assert r.returncode == 0, "\n".join(progress[-20:] + violations[:5]) + r.stderr[-2000:]
     assert "sanitize workload ok" in r.stdout
     assert "HB_CHECKED violation" not in r.stdout + r.stderr
 
