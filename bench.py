@@ -249,7 +249,46 @@ def run_reference(args):
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "mapped_repo_libs": mapped_repo_libs(),
     }
+    pkg = None if args.no_reference_package else reference_package_sample(g, cfg, threads)
+    if pkg is not None:
+        line["reference_package"] = pkg
     print(json.dumps(line), flush=True)
+
+
+def reference_package_sample(g, cfgd, threads: int):
+    """The reference package itself (numba kernels, hyperball from baseline/_ref -- the one
+    offline install of /root/reference/pkg) on the same graph: initialize, one untimed
+    iteration (numba compile), then two timed dense iterations of its own iterate()
+    (engine.py:362-399) with a CentralityAccumulator and os.cpu_count() workers.  Reported
+    beside the arm's value (the C port, which runs at or above numba speed) for
+    transparency; None when the package is not installed."""
+    path = os.path.join(REPO, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(path, "hyperball")):
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_hb_bench")
+    sys.path.insert(0, path)
+    try:
+        import hyperball as ref
+    except Exception as exc:                       # numba missing etc.
+        return {"unavailable": repr(exc)[:200]}
+    gT = ref.CsrGraph(np.asarray(g.offsets, np.int64), np.asarray(g.successors, np.int64))
+    cfg = ref.HyperBallConfig(params=ref.CounterParams(b=cfgd.log2m, seed=cfgd.hash_seed),
+                              workers=threads)
+    acc = ref.CentralityAccumulator(gT.n)
+    st = ref.initialize(gT, cfg)
+    ref.iterate(gT, st, [acc])                     # warm-up: numba compiles / loads here
+    secs, arcs = 0.0, 0
+    for _ in range(2):
+        t0 = time.perf_counter()
+        ref.iterate(gT, st, [acc])
+        secs += time.perf_counter() - t0
+        arcs += gT.m                               # iterations 2-3: (nearly) every source
+    p = 1 << cfgd.log2m                            # changed, every arc merged
+    return {"value": arcs * p / secs, "unit": UNIT, "cores": threads,
+            "kind": "reference package (numba)",
+            "sample": f"iterations 2 and 3 of hyperball.iterate on the whole graph "
+                      f"({gT.m} arcs each), {threads} workers, CentralityAccumulator observer; "
+                      f"{secs:.2f} s"}
 
 
 # ------------------------------------------------------------------------ GPU arm
@@ -596,6 +635,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0,
                     help="seconds of CPU work in the cpu_baseline sample")
+    ap.add_argument("--no-reference-package", action="store_true",
+                    help="--impl reference: skip timing the reference package (numba)")
     ap.add_argument("--ref-budget", type=float, default=120.0,
                     help="total seconds of CPU work for --impl reference")
     args = ap.parse_args()

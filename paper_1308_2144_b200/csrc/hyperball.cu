@@ -96,7 +96,14 @@ struct Geo {
   // lanes cooperating on one row: one 16-byte chunk per lane for p <= 32, two above
   // (p = 64 / 128 / 256 -> 2 / 4 / 8 lanes: more nodes per warp round amortise the
   // per-round work; measured on configs 2-4), at most 32
-  static constexpr int G = CH <= 2 ? CH : (CH / 2 < 32 ? CH / 2 : 32);
+#ifndef HB_G_P64
+#define HB_G_P64 2
+#endif
+#ifndef HB_G_P128
+#define HB_G_P128 4
+#endif
+  static constexpr int G = LOGP == 6 ? HB_G_P64 : (LOGP == 7 ? HB_G_P128 :
+                           (CH <= 2 ? CH : (CH / 2 < 32 ? CH / 2 : 32)));
   static constexpr int CPL = CH / G;              // chunks per lane
   static constexpr int NPW = 32 / G;              // rows handled side by side per warp
 };
@@ -2584,8 +2591,17 @@ int hb_union_step_runs(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets
         reinterpret_cast<unsigned long long *>(nch_out),                                       \
         reinterpret_cast<unsigned long long *>(merged_out), hot_rows, active, peers, s, ra);   \
   else
-  HB_RUNS_CASE(5, 1) HB_RUNS_CASE(6, 1) HB_RUNS_CASE(6, 2) HB_RUNS_CASE(7, 1)
-  HB_RUNS_CASE(7, 2) HB_RUNS_CASE(7, 3) HB_RUNS_CASE(8, 1) HB_RUNS_CASE(8, 2)
+#if HB_G_P64 >= 2
+  HB_RUNS_CASE(6, 1)
+#endif
+#if HB_G_P128 >= 4
+  HB_RUNS_CASE(7, 1)
+#endif
+#if HB_G_P128 >= 2
+  HB_RUNS_CASE(7, 2)
+#endif
+  HB_RUNS_CASE(5, 1) HB_RUNS_CASE(6, 2)
+  HB_RUNS_CASE(7, 3) HB_RUNS_CASE(8, 1) HB_RUNS_CASE(8, 2)
   HB_RUNS_CASE(8, 3) HB_RUNS_CASE(8, 4)
   return set_err_msg("hb_union_step_runs: unsupported (p, runs)");
 #undef HB_RUNS_CASE
