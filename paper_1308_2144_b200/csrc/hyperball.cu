@@ -102,8 +102,11 @@ struct Geo {
 #ifndef HB_G_P128
 #define HB_G_P128 4
 #endif
-  static constexpr int G = LOGP == 6 ? HB_G_P64 : (LOGP == 7 ? HB_G_P128 :
-                           (CH <= 2 ? CH : (CH / 2 < 32 ? CH / 2 : 32)));
+#ifndef HB_G_P256
+#define HB_G_P256 8
+#endif
+  static constexpr int G = LOGP == 6 ? HB_G_P64 : (LOGP == 7 ? HB_G_P128 : (LOGP == 8 ? HB_G_P256 :
+                           (CH <= 2 ? CH : (CH / 2 < 32 ? CH / 2 : 32))));
   static constexpr int CPL = CH / G;              // chunks per lane
   static constexpr int NPW = 32 / G;              // rows handled side by side per warp
 };
@@ -408,21 +411,52 @@ struct Peers {
 __device__ __forceinline__ double np_max0(double x) { return (x >= 0.0 || x != x) ? x : 0.0; }
 
 // ------------------------------------------------------------------ shared epilogue
-// Group of G lanes finishing node v: merge own row, change test, lazy write, estimate,
-// accumulate.  acc holds the max over merged sources.  Warp-uniform: EVERY lane of the
-// warp calls it (groups with nothing to do pass doit = false), so all collectives use the
-// full mask and no group's divergence serialises the others.  Returns the group's changed
-// flag.
+// Scalar tail of the epilogue for one changed node (one lane): the estimate from the
+// register sum s (or, when some register is > 31, the reference's ascending-j fp64 sum
+// over the stored row), then the accumulate (centrality.py:132-150).
+template <int P>
+__device__ __forceinline__ void node_scalar(int64_t v, double s, uint32_t zeros, bool seq,
+                                            const uint8_t *nrow, double *__restrict__ est,
+                                            double *__restrict__ sum_dist,
+                                            double *__restrict__ sum_recip, const EstConst &ec,
+                                            double tf, const double *pre_vals) {
+  if (seq) {  // reference order: ascending-j fp64 sum (_kernels.py:25-30)
+    s = 0.0;
+    for (int j = 0; j < P; j++) s = __dadd_rn(s, pow2neg(nrow[j]));
+  }
+  const double e = finish_estimate(s, (int)zeros, ec);
+  const double old = pre_vals ? pre_vals[0] : est[v];
+  est[v] = e;
+  const double d = np_max0(__dsub_rn(e, old));
+  if (sum_dist)
+    sum_dist[v] = __dadd_rn(pre_vals ? pre_vals[1] : sum_dist[v], __dmul_rn(tf, d));
+  if (sum_recip)
+    sum_recip[v] = __dadd_rn(pre_vals ? pre_vals[2] : sum_recip[v], __ddiv_rn(d, tf));
+  // Runtime-indexed on purpose: ec.disc_scale[k] makes ptxas keep the estimator
+  // constants in a (L1-resident) local copy instead of registers, which the load
+  // pipeline of the union loops needs more (measured: a statically unrolled loop or a
+  // __constant__ copy costs 8-9% on config 4).
+  for (int k = 0; k < ec.n_disc; k++) {
+    double *q = ec.disc + k * ec.disc_stride + v;
+    const double c = ((ec.disc_div >> k) & 1) ? __ddiv_rn(d, tf) : __dmul_rn(ec.disc_scale[k], d);
+    *q = __dadd_rn(*q, c);
+  }
+}
+
+// Group of G lanes finishing node v, vector part: merge own row, change test, lazy write
+// (+ push); then, when any group of the warp changed, the group's register sum s (all
+// lanes of the group), zero count and the > 31 flag.  acc holds the max over merged
+// sources.  Warp-uniform: EVERY lane of the warp calls it (groups with nothing to do pass
+// doit = false), so all collectives use the full mask and no group's divergence
+// serialises the others.  Returns the group's changed flag; *any_changed = the warp's.
 template <int LOGP, bool PUSH>
-__device__ __forceinline__ bool finish_node(const Peers &peers, bool doit, int64_t v,
+__device__ __forceinline__ bool finish_rows(const Peers &peers, bool doit, int64_t v,
                                             const uint4 (&acc)[Geo<LOGP>::CPL],
                                             const uint4 (&pre)[Geo<LOGP>::CPL], bool have_pre,
                                             bool self_chg, int grp, int gl,
                                             const uint8_t *__restrict__ cur,
-                                            uint8_t *__restrict__ nxt, double *__restrict__ est,
-                                            double *__restrict__ sum_dist,
-                                            double *__restrict__ sum_recip, const EstConst &ec,
-                                            double tf, const double *pre_vals = nullptr) {
+                                            uint8_t *__restrict__ nxt, bool &any_changed,
+                                            double &s, uint32_t &zeros, bool &seq) {
   using Gm = Geo<LOGP>;
   constexpr unsigned kLow = Gm::G == 32 ? 0xffffffffu : ((1u << (Gm::G & 31)) - 1u);
   const uint8_t *crow = cur + (size_t)v * Gm::P;
@@ -451,7 +485,12 @@ __device__ __forceinline__ bool finish_node(const Peers &peers, bool doit, int64
       }
     }
   }
-  if (bal != 0u) {   // warp-uniform
+  any_changed = bal != 0u;
+  s = 0.0;
+  zeros = 0;
+  seq = false;
+  if (bal == 0u) return changed;   // warp-uniform
+  {
     // sum_j 2^-M[j] as exact fp64 partial sums (every M <= 31 here: at most 36 significant
     // bits, so any summation order gives the reference's sequential result), zero count by
     // SWAR, and an OR of all bytes to detect registers > 31 (sequential fallback).
@@ -459,7 +498,7 @@ __device__ __forceinline__ bool finish_node(const Peers &peers, bool doit, int64
     // shift count's low 5 bits are M whenever M <= 31; larger registers take the
     // sequential path below), summed in 64 bits (< 2^37), scaled once: exact.
     uint64_t S = 0;
-    uint32_t zeros = 0, big = 0;
+    uint32_t big = 0;
 #pragma unroll
     for (int c = 0; c < Gm::CPL; c++) {
       const uint32_t ws[4] = {nw[c].x, nw[c].y, nw[c].z, nw[c].w};
@@ -475,41 +514,118 @@ __device__ __forceinline__ bool finish_node(const Peers &peers, bool doit, int64
         S += ((uint64_t)t0 + t1) + ((uint64_t)t2 + t3);
       }
     }
-    double s = __dmul_rn(__ull2double_rn(S), 0x1p-31);
+    s = __dmul_rn(__ull2double_rn(S), 0x1p-31);
 #pragma unroll
     for (int off = 1; off < Gm::G; off <<= 1) {   // xor partners stay inside the group
       s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, off));
       zeros += __shfl_xor_sync(0xffffffffu, zeros, off);
       big |= __shfl_xor_sync(0xffffffffu, big, off);
     }
-    const bool seq = (big & 0xE0E0E0E0u) != 0u;   // some register > 31
-    if (__any_sync(0xffffffffu, changed && seq)) __syncwarp();  // stored rows visible
-    if (changed && gl == 0) {
-      if (seq) {  // reference order: ascending-j fp64 sum (_kernels.py:25-30)
-        s = 0.0;
-        for (int j = 0; j < Gm::P; j++) s = __dadd_rn(s, pow2neg(nrow[j]));
-      }
-      const double e = finish_estimate(s, (int)zeros, ec);
-      const double old = pre_vals ? pre_vals[0] : est[v];
-      est[v] = e;
-      const double d = np_max0(__dsub_rn(e, old));
-      if (sum_dist)
-        sum_dist[v] = __dadd_rn(pre_vals ? pre_vals[1] : sum_dist[v], __dmul_rn(tf, d));
-      if (sum_recip)
-        sum_recip[v] = __dadd_rn(pre_vals ? pre_vals[2] : sum_recip[v], __ddiv_rn(d, tf));
-      // Runtime-indexed on purpose: ec.disc_scale[k] makes ptxas keep the estimator
-      // constants in a (L1-resident) local copy instead of registers, which the load
-      // pipeline of the union loops needs more (measured: a statically unrolled loop or a
-      // __constant__ copy costs 8-9% on config 4).
-      for (int k = 0; k < ec.n_disc; k++) {
-        double *q = ec.disc + k * ec.disc_stride + v;
-        const double c = ((ec.disc_div >> k) & 1) ? __ddiv_rn(d, tf) : __dmul_rn(ec.disc_scale[k], d);
-        *q = __dadd_rn(*q, c);
-      }
-    }
+    seq = (big & 0xE0E0E0E0u) != 0u;   // some register > 31
   }
   return changed;
 }
+
+// The whole epilogue for one node per group (heavy nodes, and the light kernel at p <= 32
+// where every lane already owns a node): finish_rows, then the scalar tail on the
+// group's first lane.  Returns the group's changed flag.
+template <int LOGP, bool PUSH>
+__device__ __forceinline__ bool finish_node(const Peers &peers, bool doit, int64_t v,
+                                            const uint4 (&acc)[Geo<LOGP>::CPL],
+                                            const uint4 (&pre)[Geo<LOGP>::CPL], bool have_pre,
+                                            bool self_chg, int grp, int gl,
+                                            const uint8_t *__restrict__ cur,
+                                            uint8_t *__restrict__ nxt, double *__restrict__ est,
+                                            double *__restrict__ sum_dist,
+                                            double *__restrict__ sum_recip, const EstConst &ec,
+                                            double tf, const double *pre_vals = nullptr) {
+  using Gm = Geo<LOGP>;
+  bool any;
+  double s;
+  uint32_t zeros;
+  bool seq;
+  const bool changed = finish_rows<LOGP, PUSH>(peers, doit, v, acc, pre, have_pre, self_chg,
+                                               grp, gl, cur, nxt, any, s, zeros, seq);
+  if (any) {   // warp-uniform
+    if (__any_sync(0xffffffffu, changed && seq)) __syncwarp();  // stored rows visible
+    if (changed && gl == 0)
+      node_scalar<Gm::P>(v, s, zeros, seq, nxt + (size_t)v * Gm::P, est, sum_dist, sum_recip,
+                         ec, tf, pre_vals);
+  }
+  return changed;
+}
+
+#ifndef HB_DEFER_TAIL
+#define HB_DEFER_TAIL 1               // light kernel: deferred scalar epilogue
+#endif
+#ifndef HB_DEFER_MIN_LOGP
+#define HB_DEFER_MIN_LOGP 8
+#endif
+#ifndef HB_DEFER_PRELOAD
+#define HB_DEFER_PRELOAD 1
+#endif
+// Deferred scalar epilogue of the light kernel for G > 1 (p >= 64): a warp round finishes
+// NPW = 32 / G nodes, and the scalar tail (two fp64 divisions, the estimate / sums
+// read-modify-write, the discounts) would run on NPW lanes only.  Instead each round's
+// (s, zeros, flags) move by shuffle to the lane that owns the node's slot in its aligned
+// block of 32 ids (lane = v & 31); once the warp leaves the block, all 32 lanes run the
+// tail at once (coalesced 256-byte estimate / sum accesses).  Rows were stored by the
+// round, so the > 31 fallback re-reads them after a __syncwarp.
+struct DeferredTail {
+  int64_t blk = -1;      // block of 32 ids (v >> 5) the pending slots belong to
+  double s = 0.0;
+  uint32_t zeros = 0;
+  uint32_t flags = 0;    // bit 0 pending, bit 1 some register > 31
+  double pv[3];          // HB_DEFER_PRELOAD: the block's old estimate / sums, loaded on entry
+  template <int P>
+  __device__ __forceinline__ void flush(const uint8_t *__restrict__ nxt,
+                                        double *__restrict__ est, double *__restrict__ sum_dist,
+                                        double *__restrict__ sum_recip, const EstConst &ec,
+                                        double tf) {
+    if (__any_sync(0xffffffffu, flags & 1u)) {   // warp-uniform
+      if (__any_sync(0xffffffffu, flags & 2u)) __syncwarp();
+      if (flags & 1u) {
+        const int64_t v = (blk << 5) + (threadIdx.x & 31);
+        node_scalar<P>(v, s, zeros, (flags & 2u) != 0u, nxt + (size_t)v * P, est, sum_dist,
+                       sum_recip, ec, tf, HB_DEFER_PRELOAD ? pv : nullptr);
+      }
+    }
+    flags = 0;
+  }
+  // enter block b: its lanes' old values start loading now, consumed at the flush
+  __device__ __forceinline__ void enter(int64_t b, int64_t lo, int64_t hi,
+                                        const double *__restrict__ est,
+                                        const double *__restrict__ sum_dist,
+                                        const double *__restrict__ sum_recip) {
+    blk = b;
+    if (HB_DEFER_PRELOAD) {
+      const int64_t v = (b << 5) + (threadIdx.x & 31);
+      const bool in = v >= lo && v < hi;
+      pv[0] = in ? est[v] : 0.0;
+      pv[1] = in && sum_dist ? sum_dist[v] : 0.0;
+      pv[2] = in && sum_recip ? sum_recip[v] : 0.0;
+    }
+  }
+  // round results of the NPW groups of G lanes (group g = node base + g) -> slot lanes
+  template <int G, int NPW>
+  __device__ __forceinline__ void take(int64_t base, bool changed, double rs, uint32_t rz,
+                                       bool rseq) {
+    const int lane = threadIdx.x & 31;
+    const int first = (int)(base & 31);
+    const int g = lane - first;
+    const bool mine = g >= 0 && g < NPW;
+    const int src = (mine ? g : 0) * G;
+    const uint32_t f = (changed ? 1u : 0u) | (rseq ? 2u : 0u);
+    const double ts = __shfl_sync(0xffffffffu, rs, src);
+    const uint32_t tz = __shfl_sync(0xffffffffu, rz, src);
+    const uint32_t tf = __shfl_sync(0xffffffffu, f, src);
+    if (mine && (tf & 1u)) {
+      s = ts;
+      zeros = tz;
+      flags = tf;
+    }
+  }
+};
 
 // Batched runs (run_multi): a row of cur holds R = 2^LOGR independent runs' registers side
 // by side (p1 = P / R bytes each, run r at bytes [r*p1, (r+1)*p1)).  The union is the same
@@ -825,6 +941,8 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
   // bitmap word.
   const int64_t lo_al = (lo / Gm::NPW) * Gm::NPW;
   constexpr int64_t CN = (int64_t)chunk_rounds<LOGP>() * Gm::NPW;
+  constexpr bool kDefer = LOGR == 0 && Gm::G > 1 && HB_DEFER_TAIL && LOGP >= HB_DEFER_MIN_LOGP;
+  DeferredTail dt;
   const int64_t nchunks = (hi - lo_al + CN - 1) / CN;
   for (int64_t chunk = warp; chunk < nchunks; chunk += nwarps) {
   const int64_t vb = lo_al + chunk * CN;
@@ -850,6 +968,12 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
     // frontier mode: only nodes with a changed in-neighbour (or a changed own row) work
     const bool act_v = !active || ((base + grp < ve) && test_bit(active, base + grp));
     if (active && !__any_sync(0xffffffffu, act_v)) continue;
+    if constexpr (kDefer) {
+      if ((base >> 5) != dt.blk) {                // left the block: run its scalar tails
+        dt.flush<Gm::P>(nxt, est, sum_dist, sum_recip, ec, tf);
+        dt.enter(base >> 5, lo, hi, est, sum_dist, sum_recip);
+      }
+    }
     if (lane == 0 && !active) {
       if (pf_a0 >= 0) {                        // ids of the batch announced last round
         l2_prefetch(succ + pf_a0, (pf_a1 - pf_a0) * 4);
@@ -894,7 +1018,7 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
     RowAcc<LOGP> macc;
     macc.init();
     double vals[3] = {0.0, 0.0, 0.0};
-    if (LOGR == 0 && pre && gl == 0) {
+    if (LOGR == 0 && !kDefer && pre && gl == 0) {
       vals[0] = est[v];
       if (sum_dist) vals[1] = sum_dist[v];
       if (sum_recip) vals[2] = sum_recip[v];
@@ -1022,7 +1146,14 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
     for (int c = 0; c < Gm::CPL; c++) acc[c] = macc.get(c);
     my_merged += (gl == 0) ? (uint32_t)total : 0u;
     bool changed;
-    if constexpr (LOGR == 0)
+    if constexpr (kDefer) {
+      bool any, seq;
+      double rs;
+      uint32_t rz;
+      changed = finish_rows<LOGP, PUSH>(peers, valid && (total > 0 || self_chg), v, acc, self,
+                                        pre, self_chg, grp, gl, cur, nxt, any, rs, rz, seq);
+      if (any) dt.take<Gm::G, Gm::NPW>(base, changed, rs, rz, seq);
+    } else if constexpr (LOGR == 0)
       changed = finish_node<LOGP, PUSH>(peers, valid && (total > 0 || self_chg), v, acc, self,
                                         pre, self_chg, grp, gl, cur, nxt, est, sum_dist,
                                         sum_recip, ec, tf, pre ? vals : nullptr);
@@ -1043,6 +1174,7 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
     }
   }
   }  // chunk
+  if constexpr (kDefer) dt.flush<Gm::P>(nxt, est, sum_dist, sum_recip, ec, tf);
   if constexpr (PUSH) __threadfence_system();   // remote rows/bits before the barrier
   block_add2(my_nch, my_merged, nch_out, merged_out);
 }
@@ -2600,9 +2732,14 @@ int hb_union_step_runs(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets
 #if HB_G_P128 >= 2
   HB_RUNS_CASE(7, 2)
 #endif
+#if HB_G_P256 >= 8
+  HB_RUNS_CASE(8, 1)
+#endif
+#if HB_G_P256 >= 4
+  HB_RUNS_CASE(8, 2)
+#endif
   HB_RUNS_CASE(5, 1) HB_RUNS_CASE(6, 2)
-  HB_RUNS_CASE(7, 3) HB_RUNS_CASE(8, 1) HB_RUNS_CASE(8, 2)
-  HB_RUNS_CASE(8, 3) HB_RUNS_CASE(8, 4)
+  HB_RUNS_CASE(7, 3) HB_RUNS_CASE(8, 3) HB_RUNS_CASE(8, 4)
   return set_err_msg("hb_union_step_runs: unsupported (p, runs)");
 #undef HB_RUNS_CASE
   if (rc) return rc;
