@@ -555,6 +555,12 @@ __device__ __forceinline__ bool finish_node(const Peers &peers, bool doit, int64
   return changed;
 }
 
+#ifndef HB_TMA_DIRECT
+#define HB_TMA_DIRECT 1               // TMA light kernel, dense batches: ids straight to the issuing lanes
+#endif
+#ifndef HB_SELF_LATE
+#define HB_SELF_LATE 1                // TMA light kernel: own row read in the epilogue
+#endif
 #ifndef HB_DEFER_TAIL
 #define HB_DEFER_TAIL 1               // light kernel: deferred scalar epilogue
 #endif
@@ -1006,6 +1012,7 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
     bool pre;                                   // own row certainly needed: load early
     if (dense) pre = valid;                     // (no wait on the bitmap word)
     else pre = self_chg;
+    if (kTma<LOGP, LOGR, HINT>() && HB_SELF_LATE) pre = false;   // own row read at the end
     uint4 self[Gm::CPL], acc[Gm::CPL];
 #pragma unroll
     for (int c = 0; c < Gm::CPL; c++) {
@@ -1036,7 +1043,67 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
     const int trips = (int)((end - beg + B::NB - 1) / B::NB);
     const int wtrips = __reduce_max_sync(0xffffffffu, (unsigned)trips);
     int total = 0;
-    for (int it = 0; it < wtrips; it++) {
+    constexpr bool kDirect = kTma<LOGP, LOGR, HINT>() && HB_TMA_DIRECT;
+    if constexpr (kDirect) {
+      if (dense) {   // warp-uniform
+        // Dense batches need no compaction, so the ids skip shared memory: lane q <
+        // NPW * GPG owns gather4 number h = q % GPG of group g = q / GPG in every batch
+        // (slots [4h, 4h + 4) of the group's U), loads those 4 ids itself one batch
+        // ahead, pads past the node's end with the group's own row, and issues the gather.
+        static_assert(B::U == B::NB && B::U % 4 == 0 && Gm::NPW * (B::U / 4) <= 32,
+                      "direct TMA layout");
+        constexpr int GPG = B::U / 4;
+        const int g = (lane / GPG) & (Gm::NPW - 1), h = lane % GPG;
+        const bool iss_lane = lane < Gm::NPW * GPG;
+        const int64_t beg_g = __shfl_sync(0xffffffffu, beg, g * Gm::G);
+        const int64_t end_g = __shfl_sync(0xffffffffu, end, g * Gm::G);
+        const int32_t fbg = (int32_t)(base + g < ve ? base + g : lo);
+        int32_t nid[4];
+        auto load_ids = [&](int64_t k0) {
+#pragma unroll
+          for (int k = 0; k < 4; k++) {
+            const int64_t kk = k0 + 4 * h + k;
+            nid[k] = (iss_lane && kk < end_g) ? __ldg(succ + kk) : fbg;
+            HB_CHK(nid[k] >= 0 && nid[k] < g_chk.rows, "k_light direct TMA row");
+          }
+        };
+        load_ids(beg_g);
+        for (int it = 0; it < wtrips; it++) {
+          const bool issue = iss_lane && 4 * h < end_g - (beg_g + (int64_t)it * B::U);
+          const uint32_t ngat = __popc(__ballot_sync(0xffffffffu, issue));
+          if (lane == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(tma_bar),
+                         "r"(ngat * 4 * Gm::P) : "memory");
+          __syncwarp();
+          if (issue) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            tma_gather4(tma_buf + (g * B::U + 4 * h) * Gm::P, &tmap, nid[0], nid[1], nid[2],
+                        nid[3], tma_bar);
+          }
+          load_ids(beg_g + (int64_t)(it + 1) * B::U);   // next batch, in flight meanwhile
+          mbar_wait(tma_bar, tma_phase);
+          tma_phase ^= 1u;
+          const int64_t left = end - (beg + (int64_t)it * B::U);
+          const int cnt = left <= 0 ? 0 : (left < B::U ? (int)left : B::U);
+          const uint4 *rows = reinterpret_cast<const uint4 *>(
+              __cvta_shared_to_generic(tma_buf + grp * B::U * Gm::P));
+#pragma unroll
+          for (int hh = 0; hh < GPG; hh++) {
+            if (4 * hh < cnt) {
+#pragma unroll
+              for (int u = 4 * hh; u < 4 * hh + 4; u += 2)
+#pragma unroll
+                for (int c = 0; c < Gm::CPL; c++)
+                  macc.add2(c, rows[u * Gm::CH + c * Gm::G + gl],
+                            rows[(u + 1) * Gm::CH + c * Gm::G + gl]);
+            }
+          }
+          total += cnt;
+          __syncwarp();                          // every lane done before the next gather
+        }
+      }
+    }
+    for (int it = 0; it < ((kDirect && dense) ? 0 : wtrips); it++) {
       const int64_t kb = beg + (int64_t)it * B::NB;
       int cnt = 0;
       if (kDenseCopy && dense) {
