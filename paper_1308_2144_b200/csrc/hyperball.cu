@@ -2193,6 +2193,21 @@ __global__ void k_finalize(int64_t n, const int32_t *__restrict__ rank,
   }
 }
 
+// Id map lookup rank[id] for the relabel kernels: a random 4-byte read of a table of n
+// entries (1 GB at config 5) that mostly misses L2; `.L2::64B` halves the DRAM line
+// fetched per miss (HB_RELABEL_64B).
+#ifndef HB_RELABEL_64B
+#define HB_RELABEL_64B 1
+#endif
+__device__ __forceinline__ int32_t ld_rank(const int32_t *rank, int32_t id) {
+#if HB_RELABEL_64B
+  int32_t r;
+  asm("ld.global.nc.L2::64B.s32 %0, [%1];" : "=r"(r) : "l"(rank + id));
+  return r;
+#else
+  return __ldg(rank + id);
+#endif
+}
 __global__ void k_relabel(int64_t r0, int64_t r1, const int64_t *__restrict__ old_off,
                           const int32_t *__restrict__ old_succ, const int32_t *__restrict__ perm,
                           const int32_t *__restrict__ rank, const int64_t *__restrict__ new_off,
@@ -2204,7 +2219,7 @@ __global__ void k_relabel(int64_t r0, int64_t r1, const int64_t *__restrict__ ol
     const int64_t o = __ldg(perm + i);
     const int64_t b0 = __ldg(old_off + o), len = __ldg(old_off + o + 1) - b0;
     const int64_t d0 = __ldg(new_off + i);
-    for (int64_t k = lane; k < len; k += 32) new_succ[d0 + k] = __ldg(rank + __ldg(old_succ + b0 + k));
+    for (int64_t k = lane; k < len; k += 32) new_succ[d0 + k] = ld_rank(rank, __ldg(old_succ + b0 + k));
   }
 }
 
@@ -2221,7 +2236,7 @@ __global__ void k_relabel_src(int64_t o0, int64_t o1, const int64_t *__restrict_
   for (int64_t o = o0 + warp; o < o1; o += nwarps) {
     const int64_t b0 = __ldg(old_off + o), len = __ldg(old_off + o + 1) - b0;
     const int64_t d0 = __ldg(new_off + __ldg(rank + o));
-    for (int64_t k = lane; k < len; k += 32) new_succ[d0 + k] = __ldg(rank + __ldg(old_succ + b0 + k));
+    for (int64_t k = lane; k < len; k += 32) new_succ[d0 + k] = ld_rank(rank, __ldg(old_succ + b0 + k));
   }
 }
 
@@ -2229,7 +2244,7 @@ __global__ void k_map_ids(int64_t m, const int32_t *ids, const int32_t *__restri
                           int32_t *out) {
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m;
        k += (int64_t)gridDim.x * blockDim.x)
-    out[k] = __ldg(rank + ids[k]);
+    out[k] = ld_rank(rank, ids[k]);
 }
 
 __global__ void k_hash(int64_t n, const uint64_t *__restrict__ items,

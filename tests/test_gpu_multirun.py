@@ -1,7 +1,8 @@
 """Batched repeated runs (multirun.py, hb_union_step_runs): R seeds sharing one union pass
 must give, run by run, the bits of independent runs -- registers, estimates, iteration
 counts, accumulator sums and centralities -- and call the observers as the reference's
-per-run loop does (cli.py:222-254, engine.py:413-435)."""
+per-run loop does (cli.py:222-254, engine.py:413-435); every run is also checked against
+the CPU oracle run with seed + r."""
 
 import hashlib
 
@@ -14,6 +15,7 @@ pytestmark = pytest.mark.gpu
 
 hb = pytest.importorskip("paper_1308_2144_b200")
 from paper_1308_2144_b200 import multirun  # noqa: E402
+import oracle as orc  # noqa: E402  (the checker; tests/conftest.py puts oracle/ on the path)
 
 CASES = {c["key"]: c for c in golden_cases()}
 
@@ -60,6 +62,22 @@ def _compare(g, cfg, runs, batch):
             assert np.array_equal(bits(fin(ab)), bits(fin(aa))), fin.__name__
         assert got_obs[r].steps == ref_obs[r].steps
         assert got_obs[r].final == ref_obs[r].final
+    # every run r also against the CPU oracle with seed + r (cli.py:222-254): iteration
+    # count, final registers, estimates and the three centralities, bit for bit
+    pr = cfg.params
+    for r in range(runs):
+        want = orc.run_oracle(np.asarray(g.offsets, np.int64), np.asarray(g.successors, np.int64),
+                              pr.b, pr.seed + r, width=pr.register_width, workers=4,
+                              skip=cfg.skip_stable_nodes,
+                              weights=None if cfg.weights is None else
+                              np.asarray(getattr(cfg.weights, "values", cfg.weights), np.int64))
+        st, acc = got[r]
+        assert st.t == want.t, (r, st.t, want.t)
+        assert sha(st.register_matrix()) == want.reg_digests[-1], r
+        assert np.array_equal(bits(st.est), bits(want.est)), r
+        for fin, arr in ((hb.finalize_harmonic, want.harmonic),
+                         (hb.finalize_closeness, want.closeness), (hb.finalize_lin, want.lin)):
+            assert np.array_equal(bits(fin(acc)), bits(arr)), (r, fin.__name__)
     return got
 
 
