@@ -2373,27 +2373,38 @@ int ensure_smem_attr(const void *func, int bytes, const char *what) {
 // set-aside limit is only ever raised (a larger limit the host set is kept).
 bool g_l2_persist = true;
 
-size_t persist_bytes() {
-  static size_t per_dev[kMaxDevices];
-  static bool done[kMaxDevices];
+// L2 set-aside for the persisting window of the current step, set per device when it
+// changes: 64 MB for rows of p <= 32 (config 5: 32.4 -> 30.6 ms against 32 MB; 48-96 MB
+// swept, >= 72 MB thrashes), 32 MB above (config 2: 0.39 -> 0.38 ms against 64 MB).  Never
+// set below the limit the host application had; HB_L2_PERSIST_MB overrides.  Returns the
+// window size to use (0 = off).
+size_t persist_bytes(size_t want) {
+  static size_t applied[kMaxDevices], host_have[kMaxDevices], max_sz[kMaxDevices];
+  static bool init[kMaxDevices];
   const int dev = current_device();
-  if (done[dev]) return per_dev[dev];
-  done[dev] = true;
-  cudaDeviceProp prop;
-  if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) {
+  if (!init[dev]) {
+    init[dev] = true;
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, dev) == cudaSuccess)
+      max_sz[dev] = std::min((size_t)prop.persistingL2CacheMaxSize,
+                             (size_t)prop.accessPolicyMaxWindowSize);
+    if (cudaDeviceGetLimit(&host_have[dev], cudaLimitPersistingL2CacheSize) != cudaSuccess)
+      host_have[dev] = 0;
+    applied[dev] = host_have[dev];
     cudaGetLastError();
-    return per_dev[dev] = 0;
   }
-  size_t want = (size_t)32 << 20;   // measured best on config 5 (16-96 MB swept)
   if (const char *e = getenv("HB_L2_PERSIST_MB")) want = (size_t)atoll(e) << 20;
-  if (want > (size_t)prop.persistingL2CacheMaxSize) want = prop.persistingL2CacheMaxSize;
-  if (want > (size_t)prop.accessPolicyMaxWindowSize) want = prop.accessPolicyMaxWindowSize;
-  size_t have = 0;
-  if (cudaDeviceGetLimit(&have, cudaLimitPersistingL2CacheSize) != cudaSuccess) have = 0;
-  if (want && have < want && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) != cudaSuccess)
-    want = have;
-  cudaGetLastError();
-  return per_dev[dev] = want;
+  want = std::min(want, max_sz[dev]);
+  if (want == 0) return 0;
+  const size_t target = std::max(want, host_have[dev]);
+  if (target != applied[dev]) {
+    if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, target) != cudaSuccess) {
+      cudaGetLastError();
+      return std::min(want, applied[dev]);
+    }
+    applied[dev] = target;
+  }
+  return want;
 }
 
 // Bytes of the evict_last head (HB_HINT_MB, default 64); HB_PERSIST_WINDOW=0 turns the
@@ -2414,10 +2425,9 @@ bool persist_window_on() {
   return on && g_l2_persist;
 }
 
-void set_hot_window(cudaStream_t s, const void *base, size_t hot_bytes) {
+void set_hot_window(cudaStream_t s, const void *base, size_t hot_bytes, size_t cap) {
   cudaStreamAttrValue attr;
   memset(&attr, 0, sizeof(attr));
-  const size_t cap = persist_bytes();
   if (cap && hot_bytes) {
     const size_t w = hot_bytes < cap ? hot_bytes : cap;
     attr.accessPolicyWindow.base_ptr = const_cast<void *>(base);
@@ -2505,9 +2515,11 @@ int union_step_impl(int64_t lo, int64_t hi, const int64_t *offsets, const int32_
                                  "k_light smem attribute"))
       return e;
   }
-  if (hot_rows > 0 && persist_window_on() && persist_bytes() > 0) {
+  const size_t win = hot_rows > 0 && persist_window_on()
+                        ? persist_bytes((size_t)(LOGP <= HB_HINT_MAX_LOGP ? 64 : 32) << 20) : 0;
+  if (win > 0) {
     cudaCtxResetPersistingL2Cache();    // lines of last iteration's buffer stop persisting
-    set_hot_window(s, cur, (size_t)hot_rows * Gm::P);
+    set_hot_window(s, cur, (size_t)hot_rows * Gm::P, win);
   }
   const int64_t hot_lim = hot_rows > 0 ? std::min<int64_t>(hot_rows, hint_bytes() / Gm::P) : 0;
   constexpr bool kCanHint = LOGP <= HB_HINT_MAX_LOGP;
@@ -2553,7 +2565,7 @@ int union_step_impl(int64_t lo, int64_t hi, const int64_t *offsets, const int32_
               chg_prev, chg_now, est, sum_dist, sum_recip, ec, tf, nch, active, peers, ra);
     if (int e = check_launch("k_heavy_finish")) return e;
   }
-  if (hot_rows > 0 && persist_window_on()) set_hot_window(s, nullptr, 0);
+  if (win > 0) set_hot_window(s, nullptr, 0, 0);
   return 0;
 }
 
