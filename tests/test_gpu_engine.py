@@ -236,3 +236,29 @@ class TestLazyCoreach:
         st = hb.run(g, cfg(b=6, seed=2), [acc, last])
         assert last.final is not None and acc._coreach_fetch is None
         assert np.array_equal(acc.coreach, st.est) and np.array_equal(last.final, st.est)
+
+
+@pytest.mark.skipif(not __import__("torch").cuda.is_available()
+                    or __import__("torch").cuda.device_count() < 2,
+                    reason="needs two GPUs in one process")
+def test_two_devices_in_one_process():
+    """Per-device library state (SM count, opt-in shared memory of the p = 256 TMA kernel,
+    L2 set-aside) and the stream-device guard: runs on devices 0 and 1 stepped
+    alternately from one thread, with device 0 current throughout, give identical bits."""
+    import torch
+    torch.cuda.set_device(0)
+    g = random_graph(5, 3000, 6.0)
+    for b in (4, 8):
+        states = [hb.initialize(g, cfg(b=b, seed=3, device=d)) for d in (0, 1)]
+        accs = [hb.CentralityAccumulator(g.n) for _ in states]
+        while True:
+            nch = [hb.iterate(g, st, [a]) for st, a in zip(states, accs)]
+            assert nch[0] == nch[1]
+            assert np.array_equal(states[0].register_matrix(), states[1].register_matrix())
+            if nch[0] == 0:
+                break
+        for a in accs:
+            a.on_converged(states[accs.index(a)].est)
+        for fin in (hb.finalize_harmonic, hb.finalize_lin):
+            assert np.array_equal(fin(accs[0]).view(np.uint64), fin(accs[1]).view(np.uint64))
+        assert torch.cuda.current_device() == 0
