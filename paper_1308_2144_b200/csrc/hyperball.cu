@@ -284,11 +284,27 @@ __device__ __forceinline__ uint4 ld_pol_64b(const uint4 *p, uint64_t pol) {
       : "l"(p), "l"(pol));
   return r;
 }
-template <int LOGP>
+// Same without L1 allocation, for register arrays far larger than L2 (config 5): a random
+// row fetched into L1 is rarely read again by the same SM before the misses behind it
+// evict it, and the hubs it would displace stay in L2 anyway (config 5: 30.6 -> 30.0 ms;
+// config 5s, a 268 MB array, loses with it: 1.57 -> 1.75 ms -- hence the size switch).
+__device__ __forceinline__ uint4 ld_pol_64b_na(const uint4 *p, uint64_t pol) {
+  uint4 r;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.L2::64B.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "l"(p), "l"(pol));
+  return r;
+}
+#ifndef HB_L1NA_MIN_MB
+#define HB_L1NA_MIN_MB 1024            // register arrays from this size gather without L1
+#endif
+template <int LOGP, bool L1NA = false>
 __device__ __forceinline__ uint4 ld_row_chunk_hint(const uint4 *__restrict__ cur4, int32_t w,
                                                    uint32_t ch, uint32_t k, uint64_t pol) {
-  if constexpr (LOGP <= HB_L2_64B_MAX_LOGP)
+  if constexpr (LOGP <= HB_L2_64B_MAX_LOGP) {
+    if constexpr (L1NA) return ld_pol_64b_na(cur4 + ((uint32_t)w * ch + k), pol);
     return ld_pol_64b(cur4 + ((uint32_t)w * ch + k), pol);
+  }
   else return ld_chunk_hint(cur4, w, ch, k, pol);
 }
 
@@ -896,7 +912,7 @@ __host__ __device__ constexpr int chunk_rounds() { return LOGP >= 8 ? HB_CHUNK_B
 // prefetches them into L2 kLookRounds rounds ahead, leaving the random source-row
 // gather as the only exposed memory latency of a round.
 // _kernels.py:67-114 restated with the source-skip rule.
-template <int LOGP, bool PUSH, int LOGR = 0, bool HINT = false>
+template <int LOGP, bool PUSH, int LOGR = 0, bool HINT = false, bool L1NA = false>
 __global__ void __launch_bounds__(kThreads, Batch<LOGP>::MINB)
 k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
         const uint8_t *__restrict__ cur, uint8_t *__restrict__ nxt,
@@ -1191,7 +1207,7 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
 #pragma unroll
           for (int c = 0; c < Gm::CPL; c++)
             r[u][c] = (LOGP >= HB_PAD_MIN_LOGP || ok)
-                          ? (kHint ? ld_row_chunk_hint<LOGP>(cur4, w, Gm::CH, c * Gm::G + gl, pol)
+                          ? (kHint ? ld_row_chunk_hint<LOGP, L1NA>(cur4, w, Gm::CH, c * Gm::G + gl, pol)
                                    : ld_row_chunk<LOGP>(cur4, w, Gm::CH, c * Gm::G + gl))
                           : make_uint4(0, 0, 0, 0);
         }
@@ -1248,7 +1264,7 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
 
 // Heavy nodes, phase 1: one warp per work item (a slice of one node's arcs) leaves the
 // max over the slice's changed sources as a partial row.
-template <int LOGP, bool HINT = false>
+template <int LOGP, bool HINT = false, bool L1NA = false>
 __global__ void __launch_bounds__(kThreads, (LOGP >= 10 ? 2 : 4))
 k_heavy_partial(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
                 const uint8_t *__restrict__ cur, const uint32_t *__restrict__ chg_prev,
@@ -1325,7 +1341,7 @@ k_heavy_partial(const int64_t *__restrict__ offsets, const int32_t *__restrict__
 #pragma unroll
           for (int c = 0; c < Gm::CPL; c++)
             r[u][c] = (LOGP >= HB_PAD_MIN_LOGP || ok)
-                          ? (kHint ? ld_row_chunk_hint<LOGP>(cur4, w, Gm::CH, c * Gm::G + gl, pol)
+                          ? (kHint ? ld_row_chunk_hint<LOGP, L1NA>(cur4, w, Gm::CH, c * Gm::G + gl, pol)
                                    : ld_row_chunk<LOGP>(cur4, w, Gm::CH, c * Gm::G + gl))
                           : make_uint4(0, 0, 0, 0);
         }
@@ -2524,9 +2540,14 @@ int union_step_impl(int64_t lo, int64_t hi, const int64_t *offsets, const int32_
   const int64_t hot_lim = hot_rows > 0 ? std::min<int64_t>(hot_rows, hint_bytes() / Gm::P) : 0;
   constexpr bool kCanHint = LOGP <= HB_HINT_MAX_LOGP;
   const bool hint = kCanHint && hot_lim > 0;
+  const bool l1na = (size_t)n_rows * Gm::P >= ((size_t)HB_L1NA_MIN_MB << 20);
   if (n_items > 0) {
     if constexpr (kCanHint) {
-      if (hint)
+      if (hint && l1na)
+        k_heavy_partial<LOGP, true, true><<<grid_for_warps(n_items), kThreads, 0, s>>>(
+            offsets, succ, cur, chg_prev, item_node, item_beg, n_items, item_arcs, dense,
+            partial, merged, active, hot_lim);
+      else if (hint)
         k_heavy_partial<LOGP, true><<<grid_for_warps(n_items), kThreads, 0, s>>>(
             offsets, succ, cur, chg_prev, item_node, item_beg, n_items, item_arcs, dense,
             partial, merged, active, hot_lim);
@@ -2540,7 +2561,11 @@ int union_step_impl(int64_t lo, int64_t hi, const int64_t *offsets, const int32_
   if (hi > lo) {
     const int64_t warps = (hi - lo + Gm::NPW - 1) / Gm::NPW + 1;   // capped at the resident set
     if constexpr (kCanHint) {
-      if (hint)
+      if (hint && l1na)
+        k_light<LOGP, PUSH, LOGR, true, true><<<grid_for_warps(warps), kThreads, 0, s>>>(
+            offsets, succ, cur, nxt, chg_prev, chg_now, est, sum_dist, sum_recip, ec, lo, hi,
+            light_max_deg, dense, tf, nch, merged, active, peers, ra, hot_lim, tmap);
+      else if (hint)
         k_light<LOGP, PUSH, LOGR, true><<<grid_for_warps(warps), kThreads, 0, s>>>(
             offsets, succ, cur, nxt, chg_prev, chg_now, est, sum_dist, sum_recip, ec, lo, hi,
             light_max_deg, dense, tf, nch, merged, active, peers, ra, hot_lim, tmap);
