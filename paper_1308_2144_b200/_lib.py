@@ -137,6 +137,8 @@ GRAPH_SIGNATURES = {
     "hbg_poisson_cdf": (_int, [_dbl, _vp]),
     "hbg_zipf_cdf": (None, [_dbl, _i64, _i64, _vp]),
     "hbg_gather_rows": (_i64, [_vp, _vp, _int, _vp, _i64, _vp, _vp, _int]),
+    "hbg_stage_ids": (_int, [_vp, _int, _i64, _vp, _int]),
+    "hbg_stage_bytes": (None, [_vp, _i64, _vp, _int]),
     "hbg_n": (_i64, [_vp]),
     "hbg_m": (_i64, [_vp]),
     "hbg_copy": (None, [_vp, _vp, _vp]),

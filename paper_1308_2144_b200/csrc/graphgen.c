@@ -463,6 +463,45 @@ int64_t hbg_gather_rows(const int64_t *off, const void *succ, int succ_bytes,
     return acc;
 }
 
+/* Staging for uploads from pageable host memory (schedule.py _upload_slices): n elements
+ * of src (src_bytes = 4: int32, copied; 8: the reference's int64 ids, narrowed to int32)
+ * into dst (a pinned buffer the caller then copies to the device), over `threads`
+ * pthreads -- the narrowing and the page walk run at host-memory speed on every core
+ * while the previous slice crosses PCIe.  hbg_stage_bytes: the same as a plain copy. */
+typedef struct {
+    const void *src;
+    int src_bytes;
+    void *dst;
+} stage_ctx;
+
+static void stage_fn(void *ctx, int64_t lo, int64_t hi, int tid) {
+    (void)tid;
+    stage_ctx *c = (stage_ctx *)ctx;
+    if (c->src_bytes == 8) {
+        const int64_t *s = (const int64_t *)c->src;
+        int32_t *d = (int32_t *)c->dst;
+        for (int64_t i = lo; i < hi; i++) d[i] = (int32_t)s[i];
+    } else {
+        memcpy((char *)c->dst + (size_t)lo * (size_t)c->src_bytes,
+               (const char *)c->src + (size_t)lo * (size_t)c->src_bytes,
+               (size_t)(hi - lo) * (size_t)c->src_bytes);
+    }
+}
+
+int hbg_stage_ids(const void *src, int src_bytes, int64_t n, int32_t *dst, int threads) {
+    if (src_bytes != 4 && src_bytes != 8) return -1;
+    if (threads <= 0) threads = nthreads_default();
+    stage_ctx c = {src, src_bytes, dst};
+    parallel_for(n, threads, stage_fn, &c);
+    return 0;
+}
+
+void hbg_stage_bytes(const void *src, int64_t nbytes, void *dst, int threads) {
+    if (threads <= 0) threads = nthreads_default();
+    stage_ctx c = {src, 1, dst};
+    parallel_for(nbytes, threads, stage_fn, &c);
+}
+
 int64_t hbg_n(void *h) { return ((hbg_graph *)h)->n; }
 int64_t hbg_m(void *h) { return ((hbg_graph *)h)->m; }
 void hbg_copy(void *h, int64_t *offsets, int32_t *succ) {

@@ -185,9 +185,63 @@ def slice_rows(off_host: np.ndarray, nslices: int, align: int) -> np.ndarray:
     return np.unique(np.concatenate([[0], rows, [n]])).astype(np.int64)
 
 
+# Pinned staging buffers for uploads from pageable host memory, per device: two slice
+# buffers (int32 ids) and one for the offsets, grown on demand and kept (pinning is slow),
+# each with the event of the last copy out of it.
+_STAGING = {}
+_STAGE_THREADS = int(os.environ.get("HB_STAGE_THREADS", "0"))   # 0 = every core
+
+
+def _staging(device, key: str, nbytes: int) -> list:
+    """[pinned uint8 tensor, event of its last copy] of at least `nbytes` for `device`."""
+    pool = _STAGING.setdefault(device, {})
+    ent = pool.get(key)
+    if ent is None or ent[0].numel() < nbytes:
+        if ent is not None and ent[1] is not None:
+            ent[1].synchronize()
+        ent = pool[key] = [torch.empty(max(nbytes, 1), dtype=torch.uint8, pin_memory=True),
+                           None]
+    return ent
+
+
+def _is_pinned(a: np.ndarray) -> bool:
+    try:
+        with warnings.catch_warnings():   # read-only arrays are only inspected
+            warnings.simplefilter("ignore", UserWarning)
+            return torch.from_numpy(a[:1]).is_pinned() if a.size else True
+    except Exception:
+        return False
+
+
+def _upload_offsets(offsets, device, main) -> torch.Tensor:
+    """int64 offsets on the device: a pageable host array is first copied into a pinned
+    staging buffer by every core (libhbgraph hbg_stage_bytes), so the DMA runs at the PCIe
+    rate instead of through the driver's pageable path."""
+    if isinstance(offsets, torch.Tensor):
+        return _as_device(offsets, torch.int64, device)
+    a = np.ascontiguousarray(np.asarray(offsets, dtype=np.int64))
+    if a.size < (1 << 20) or _is_pinned(a):
+        return _as_device(a, torch.int64, device)
+    ent = _staging(device, "off", a.nbytes)
+    if ent[1] is not None:
+        ent[1].synchronize()
+    _lib.graphlib().hbg_stage_bytes(a.ctypes.data, a.nbytes, ent[0].data_ptr(),
+                                    _STAGE_THREADS)
+    out = torch.empty(a.shape[0], dtype=torch.int64, device=device)
+    with torch.cuda.stream(main):
+        out.copy_(ent[0][:a.nbytes].view(torch.int64), non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(main)
+    ent[1] = ev
+    return out
+
+
 def _upload_slices(successors, off_host: np.ndarray, device, main, nslices: int, align: int):
     """int32 ids uploaded on the side stream in row slices aligned to `align` rows; returns
-    the device tensor and [(r0, r1, event)]."""
+    the device tensor and [(r0, r1, event)].  Pinned int32 ids are copied as they are;
+    pageable or int64 ids (the reference's CsrGraph) go through two pinned staging
+    buffers: every core narrows / copies slice k + 1 into one (hbg_stage_ids) while
+    slice k crosses PCIe from the other."""
     n = off_host.shape[0] - 1
     m = int(off_host[-1])
     side = _SIDE_STREAMS.get(device)
@@ -195,21 +249,45 @@ def _upload_slices(successors, off_host: np.ndarray, device, main, nslices: int,
         side = _SIDE_STREAMS[device] = torch.cuda.Stream(device=device)
     side.wait_stream(main)
     dst = torch.empty(m, dtype=torch.int32, device=device)
+    arr = np.ascontiguousarray(successors)
+    direct = arr.dtype == np.int32 and _is_pinned(arr)
     with warnings.catch_warnings():
         warnings.simplefilter("ignore", UserWarning)
-        ht = torch.from_numpy(np.ascontiguousarray(successors))
+        ht = torch.from_numpy(arr)
     rows = slice_rows(off_host, nslices, align)
+    bounds = list(zip(rows[:-1].tolist(), rows[1:].tolist()))
     slices = []
-    with torch.cuda.stream(side):
-        for r0, r1 in zip(rows[:-1].tolist(), rows[1:].tolist()):
-            a0, a1 = int(off_host[r0]), int(off_host[r1])
-            if a1 > a0:
-                if ht.dtype == torch.int32:
+    if direct:
+        with torch.cuda.stream(side):
+            for r0, r1 in bounds:
+                a0, a1 = int(off_host[r0]), int(off_host[r1])
+                if a1 > a0:
                     dst[a0:a1].copy_(ht[a0:a1], non_blocking=True)
-                else:                            # int64 ids (the reference's CsrGraph):
-                    dst[a0:a1].copy_(ht[a0:a1].to(device, non_blocking=True))  # narrow on
-            ev = torch.cuda.Event()                                             # the device
-            ev.record(side)
+                ev = torch.cuda.Event()
+                ev.record(side)
+                slices.append((r0, r1, ev))
+    else:
+        G = _lib.graphlib()
+        widest = max((int(off_host[r1]) - int(off_host[r0]) for r0, r1 in bounds), default=0)
+        bufs = [_staging(device, f"ids{i}", 4 * widest) for i in range(2)]
+        for k, (r0, r1) in enumerate(bounds):
+            a0, a1 = int(off_host[r0]), int(off_host[r1])
+            ent = bufs[k % 2]
+            if a1 > a0:
+                if ent[1] is not None:
+                    ent[1].synchronize()          # its previous slice has left the buffer
+                rc = G.hbg_stage_ids(arr.ctypes.data + a0 * arr.itemsize, arr.itemsize,
+                                     a1 - a0, ent[0].data_ptr(), _STAGE_THREADS)
+                if rc != 0:
+                    raise ValueError(f"successor ids of dtype {arr.dtype} are not int32/int64")
+                with torch.cuda.stream(side):
+                    dst[a0:a1].copy_(ent[0][:4 * (a1 - a0)].view(torch.int32),
+                                     non_blocking=True)
+            with torch.cuda.stream(side):
+                ev = torch.cuda.Event()
+                ev.record(side)
+            if a1 > a0:
+                ent[1] = ev
             slices.append((r0, r1, ev))
     dst.record_stream(side)
     return dst, slices
@@ -448,7 +526,7 @@ def build_schedule(offsets, successors, b: int, device, order: str = "auto", wor
     if world > 1 and RANK_LOCAL:
         return build_rank_local(offsets, successors, b, device, order, world, rank_id,
                                 s_main, on_order)
-    off = _as_device(offsets, torch.int64, device)
+    off = _upload_offsets(offsets, device, s_main)
     slices = None
     if (world == 1 and STREAM_SLICES > 1 and not isinstance(successors, torch.Tensor)
             and not isinstance(offsets, torch.Tensor)

@@ -145,3 +145,31 @@ def test_streamed_random_small_graphs(seed, monkeypatch):
         ref, _, _ = _run(g, b, schedule, 1, monkeypatch)
         got, _, _ = _run(g, b, schedule, int(rng.integers(2, 17)), monkeypatch)
         _same(got, ref)
+
+
+@pytest.mark.parametrize("dtype", ["int32", "int64"])
+@pytest.mark.parametrize("pinned", [True, False])
+def test_staged_and_pinned_uploads(weblike, dtype, pinned, monkeypatch):
+    """The two upload routes of the streamed path: pinned int32 ids are copied as they
+    are; pageable or int64 ids (the reference's CsrGraph) go through the pinned staging
+    ring (hbg_stage_ids narrows on every core); pageable int64 offsets through
+    hbg_stage_bytes.  Both equal the unstreamed run bit for bit."""
+    import torch
+    ref, _, _ = _run(weblike, 8, "window", 1, monkeypatch)
+    off = np.asarray(weblike.offsets, np.int64)
+    suc = np.asarray(weblike.successors).astype(dtype)
+    if pinned:
+        po = torch.empty(off.shape[0], dtype=torch.int64, pin_memory=True)
+        po.numpy()[:] = off
+        ps = torch.empty(suc.shape[0], dtype=getattr(torch, dtype), pin_memory=True)
+        ps.numpy()[:] = suc
+        off, suc = po.numpy(), ps.numpy()
+    got, pend, _ = _run(hb.CsrGraph(off, suc), 8, "window", 5, monkeypatch)
+    assert pend > 1
+    _same(ref, got)
+    # offsets above the staging threshold also take the staged route
+    big = np.zeros((1 << 20) + 1, np.int64)
+    t = sched_mod._upload_offsets(big, torch.device("cuda", 0),
+                                  torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    assert t.shape[0] == big.shape[0] and int(t.abs().sum().item()) == 0
