@@ -324,6 +324,12 @@ __device__ __forceinline__ int32_t ld_stream_id(const int32_t *p) {
                : "=r"(v) : "l"(p), "l"(evict_first_policy()));
   return v;
 }
+__device__ __forceinline__ int4 ld_stream_ids4(const int4 *p) {
+  int4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(evict_first_policy()));
+  return v;
+}
 __device__ __forceinline__ bool test_bit(const uint32_t *bm, int64_t v) {
   return (__ldg(bm + (v >> 5)) >> (v & 31)) & 1u;
 }
@@ -1288,6 +1294,22 @@ k_heavy_partial(const int64_t *__restrict__ offsets, const int32_t *__restrict__
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   uint32_t my_merged = 0;
   for (int64_t it = warp; it < n_items; it += nwarps) {
+    if (active) {
+      // frontier mode: most items are inactive -- the lanes test the warp's next 32
+      // items (it, it + nwarps, ...) at once and the warp jumps to the first active one
+      for (;;) {
+        const int64_t c = it + (int64_t)lane * nwarps;
+        const bool a = c < n_items && test_bit(active, __ldg(item_node + c));
+        const unsigned bal = __ballot_sync(0xffffffffu, a);
+        if (bal) {
+          it += (int64_t)(__ffs(bal) - 1) * nwarps;
+          break;
+        }
+        it += 32 * nwarps;
+        if (it >= n_items) break;
+      }
+      if (it >= n_items) break;
+    }
     const int64_t v = __ldg(item_node + it);
     HB_CHK(it < g_chk.items && v >= 0 && v < g_chk.rows, "k_heavy_partial item / node");
     if (active && !test_bit(active, v)) continue;   // warp-uniform: one node per item
@@ -1935,26 +1957,42 @@ __global__ void k_mark_heavy_flat(const int64_t *__restrict__ offsets,
                                   uint32_t *__restrict__ active,
                                   const uint32_t *__restrict__ filter) {
   const auto changed = make_change_test<FILT>(chg_prev, filter);
-  constexpr int IL = 8;
   const int64_t a0 = __ldg(offsets + h0), a1 = __ldg(offsets + h1);
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x * IL;
-  for (int64_t kb = a0 + ((int64_t)blockIdx.x * blockDim.x) * IL; kb < a1; kb += stride) {
-    int32_t id[IL];
-#pragma unroll
-    for (int j = 0; j < IL; j++) {
-      const int64_t k = kb + (int64_t)j * blockDim.x + threadIdx.x;
-      id[j] = k < a1 ? ld_stream_id(succ + k) : -1;
+  auto hit = [&](int64_t k) {                // id at arc k changed: mark its row
+    int64_t lo = h0, hi = h1;                // last row r with offsets[r] <= k
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (__ldg(offsets + mid) <= k) lo = mid; else hi = mid;
     }
+    if (!test_bit(active, lo)) atomicOr(active + (lo >> 5), 1u << (lo & 31));
+  };
+  // 16-byte id loads (4 ids each, IL in flight per thread) over the aligned body; the
+  // unaligned head and tail (< 4 ids each) by the first threads
+  const int64_t b0 = (a0 + 3) & ~(int64_t)3, b1 = a1 & ~(int64_t)3;
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gt < 8) {
+    const int64_t k = gt < 4 ? a0 + gt : b1 + (gt - 4);
+    if ((gt < 4 ? k < b0 && k < a1 : k < a1 && k >= b0) && changed(__ldg(succ + k))) hit(k);
+  }
+  if (b1 > b0) {
+    constexpr int IL = 4;
+    const int4 *q = reinterpret_cast<const int4 *>(succ + b0);
+    const int64_t nq = (b1 - b0) >> 2;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * IL;
+    for (int64_t qb = (int64_t)blockIdx.x * blockDim.x * IL; qb < nq; qb += stride) {
+      int4 v[IL];
 #pragma unroll
-    for (int j = 0; j < IL; j++) {
-      if (id[j] >= 0 && changed(id[j])) {
-        const int64_t k = kb + (int64_t)j * blockDim.x + threadIdx.x;
-        int64_t lo = h0, hi = h1;            // last row r with offsets[r] <= k
-        while (hi - lo > 1) {
-          const int64_t mid = (lo + hi) >> 1;
-          if (__ldg(offsets + mid) <= k) lo = mid; else hi = mid;
-        }
-        if (!test_bit(active, lo)) atomicOr(active + (lo >> 5), 1u << (lo & 31));
+      for (int j = 0; j < IL; j++) {
+        const int64_t i = qb + (int64_t)j * blockDim.x + threadIdx.x;
+        v[j] = i < nq ? ld_stream_ids4(q + i) : make_int4(-1, -1, -1, -1);
+      }
+#pragma unroll
+      for (int j = 0; j < IL; j++) {
+        const int64_t k = b0 + 4 * (qb + (int64_t)j * blockDim.x + threadIdx.x);
+        if (v[j].x >= 0 && changed(v[j].x)) hit(k);
+        if (v[j].y >= 0 && changed(v[j].y)) hit(k + 1);
+        if (v[j].z >= 0 && changed(v[j].z)) hit(k + 2);
+        if (v[j].w >= 0 && changed(v[j].w)) hit(k + 3);
       }
     }
   }
