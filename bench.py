@@ -340,14 +340,18 @@ def dense_steps(g, cfgd, local: int, steps: int, warmup: int, schedule: str = "a
     outputs = tuple(cfgd.outputs)
     need_dist = "closeness" in outputs or "lin" in outputs
 
+    step_no = [0]
+
     def step(ev0=None, ev1=None):
         """One dense iteration: union kernels (+ exchange of changed rows when N > 1: fused
         into the union epilogue with --exchange push, else pack / all-gather / scatter)."""
         from paper_1308_2144_b200.distributed import _ptr_array
         import ctypes
         npeer, pn, pc, clear = 0, None, None, 1
+        k_step = step_no[0]
+        step_no[0] += 1
         if symm is not None:
-            pnl, pcl = symm.peer_pointers(dev)
+            pnl, pcl = symm.peer_pointers(dev, k_step)     # inbox parity by step (packed)
             npeer, pn, pc, clear = len(pnl), _ptr_array(pnl), _ptr_array(pcl), 0
         if ev0 is not None:
             ev0.record(stream)
@@ -361,6 +365,7 @@ def dense_steps(g, cfgd, local: int, steps: int, warmup: int, schedule: str = "a
             sum_recip=sums.sum_recip.data_ptr(), n_peers=npeer,
             peer_nxt=ctypes.cast(pn, ctypes.c_void_p) if pn is not None else None,
             peer_chg=ctypes.cast(pc, ctypes.c_void_p) if pc is not None else None,
+            peer_packed_stride=symm.pstride if symm is not None else 0,
             nch_out=dev.counts.data_ptr(), merged_out=dev.counts.data_ptr() + 8,
             stream=stream.cuda_stream, **_lib.schedule_args(s)))
         if ev1 is not None:
@@ -371,6 +376,9 @@ def dense_steps(g, cfgd, local: int, steps: int, warmup: int, schedule: str = "a
             # pushed rows are visible; chg_prev stays all-ones so each step is iteration 1
             tot = torch.tensor([nch], dtype=torch.int64, device=dev.device)
             dist.all_reduce(tot)
+            if symm.pstride:   # packed push: unpack the peers' rows (chg_prev is all ones)
+                from paper_1308_2144_b200.distributed import unpack_inbox
+                unpack_inbox(rs, symm.inbox_of(k_step), dev.chg_prev)
         elif rs is not None:
             rs.refresh_unowned()
             ids, rows, k = rs.gather_changed()
@@ -383,6 +391,8 @@ def dense_steps(g, cfgd, local: int, steps: int, warmup: int, schedule: str = "a
         s.n_mega > 0 and s.n_heavy > s.n_mega)
     if world > 1 and symm is None:
         launches_per_step += 2 + (world - 1)   # refresh, gather, one scatter per peer
+    elif symm is not None and symm.pstride:
+        launches_per_step += 1                 # unpack of the peers' packed rows
     for _ in range(warmup):
         step()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))

@@ -147,7 +147,7 @@ int hb_union_step(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets,
  * host: fields are named, and later versions only append fields, so a caller built
  * against this header keeps working -- struct_size tells the library which fields the
  * caller knows).  Field meanings are those of hb_union_step above; struct_size must be
- * sizeof(hb_step_args).  hb_union_step is a thin wrapper that fills this struct. */
+ * at least hb_step_args_min_size().  hb_union_step is a thin wrapper that fills this struct. */
 typedef struct hb_step_args {
   uint64_t struct_size;
   /* graph (internal ids) and the row range of this call */
@@ -190,10 +190,28 @@ typedef struct hb_step_args {
   /* bounds for the checked build (libhyperball_b200_checked.so; ignored otherwise):
    * addressable register rows (0 = n) and successor ids in succ (0 = unchecked) */
   int64_t check_rows, check_m;
+  /* appended (read only when struct_size covers it; a caller built before passes the
+   * size up to check_m, hb_step_args_min_size()): with n_peers > 0, 0 stores the written
+   * rows unpacked into peer_nxt[q]; hb_push_row_stride(b) stores the rows that changed
+   * 5-bit packed into peer_nxt[q] = the peer's inbox of this step (register_width <= 5
+   * only), which the peer unpacks with hb_unpack_inbox after the step's barrier
+   * (DESIGN.md section 6). */
+  int64_t peer_packed_stride;
 } hb_step_args;
 
 int hb_union_step_v2(const hb_step_args *args);
 uint64_t hb_step_args_size(void);   /* sizeof(hb_step_args) as built */
+uint64_t hb_step_args_min_size(void); /* smallest struct_size accepted (fields up to check_m) */
+
+/* Packed push (multi-GPU, register_width <= 5): bytes per row of a peer inbox for 2^b
+ * registers (12 for b = 4, 10 * 2^b / 16 above), -1 for a bad b.  The writer stores only
+ * rows that changed this step.  hb_unpack_inbox, for every v in [0, n) outside [lo, hi):
+ * bit v set in chg_now -> nxt row v = the unpacked inbox row v; else set in
+ * chg_prev_copy (changed in the previous step only) -> nxt row v = cur row v. */
+int hb_push_row_stride(int b);
+int hb_unpack_inbox(int64_t n, int64_t lo, int64_t hi, int b, const uint32_t *chg_now,
+                    const uint32_t *chg_prev_copy, const uint8_t *inbox, const uint8_t *cur,
+                    uint8_t *nxt, void *stream);
 
 /* L2 persistence (hot_rows above): on by default.  hb_set_l2_persist(0) stops the
  * library from touching the persisting-L2 set-aside and the stream's access-policy

@@ -46,6 +46,9 @@ HB_SIGNATURES = {
     "hb_union_step_v2": (_int, [_vp]),
     "hb_set_l2_persist": (None, [_int]),
     "hb_step_args_size": (_u64, []),
+    "hb_step_args_min_size": (_u64, []),
+    "hb_push_row_stride": (_int, [_int]),
+    "hb_unpack_inbox": (_int, [_i64, _i64, _i64, _int, _vp, _vp, _vp, _vp, _vp, _vp]),
     "hb_union_step_runs": (_int, [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                   _vp, _vp, _i64, _i64, _vp, _dbl, _dbl, _int, _int, _int,
                                   _i64, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _i64, _i64, _vp,
@@ -106,6 +109,7 @@ class StepArgs(ctypes.Structure):
         ("nch_out", _vp), ("merged_out", _vp), ("hot_rows", _i64), ("active", _vp),
         ("peer_nxt", _vp), ("peer_chg", _vp), ("stream", _vp),
         ("check_rows", _i64), ("check_m", _i64),
+        ("peer_packed_stride", _i64),
     ]
 
     def __init__(self, **kw):

@@ -425,9 +425,36 @@ __device__ double estimate_row_thread(const uint8_t *row, const EstConst &ec) {
 constexpr int kMaxPeers = 7;
 struct Peers {
   int n;
+  int pstride;   // 0: rows go unpacked into the peers' nxt; > 0: 5-bit packed into their
+                 // inbox (nxt[q] = the inbox of this step), this many bytes per row
   uint8_t *nxt[kMaxPeers];
   uint32_t *chg[kMaxPeers];
 };
+
+// Packed push rows (register_width <= 5, every register < 32): each 16-register chunk ci
+// of a row travels as 80 bits -- its low 64 at byte 8 ci (two 32-bit words), its high 16
+// at byte 8 (p = 16, 12-byte stride) or 8 CH + 2 ci (p >= 32, 10 CH-byte stride).
+__host__ __device__ constexpr int push_stride(int ch) { return ch == 1 ? 12 : 10 * ch; }
+__host__ __device__ constexpr int push_hi_off(int ch, int ci) { return ch == 1 ? 8 : 8 * ch + 2 * ci; }
+// 4 registers (bytes < 32) -> 20 bits, and back
+__device__ __forceinline__ uint32_t gather5(uint32_t w) {
+  return (w & 0x1Fu) | ((w >> 3) & 0x3E0u) | ((w >> 6) & 0x7C00u) | ((w >> 9) & 0xF8000u);
+}
+__device__ __forceinline__ uint32_t spread5(uint32_t x) {
+  const uint32_t e = (x & 0x7C1Fu) * 0x41u;      // fields 0, 2 -> bytes 0, 2
+  const uint32_t o = (x & 0xF83E0u) * 0x208u;    // fields 1, 3 -> bytes 1, 3
+  return (e & 0x001F001Fu) | (o & 0x1F001F00u);
+}
+__device__ __forceinline__ void pack_chunk5(uint4 q, uint32_t &l0, uint32_t &l1, uint32_t &h) {
+  const uint32_t g0 = gather5(q.x), g1 = gather5(q.y), g2 = gather5(q.z), g3 = gather5(q.w);
+  l0 = g0 | (g1 << 20);
+  l1 = (g1 >> 12) | (g2 << 8) | (g3 << 28);
+  h = g3 >> 4;
+}
+__device__ __forceinline__ uint4 unpack_chunk5(uint32_t l0, uint32_t l1, uint32_t h) {
+  return make_uint4(spread5(l0), spread5(__funnelshift_r(l0, l1, 20)), spread5(l1 >> 8),
+                    spread5(__funnelshift_r(l1, h, 28)));
+}
 
 // numpy.maximum(x, 0.0) (centrality.py:134)
 __device__ __forceinline__ double np_max0(double x) { return (x >= 0.0 || x != x) ? x : 0.0; }
@@ -499,11 +526,27 @@ __device__ __forceinline__ bool finish_rows(const Peers &peers, bool doit, int64
     for (int c = 0; c < Gm::CPL; c++)
       *reinterpret_cast<uint4 *>(nrow + 16 * (c * Gm::G + gl)) = nw[c];
     if constexpr (PUSH) {
-      for (int q = 0; q < peers.n; q++) {
-        uint8_t *prow = peers.nxt[q] + (size_t)v * Gm::P;
+      if (peers.pstride == 0) {
+        for (int q = 0; q < peers.n; q++) {
+          uint8_t *prow = peers.nxt[q] + (size_t)v * Gm::P;
 #pragma unroll
-        for (int c = 0; c < Gm::CPL; c++)
-          *reinterpret_cast<uint4 *>(prow + 16 * (c * Gm::G + gl)) = nw[c];
+          for (int c = 0; c < Gm::CPL; c++)
+            *reinterpret_cast<uint4 *>(prow + 16 * (c * Gm::G + gl)) = nw[c];
+        }
+      } else if (changed) {   // 5-bit packed into the peers' inboxes, changed rows only:
+                              // a receiver refreshes the lazy-only rows from its own cur
+#pragma unroll
+        for (int c = 0; c < Gm::CPL; c++) {
+          const int ci = c * Gm::G + gl;
+          uint32_t l0, l1, h;
+          pack_chunk5(nw[c], l0, l1, h);
+          for (int q = 0; q < peers.n; q++) {
+            uint8_t *prow = peers.nxt[q] + (size_t)v * push_stride(Gm::CH);
+            *reinterpret_cast<uint32_t *>(prow + 8 * ci) = l0;
+            *reinterpret_cast<uint32_t *>(prow + 8 * ci + 4) = l1;
+            *reinterpret_cast<uint16_t *>(prow + push_hi_off(Gm::CH, ci)) = (uint16_t)h;
+          }
+        }
       }
     }
   }
@@ -1612,6 +1655,36 @@ __global__ void k_gather_changed(int64_t lo, int64_t hi, const uint32_t *__restr
 
 // Apply received rows: dst[ids[k]] = rows[k] (byte rows: thread per 16-byte chunk; 5-bit
 // packed rows: thread per row) and set their change bits.
+// Receiver side of the packed push, after the step's barrier, for every row v outside
+// the rank's [lo, hi): changed this step (chg_now) -> unpacked from the inbox, where its
+// owner stored it; changed only in the previous step (prev: a copy of chg_prev taken
+// before it was cleared) -> nxt = cur (the lazy double buffer, refreshed locally: nothing
+// crosses NVLink for it).  Only this rank writes its nxt, so a peer already in the next
+// step (storing into the other inbox) cannot race it.  Thread per (row, chunk).
+__global__ void k_unpack_inbox(int64_t n, int64_t lo, int64_t hi, int ch,
+                               const uint32_t *__restrict__ chg_now,
+                               const uint32_t *__restrict__ prev,
+                               const uint8_t *__restrict__ inbox,
+                               const uint8_t *__restrict__ cur, uint8_t *__restrict__ nxt) {
+  const int stride = push_stride(ch);
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n * ch;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = t / ch;
+    const int ci = (int)(t - v * ch);
+    if (v >= lo && v < hi) continue;
+    const uint32_t bit = 1u << (v & 31);
+    uint4 *dst = reinterpret_cast<uint4 *>(nxt + (size_t)v * 16 * ch) + ci;
+    if (__ldg(chg_now + (v >> 5)) & bit) {
+      const uint8_t *row = inbox + (size_t)v * stride;
+      const uint32_t l0 = __ldg(reinterpret_cast<const uint32_t *>(row + 8 * ci));
+      const uint32_t l1 = __ldg(reinterpret_cast<const uint32_t *>(row + 8 * ci + 4));
+      const uint32_t h = __ldg(reinterpret_cast<const uint16_t *>(row + push_hi_off(ch, ci)));
+      *dst = unpack_chunk5(l0, l1, h);
+    } else if (__ldg(prev + (v >> 5)) & bit) {
+      *dst = __ldg(reinterpret_cast<const uint4 *>(cur + (size_t)v * 16 * ch) + ci);
+    }
+  }
+}
 __global__ void k_scatter_rows(int64_t k, const int32_t *__restrict__ ids,
                                const uint8_t *__restrict__ rows, int p, int packed,
                                uint8_t *__restrict__ dst, uint32_t *__restrict__ bits) {
@@ -2724,8 +2797,9 @@ int hb_estimate_rows(const uint8_t *regs, int64_t lo, int64_t hi, int b,
 }
 
 int hb_union_step_v2(const hb_step_args *a) {
-  if (!a || a->struct_size < sizeof(hb_step_args))
-    return set_err_msg("hb_union_step_v2: null args or struct_size < sizeof(hb_step_args)");
+  if (!a || a->struct_size < offsetof(hb_step_args, peer_packed_stride))
+    return set_err_msg("hb_union_step_v2: null args or struct_size < hb_step_args_min_size()");
+  const int64_t pstride = a->struct_size >= sizeof(hb_step_args) ? a->peer_packed_stride : 0;
   DevGuard dg_((cudaStream_t)a->stream);
   const int n_peers = a->n_peers, n_disc = a->n_disc;
   const int64_t n = a->n, lo = a->lo, hi = a->hi, t = a->t;
@@ -2737,6 +2811,11 @@ int hb_union_step_v2(const hb_step_args *a) {
   for (int q = 0; q < n_peers; q++) {
     peers.nxt[q] = a->peer_nxt[q];
     peers.chg[q] = a->peer_chg[q];
+  }
+  if (n_peers > 0 && pstride != 0) {
+    if (pstride != push_stride((1 << a->b) / 16))
+      return set_err_msg("hb_union_step: peer_packed_stride must be hb_push_row_stride(b)");
+    peers.pstride = (int)pstride;
   }
   if (n_disc < 0 || n_disc > kMaxDisc || (n_disc > 0 && (!a->disc || !a->disc_scale)))
     return set_err_msg("hb_union_step: bad discount arguments (at most 8 fused)");
@@ -2822,6 +2901,27 @@ int hb_union_step(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets,
 
 void hb_set_l2_persist(int enable) { g_l2_persist = enable != 0; }
 uint64_t hb_step_args_size(void) { return sizeof(hb_step_args); }
+uint64_t hb_step_args_min_size(void) { return offsetof(hb_step_args, peer_packed_stride); }
+
+int hb_push_row_stride(int b) {
+  if (b < HB_MIN_B || b > HB_MAX_B) return -1;
+  return push_stride((1 << b) / 16);
+}
+
+int hb_unpack_inbox(int64_t n, int64_t lo, int64_t hi, int b, const uint32_t *chg_now,
+                    const uint32_t *chg_prev_copy, const uint8_t *inbox, const uint8_t *cur,
+                    uint8_t *nxt, void *stream) {
+  DevGuard dg_((cudaStream_t)stream);
+  if (b < HB_MIN_B || b > HB_MAX_B || n < 0 || lo < 0 || hi > n || lo > hi)
+    return set_err_msg("hb_unpack_inbox: bad arguments");
+  if (n == 0) return 0;
+  if (!chg_now || !chg_prev_copy || !inbox || !cur || !nxt)
+    return set_err_msg("hb_unpack_inbox: null array");
+  const int ch = (1 << b) / 16;
+  k_unpack_inbox<<<grid_for_threads(n * ch), kThreads, 0, (cudaStream_t)stream>>>(
+      n, lo, hi, ch, chg_now, chg_prev_copy, inbox, cur, nxt);
+  return check_launch("k_unpack_inbox");
+}
 
 int hb_union_step_runs(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets,
                        const int32_t *succ, const uint8_t *cur, uint8_t *nxt,

@@ -267,13 +267,29 @@ def iterate_push(state: "CudaRankState", symm: SymmetricBuffers, t: int, dense: 
                  group=None) -> int:
     """One fused-push iteration: union epilogue stores into the peers, then one NCCL
     all-reduce of the changed count -- the termination test (engine.py:390) and the
-    barrier after which every rank's pushed rows are visible -- then swap."""
-    peer_nxt, peer_chg = symm.peer_pointers(state.dev)
-    nch = push_step(state, t, dense, peer_nxt, peer_chg)
+    barrier after which every rank's pushed rows are visible -- then (packed push) the
+    rows the peers wrote are unpacked from this step's inbox, then swap."""
+    peer_nxt, peer_chg = symm.peer_pointers(state.dev, t)
+    nch = push_step(state, t, dense, peer_nxt, peer_chg, symm.pstride, symm.prev_copy)
     tot = torch.tensor([nch], dtype=torch.int64, device=state.dev.device)
     dist.all_reduce(tot, group=group)
+    if symm.pstride:
+        unpack_inbox(state, symm.inbox_of(t), symm.prev_copy)
     state.swap()
     return int(tot.item())
+
+
+def unpack_inbox(state: "CudaRankState", inbox: torch.Tensor, prev_copy: torch.Tensor) -> None:
+    """Packed push, receiver side (after the step's barrier), rows of the other ranks:
+    changed this step -> unpacked from `inbox`; changed in the previous step only -> nxt =
+    cur (the lazy double buffer, refreshed locally)."""
+    d = state.dev
+    _lib.check(_lib.hb().hb_unpack_inbox(d.n, state.lo, state.hi, d.b, d.chg_now.data_ptr(),
+                                         prev_copy.data_ptr(), inbox.data_ptr(),
+                                         d.cur.data_ptr(), d.nxt.data_ptr(),
+                                         d.stream.cuda_stream),
+               "hb_unpack_inbox")
+    d.launches += 1
 
 
 def run_distributed(g, config: HyperBallConfig, observers: Iterable = (), group=None,
@@ -340,30 +356,54 @@ def _ptr_array(ptrs):
     return arr
 
 
-def push_step(state: "CudaRankState", t: int, dense: bool, peer_nxt, peer_chg) -> int:
+def push_step(state: "CudaRankState", t: int, dense: bool, peer_nxt, peer_chg,
+              pstride: int = 0, prev_copy: torch.Tensor | None = None) -> int:
     """Union step whose epilogue stores this rank's written rows and change bits straight
-    into every peer's replica (hb_union_step with peers).  Afterwards this rank's chg_prev
-    is cleared: it becomes chg_now of the next step, into which peers may push only after
-    the barrier that follows.  Returns the LOCAL changed count."""
+    into every peer's replica (hb_union_step with peers) -- or, with pstride > 0, into
+    the peers' inboxes 5-bit packed (peer_nxt are then inbox addresses).  Afterwards this
+    rank's chg_prev is cleared: it becomes chg_now of the next step, into which peers may
+    push only after the barrier that follows; a packed push first keeps a copy of it
+    (prev_copy) for the unpack after the barrier.  Returns the LOCAL changed count."""
     d = state.dev
     n_peers = len(peer_nxt)
     nch = d.union_step(t, dense, state.sums,
-                       peers=(n_peers, _ptr_array(peer_nxt), _ptr_array(peer_chg)),
+                       peers=(n_peers, _ptr_array(peer_nxt), _ptr_array(peer_chg), pstride),
                        clear_chg_now=False)
+    if pstride:
+        prev_copy.copy_(d.chg_prev)
     d.chg_prev.zero_()
     return nch
+
+
+def packed_push_stride(state: "CudaRankState", packed: bool = True) -> int:
+    """Bytes per inbox row of the packed push (0 = rows travel unpacked): 5-bit fields need
+    every register < 32, i.e. register_width <= 5."""
+    if not packed or state.dev.params.register_width > 5:
+        return 0
+    return int(_lib.hb().hb_push_row_stride(state.dev.b))
 
 
 class SymmetricBuffers:
     """The register double buffer and the two change bitmaps of one rank in symmetric
     memory (torch.distributed._symmetric_memory): every peer maps them, so the union
-    epilogue can store into them over NVLink."""
+    epilogue can store into them over NVLink.  With the packed push (register_width <=
+    5) the peers store 5-bit packed rows into a double-buffered inbox instead (step t
+    uses inbox t % 2: a peer one step ahead writes the other one), and this rank unpacks
+    them after the step's barrier -- 37.5% fewer NVLink bytes per row (25% at p = 16)."""
 
-    def __init__(self, state: "CudaRankState", group=None):
+    def __init__(self, state: "CudaRankState", group=None, packed: bool = True):
         import torch.distributed._symmetric_memory as symm
         d = state.dev
         n, p = d.n, d.p
         words = d.chg_prev.numel()
+        self.pstride = packed_push_stride(state, packed)
+        gname = group.group_name if group is not None else dist.group.WORLD.group_name
+        if self.pstride:
+            self.inbox = symm.empty((2, n, self.pstride), dtype=torch.uint8, device=d.device)
+            self.h_inbox = symm.rendezvous(self.inbox, gname)
+            self.prev_copy = torch.zeros_like(d.chg_prev)
+        else:
+            self.inbox = self.h_inbox = self.prev_copy = None
         self.regs = symm.empty((2, n, p), dtype=torch.uint8, device=d.device)
         self.bits = symm.empty((2, words), dtype=torch.int32, device=d.device)
         self.regs[0].copy_(d.cur)
@@ -372,18 +412,26 @@ class SymmetricBuffers:
         self.bits[1].zero_()
         d.cur, d.nxt = self.regs[0], self.regs[1]
         d.chg_prev, d.chg_now = self.bits[0], self.bits[1]
-        gname = group.group_name if group is not None else dist.group.WORLD.group_name
         self.h_regs = symm.rendezvous(self.regs, gname)
         self.h_bits = symm.rendezvous(self.bits, gname)
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
 
-    def peer_pointers(self, d):
-        on = d.nxt.data_ptr() - self.regs.data_ptr()
+    def inbox_of(self, t: int) -> torch.Tensor:
+        return self.inbox[t & 1]
+
+    def peer_pointers(self, d, t: int = 0):
+        """Peer addresses the union epilogue of step t stores into: their nxt buffers (or
+        their step-t inboxes, packed) and their chg_now bitmaps."""
         oc = d.chg_now.data_ptr() - self.bits.data_ptr()
         qs = [q for q in range(self.world) if q != self.rank]
-        return ([int(self.h_regs.buffer_ptrs[q]) + on for q in qs],
-                [int(self.h_bits.buffer_ptrs[q]) + oc for q in qs])
+        if self.pstride:
+            oi = self.inbox_of(t).data_ptr() - self.inbox.data_ptr()
+            rows = [int(self.h_inbox.buffer_ptrs[q]) + oi for q in qs]
+        else:
+            on = d.nxt.data_ptr() - self.regs.data_ptr()
+            rows = [int(self.h_regs.buffer_ptrs[q]) + on for q in qs]
+        return rows, [int(self.h_bits.buffer_ptrs[q]) + oc for q in qs]
 
 
 def run_simulated(g, config: HyperBallConfig, world: int, observers: Iterable = (),
@@ -392,6 +440,13 @@ def run_simulated(g, config: HyperBallConfig, world: int, observers: Iterable = 
     another rank).  Exercises the partition and every exchange kernel; results must be
     bit-identical to the single-GPU run."""
     states = [CudaRankState(g, config, world, r, packed) for r in range(world)]
+    pstride = packed_push_stride(states[0], packed) if exchange == "push" else 0
+    inboxes, prev_copies = {}, {}
+    if pstride:
+        for s in states:
+            inboxes[id(s)] = torch.empty((2, s.n, pstride), dtype=torch.uint8,
+                                         device=s.dev.device)
+            prev_copies[id(s)] = torch.zeros_like(s.dev.chg_prev)
     observers = list(observers)
     accs = [o for o in observers if fusable(o, states[0].n)]
     if accs:
@@ -405,13 +460,22 @@ def run_simulated(g, config: HyperBallConfig, world: int, observers: Iterable = 
             dense = (t == 0 or not config.skip_stable_nodes
                      or nch >= DENSE_FRAC * states[0].n)
             if exchange == "push":
-                # every rank's epilogue writes into the other ranks' buffers; the ranks
-                # run one after another, so no kernel ever waits on another
+                # every rank's epilogue writes into the other ranks' buffers (or packed
+                # inboxes); the ranks run one after another, so no kernel ever waits on
+                # another; the packed rows are unpacked once every rank has pushed
                 nch = 0
                 for s in states:
                     peers = [q for q in states if q is not s]
-                    nch += push_step(s, t + 1, dense, [q.dev.nxt.data_ptr() for q in peers],
-                                     [q.dev.chg_now.data_ptr() for q in peers])
+                    if pstride:
+                        rows = [inboxes[id(q)][(t + 1) & 1].data_ptr() for q in peers]
+                    else:
+                        rows = [q.dev.nxt.data_ptr() for q in peers]
+                    nch += push_step(s, t + 1, dense, rows,
+                                     [q.dev.chg_now.data_ptr() for q in peers], pstride,
+                                     prev_copies.get(id(s)))
+                if pstride:
+                    for s in states:
+                        unpack_inbox(s, inboxes[id(s)][(t + 1) & 1], prev_copies[id(s)])
             else:
                 for s in states:
                     s.local_step(t + 1, dense)

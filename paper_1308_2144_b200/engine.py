@@ -549,11 +549,13 @@ class _Device:
 
     def union_step(self, t: int, dense: bool, sums: _DeviceSums | None, peers=None,
                    clear_chg_now: bool = True, flag_arcs: bool = False) -> int:
-        """One hb_union_step.  peers: (n, host uint8** array, host uint32** array) of peer
-        nxt / chg_now device addresses for the fused multi-GPU push (distributed.py)."""
+        """One hb_union_step.  peers: (n, host uint8** array, host uint32** array[, packed
+        row stride]) of peer nxt (or, packed, inbox) / chg_now device addresses for the
+        fused multi-GPU push (distributed.py)."""
         s = self.sched
         active = self._frontier_ptr(dense) if peers is None else None
-        n_peers, peer_nxt, peer_chg = peers if peers is not None else (0, None, None)
+        n_peers, peer_nxt, peer_chg = peers[:3] if peers is not None else (0, None, None)
+        pstride = peers[3] if peers is not None and len(peers) > 3 else 0
         light_hi = s.light_hi if self.full_pass else s.light_hi_steady
         sd = sums.sum_dist.data_ptr() if sums is not None else None
         sr = sums.sum_recip.data_ptr() if sums is not None else None
@@ -591,7 +593,7 @@ class _Device:
                 peer_nxt=ctypes.cast(peer_nxt, ctypes.c_void_p) if peer_nxt is not None
                 else None,
                 peer_chg=ctypes.cast(peer_chg, ctypes.c_void_p) if peer_chg is not None
-                else None,
+                else None, peer_packed_stride=pstride,
                 stream=self.stream.cuda_stream, **_lib.schedule_args(s)))
             self.launches += (hi > lo) + (s.n_items > 0) + (s.n_heavy > 0)
         if len(parts) > 1:

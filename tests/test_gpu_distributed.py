@@ -60,20 +60,22 @@ def test_simulated_heavy_rmat_matches_single_gpu():
     assert np.array_equal(a1.sum_recip.view(np.uint64), a4.sum_recip.view(np.uint64))
 
 
+@pytest.mark.parametrize("packed", [True, False])
 @pytest.mark.parametrize("world", [2, 4, 8])
 @pytest.mark.parametrize("schedule", ["identity", "degree"])
 @pytest.mark.parametrize("key", ["random300_b6_s42_w5", "disc14_b4_s42_w5", "rmat12_b7_s42_w5",
                                  "config1_b6_s42_w5", "web14_b8_s42_w5"])
-def test_fused_push_matches_reference(key, world, schedule):
+def test_fused_push_matches_reference(key, world, schedule, packed):
     """The fused push (hb_union_step storing rows and change bits into every peer's
-    replica) on simulated ranks: bit-identical to the reference."""
+    replica -- or 5-bit packed into the peers' inboxes, unpacked after the step) on
+    simulated ranks: bit-identical to the reference."""
     case = CASES[key]
     off, suc = golden_graph(case)
     g = hb.CsrGraph(off, suc)
     acc = hb.CentralityAccumulator(g.n)
     cfg = hb.HyperBallConfig(params=hb.CounterParams(b=case["b"], seed=int(case["seed"])),
                              schedule=schedule)
-    res = run_simulated(g, cfg, world, [acc], exchange="push")
+    res = run_simulated(g, cfg, world, [acc], exchange="push", packed=packed)
     assert res.t == case["t"]
     for regs in res.registers:
         assert sha(regs) == case["reg_digests"][-1]
@@ -242,3 +244,36 @@ def test_rank_local_csr(world, schedule, on_device):
     assert res.t == case["t"]
     for regs in res.registers:
         assert sha(regs) == case["reg_digests"][-1]
+
+
+def test_packed_push_layout():
+    """hb_push_row_stride: 12 bytes per row at p = 16 (25% below 16), 10 per 16 registers
+    above (37.5% below p); wider registers fall back to the unpacked push."""
+    from paper_1308_2144_b200 import _lib
+    from paper_1308_2144_b200.distributed import CudaRankState, packed_push_stride
+    L = _lib.hb()
+    assert [L.hb_push_row_stride(b) for b in (4, 5, 6, 8, 12)] == [12, 20, 40, 160, 2560]
+    assert L.hb_push_row_stride(3) == -1
+    g = hb.CsrGraph.from_edges(np.arange(9), np.arange(1, 10), n=10)
+    for width, want in ((5, 40), (6, 0)):
+        cfg = hb.HyperBallConfig(params=hb.CounterParams(b=6, register_width=width))
+        assert packed_push_stride(CudaRankState(g, cfg, 2, 0)) == want
+
+
+def test_packed_push_wide_registers_unpacked():
+    """register_width 6 (registers up to 59 need 6 bits): the push stays unpacked and the
+    run is still bit-identical to one device."""
+    case = CASES["rmat12_b7_s42_w5"]
+    off, suc = golden_graph(case)
+    g = hb.CsrGraph(off, suc)
+    cfg = hb.HyperBallConfig(params=hb.CounterParams(b=7, seed=3, register_width=6),
+                             schedule="degree")
+    a1 = hb.CentralityAccumulator(g.n)
+    st = hb.run(g, cfg, [a1])
+    a2 = hb.CentralityAccumulator(g.n)
+    res = run_simulated(g, cfg, 3, [a2], exchange="push")
+    assert res.t == st.t
+    for regs in res.registers:
+        assert sha(regs) == sha(st.register_matrix())
+    assert np.array_equal(hb.finalize_harmonic(a1).view(np.uint64),
+                          hb.finalize_harmonic(a2).view(np.uint64))
