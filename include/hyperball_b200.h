@@ -247,6 +247,34 @@ int hb_scatter_rows(int64_t k, const int32_t *ids, const uint8_t *rows, int b, i
 int hb_refresh_rows(int64_t n, int64_t lo, int64_t hi, const uint32_t *bits, const uint8_t *src,
                     uint8_t *dst, int b, void *stream);
 
+/* Schedule setup on the device (schedule.py).
+ * hb_max_degree: *out (host) = max in-degree offsets[v+1] - offsets[v] over v < n;
+ *   scratch: device uint64 [1].  Synchronises the stream.
+ * hb_schedule_order: node order of the `degree` (order 1: stable sort by descending
+ *   in-degree; with world > 1 the ranking is dealt round-robin, position j to rank j % W,
+ *   slot bounds[j % W] + j / W) or `window` (order 2: stable sort by descending in-degree
+ *   inside each light-kernel chunk window of each rank's range) schedule: perm[i] = old
+ *   row of internal id i, rank = its inverse, new_offsets [n+1] = the prefix sums of the
+ *   permuted in-degrees.  bounds: host int64 [world + 1] rank ranges.  temp == NULL
+ *   queries *temp_bytes (keys / values / cub scratch).
+ * hb_heavy_items: work items of the heavy rows (in-degree > light_max_deg) among rows
+ *   [lo, lo + nrows) whose offsets are row_offsets[0..nrows] (global or rank-local
+ *   positions): heavy[j] = row id, item_first [n_heavy + 1], item_node / item_beg
+ *   [n_items] (slices of <= item_arcs arcs), finish_order = heavy indices, those with
+ *   more than mega_items items first.  counts (host int64 [4]) receives n_heavy, n_items,
+ *   n_mega and the number of rows with in-degree > 0; a call with heavy == NULL only
+ *   counts (the caller then allocates the outputs and calls again).  temp == NULL
+ *   queries *temp_bytes.  Synchronises the stream. */
+int hb_max_degree(int64_t n, const int64_t *offsets, uint64_t *scratch, int64_t *out,
+                  void *stream);
+int hb_schedule_order(int64_t n, const int64_t *offsets, int order, int b, int world,
+                      const int64_t *bounds, int32_t *perm, int32_t *rank,
+                      int64_t *new_offsets, void *temp, uint64_t *temp_bytes, void *stream);
+int hb_heavy_items(int64_t nrows, int64_t lo, const int64_t *row_offsets, int64_t light_max_deg,
+                   int64_t item_arcs, int64_t mega_items, int32_t *heavy, int32_t *item_first,
+                   int32_t *item_node, int64_t *item_beg, int32_t *finish_order,
+                   int64_t *counts, void *temp, uint64_t *temp_bytes, void *stream);
+
 /* Relabel a CSR into schedule order: new row i is old row perm[i] with every id mapped
  * through rank (rank[perm[i]] == i).  new_offsets (device int64 [n+1]) must already hold
  * the prefix sums of the permuted degrees. */

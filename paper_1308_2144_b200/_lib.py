@@ -48,6 +48,11 @@ HB_SIGNATURES = {
     "hb_step_args_size": (_u64, []),
     "hb_step_args_min_size": (_u64, []),
     "hb_push_row_stride": (_int, [_int]),
+    "hb_max_degree": (_int, [_i64, _vp, _vp, _vp, _vp]),
+    "hb_schedule_order": (_int, [_i64, _vp, _int, _int, _int, _vp, _vp, _vp, _vp, _vp, _vp,
+                                 _vp]),
+    "hb_heavy_items": (_int, [_i64, _i64, _vp, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp,
+                              _vp, _vp, _vp, _vp]),
     "hb_unpack_inbox": (_int, [_i64, _i64, _i64, _int, _vp, _vp, _vp, _vp, _vp, _vp]),
     "hb_union_step_runs": (_int, [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                   _vp, _vp, _i64, _i64, _vp, _dbl, _dbl, _int, _int, _int,

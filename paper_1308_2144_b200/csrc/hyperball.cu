@@ -3356,6 +3356,245 @@ int hb_keys_to_csr(int64_t n, int64_t m, uint64_t *keys, uint64_t *alt, void *te
   return check_launch("k_keys_to_csr");
 }
 
+// ------------------------------------------------------------------ schedule setup
+// Node order, relabelled offsets and heavy-node work items of schedule.py, on the device.
+struct RankBounds {
+  int64_t b[kMaxPeers + 2];
+  int world;
+};
+__device__ __forceinline__ int owner_rank(const RankBounds &rb, int64_t v) {
+  int r = 0;
+  while (r + 1 < rb.world && v >= rb.b[r + 1]) r++;
+  return r;
+}
+// key per node: order 1 (degree) 0xFFFFFFFF - in-degree, so an ascending stable sort is by
+// descending in-degree; order 2 (window) the same in the low 32 bits under the global index
+// of the node's light-kernel chunk window (rank r, window w of its range) in the high 32
+__global__ void k_order_keys(int64_t n, const int64_t *__restrict__ off, int order, int64_t win,
+                             int64_t npw, RankBounds rb, uint64_t *__restrict__ keys,
+                             int32_t *__restrict__ vals) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t dk = 0xFFFFFFFFull - (uint64_t)(__ldg(off + v + 1) - __ldg(off + v));
+    uint64_t key = dk;
+    if (order == 2) {
+      const int r = owner_rank(rb, v);
+      const int64_t lo_al = rb.b[r] / npw * npw;
+      const uint64_t g = (uint64_t)r * (uint64_t)(n / win + 2) + (uint64_t)((v - lo_al) / win);
+      key |= g << 32;
+    }
+    keys[v] = key;
+    vals[v] = (int32_t)v;
+  }
+}
+// sorted position j -> internal id (degree order dealt round-robin over the ranks: ranking
+// position j goes to rank j % W, slot j / W of its range); perm, rank, permuted degrees
+__global__ void k_order_finish(int64_t n, const int32_t *__restrict__ sorted, int deal,
+                               RankBounds rb, const int64_t *__restrict__ off,
+                               int32_t *__restrict__ perm, int32_t *__restrict__ rank,
+                               int64_t *__restrict__ new_deg) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = __ldg(sorted + j);
+    const int64_t pos = deal ? rb.b[j % rb.world] + j / rb.world : j;
+    perm[pos] = v;
+    rank[v] = (int32_t)pos;
+    new_deg[pos] = __ldg(off + v + 1) - __ldg(off + v);
+  }
+}
+__global__ void k_degree_max(int64_t n, const int64_t *__restrict__ off,
+                             unsigned long long *__restrict__ out) {
+  int64_t mx = 0;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x)
+    mx = max(mx, __ldg(off + v + 1) - __ldg(off + v));
+  mx = (int64_t)__reduce_max_sync(0xffffffffu, (unsigned)mx);
+  if ((threadIdx.x & 31) == 0 && mx) atomicMax(out, (unsigned long long)mx);
+}
+// heavy rows of rows [lo, lo + nrows): flags and counts per row for the scans
+__global__ void k_heavy_flags(int64_t nrows, const int64_t *__restrict__ row_off,
+                              int64_t light_max_deg, int64_t item_arcs, int64_t mega_items,
+                              int64_t *__restrict__ hflag, int64_t *__restrict__ icnt,
+                              int64_t *__restrict__ mflag, unsigned long long *__restrict__ nonzero) {
+  uint32_t nz = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nrows;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t d = __ldg(row_off + i + 1) - __ldg(row_off + i);
+    const bool h = d > light_max_deg;
+    const int64_t c = h ? (d + item_arcs - 1) / item_arcs : 0;
+    hflag[i] = h;
+    icnt[i] = c;
+    mflag[i] = c > mega_items;
+    nz += d > 0;
+  }
+  nz = __reduce_add_sync(0xffffffffu, nz);
+  if ((threadIdx.x & 31) == 0 && nz) atomicAdd(nonzero, (unsigned long long)nz);
+}
+__global__ void k_heavy_fill(int64_t nrows, int64_t lo, const int64_t *__restrict__ row_off,
+                             int64_t item_arcs, const int64_t *__restrict__ hflag,
+                             const int64_t *__restrict__ icnt, const int64_t *__restrict__ mflag,
+                             const int64_t *__restrict__ hidx, const int64_t *__restrict__ isum,
+                             const int64_t *__restrict__ midx, int64_t n_heavy, int64_t n_items,
+                             int64_t n_mega, int32_t *__restrict__ heavy,
+                             int32_t *__restrict__ item_first, int32_t *__restrict__ item_node,
+                             int64_t *__restrict__ item_beg, int32_t *__restrict__ finish_order) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nrows;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i == 0) item_first[n_heavy] = (int32_t)n_items;
+    if (!hflag[i]) continue;
+    const int64_t j = hidx[i], f = isum[i], c = icnt[i], b0 = __ldg(row_off + i);
+    heavy[j] = (int32_t)(lo + i);
+    item_first[j] = (int32_t)f;
+    for (int64_t k = 0; k < c; k++) {
+      item_node[f + k] = (int32_t)(lo + i);
+      item_beg[f + k] = b0 + k * item_arcs;
+    }
+    // mega nodes first (in heavy order), then the others
+    finish_order[mflag[i] ? midx[i] : n_mega + (j - midx[i])] = (int32_t)j;
+  }
+}
+__global__ void k_heavy_totals(int64_t nrows, const int64_t *__restrict__ hflag,
+                               const int64_t *__restrict__ icnt, const int64_t *__restrict__ mflag,
+                               const int64_t *__restrict__ hidx, const int64_t *__restrict__ isum,
+                               const int64_t *__restrict__ midx, int64_t *__restrict__ out) {
+  const int64_t l = nrows - 1;
+  out[0] = nrows ? hidx[l] + hflag[l] : 0;
+  out[1] = nrows ? isum[l] + icnt[l] : 0;
+  out[2] = nrows ? midx[l] + mflag[l] : 0;
+}
+
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+int hb_max_degree(int64_t n, const int64_t *offsets, uint64_t *scratch, int64_t *out,
+                  void *stream) {
+  DevGuard dg_((cudaStream_t)stream);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!out || !scratch || n < 0 || (n > 0 && !offsets))
+    return set_err_msg("hb_max_degree: bad arguments");
+  *out = 0;
+  if (n == 0) return 0;
+  unsigned long long *d = reinterpret_cast<unsigned long long *>(scratch);
+  cudaError_t e = cudaMemsetAsync(d, 0, sizeof(*d), s);
+  if (e != cudaSuccess) return set_err("hb_max_degree memset", e);
+  k_degree_max<<<grid_for_threads(n), kThreads, 0, s>>>(n, offsets, d);
+  unsigned long long h = 0;
+  e = cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return set_err("hb_max_degree", e);
+  *out = (int64_t)h;
+  return 0;
+}
+
+int hb_schedule_order(int64_t n, const int64_t *offsets, int order, int b, int world,
+                      const int64_t *bounds, int32_t *perm, int32_t *rank,
+                      int64_t *new_offsets, void *temp, uint64_t *temp_bytes, void *stream) {
+  DevGuard dg_((cudaStream_t)stream);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!temp_bytes || (order != 1 && order != 2) || world < 1 || world > kMaxPeers + 1 ||
+      b < HB_MIN_B || b > HB_MAX_B || n < 0 || n > INT32_MAX || !bounds)
+    return set_err_msg("hb_schedule_order: bad arguments");
+  const int end_bit = order == 1 ? 32 : 64;
+  size_t b_sort = 0, b_scan = 0;
+  cub::DoubleBuffer<uint64_t> dk(nullptr, nullptr);
+  cub::DoubleBuffer<int32_t> dv(nullptr, nullptr);
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, b_sort, dk, dv, (int)n, 0, end_bit, s);
+  if (e == cudaSuccess)
+    e = cub::DeviceScan::InclusiveSum(nullptr, b_scan, (int64_t *)nullptr, (int64_t *)nullptr,
+                                      (int)n, s);
+  if (e != cudaSuccess) return set_err("hb_schedule_order size", e);
+  const size_t k8 = align256(8 * (size_t)n), v4 = align256(4 * (size_t)n);
+  const size_t need = 2 * k8 + 2 * v4 + std::max(b_sort, b_scan) + 256;
+  if (!temp) {
+    *temp_bytes = need;
+    return 0;
+  }
+  if (*temp_bytes < need) return set_err_msg("hb_schedule_order: temp buffer too small");
+  if (n == 0) return cudaMemsetAsync(new_offsets, 0, 8, s) == cudaSuccess ? 0 : set_err_msg("memset");
+  if (!offsets || !perm || !rank || !new_offsets) return set_err_msg("hb_schedule_order: null array");
+  char *t = reinterpret_cast<char *>(temp);
+  uint64_t *k0 = reinterpret_cast<uint64_t *>(t), *k1 = reinterpret_cast<uint64_t *>(t + k8);
+  int32_t *v0 = reinterpret_cast<int32_t *>(t + 2 * k8);
+  int32_t *v1 = reinterpret_cast<int32_t *>(t + 2 * k8 + v4);
+  void *scratch = t + 2 * k8 + 2 * v4;
+  RankBounds rb;
+  memset(&rb, 0, sizeof(rb));
+  rb.world = world;
+  for (int r = 0; r <= world; r++) rb.b[r] = bounds[r];
+  k_order_keys<<<grid_for_threads(n), kThreads, 0, s>>>(n, offsets, order, hb_light_window(b),
+                                                        hb_light_npw(b), rb, k0, v0);
+  if (int er = check_launch("k_order_keys")) return er;
+  cub::DoubleBuffer<uint64_t> keys(k0, k1);
+  cub::DoubleBuffer<int32_t> vals(v0, v1);
+  size_t bytes = need - 2 * k8 - 2 * v4;
+  e = cub::DeviceRadixSort::SortPairs(scratch, bytes, keys, vals, (int)n, 0, end_bit, s);
+  if (e != cudaSuccess) return set_err("hb_schedule_order sort", e);
+  int64_t *new_deg = reinterpret_cast<int64_t *>(keys.Alternate());   // free after the sort
+  k_order_finish<<<grid_for_threads(n), kThreads, 0, s>>>(n, vals.Current(),
+                                                          order == 1 && world > 1, rb, offsets,
+                                                          perm, rank, new_deg);
+  if (int er = check_launch("k_order_finish")) return er;
+  if ((e = cudaMemsetAsync(new_offsets, 0, 8, s)) != cudaSuccess)
+    return set_err("hb_schedule_order memset", e);
+  bytes = need - 2 * k8 - 2 * v4;
+  e = cub::DeviceScan::InclusiveSum(scratch, bytes, new_deg, new_offsets + 1, (int)n, s);
+  if (e != cudaSuccess) return set_err("hb_schedule_order scan", e);
+  return 0;
+}
+
+int hb_heavy_items(int64_t nrows, int64_t lo, const int64_t *row_offsets, int64_t light_max_deg,
+                   int64_t item_arcs, int64_t mega_items, int32_t *heavy, int32_t *item_first,
+                   int32_t *item_node, int64_t *item_beg, int32_t *finish_order,
+                   int64_t *counts, void *temp, uint64_t *temp_bytes, void *stream) {
+  DevGuard dg_((cudaStream_t)stream);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!temp_bytes || nrows < 0 || nrows > INT32_MAX || item_arcs < 1)
+    return set_err_msg("hb_heavy_items: bad arguments");
+  size_t b_scan = 0;
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, b_scan, (int64_t *)nullptr,
+                                                (int64_t *)nullptr, (int)std::max<int64_t>(nrows, 1), s);
+  if (e != cudaSuccess) return set_err("hb_heavy_items size", e);
+  const size_t a8 = align256(8 * (size_t)std::max<int64_t>(nrows, 1));
+  const size_t need = 6 * a8 + 256 + b_scan;
+  if (!temp) {
+    *temp_bytes = need;
+    return 0;
+  }
+  if (*temp_bytes < need) return set_err_msg("hb_heavy_items: temp buffer too small");
+  if (!counts) return set_err_msg("hb_heavy_items: counts");
+  char *t = reinterpret_cast<char *>(temp);
+  int64_t *hflag = (int64_t *)t, *icnt = (int64_t *)(t + a8), *mflag = (int64_t *)(t + 2 * a8);
+  int64_t *hidx = (int64_t *)(t + 3 * a8), *isum = (int64_t *)(t + 4 * a8), *midx = (int64_t *)(t + 5 * a8);
+  int64_t *dtot = (int64_t *)(t + 6 * a8);              // n_heavy, n_items, n_mega, nonzero
+  void *scratch = t + 6 * a8 + 256;
+  if ((e = cudaMemsetAsync(dtot, 0, 32, s)) != cudaSuccess) return set_err("hb_heavy_items memset", e);
+  if (nrows > 0) {
+    if (!row_offsets) return set_err_msg("hb_heavy_items: null offsets");
+    k_heavy_flags<<<grid_for_threads(nrows), kThreads, 0, s>>>(
+        nrows, row_offsets, light_max_deg, item_arcs, mega_items, hflag, icnt, mflag,
+        reinterpret_cast<unsigned long long *>(dtot + 3));
+    size_t bytes = b_scan;
+    e = cub::DeviceScan::ExclusiveSum(scratch, bytes, hflag, hidx, (int)nrows, s);
+    if (e == cudaSuccess) { bytes = b_scan; e = cub::DeviceScan::ExclusiveSum(scratch, bytes, icnt, isum, (int)nrows, s); }
+    if (e == cudaSuccess) { bytes = b_scan; e = cub::DeviceScan::ExclusiveSum(scratch, bytes, mflag, midx, (int)nrows, s); }
+    if (e != cudaSuccess) return set_err("hb_heavy_items scan", e);
+    k_heavy_totals<<<1, 1, 0, s>>>(nrows, hflag, icnt, mflag, hidx, isum, midx, dtot);
+  }
+  if ((e = cudaMemcpyAsync(counts, dtot, 32, cudaMemcpyDeviceToHost, s)) == cudaSuccess)
+    e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return set_err("hb_heavy_items counts", e);
+  if (!heavy) return 0;                                  // count phase
+  if (counts[1] > INT32_MAX) return set_err_msg("hb_heavy_items: more than 2^31 work items");
+  if (!item_first) return set_err_msg("hb_heavy_items: null outputs");
+  if (counts[0] == 0) {
+    return cudaMemsetAsync(item_first, 0, 4, s) == cudaSuccess ? 0 : set_err_msg("memset");
+  }
+  if (!item_node || !item_beg || !finish_order) return set_err_msg("hb_heavy_items: null outputs");
+  k_heavy_fill<<<grid_for_threads(nrows), kThreads, 0, s>>>(
+      nrows, lo, row_offsets, item_arcs, hflag, icnt, mflag, hidx, isum, midx, counts[0],
+      counts[1], counts[2], heavy, item_first, item_node, item_beg, finish_order);
+  return check_launch("k_heavy_fill");
+}
+
 int hb_gen_degrees(int kind, int64_t n, uint64_t seed, const double *cdf, int64_t cdf_len,
                    int64_t kmin, int64_t *deg, void *stream) {
   DevGuard dg_((cudaStream_t)stream);

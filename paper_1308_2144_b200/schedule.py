@@ -327,24 +327,78 @@ def choose_order(max_deg: int, light_max_deg: int, n: int = 0) -> str:
     return "window" if n >= WINDOW_MIN_NODES else "identity"
 
 
-def window_order(deg: torch.Tensor, b: int, bounds, max_deg: int) -> torch.Tensor:
-    """Node order of the "window" schedule: ids stay inside the light kernel's grid-stride
-    chunk (hb_light_window nodes, aligned as the kernel aligns them per rank), sorted by
-    descending in-degree there -- the NPW nodes of a warp round then have near-equal
-    in-degrees, so the round's warp-uniform loop wastes few load slots, while id locality
-    (e.g. config 4's +-1024 window) is kept to within one chunk."""
-    n = deg.numel()
-    dv = deg.device
+def _max_degree(off: torch.Tensor, stream) -> int:
+    """Largest in-degree of the CSR with device offsets `off` (hb_max_degree)."""
+    import ctypes
+    n = off.numel() - 1
+    if n <= 0:
+        return 0
+    scratch = torch.empty(1, dtype=torch.int64, device=off.device)
+    out = ctypes.c_int64(0)
+    _lib.check(_lib.hb().hb_max_degree(n, off.data_ptr(), scratch.data_ptr(), ctypes.byref(out),
+                                       stream.cuda_stream), "hb_max_degree")
+    return int(out.value)
+
+
+def node_order(off: torch.Tensor, order: str, b: int, bounds, world: int, stream):
+    """(perm, rank, new_offsets) of the `degree` / `window` schedule (hb_schedule_order):
+    perm: internal id -> old row; degree: stable sort by descending in-degree, dealt
+    round-robin over the ranks (rank r gets ranking positions r, r+W, ...); window: ids
+    stay inside the light kernel's grid-stride chunk (aligned as the kernel aligns them per
+    rank), sorted by descending in-degree there -- the NPW nodes of a warp round then have
+    near-equal in-degrees while id locality (config 4's +-1024 window) is kept.  new_offsets:
+    the relabelled CSR's offsets."""
+    import ctypes
+    n = off.numel() - 1
+    dev = off.device
+    perm = torch.empty(n, dtype=torch.int32, device=dev)
+    rank = torch.empty(n, dtype=torch.int32, device=dev)
+    new_off = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    bnd = np.ascontiguousarray(np.asarray(bounds, dtype=np.int64))
+    code = {"degree": 1, "window": 2}[order]
     L = _lib.hb()
-    win = int(L.hb_light_window(b))
-    npw = int(L.hb_light_npw(b))
-    v = torch.arange(n, dtype=torch.int64, device=dv)
-    bt = torch.tensor(bounds, dtype=torch.int64, device=dv)
-    r = torch.searchsorted(bt, v, right=True) - 1
-    lo_al = (bt[:-1] // npw) * npw
-    w = (v - lo_al[r]) // win
-    key = (r * (n // win + 2) + w) * (max_deg + 1) + (max_deg - deg)
-    return torch.sort(key, stable=True).indices
+    tb = ctypes.c_uint64(0)
+    args = (n, off.data_ptr(), code, b, world, bnd.ctypes.data, perm.data_ptr(),
+            rank.data_ptr(), new_off.data_ptr())
+    _lib.check(L.hb_schedule_order(*args, None, ctypes.byref(tb), stream.cuda_stream),
+               "hb_schedule_order(size)")
+    temp = torch.empty(max(int(tb.value), 1), dtype=torch.uint8, device=dev)
+    _lib.check(L.hb_schedule_order(*args, temp.data_ptr(), ctypes.byref(tb), stream.cuda_stream),
+               "hb_schedule_order")
+    temp.record_stream(stream)
+    return perm, rank, new_off
+
+
+def heavy_items(row_off: torch.Tensor, nrows: int, lo: int, light_max_deg: int, item_arcs: int,
+                stream):
+    """Work items of the heavy rows (in-degree > light_max_deg) among rows [lo, lo + nrows)
+    whose offsets are row_off[0..nrows] (hb_heavy_items): heavy row ids, item_first,
+    item_node, item_beg, finish_order (hubs with more than MEGA_ITEMS items first), n_mega,
+    and the number of rows with in-degree > 0."""
+    import ctypes
+    dev = row_off.device
+    L = _lib.hb()
+    tb = ctypes.c_uint64(0)
+    counts_buf = (ctypes.c_int64 * 4)()
+    counts = ctypes.cast(counts_buf, ctypes.c_void_p)
+    base = (nrows, lo, row_off.data_ptr(), light_max_deg, item_arcs, MEGA_ITEMS)
+    _lib.check(L.hb_heavy_items(*base, None, None, None, None, None, counts, None,
+                                ctypes.byref(tb), stream.cuda_stream), "hb_heavy_items(size)")
+    temp = torch.empty(max(int(tb.value), 1), dtype=torch.uint8, device=dev)
+    _lib.check(L.hb_heavy_items(*base, None, None, None, None, None, counts, temp.data_ptr(),
+                                ctypes.byref(tb), stream.cuda_stream), "hb_heavy_items(count)")
+    n_heavy, n_items, n_mega, n_nonzero = (int(c) for c in counts_buf)
+    heavy = torch.empty(n_heavy, dtype=torch.int32, device=dev)
+    item_first = torch.zeros(n_heavy + 1, dtype=torch.int32, device=dev)
+    item_node = torch.empty(n_items, dtype=torch.int32, device=dev)
+    item_beg = torch.empty(n_items, dtype=torch.int64, device=dev)
+    finish_order = torch.empty(n_heavy, dtype=torch.int32, device=dev)
+    _lib.check(L.hb_heavy_items(*base, heavy.data_ptr(), item_first.data_ptr(),
+                                item_node.data_ptr(), item_beg.data_ptr(),
+                                finish_order.data_ptr(), counts, temp.data_ptr(),
+                                ctypes.byref(tb), stream.cuda_stream), "hb_heavy_items")
+    temp.record_stream(stream)
+    return heavy, item_first, n_items, item_node, item_beg, finish_order, n_mega, n_nonzero
 
 
 def _row_batches(off: torch.Tensor, n: int, m: int, limit: int = (1 << 31) - 1):
@@ -377,42 +431,6 @@ def partition_bounds(n: int, world: int):
     return bounds
 
 
-def _deal_order(deg: torch.Tensor, order: str, b: int, bounds, max_deg: int, world: int):
-    """Internal order (perm: internal id -> old row) of the schedule, or None (identity)."""
-    n = deg.numel()
-    if order == "window" and n > 0:
-        return window_order(deg, b, bounds, max_deg)
-    if order == "degree" and n > 0:
-        srt = torch.sort(deg, descending=True, stable=True).indices
-        if world > 1:
-            # deal the degree ranking round-robin: rank r gets ranks r, r+W, r+2W, ...
-            # (bounds[r+1]-bounds[r] of them), each slice still in descending degree.
-            srt = torch.cat([srt[r::world] for r in range(world)])
-        return srt
-    return None
-
-
-def _heavy_items(deg_loc: torch.Tensor, off_loc: torch.Tensor, lo: int, light_max_deg: int,
-                 item_arcs: int, device):
-    """Heavy nodes of rows [lo, lo + len(deg_loc)) (global internal ids) and their work
-    items; off_loc[i] is the (local or global) position of row lo + i."""
-    heavy_l = torch.nonzero(deg_loc > light_max_deg).squeeze(1)
-    heavy = heavy_l + lo
-    cnt = (deg_loc[heavy_l] + item_arcs - 1) // item_arcs
-    item_first = torch.zeros(heavy.numel() + 1, dtype=torch.int64, device=device)
-    if heavy.numel():
-        torch.cumsum(cnt, 0, out=item_first[1:])
-    n_items = int(item_first[-1].item())
-    owner = torch.repeat_interleave(torch.arange(heavy.numel(), device=device), cnt)
-    item_node = heavy[owner]
-    item_beg = (off_loc[heavy_l[owner]]
-                + (torch.arange(n_items, device=device) - item_first[owner]) * item_arcs)
-    mega = cnt > MEGA_ITEMS
-    finish_order = torch.cat([torch.nonzero(mega).squeeze(1),
-                              torch.nonzero(~mega).squeeze(1)]).to(torch.int32)
-    return heavy, item_first, n_items, item_node, item_beg, finish_order, int(mega.sum().item())
-
-
 def build_rank_local(offsets, successors, b: int, device, order: str, world: int,
                      rank_id: int, s_main, on_order=None) -> Schedule:
     """Schedule of one rank of a multi-GPU run with a RANK-LOCAL CSR: the full offsets are
@@ -428,33 +446,30 @@ def build_rank_local(offsets, successors, b: int, device, order: str, world: int
     lo, hi = bounds[rank_id], bounds[rank_id + 1]
     light_max_deg = int(L.hb_light_max_deg(b))
     item_arcs = int(L.hb_item_arcs(b))
-    deg = off[1:] - off[:-1]
-    max_deg = int(deg.max().item()) if n else 0
+    max_deg = _max_degree(off, s_main)
     if order == "auto":
         order = choose_order(max_deg, light_max_deg, n)
     if order not in ("identity", "degree", "window"):
         raise ValueError(f"unknown schedule order {order!r}")
-    srt = _deal_order(deg, order, b, bounds, max_deg, world)
     perm = rank = None
-    if srt is not None:
-        perm = srt.to(torch.int32)
-        rank = torch.empty_like(perm)
-        rank[srt] = torch.arange(n, dtype=torch.int32, device=device)
+    new_off = off
+    if order in ("degree", "window") and n > 0:
+        perm, rank, new_off = node_order(off, order, b, bounds, world, s_main)
     if on_order is not None:
         on_order(perm)
     rows = perm[lo:hi] if perm is not None else torch.arange(lo, hi, dtype=torch.int32,
                                                              device=device)
     nloc = hi - lo
-    deg_loc = deg[rows.long()] if nloc else deg[:0]
     # offsets of rows [base, hi], base = lo rounded down to 64 rows: the light kernel
     # aligns its warp rounds (and its L2 prefetch of the offsets) below lo; those leading
-    # rows are empty here and never valid there
+    # rows are empty here and never valid there.  Positions are local: the owned rows'
+    # relabelled offsets minus the first one.
     base = (lo // 64) * 64
     pad = lo - base
     off_pad = torch.zeros(pad + nloc + 1, dtype=torch.int64, device=device)
     off_loc = off_pad[pad:]
     if nloc:
-        torch.cumsum(deg_loc, 0, out=off_loc[1:])
+        torch.sub(new_off[lo:hi + 1], new_off[lo], out=off_loc)
     mloc = int(off_loc[-1].item())
     succ = torch.empty(max(mloc, 1), dtype=torch.int32, device=device)
     if isinstance(successors, torch.Tensor) and successors.is_cuda:
@@ -490,13 +505,12 @@ def build_rank_local(offsets, successors, b: int, device, order: str, world: int
             _lib.check(L.hb_map_ids(mloc, succ.data_ptr(), rank.data_ptr(), succ.data_ptr(),
                                     s_main.cuda_stream), "hb_map_ids")
         s_main.synchronize()                      # the pinned staging buffers die here
-    heavy, item_first, n_items, item_node, item_beg, finish_order, n_mega = _heavy_items(
-        deg_loc, off_loc, lo, light_max_deg, item_arcs, device)
+    heavy, item_first, n_items, item_node, item_beg, finish_order, n_mega, n_nonzero = \
+        heavy_items(off_loc, nloc, lo, light_max_deg, item_arcs, s_main)
     p = 1 << b
     partial = torch.empty((max(n_items, 1), p), dtype=torch.uint8, device=device)
     if order == "degree":
         n_heavy = int(heavy.numel())
-        n_nonzero = int((deg_loc > 0).sum().item())
         light_lo, light_hi = lo + n_heavy, hi
         steady = lo + max(n_nonzero, n_heavy)
     else:
@@ -504,9 +518,9 @@ def build_rank_local(offsets, successors, b: int, device, order: str, world: int
     return Schedule(n=n, m=mloc, b=b, order=order, perm=perm, rank=rank, offsets=off_pad,
                     succ_buf=succ[:mloc], lo=lo, hi=hi, light_lo=light_lo, light_hi=light_hi,
                     light_hi_steady=steady, light_max_deg=light_max_deg, item_arcs=item_arcs,
-                    heavy_nodes=heavy.to(torch.int32), item_first=item_first.to(torch.int32),
+                    heavy_nodes=heavy, item_first=item_first,
                     finish_order=finish_order, n_mega=n_mega,
-                    item_node=item_node.to(torch.int32), item_beg=item_beg.contiguous(),
+                    item_node=item_node, item_beg=item_beg,
                     partial=partial, max_deg=max_deg,
                     hot_rows=n if order == "degree" else 0, stream=s_main, row_base=base,
                     local=True)
@@ -544,24 +558,15 @@ def build_schedule(offsets, successors, b: int, device, order: str = "auto", wor
     lo, hi = bounds[rank_id], bounds[rank_id + 1]
     light_max_deg = int(L.hb_light_max_deg(b))
     item_arcs = int(L.hb_item_arcs(b))
-    deg = off[1:] - off[:-1]
-    max_deg = int(deg.max().item()) if n else 0
+    max_deg = _max_degree(off, s_main)
     if order == "auto":
         order = choose_order(max_deg, light_max_deg, n)
     if order not in ("identity", "degree", "window"):
         raise ValueError(f"unknown schedule order {order!r}")
-    perm = rank = None
-    srt = None
-    if order == "window" and n > 0:
-        srt = window_order(deg, b, bounds, max_deg)
-    elif order == "degree" and n > 0:
-        srt = torch.sort(deg, descending=True, stable=True).indices
-        if world > 1:
-            # deal the degree ranking round-robin: rank r gets ranks r, r+W, r+2W, ...
-            # (bounds[r+1]-bounds[r] of them), each slice still in descending degree.
-            srt = torch.cat([srt[r::world] for r in range(world)])
-    if srt is not None:
-        perm = srt.to(torch.int32)
+    perm = rank = new_off = None
+    if order in ("window", "degree") and n > 0:
+        # perm, its inverse and the relabelled offsets, on the device (hb_schedule_order)
+        perm, rank, new_off = node_order(off, order, b, bounds, world, s_main)
     if on_order is not None:
         on_order(perm)
     if ids_ready is not None:
@@ -576,34 +581,17 @@ def build_schedule(offsets, successors, b: int, device, order: str = "auto", wor
             for _, _, ev in slices:
                 s_main.wait_event(ev)
     if order == "window" and n > 0 and pending:
-        rank = torch.empty_like(perm)
-        rank[srt] = torch.arange(n, dtype=torch.int32, device=device)
-        new_deg = deg[srt]
-        new_off = torch.zeros(n + 1, dtype=torch.int64, device=device)
-        torch.cumsum(new_deg, 0, out=new_off[1:])
         relabel = (off, succ, perm, rank)      # window slices map onto themselves
-        off, succ, deg = new_off, torch.empty(m, dtype=torch.int32, device=device), new_deg
-        del srt
+        off, succ = new_off, torch.empty(m, dtype=torch.int32, device=device)
     elif order == "window" and n > 0:
-        rank = torch.empty_like(perm)
-        rank[srt] = torch.arange(n, dtype=torch.int32, device=device)
-        new_deg = deg[srt]
-        new_off = torch.zeros(n + 1, dtype=torch.int64, device=device)
-        torch.cumsum(new_deg, 0, out=new_off[1:])
         new_succ = torch.empty(m, dtype=torch.int32, device=device)
         s = s_main
         _lib.check(L.hb_relabel_csr(n, off.data_ptr(), succ.data_ptr(), perm.data_ptr(),
                                     rank.data_ptr(), new_off.data_ptr(), new_succ.data_ptr(),
                                     s.cuda_stream), "hb_relabel_csr")
         # ids move by less than a window: rows stay nearly ascending, no re-sort needed
-        off, succ, deg = new_off, new_succ, new_deg
-        del srt
+        off, succ = new_off, new_succ
     if order == "degree" and n > 0:
-        rank = torch.empty_like(perm)
-        rank[srt] = torch.arange(n, dtype=torch.int32, device=device)
-        new_deg = deg[srt]
-        new_off = torch.zeros(n + 1, dtype=torch.int64, device=device)
-        torch.cumsum(new_deg, 0, out=new_off[1:])
         new_succ = torch.empty(m, dtype=torch.int32, device=device)
         s = s_main
         if src_slices is not None and not SORT_ROWS:
@@ -648,28 +636,15 @@ def build_schedule(offsets, successors, b: int, device, order: str = "auto", wor
                                       succ.data_ptr(), temp.data_ptr(), ctypes.byref(tb), None,
                                       s.cuda_stream), "hb_sort_rows")
             del temp
-        off, succ, deg = new_off, new_succ, new_deg
-        del srt
-    dloc = deg[lo:hi]
-    heavy = torch.nonzero(dloc > light_max_deg).squeeze(1) + lo
-    cnt = (deg[heavy] + item_arcs - 1) // item_arcs
-    item_first = torch.zeros(heavy.numel() + 1, dtype=torch.int64, device=device)
-    if heavy.numel():
-        torch.cumsum(cnt, 0, out=item_first[1:])
-    n_items = int(item_first[-1].item())
-    owner = torch.repeat_interleave(torch.arange(heavy.numel(), device=device), cnt)
-    item_node = heavy[owner]
-    item_beg = off[item_node] + (torch.arange(n_items, device=device) - item_first[owner]) * item_arcs
+        off, succ = new_off, new_succ
+    # heavy rows of [lo, hi) and their work items, on the device (hb_heavy_items)
+    heavy, item_first, n_items, item_node, item_beg, finish_order, n_mega, n_nonzero = \
+        heavy_items(off[lo:], hi - lo, lo, light_max_deg, item_arcs, s_main)
     p = 1 << b
     partial = torch.empty((max(n_items, 1), p), dtype=torch.uint8, device=device)
-    mega = cnt > MEGA_ITEMS
-    finish_order = torch.cat([torch.nonzero(mega).squeeze(1),
-                              torch.nonzero(~mega).squeeze(1)]).to(torch.int32)
-    n_mega = int(mega.sum().item())
     if order == "degree":
         # this rank's slice is in descending degree: heavy first, zero in-degree last
         n_heavy = int(heavy.numel())
-        n_nonzero = int((dloc > 0).sum().item())
         light_lo, light_hi = lo + n_heavy, hi
         steady = lo + max(n_nonzero, n_heavy)
     else:
@@ -679,9 +654,9 @@ def build_schedule(offsets, successors, b: int, device, order: str = "auto", wor
     return Schedule(n=n, m=m, b=b, order=order, perm=perm, rank=rank, offsets=off, succ_buf=succ,
                     lo=lo, hi=hi, light_lo=light_lo, light_hi=light_hi,
                     light_hi_steady=steady, light_max_deg=light_max_deg, item_arcs=item_arcs,
-                    heavy_nodes=heavy.to(torch.int32), item_first=item_first.to(torch.int32),
+                    heavy_nodes=heavy, item_first=item_first,
                     finish_order=finish_order, n_mega=n_mega,
-                    item_node=item_node.to(torch.int32), item_beg=item_beg.contiguous(),
+                    item_node=item_node, item_beg=item_beg,
                     partial=partial, max_deg=max_deg,
                     hot_rows=n if order == "degree" else 0, pending=pending,
                     relabel=relabel, stream=s_main)
