@@ -431,6 +431,54 @@ def partition_bounds(n: int, world: int):
     return bounds
 
 
+def _upload_owned_rows(ho: np.ndarray, hs: np.ndarray, rows_h: np.ndarray,
+                       off_loc_h: np.ndarray, succ: torch.Tensor, rank, device, main) -> None:
+    """Successor ids of the owned rows `rows_h` (old row ids, in internal order) into the
+    rank-local `succ`, streamed: the rows are cut into up to STREAM_SLICES slices of about
+    equal arcs; every host core gathers slice k + 1 (hbg_gather_rows: int32 copy or int64
+    narrowing) into one pinned staging buffer while slice k crosses PCIe from the other on
+    the side stream, and `main` maps each slice's ids into the internal order
+    (hb_map_ids) as it lands."""
+    import ctypes
+    nloc = rows_h.shape[0]
+    mloc = int(off_loc_h[-1]) if nloc else 0
+    if mloc == 0:
+        return
+    nsl = STREAM_SLICES if mloc >= STREAM_MIN_ARCS else 1
+    targets = np.arange(1, nsl, dtype=np.int64) * mloc // nsl
+    cuts = np.unique(np.concatenate([[0], np.searchsorted(off_loc_h, targets), [nloc]]))
+    bounds = [(int(a), int(b)) for a, b in zip(cuts[:-1], cuts[1:]) if b > a]
+    widest = max(int(off_loc_h[b] - off_loc_h[a]) for a, b in bounds)
+    side = _SIDE_STREAMS.get(device)
+    if side is None:
+        side = _SIDE_STREAMS[device] = torch.cuda.Stream(device=device)
+    side.wait_stream(main)
+    bufs = [_staging(device, f"rl{i}", 4 * widest) for i in range(2)]
+    out_off = np.empty(max(b - a for a, b in bounds) + 1, dtype=np.int64)
+    G = _lib.graphlib()
+    L = _lib.hb()
+    vp = ctypes.c_void_p
+    for k, (r0, r1) in enumerate(bounds):
+        ent = bufs[k % 2]
+        if ent[1] is not None:
+            ent[1].synchronize()                # its previous slice has left the buffer
+        got = G.hbg_gather_rows(vp(ho.ctypes.data), vp(hs.ctypes.data), hs.itemsize,
+                                vp(rows_h.ctypes.data + 4 * r0), r1 - r0, vp(out_off.ctypes.data),
+                                vp(ent[0].data_ptr()), 0)
+        a0 = int(off_loc_h[r0])
+        assert got == int(off_loc_h[r1]) - a0, (got, r0, r1)
+        with torch.cuda.stream(side):
+            succ[a0:a0 + got].copy_(ent[0][:4 * got].view(torch.int32), non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(side)
+        ent[1] = ev
+        main.wait_event(ev)
+        if rank is not None:
+            _lib.check(L.hb_map_ids(got, succ.data_ptr() + 4 * a0, rank.data_ptr(),
+                                    succ.data_ptr() + 4 * a0, main.cuda_stream), "hb_map_ids")
+    succ.record_stream(side)
+
+
 def build_rank_local(offsets, successors, b: int, device, order: str, world: int,
                      rank_id: int, s_main, on_order=None) -> Schedule:
     """Schedule of one rank of a multi-GPU run with a RANK-LOCAL CSR: the full offsets are
@@ -440,7 +488,7 @@ def build_rank_local(offsets, successors, b: int, device, order: str, world: int
     gathered there.  Ids are relabelled into the internal order (hashes still use the
     original ids, so registers are bit-identical)."""
     L = _lib.hb()
-    off = _as_device(offsets, torch.int64, device)
+    off = _upload_offsets(offsets, device, s_main)
     n = off.numel() - 1
     bounds = partition_bounds(n, world)
     lo, hi = bounds[rank_id], bounds[rank_id + 1]
@@ -491,20 +539,7 @@ def build_rank_local(offsets, successors, b: int, device, order: str, world: int
         hs = np.ascontiguousarray(hs)
         ho = np.ascontiguousarray(np.asarray(offsets, dtype=np.int64))
         rows_h = np.ascontiguousarray(rows.cpu().numpy().astype(np.int32))
-        pin_off = torch.empty(nloc + 1, dtype=torch.int64, pin_memory=True)
-        pin_ids = torch.empty(max(mloc, 1), dtype=torch.int32, pin_memory=True)
-        G = _lib.graphlib()
-        import ctypes
-        vp = ctypes.c_void_p
-        got = G.hbg_gather_rows(vp(ho.ctypes.data), vp(hs.ctypes.data), hs.itemsize,
-                                vp(rows_h.ctypes.data), nloc, vp(pin_off.data_ptr()),
-                                vp(pin_ids.data_ptr()), 0)
-        assert got == mloc, (got, mloc)
-        succ[:mloc].copy_(pin_ids[:mloc], non_blocking=True)
-        if rank is not None and mloc:
-            _lib.check(L.hb_map_ids(mloc, succ.data_ptr(), rank.data_ptr(), succ.data_ptr(),
-                                    s_main.cuda_stream), "hb_map_ids")
-        s_main.synchronize()                      # the pinned staging buffers die here
+        _upload_owned_rows(ho, hs, rows_h, off_loc.cpu().numpy(), succ, rank, device, s_main)
     heavy, item_first, n_items, item_node, item_beg, finish_order, n_mega, n_nonzero = \
         heavy_items(off_loc, nloc, lo, light_max_deg, item_arcs, s_main)
     p = 1 << b

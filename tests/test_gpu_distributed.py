@@ -198,14 +198,21 @@ def test_simulated_ranks_fused_discounts(key, world, exchange):
                           arrays[f"{key}/harmonic"].view(np.uint64))
 
 
+@pytest.mark.parametrize("slices", [1, 5])
 @pytest.mark.parametrize("on_device", [False, True])
 @pytest.mark.parametrize("schedule", ["identity", "degree", "window"])
 @pytest.mark.parametrize("world", [2, 3, 8])
-def test_rank_local_csr(world, schedule, on_device):
-    """Every rank holds only the successor ids of the rows it owns (~m/W, uploaded or
-    gathered alone), ids in the internal order; the union over ranks is the graph, and the
-    simulated-rank run stays bit-identical to the reference."""
+def test_rank_local_csr(world, schedule, on_device, slices, monkeypatch):
+    """Every rank holds only the successor ids of the rows it owns (~m/W, uploaded -- in
+    `slices` streamed slices from the host -- or gathered alone), ids in the internal order;
+    the union over ranks is the graph, and the simulated-rank run stays bit-identical to
+    the reference."""
     import torch
+    from paper_1308_2144_b200 import schedule as sched_mod
+    if on_device and slices > 1:
+        pytest.skip("streamed slices are a host-upload feature")
+    monkeypatch.setattr(sched_mod, "STREAM_SLICES", slices)
+    monkeypatch.setattr(sched_mod, "STREAM_MIN_ARCS", 0)
     from paper_1308_2144_b200.distributed import CudaRankState
     from paper_1308_2144_b200.schedule import partition_bounds
     case = CASES["rmat12_b7_s42_w5"]
