@@ -204,6 +204,16 @@ def _staging(device, key: str, nbytes: int) -> list:
     return ent
 
 
+def release_staging_buffers(device=None) -> None:
+    """Free the pinned staging buffers kept for uploads from pageable host memory (all
+    devices, or one), after their last copies completed.  They are kept between runs
+    because pinning is slow; a process that is done uploading large graphs calls this."""
+    for dev in list(_STAGING) if device is None else [device]:
+        for ent in _STAGING.pop(dev, {}).values():
+            if ent[1] is not None:
+                ent[1].synchronize()
+
+
 def _is_pinned(a: np.ndarray) -> bool:
     try:
         with warnings.catch_warnings():   # read-only arrays are only inspected

@@ -173,3 +173,20 @@ def test_staged_and_pinned_uploads(weblike, dtype, pinned, monkeypatch):
                                   torch.cuda.current_stream())
     torch.cuda.synchronize()
     assert t.shape[0] == big.shape[0] and int(t.abs().sum().item()) == 0
+
+
+def test_release_staging_buffers(weblike, monkeypatch):
+    """The pinned staging buffers of a pageable upload are kept for the next run and freed
+    on request (after their copies completed); a run afterwards allocates them again."""
+    ref, _, _ = _run(weblike, 8, "window", 1, monkeypatch)
+    got, _, _ = _run(hb.CsrGraph(np.asarray(weblike.offsets, np.int64),
+                                 np.asarray(weblike.successors, np.int64)), 8, "window", 4,
+                     monkeypatch)
+    assert sched_mod._STAGING
+    hb.release_staging_buffers()
+    assert not sched_mod._STAGING
+    again, _, _ = _run(hb.CsrGraph(np.asarray(weblike.offsets, np.int64),
+                                   np.asarray(weblike.successors, np.int64)), 8, "window", 4,
+                       monkeypatch)
+    _same(ref, got)
+    _same(ref, again)
