@@ -29,7 +29,8 @@ for rep in range(3):
     torch.cuda.synchronize()
     T = {}
     t0 = time.perf_counter()
-    st = hb.initialize(gp, hb.HyperBallConfig(params=params, device=0))
+    st = hb.initialize(gp, hb.HyperBallConfig(params=params, device=0,
+                                              schedule=os.environ.get("HB_SCHEDULE", "auto")))
     torch.cuda.synchronize()
     T["init"] = time.perf_counter() - t0
     acc = hb.CentralityAccumulator(n)
