@@ -623,6 +623,12 @@ __device__ __forceinline__ bool finish_node(const Peers &peers, bool doit, int64
 #ifndef HB_TMA_DIRECT
 #define HB_TMA_DIRECT 1               // TMA light kernel, dense batches: ids straight to the issuing lanes
 #endif
+#ifndef HB_L1_NEXT_IDS
+#define HB_L1_NEXT_IDS 2               // lines of the next round's ids prefetched into L1
+#endif
+#ifndef HB_L1_OWN_ROW
+#define HB_L1_OWN_ROW 1
+#endif
 #ifndef HB_SELF_LATE
 #define HB_SELF_LATE 1                // TMA light kernel: own row read in the epilogue
 #endif
@@ -1068,6 +1074,21 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
       end = __ldg(offsets + v + 1);
       HB_CHK(v >= 0 && v < g_chk.rows && 0 <= beg && beg <= end && end <= g_chk.m,
              "k_light row / offsets");
+      if constexpr (HB_L1_NEXT_IDS && kTma<LOGP, LOGR, HINT>()) {
+        // the last group's row end is where the next round's ids start: pull their first
+        // lines into L1 now, so the next round's first gathers need not wait on L2
+        if (grp == Gm::NPW - 1 && gl == 0 && v + 1 < ve) {
+          const int32_t *nx = succ + end;
+#pragma unroll
+          for (int q = 0; q < HB_L1_NEXT_IDS; q++)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(nx + 32 * q));
+        }
+      }
+      if constexpr (HB_L1_OWN_ROW && kTma<LOGP, LOGR, HINT>()) {
+        // own row, read in the epilogue (HB_SELF_LATE): into L1 now
+        if (gl < Gm::P / 128)
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(cur + (size_t)v * Gm::P + 128 * gl));
+      }
       if (end - beg > max_deg) {               // heavy: handled by the item path
         valid = false;
         end = beg;
