@@ -197,6 +197,12 @@ typedef struct hb_step_args {
    * only), which the peer unpacks with hb_unpack_inbox after the step's barrier
    * (DESIGN.md section 6). */
   int64_t peer_packed_stride;
+  /* appended: device uint64 scratch, or NULL.  With it the light kernel deals its node
+   * chunks to the warps in the order they ask (a ticket counter the call zeroes on the
+   * stream) instead of grid-stride: warps that drew long chunks take fewer, the launch
+   * ends without a tail.  Results do not depend on it.  One scratch
+   * word per stream: calls that may run concurrently must not share it. */
+  uint64_t *ticket;
 } hb_step_args;
 
 int hb_union_step_v2(const hb_step_args *args);

@@ -115,6 +115,7 @@ class StepArgs(ctypes.Structure):
         ("peer_nxt", _vp), ("peer_chg", _vp), ("stream", _vp),
         ("check_rows", _i64), ("check_m", _i64),
         ("peer_packed_stride", _i64),
+        ("ticket", _vp),
     ]
 
     def __init__(self, **kw):

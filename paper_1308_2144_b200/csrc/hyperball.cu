@@ -950,14 +950,16 @@ constexpr bool kDenseCopy = HB_DENSE_COPY != 0;   // dense batches skip the id c
 #define HB_LOOK_ROUNDS 4
 #endif
 #ifndef HB_CHUNK_BIG
-#define HB_CHUNK_BIG 16
+#define HB_CHUNK_BIG 8
 #endif
 #ifndef HB_CHUNK_SMALL
 #define HB_CHUNK_SMALL 4
 #endif
 constexpr int kLookRounds = HB_LOOK_ROUNDS;   // L2 prefetch distance of the light kernel, in warp rounds
 // warp rounds per grid-stride chunk of the light kernel (resident warps x chunk nodes is
-// the id window the GPU sweeps): 16 for p >= 256, 4 below (measured on configs 3-5)
+// the id window the GPU sweeps): 8 for p >= 256 (16 before the chunk tickets; with them
+// config 4 takes 7.17 ms at 16, 7.06 ms at 8, 7.43 ms at 32), 4 below (configs 2, 3, 5s:
+// 2 and 8 are within noise or slower)
 template <int LOGP>
 __host__ __device__ constexpr int chunk_rounds() { return LOGP >= 8 ? HB_CHUNK_BIG : HB_CHUNK_SMALL; }
 
@@ -976,7 +978,7 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
         EstConst ec, int64_t lo, int64_t hi, int64_t max_deg, int dense, double tf,
         unsigned long long *__restrict__ nch_out, unsigned long long *__restrict__ merged_out,
         const uint32_t *__restrict__ active, Peers peers, RunArgs ra, int64_t hot_lim,
-        const __grid_constant__ CUtensorMap tmap) {
+        unsigned long long *__restrict__ ticket, const __grid_constant__ CUtensorMap tmap) {
   static_assert(LOGR == 0 || !PUSH, "batched runs are single-device");
   constexpr bool kHint = HINT;
   uint64_t pol = 0;
@@ -1021,7 +1023,20 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
   constexpr bool kDefer = LOGR == 0 && Gm::G > 1 && HB_DEFER_TAIL && LOGP >= HB_DEFER_MIN_LOGP;
   DeferredTail dt;
   const int64_t nchunks = (hi - lo_al + CN - 1) / CN;
-  for (int64_t chunk = warp; chunk < nchunks; chunk += nwarps) {
+  // Chunks are dealt grid-stride, or -- with a ticket counter (zeroed by the launcher) --
+  // in the order the warps ask for them: the sweep stays one contiguous window of the id
+  // space, and a warp whose chunks ran long (more arcs, more DRAM misses) simply takes
+  // fewer of them.  The next ticket is drawn at the start of a chunk, so the atomic's
+  // round trip hides behind the chunk's work.  (Several chunks per draw only lengthen the
+  // tail: config 2 0.38 -> 0.45 / 0.59 / 0.84 ms at 2 / 4 / 8 chunks per draw.)
+  // (32-bit draws: chunks + one overshoot per warp stay far below 2^32)
+  auto draw = [&]() -> uint32_t {
+    return lane == 0 ? atomicAdd(reinterpret_cast<unsigned int *>(ticket), 1u) : 0u;
+  };
+  uint32_t drawn = ticket ? draw() : 0u;
+  int64_t chunk = ticket ? (int64_t)__shfl_sync(0xffffffffu, drawn, 0) : warp;
+  for (; chunk < nchunks;) {
+  if (ticket) drawn = draw();
   const int64_t vb = lo_al + chunk * CN;
   const int64_t ve = vb + CN < hi ? vb + CN : hi;
   // prefetch of the per-round streams, kLookRounds rounds per batch: own rows, estimates,
@@ -1326,6 +1341,7 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
       my_nch += __popc(m);
     }
   }
+  chunk = ticket ? (int64_t)__shfl_sync(0xffffffffu, drawn, 0) : chunk + nwarps;
   }  // chunk
   if constexpr (kDefer) dt.flush<Gm::P>(nxt, est, sum_dist, sum_recip, ec, tf);
   if constexpr (PUSH) __threadfence_system();   // remote rows/bits before the barrier
@@ -2612,6 +2628,44 @@ unsigned grid_for_warps(int64_t work_warps) {
 }
 unsigned grid_for_threads(int64_t work) { return grid_for_warps((work + 31) / 32); }
 
+// Grid of the light kernel: whole waves of its resident set.  The 8-CTAs-per-SM cap above
+// is 2 2/3 waves of a kernel that fits 3 CTAs per SM (the TMA kernel at p = 256, the
+// p = 64 / 128 kernels), so the last third of the launch ran at 2/3 occupancy (ncu: 34.0%
+// warps active against 37.5% theoretical).  One wave (HB_GRID_WAVES, env override for
+// sweeps) also keeps the resident warps sweeping one window of the id space in step.
+#ifndef HB_GRID_WAVES
+#define HB_GRID_WAVES 1
+#endif
+int resident_ctas(const void *func, size_t smem) {
+  static struct { const void *f; int dev; size_t smem; int occ; } memo[256];
+  static int n_memo = 0;
+  const int dev = current_device();
+  for (int i = 0; i < n_memo; i++)
+    if (memo[i].f == func && memo[i].dev == dev && memo[i].smem == smem) return memo[i].occ;
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, func, kThreads, smem) != cudaSuccess ||
+      occ <= 0)
+    occ = 0;
+  cudaGetLastError();
+  if (n_memo < 256) memo[n_memo++] = {func, dev, smem, occ};
+  return occ;
+}
+unsigned grid_resident(const void *func, size_t smem, int64_t work_warps) {
+  static const int waves = [] {
+    const char *e = getenv("HB_GRID_WAVES");
+    const int w = e ? atoi(e) : HB_GRID_WAVES;
+    return w;
+  }();
+  const int occ = resident_ctas(func, smem);
+  if (waves <= 0 || occ <= 0) return grid_for_warps(work_warps);
+  const int64_t per_cta = kThreads / 32;
+  int64_t ctas = (work_warps + per_cta - 1) / per_cta;
+  const int64_t cap = (int64_t)num_sms() * occ * waves;
+  if (ctas > cap) ctas = cap;
+  if (ctas < 1) ctas = 1;
+  return (unsigned)ctas;
+}
+
 #ifndef HB_TMA_L2PROMO
 #define HB_TMA_L2PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_256B
 #endif
@@ -2651,7 +2705,7 @@ int union_step_impl(int64_t lo, int64_t hi, const int64_t *offsets, const int32_
                     int64_t item_arcs, uint8_t *partial, unsigned long long *nch,
                     unsigned long long *merged, int64_t hot_rows, const uint32_t *active,
                     const Peers &peers, cudaStream_t s, RunArgs ra = RunArgs{nullptr, 0, 0},
-                    int64_t n_rows = 0) {
+                    int64_t n_rows = 0, unsigned long long *ticket = nullptr) {
   using Gm = Geo<LOGP>;
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof(tmap));
@@ -2694,18 +2748,18 @@ int union_step_impl(int64_t lo, int64_t hi, const int64_t *offsets, const int32_
     const int64_t warps = (hi - lo + Gm::NPW - 1) / Gm::NPW + 1;   // capped at the resident set
     if constexpr (kCanHint) {
       if (hint && l1na)
-        k_light<LOGP, PUSH, LOGR, true, true><<<grid_for_warps(warps), kThreads, 0, s>>>(
+        k_light<LOGP, PUSH, LOGR, true, true><<<grid_resident((const void *)k_light<LOGP, PUSH, LOGR, true, true>, 0, warps), kThreads, 0, s>>>(
             offsets, succ, cur, nxt, chg_prev, chg_now, est, sum_dist, sum_recip, ec, lo, hi,
-            light_max_deg, dense, tf, nch, merged, active, peers, ra, hot_lim, tmap);
+            light_max_deg, dense, tf, nch, merged, active, peers, ra, hot_lim, ticket, tmap);
       else if (hint)
-        k_light<LOGP, PUSH, LOGR, true><<<grid_for_warps(warps), kThreads, 0, s>>>(
+        k_light<LOGP, PUSH, LOGR, true><<<grid_resident((const void *)k_light<LOGP, PUSH, LOGR, true>, 0, warps), kThreads, 0, s>>>(
             offsets, succ, cur, nxt, chg_prev, chg_now, est, sum_dist, sum_recip, ec, lo, hi,
-            light_max_deg, dense, tf, nch, merged, active, peers, ra, hot_lim, tmap);
+            light_max_deg, dense, tf, nch, merged, active, peers, ra, hot_lim, ticket, tmap);
     }
     if (!hint)
-      k_light<LOGP, PUSH, LOGR, false><<<grid_for_warps(warps), kThreads, tma_smem, s>>>(
+      k_light<LOGP, PUSH, LOGR, false><<<grid_resident((const void *)k_light<LOGP, PUSH, LOGR, false>, tma_smem, warps), kThreads, tma_smem, s>>>(
           offsets, succ, cur, nxt, chg_prev, chg_now, est, sum_dist, sum_recip, ec, lo, hi,
-          light_max_deg, dense, tf, nch, merged, active, peers, ra, hot_lim, tmap);
+          light_max_deg, dense, tf, nch, merged, active, peers, ra, hot_lim, ticket, tmap);
     if (int e = check_launch("k_light")) return e;
   }
   if (n_heavy > 0) {
@@ -2820,7 +2874,15 @@ int hb_estimate_rows(const uint8_t *regs, int64_t lo, int64_t hi, int b,
 int hb_union_step_v2(const hb_step_args *a) {
   if (!a || a->struct_size < offsetof(hb_step_args, peer_packed_stride))
     return set_err_msg("hb_union_step_v2: null args or struct_size < hb_step_args_min_size()");
-  const int64_t pstride = a->struct_size >= sizeof(hb_step_args) ? a->peer_packed_stride : 0;
+  const int64_t pstride =
+      a->struct_size >= offsetof(hb_step_args, peer_packed_stride) + sizeof(int64_t)
+          ? a->peer_packed_stride : 0;
+  static const bool tickets_on = [] {          // HB_TICKETS=0: grid-stride chunks (sweeps)
+    const char *e = getenv("HB_TICKETS");
+    return !(e && e[0] == '0');
+  }();
+  uint64_t *ticket = tickets_on && a->struct_size >= offsetof(hb_step_args, ticket) + sizeof(uint64_t *)
+                         ? a->ticket : nullptr;
   DevGuard dg_((cudaStream_t)a->stream);
   const int n_peers = a->n_peers, n_disc = a->n_disc;
   const int64_t n = a->n, lo = a->lo, hi = a->hi, t = a->t;
@@ -2855,6 +2917,8 @@ int hb_union_step_v2(const hb_step_args *a) {
     return set_err("hb_union_step memset nch", e);
   if (a->merged_out && (e = cudaMemsetAsync(a->merged_out, 0, sizeof(uint64_t), s)) != cudaSuccess)
     return set_err("hb_union_step memset merged", e);
+  if (ticket && (e = cudaMemsetAsync(ticket, 0, sizeof(uint64_t), s)) != cudaSuccess)
+    return set_err("hb_union_step memset ticket", e);
   if (a->clear_chg_now && n > 0) {
     if ((e = cudaMemsetAsync(a->chg_now, 0, sizeof(uint32_t) * (size_t)((n + 31) / 32), s)) !=
         cudaSuccess)
@@ -2878,14 +2942,16 @@ int hb_union_step_v2(const hb_step_args *a) {
                        a->est, a->sum_dist, a->sum_recip, tf, ec, a->dense, a->light_max_deg,
                        a->heavy_nodes, a->item_first, a->n_heavy, a->finish_order, a->n_mega,
                        a->item_node, a->item_beg, a->n_items, a->item_arcs, a->partial, nch,
-                       merged, a->hot_rows, a->active, peers, s, RunArgs{nullptr, 0, 0}, n)));
+                       merged, a->hot_rows, a->active, peers, s, RunArgs{nullptr, 0, 0}, n,
+                       reinterpret_cast<unsigned long long *>(ticket))));
   }
   HB_DISPATCH(a->b, return (union_step_impl<LB, false>(
                      lo, hi, a->offsets, a->succ, a->cur, a->nxt, a->chg_prev, a->chg_now,
                      a->est, a->sum_dist, a->sum_recip, tf, ec, a->dense, a->light_max_deg,
                      a->heavy_nodes, a->item_first, a->n_heavy, a->finish_order, a->n_mega,
                      a->item_node, a->item_beg, a->n_items, a->item_arcs, a->partial, nch,
-                     merged, a->hot_rows, a->active, peers, s, RunArgs{nullptr, 0, 0}, n)));
+                     merged, a->hot_rows, a->active, peers, s, RunArgs{nullptr, 0, 0}, n,
+                       reinterpret_cast<unsigned long long *>(ticket))));
   return 0;
 }
 

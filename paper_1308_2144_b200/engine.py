@@ -341,6 +341,7 @@ class _Device:
         self.lc = torch.from_numpy(lc_table(p)).to(dv)
         self.alpha_p2, self.lc_cut, _ = estimator_constants(p)
         self.counts = torch.zeros(2, dtype=torch.int64, device=dv)   # [changed, merged arcs]
+        self.ticket = torch.zeros(1, dtype=torch.int64, device=dv)   # light-kernel chunk tickets
         self.merged_total = 0         # arcs whose source row was merged, all iterations
         self.prev_all = True          # chg_prev is all-ones (first iteration)
         self.full_pass = True         # zero in-degree nodes may still need their copy
@@ -377,6 +378,7 @@ class _Device:
         other.chg_now = torch.zeros_like(self.chg_now)
         other.est = torch.zeros(n, dtype=torch.float64, device=dv)
         other.counts = torch.zeros(2, dtype=torch.int64, device=dv)
+        other.ticket = torch.zeros(1, dtype=torch.int64, device=dv)
         other.merged_total = 0
         other.prev_all = True
         other.full_pass = True
@@ -593,7 +595,7 @@ class _Device:
                 peer_nxt=ctypes.cast(peer_nxt, ctypes.c_void_p) if peer_nxt is not None
                 else None,
                 peer_chg=ctypes.cast(peer_chg, ctypes.c_void_p) if peer_chg is not None
-                else None, peer_packed_stride=pstride,
+                else None, peer_packed_stride=pstride, ticket=self.ticket.data_ptr(),
                 stream=self.stream.cuda_stream, **_lib.schedule_args(s)))
             self.launches += (hi > lo) + (s.n_items > 0) + (s.n_heavy > 0)
         if len(parts) > 1:

@@ -58,6 +58,7 @@ class CudaBackend:
         self.lc = torch.from_numpy(lc_table(p)).to(dv)
         self.alpha_p2, self.lc_cut, _ = estimator_constants(p)
         self.counts = torch.zeros(2, dtype=torch.int64, device=dv)
+        self.ticket = torch.zeros(1, dtype=torch.int64, device=dv)
         self.t = 0
         self.sched = None
         self._lock = threading.Lock()
@@ -130,8 +131,8 @@ class CudaBackend:
             est=self.est.data_ptr(), b=self.params.b, dense=int(dense), clear_chg_now=1,
             t=self.t, lc_table=self.lc.data_ptr(), alpha_p2=self.alpha_p2,
             lc_cut=self.lc_cut, nch_out=self.counts.data_ptr(),
-            merged_out=self.counts.data_ptr() + 8, stream=self.stream.cuda_stream,
-            **_lib.schedule_args(s)))
+            merged_out=self.counts.data_ptr() + 8, ticket=self.ticket.data_ptr(),
+            stream=self.stream.cuda_stream, **_lib.schedule_args(s)))
         new = s.to_original(self.est).cpu().numpy()
         chg = s.to_original_bits(self.bits[1], self.n).cpu().numpy()
         return new, chg
@@ -196,6 +197,7 @@ class CudaExactBackend:
         self.est = torch.zeros(n, dtype=torch.float64, device=dv)
         self.chg_now = torch.zeros(self.words, dtype=torch.int32, device=dv)
         self.counts = torch.zeros(2, dtype=torch.int64, device=dv)
+        self.ticket = torch.zeros(1, dtype=torch.int64, device=dv)
         self.t = 0
 
     def seed(self, weights, est: np.ndarray) -> None:
