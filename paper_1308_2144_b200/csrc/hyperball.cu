@@ -978,7 +978,7 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
         EstConst ec, int64_t lo, int64_t hi, int64_t max_deg, int dense, double tf,
         unsigned long long *__restrict__ nch_out, unsigned long long *__restrict__ merged_out,
         const uint32_t *__restrict__ active, Peers peers, RunArgs ra, int64_t hot_lim,
-        unsigned long long *__restrict__ ticket, const __grid_constant__ CUtensorMap tmap) {
+        unsigned int *__restrict__ ticket, const __grid_constant__ CUtensorMap tmap) {
   static_assert(LOGR == 0 || !PUSH, "batched runs are single-device");
   constexpr bool kHint = HINT;
   uint64_t pol = 0;
@@ -1031,7 +1031,7 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
   // tail: config 2 0.38 -> 0.45 / 0.59 / 0.84 ms at 2 / 4 / 8 chunks per draw.)
   // (32-bit draws: chunks + one overshoot per warp stay far below 2^32)
   auto draw = [&]() -> uint32_t {
-    return lane == 0 ? atomicAdd(reinterpret_cast<unsigned int *>(ticket), 1u) : 0u;
+    return lane == 0 ? atomicAdd(ticket, 1u) : 0u;
   };
   uint32_t drawn = ticket ? draw() : 0u;
   int64_t chunk = ticket ? (int64_t)__shfl_sync(0xffffffffu, drawn, 0) : warp;
@@ -1357,7 +1357,7 @@ k_heavy_partial(const int64_t *__restrict__ offsets, const int32_t *__restrict__
                 const int32_t *__restrict__ item_node, const int64_t *__restrict__ item_beg,
                 int64_t n_items, int64_t item_arcs, int dense, uint8_t *__restrict__ partial,
                 unsigned long long *__restrict__ merged_out, const uint32_t *__restrict__ active,
-                int64_t hot_lim) {
+                int64_t hot_lim, unsigned int *__restrict__ ticket, int draw_items) {
   constexpr bool kHint = HINT;
   uint64_t pol = 0;
   if (kHint) pol = range_policy(cur, (uint32_t)((uint64_t)hot_lim << LOGP), 0xFFFFFFF0u);
@@ -1373,7 +1373,27 @@ k_heavy_partial(const int64_t *__restrict__ offsets, const int32_t *__restrict__
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   uint32_t my_merged = 0;
-  for (int64_t it = warp; it < n_items; it += nwarps) {
+  // Items are dealt grid-stride, or -- with a ticket counter (not in frontier mode) -- in
+  // runs of draw_items consecutive items in the order the warps ask for them (the next
+  // run is drawn when a run starts), as in k_light: no tail at the end of the launch.
+  auto draw = [&]() -> uint32_t {
+    return lane == 0 ? atomicAdd(ticket, 1u) : 0u;
+  };
+  uint32_t drawn = 0;
+  int64_t it = warp, run_end = 0;
+  if (ticket) {
+    drawn = draw();
+    it = (int64_t)__shfl_sync(0xffffffffu, drawn, 0) * draw_items;
+    run_end = it + draw_items;
+    drawn = draw();
+  }
+  for (;; it += ticket ? 1 : nwarps) {
+    if (ticket && it >= run_end) {
+      it = (int64_t)__shfl_sync(0xffffffffu, drawn, 0) * draw_items;
+      run_end = it + draw_items;
+      if (it < n_items) drawn = draw();
+    }
+    if (it >= n_items) break;
     if (active) {
       // frontier mode: most items are inactive -- the lanes test the warp's next 32
       // items (it, it + nwarps, ...) at once and the warp jumps to the first active one
@@ -2705,7 +2725,7 @@ int union_step_impl(int64_t lo, int64_t hi, const int64_t *offsets, const int32_
                     int64_t item_arcs, uint8_t *partial, unsigned long long *nch,
                     unsigned long long *merged, int64_t hot_rows, const uint32_t *active,
                     const Peers &peers, cudaStream_t s, RunArgs ra = RunArgs{nullptr, 0, 0},
-                    int64_t n_rows = 0, unsigned long long *ticket = nullptr) {
+                    int64_t n_rows = 0, unsigned int *ticket = nullptr) {
   using Gm = Geo<LOGP>;
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof(tmap));
@@ -2728,20 +2748,30 @@ int union_step_impl(int64_t lo, int64_t hi, const int64_t *offsets, const int32_
   const bool hint = kCanHint && hot_lim > 0;
   const bool l1na = (size_t)n_rows * Gm::P >= ((size_t)HB_L1NA_MIN_MB << 20);
   if (n_items > 0) {
+    // ticket word 1 deals the heavy items (word 0 the light kernel's chunks), except in
+    // frontier mode, whose skip-ahead probe walks the grid-stride order
+    unsigned int *hticket = ticket && !active ? ticket + 1 : nullptr;
+    const void *hfunc = !hint ? (const void *)k_heavy_partial<LOGP, false>
+                        : (l1na ? (const void *)k_heavy_partial<LOGP, kCanHint, kCanHint>
+                                : (const void *)k_heavy_partial<LOGP, kCanHint>);
+    const unsigned hgrid = hticket ? grid_resident(hfunc, 0, n_items) : grid_for_warps(n_items);
+    // items per draw: ~16 draws per resident warp, at most 32 items
+    const int draw_items = (int)std::max<int64_t>(
+        1, std::min<int64_t>(32, n_items / ((int64_t)hgrid * (kThreads / 32) * 16)));
     if constexpr (kCanHint) {
       if (hint && l1na)
-        k_heavy_partial<LOGP, true, true><<<grid_for_warps(n_items), kThreads, 0, s>>>(
+        k_heavy_partial<LOGP, true, true><<<hgrid, kThreads, 0, s>>>(
             offsets, succ, cur, chg_prev, item_node, item_beg, n_items, item_arcs, dense,
-            partial, merged, active, hot_lim);
+            partial, merged, active, hot_lim, hticket, draw_items);
       else if (hint)
-        k_heavy_partial<LOGP, true><<<grid_for_warps(n_items), kThreads, 0, s>>>(
+        k_heavy_partial<LOGP, true><<<hgrid, kThreads, 0, s>>>(
             offsets, succ, cur, chg_prev, item_node, item_beg, n_items, item_arcs, dense,
-            partial, merged, active, hot_lim);
+            partial, merged, active, hot_lim, hticket, draw_items);
     }
     if (!hint)
-      k_heavy_partial<LOGP, false><<<grid_for_warps(n_items), kThreads, 0, s>>>(
+      k_heavy_partial<LOGP, false><<<hgrid, kThreads, 0, s>>>(
           offsets, succ, cur, chg_prev, item_node, item_beg, n_items, item_arcs, dense,
-          partial, merged, active, hot_lim);
+          partial, merged, active, hot_lim, hticket, draw_items);
     if (int e = check_launch("k_heavy_partial")) return e;
   }
   if (hi > lo) {
@@ -2943,7 +2973,7 @@ int hb_union_step_v2(const hb_step_args *a) {
                        a->heavy_nodes, a->item_first, a->n_heavy, a->finish_order, a->n_mega,
                        a->item_node, a->item_beg, a->n_items, a->item_arcs, a->partial, nch,
                        merged, a->hot_rows, a->active, peers, s, RunArgs{nullptr, 0, 0}, n,
-                       reinterpret_cast<unsigned long long *>(ticket))));
+                       reinterpret_cast<unsigned int *>(ticket))));
   }
   HB_DISPATCH(a->b, return (union_step_impl<LB, false>(
                      lo, hi, a->offsets, a->succ, a->cur, a->nxt, a->chg_prev, a->chg_now,
@@ -2951,7 +2981,7 @@ int hb_union_step_v2(const hb_step_args *a) {
                      a->heavy_nodes, a->item_first, a->n_heavy, a->finish_order, a->n_mega,
                      a->item_node, a->item_beg, a->n_items, a->item_arcs, a->partial, nch,
                      merged, a->hot_rows, a->active, peers, s, RunArgs{nullptr, 0, 0}, n,
-                       reinterpret_cast<unsigned long long *>(ticket))));
+                       reinterpret_cast<unsigned int *>(ticket))));
   return 0;
 }
 

@@ -277,6 +277,7 @@ def _parked_device(bt: _Batch, cfg: HyperBallConfig, cur: torch.Tensor,
     dev.est = est
     dev.lc, dev.alpha_p2, dev.lc_cut = bt.lc, bt.alpha_p2, bt.lc_cut
     dev.counts = torch.zeros(2, dtype=torch.int64, device=bt.device)
+    dev.ticket = torch.zeros(1, dtype=torch.int64, device=bt.device)
     dev.merged_total = 0
     dev.prev_all = dev.full_pass = False
     dev.launches = dev.launches_at_last_step = bt.launches
