@@ -2755,9 +2755,13 @@ int union_step_impl(int64_t lo, int64_t hi, const int64_t *offsets, const int32_
                         : (l1na ? (const void *)k_heavy_partial<LOGP, kCanHint, kCanHint>
                                 : (const void *)k_heavy_partial<LOGP, kCanHint>);
     const unsigned hgrid = hticket ? grid_resident(hfunc, 0, n_items) : grid_for_warps(n_items);
-    // items per draw: ~16 draws per resident warp, at most 32 items
+    // items per draw: ~16 draws per resident warp, at most 8 items (config 5: 27.8 ms; 28.0 /
+    // 28.2 ms at 32 / 128; 4 is 27.6 ms but the draws start to queue on config 5s; env
+    // overrides for sweeps)
+    static const int dpw = [] { const char *e = getenv("HB_DRAWS_PER_WARP"); return e ? atoi(e) : 16; }();
+    static const int dmax = [] { const char *e = getenv("HB_DRAW_MAX"); return e ? atoi(e) : 8; }();
     const int draw_items = (int)std::max<int64_t>(
-        1, std::min<int64_t>(32, n_items / ((int64_t)hgrid * (kThreads / 32) * 16)));
+        1, std::min<int64_t>(dmax, n_items / ((int64_t)hgrid * (kThreads / 32) * dpw)));
     if constexpr (kCanHint) {
       if (hint && l1na)
         k_heavy_partial<LOGP, true, true><<<hgrid, kThreads, 0, s>>>(
