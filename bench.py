@@ -367,7 +367,8 @@ def dense_steps(g, cfgd, local: int, steps: int, warmup: int, schedule: str = "a
             peer_chg=ctypes.cast(pc, ctypes.c_void_p) if pc is not None else None,
             peer_packed_stride=symm.pstride if symm is not None else 0,
             nch_out=dev.counts.data_ptr(), merged_out=dev.counts.data_ptr() + 8,
-            ticket=dev.ticket.data_ptr(), stream=stream.cuda_stream, **_lib.schedule_args(s)))
+            ticket=dev.ticket.data_ptr(), stream=stream.cuda_stream,
+            **(dev.die_args() if symm is None else {}), **_lib.schedule_args(s)))
         if ev1 is not None:
             ev1.record(stream)
         nch, merged = (int(x) for x in dev.counts.cpu())   # the per-iteration termination read

@@ -88,6 +88,9 @@ HB_SIGNATURES = {
     "hb_gen_blocks": (_int, [_i64, _i64, _dbl, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "hb_gen_arc_keys": (_int, [_int, _i64, _u64, _vp, _vp, _vp, _dbl, _i64, _vp, _vp]),
     "hb_transpose_csr": (_int, [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "hb_die_map": (_int, [_vp, _i64, _vp, _vp, _vp]),
+    "hb_die_map_words": (_i64, [_vp, _i64]),
+    "hb_die_partition": (_int, [_i64, _vp, _vp, _vp, _vp, _i64, _int, _vp, _i64, _vp, _vp, _vp]),
     "hb_item_arcs": (_i64, [_int]),
     "hb_light_max_deg": (_i64, [_int]),
     "hb_light_npw": (_i64, [_int]),
@@ -116,6 +119,7 @@ class StepArgs(ctypes.Structure):
         ("check_rows", _i64), ("check_m", _i64),
         ("peer_packed_stride", _i64),
         ("ticket", _vp),
+        ("die_head", _vp), ("die_rows", _i64), ("item_split", _vp),
     ]
 
     def __init__(self, **kw):

@@ -20,6 +20,8 @@
 #include <cuda_runtime.h>
 #include <type_traits>
 #include <algorithm>
+#include <cmath>
+#include <vector>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_sort.cuh>
@@ -1348,22 +1350,60 @@ k_light(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
   block_add2(my_nch, my_merged, nch_out, merged_out);
 }
 
+#ifndef HB_SHORT_ROUNDS
+#define HB_SHORT_ROUNDS 0   // measured: config 5 28.3 -> 28.4 ms (more instructions, not fewer)
+#endif
+template <int LOGP>
+__host__ __device__ constexpr bool kShortRounds() {
+  return HB_SHORT_ROUNDS && LOGP < HB_PAD_MIN_LOGP && Batch<LOGP>::U % 2 == 0;
+}
 // Heavy nodes, phase 1: one warp per work item (a slice of one node's arcs) leaves the
 // max over the slice's changed sources as a partial row.
-template <int LOGP, bool HINT = false, bool L1NA = false>
+//
+// DIE (die-affine items): a B200 is two dies, each with half of the L2;
+// a line read by SMs of both dies is kept in both halves, so a gather every SM issues can
+// use ~64 MB of the 126 MB.  The hot head of the register array is copied into a fixed
+// buffer (`head`, die_rows rows) at the start of the step; with the home die of each of
+// its 2 KB chunks known (hb_die_map), hb_die_partition has reordered the ids of every item
+// once per graph -- first the sources whose head row lives on die 0, then those of die 1,
+// the cold rows filling both halves evenly, item_split[i] of the former.  Pass d of item i merges its half and is drawn from queue d (ticket word 1 + d)
+// by the warps of die d's SMs (g_sm_die), which take the other queue's leftovers at the
+// end.  Each die then caches only its own half of the head: ~2x the hot rows stay on chip
+// (tools/die_probe.cu: 265 G rows/s up to 96 MB, against 64 MB).  Pass d of item i leaves
+// partial row 2 i + d.  The result does not depend on the maps.
+// Opt-in (HB_DIE=1).  On config 5 it does not pay: the step's DRAM reads fall 71 -> 64 GB,
+// but the 15.5 M items average 242 arcs, so two passes each double the fixed per-item work
+// (8.3 -> 14.7 G warp instructions, issue 35% -> 56%): 20.5 -> 22.8 ms.
+__device__ int8_t g_sm_die[256];
+__device__ __forceinline__ uint32_t sm_id() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+template <int LOGP, bool HINT = false, bool L1NA = false, bool DIE = false>
 __global__ void __launch_bounds__(kThreads, (LOGP >= 10 ? 2 : 4))
 k_heavy_partial(const int64_t *__restrict__ offsets, const int32_t *__restrict__ succ,
                 const uint8_t *__restrict__ cur, const uint32_t *__restrict__ chg_prev,
                 const int32_t *__restrict__ item_node, const int64_t *__restrict__ item_beg,
                 int64_t n_items, int64_t item_arcs, int dense, uint8_t *__restrict__ partial,
                 unsigned long long *__restrict__ merged_out, const uint32_t *__restrict__ active,
-                int64_t hot_lim, unsigned int *__restrict__ ticket, int draw_items) {
+                int64_t hot_lim, unsigned int *__restrict__ ticket, int draw_items,
+                const int32_t *__restrict__ item_split = nullptr,
+                const uint8_t *__restrict__ head = nullptr, int64_t die_rows = 0) {
   constexpr bool kHint = HINT;
   uint64_t pol = 0;
-  if (kHint) pol = range_policy(cur, (uint32_t)((uint64_t)hot_lim << LOGP), 0xFFFFFFF0u);
+  // DIE: the head copy is the evict_last range (cold rows, read from cur, lie outside it)
+  if (kHint) pol = range_policy(DIE ? head : cur, (uint32_t)((uint64_t)hot_lim << LOGP), 0xFFFFFFF0u);
   using Gm = Geo<LOGP>;
   using B = Batch<LOGP>;
   __shared__ int32_t sids[kThreads / 32][B::HEAVY_IDS];
+  uint32_t cls = 0;                             // DIE: the pass (source die) being merged
+  if constexpr (DIE) {
+    cls = (uint32_t)g_sm_die[sm_id() & 255u] & 1u;
+    ticket += cls;
+  }
+  bool stolen = false;
+  const uint4 *head4 = reinterpret_cast<const uint4 *>(head);
   const int lane = threadIdx.x & 31;
   const int gl = lane % Gm::G;
   const int slot = lane / Gm::G;
@@ -1393,6 +1433,17 @@ k_heavy_partial(const int64_t *__restrict__ offsets, const int32_t *__restrict__
       run_end = it + draw_items;
       if (it < n_items) drawn = draw();
     }
+    if constexpr (DIE) {
+      if (it >= n_items && !stolen) {           // own queue empty: the other die's leftovers
+        stolen = true;
+        ticket += cls ? -1 : 1;
+        cls ^= 1u;
+        drawn = draw();
+        it = (int64_t)__shfl_sync(0xffffffffu, drawn, 0) * draw_items;
+        run_end = it + draw_items;
+        if (it < n_items) drawn = draw();
+      }
+    }
     if (it >= n_items) break;
     if (active) {
       // frontier mode: most items are inactive -- the lanes test the warp's next 32
@@ -1413,10 +1464,15 @@ k_heavy_partial(const int64_t *__restrict__ offsets, const int32_t *__restrict__
     const int64_t v = __ldg(item_node + it);
     HB_CHK(it < g_chk.items && v >= 0 && v < g_chk.rows, "k_heavy_partial item / node");
     if (active && !test_bit(active, v)) continue;   // warp-uniform: one node per item
-    const int64_t beg = __ldg(item_beg + it);
+    int64_t beg = __ldg(item_beg + it);
     int64_t end = __ldg(offsets + v + 1);
     if (end > beg + item_arcs) end = beg + item_arcs;
     HB_CHK(0 <= beg && beg <= end && end <= g_chk.m, "k_heavy_partial arc range");
+    if constexpr (DIE) {
+      const int64_t sp = beg + __ldg(item_split + it);
+      HB_CHK(beg <= sp && sp <= end, "k_heavy_partial item split");
+      if (cls == 0) end = sp; else beg = sp;
+    }
     uint4 acc[Gm::CPL];
     RowAcc<LOGP> macc;
     macc.init();
@@ -1453,24 +1509,35 @@ k_heavy_partial(const int64_t *__restrict__ offsets, const int32_t *__restrict__
         // slots past cnt re-load the batch's first row (already merged: no effect), from
         // p = 64 up; predicated off below
         uint4 r[B::U][Gm::CPL];
+        // rows of this round that exist (warp-uniform): short items -- half of them at
+        // p = 16 -- skip the pairs of row loads and merges past their last id
+        const int need = kShortRounds<LOGP>() ? (cnt - (i - slot) + Gm::NPW - 1) / Gm::NPW : B::U;
 #pragma unroll
         for (int u = 0; u < B::U; u++) {
+          if (kShortRounds<LOGP>() && (u & ~1) >= need) {
+#pragma unroll
+            for (int c = 0; c < Gm::CPL; c++) r[u][c] = make_uint4(0, 0, 0, 0);
+            continue;
+          }
           const int e = i + u * Gm::NPW;
           const bool ok = e < cnt;
           HB_CHK(!ok || e < B::HEAVY_IDS, "k_heavy_partial shared id read");
           const int32_t w = wids[ok ? e : 0];
           HB_CHK(w >= 0 && w < g_chk.rows, "k_heavy_partial source row");
+          const uint4 *src4 = DIE && w < die_rows ? head4 : cur4;   // hot rows: the head copy
 #pragma unroll
           for (int c = 0; c < Gm::CPL; c++)
             r[u][c] = (LOGP >= HB_PAD_MIN_LOGP || ok)
-                          ? (kHint ? ld_row_chunk_hint<LOGP, L1NA>(cur4, w, Gm::CH, c * Gm::G + gl, pol)
-                                   : ld_row_chunk<LOGP>(cur4, w, Gm::CH, c * Gm::G + gl))
+                          ? (kHint ? ld_row_chunk_hint<LOGP, L1NA>(src4, w, Gm::CH, c * Gm::G + gl, pol)
+                                   : ld_row_chunk<LOGP>(src4, w, Gm::CH, c * Gm::G + gl))
                           : make_uint4(0, 0, 0, 0);
         }
 #pragma unroll
-        for (int u = 0; u + 1 < B::U; u += 2)
+        for (int u = 0; u + 1 < B::U; u += 2) {
+          if (kShortRounds<LOGP>() && u >= need) continue;
 #pragma unroll
           for (int c = 0; c < Gm::CPL; c++) macc.add2(c, r[u][c], r[u + 1][c]);
+        }
         if constexpr (B::U % 2 == 1) {
 #pragma unroll
           for (int c = 0; c < Gm::CPL; c++) macc.add(c, r[B::U - 1][c]);
@@ -1488,7 +1555,8 @@ k_heavy_partial(const int64_t *__restrict__ offsets, const int32_t *__restrict__
     if (slot == 0) {
 #pragma unroll
       for (int c = 0; c < Gm::CPL; c++)
-        *reinterpret_cast<uint4 *>(partial + (size_t)it * Gm::P + 16 * (c * Gm::G + gl)) = acc[c];
+        *reinterpret_cast<uint4 *>(partial + (size_t)(DIE ? 2 * it + cls : it) * Gm::P +
+                                   16 * (c * Gm::G + gl)) = acc[c];
     }
   }
   block_add2(my_merged, 0u, merged_out, nullptr);
@@ -1508,7 +1576,8 @@ k_heavy_finish(const int32_t *__restrict__ heavy_nodes, const int32_t *__restric
                double *__restrict__ est, double *__restrict__ sum_dist,
                double *__restrict__ sum_recip, EstConst ec, double tf,
                unsigned long long *__restrict__ nch_out, const uint32_t *__restrict__ active,
-               Peers peers, RunArgs ra) {
+               Peers peers, RunArgs ra, int pshift = 0) {
+  // pshift = 1: die-affine items, two partial rows per item (k_heavy_partial<.., DIE>)
   using Gm = Geo<LOGP>;
   constexpr int UF = 4;
   const int lane = threadIdx.x & 31;
@@ -1524,9 +1593,11 @@ k_heavy_finish(const int32_t *__restrict__ heavy_nodes, const int32_t *__restric
     const bool valid = e < o1;
     const int64_t j = valid ? __ldg(order + e) : 0;
     const int64_t v = valid ? __ldg(heavy_nodes + j) : 0;
-    const int i0 = valid ? __ldg(item_first + j) : 0, i1 = valid ? __ldg(item_first + j + 1) : 0;
+    int i0 = valid ? __ldg(item_first + j) : 0, i1 = valid ? __ldg(item_first + j + 1) : 0;
     HB_CHK(!valid || (v >= 0 && v < g_chk.rows && 0 <= i0 && i0 <= i1 && i1 <= g_chk.items),
            "k_heavy_finish node / items");
+    i0 <<= pshift;
+    i1 <<= pshift;
     const int first = mega ? i0 + grp : i0, stride = mega ? Gm::NPW : 1;
     uint4 acc[Gm::CPL];
 #pragma unroll
@@ -2514,6 +2585,130 @@ __global__ void k_count_bits(const uint32_t *__restrict__ bits, int64_t words,
 // ordinal (SM count, L2 set-aside, opt-in shared-memory sizes).
 constexpr int kMaxDevices = 64;
 
+// ---- L2 die maps (die-affine heavy items, see k_heavy_partial) ----------------------
+// An atomic executes at the home L2 slice of its address: from an SM of the other die it
+// takes ~400 cycles longer on a B200 (tools/die_probe.cu: 263-291 against 656-727 cycles),
+// so the latency of atomicOr(p, 0) -- which leaves the data alone -- tells the dies apart.
+__device__ __forceinline__ uint32_t timed_atomic(uint32_t *p, int reps) {
+  __shared__ uint32_t sink_word[32];
+  const uint32_t sink = (uint32_t)__cvta_generic_to_shared(sink_word + (threadIdx.x & 31));
+  uint32_t best = 0xffffffffu;
+  for (int r = 0; r < reps; r++) {
+    long long t0, t1;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t0) :: "memory");
+    const uint32_t v = atomicOr(p, 0u);
+    // the store needs v: the second clock read issues after the atomic has returned
+    asm volatile("st.volatile.shared.u32 [%0], %1;" :: "r"(sink), "r"(v) : "memory");
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t1) :: "memory");
+    const uint32_t d = (uint32_t)(t1 - t0);
+    best = d < best ? d : best;
+  }
+  return best;
+}
+// word to probe in chunk c of the 2 KB grid over [base, base + bytes)
+__device__ __forceinline__ uint32_t *probe_word(uint8_t *base, int64_t bytes, int64_t c) {
+  const uintptr_t b = reinterpret_cast<uintptr_t>(base);
+  uintptr_t a = ((b >> 11) + (uintptr_t)c) << 11;
+  a = a < b ? ((b + 3) & ~(uintptr_t)3) : a;
+  const uintptr_t lim = b + (uintptr_t)bytes - 4;
+  return reinterpret_cast<uint32_t *>(a < lim ? a : (lim & ~(uintptr_t)3));
+}
+constexpr int kDieTest = 128;      // test chunks of the SM classification
+// one warp per SM (the first CTA to claim it): latency of kDieTest spread-out chunks
+__global__ void k_sm_probe(uint8_t *base, int64_t bytes, int64_t stride, int *claimed,
+                           uint32_t *lat) {
+  __shared__ int mine;
+  const uint32_t sm = sm_id() & 255u;
+  if (threadIdx.x == 0) mine = atomicCAS(claimed + sm, 0, 1) == 0;
+  __syncthreads();
+  if (!mine || threadIdx.x != 0) return;
+  for (int k = 0; k < kDieTest; k++)
+    lat[sm * kDieTest + k] = timed_atomic(probe_word(base, bytes, k * stride), 6);
+}
+// every chunk timed from both dies (chunks dealt 16 at a time by a counter per die)
+__global__ void k_chunk_probe(uint8_t *base, int64_t bytes, int64_t chunks, unsigned int *next,
+                              uint32_t *lat2) {
+  const int d = g_sm_die[sm_id() & 255u] & 1;
+  if (threadIdx.x != 0) return;
+  for (;;) {
+    const int64_t c0 = (int64_t)atomicAdd(next + d, 16u);
+    if (c0 >= chunks) break;
+    for (int64_t c = c0; c < c0 + 16 && c < chunks; c++)
+      lat2[d * chunks + c] = timed_atomic(probe_word(base, bytes, c), 4);
+  }
+}
+// bit c = 1 when die 1 is closer; stats: [chunks on die 1, chunks with a gap < 64 cycles]
+__global__ void k_chunk_bits(const uint32_t *__restrict__ lat2, int64_t chunks,
+                             uint32_t *__restrict__ bits, unsigned long long *stats) {
+  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= (chunks + 31) / 32) return;
+  uint32_t m = 0;
+  int ones = 0, weak = 0;
+  for (int i = 0; i < 32 && w * 32 + i < chunks; i++) {
+    const int64_t c = w * 32 + i;
+    const int a = (int)lat2[c], b = (int)lat2[chunks + c];
+    if (b < a) { m |= 1u << i; ones++; }
+    weak += (a > b ? a - b : b - a) < 64;
+  }
+  bits[w] = m;
+  atomicAdd(stats, (unsigned long long)ones);
+  atomicAdd(stats + 1, (unsigned long long)weak);
+}
+
+// Reorder the ids of every heavy item by the pass that merges them (see k_heavy_partial):
+// pass 0 = the sources whose head row is homed on die 0, pass 1 those of die 1; the cold
+// sources (ids >= die_rows, read from DRAM wherever they live) fill pass 0 up to half of
+// the item, the rest go to pass 1, so both passes are as even as the hot ids allow (a pass
+// of 257 ids would cost a second, almost empty, batch of row loads).  The order inside a
+// class is kept.  One warp per item (<= 512 ids); split[i] = ids of pass 0.
+constexpr int kDieItemMax = 512;
+__global__ void __launch_bounds__(kThreads)
+k_die_partition(int64_t n_items, const int32_t *__restrict__ item_node,
+                const int64_t *__restrict__ item_beg, const int64_t *__restrict__ offsets,
+                int32_t *succ, int64_t item_arcs, int logp, uint32_t head_off, int64_t die_rows,
+                const uint32_t *__restrict__ die_bits, int32_t *__restrict__ split) {
+  __shared__ int32_t buf[kThreads / 32][3][kDieItemMax];
+  const int lane = threadIdx.x & 31;
+  const unsigned below = (1u << lane) - 1u;
+  int32_t(*my)[kDieItemMax] = buf[threadIdx.x >> 5];
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t it = warp; it < n_items; it += nwarps) {
+    const int64_t v = __ldg(item_node + it);
+    const int64_t beg = __ldg(item_beg + it);
+    int64_t end = __ldg(offsets + v + 1);
+    if (end > beg + item_arcs) end = beg + item_arcs;
+    int n[3] = {0, 0, 0};
+    for (int64_t k = beg; k < end; k += 32) {
+      const bool ok = k + lane < end;
+      const uint32_t id = ok ? (uint32_t)succ[k + lane] : 0u;
+      const uint32_t c = (head_off + (id << logp)) >> 11;
+      const int cls = (int64_t)id < die_rows ? (int)((__ldg(die_bits + (c >> 5)) >> (c & 31)) & 1u) : 2;
+#pragma unroll
+      for (int q = 0; q < 3; q++) {
+        const unsigned bq = __ballot_sync(0xffffffffu, ok && cls == q);
+        if (ok && cls == q) my[q][n[q] + __popc(bq & below)] = (int32_t)id;
+        n[q] += __popc(bq);
+      }
+    }
+    __syncwarp();
+    const int total = n[0] + n[1] + n[2];
+    int c0 = (total + 1) / 2 - n[0];             // cold ids of pass 0
+    c0 = c0 < 0 ? 0 : (c0 > n[2] ? n[2] : c0);
+    const int p0 = n[0] + c0;
+    for (int i = lane; i < total; i += 32) {
+      int32_t id;
+      if (i < n[0]) id = my[0][i];
+      else if (i < p0) id = my[2][i - n[0]];
+      else if (i < p0 + n[1]) id = my[1][i - p0];
+      else id = my[2][c0 + (i - p0 - n[1])];
+      succ[beg + i] = id;
+    }
+    if (lane == 0) split[it] = p0;
+    __syncwarp();
+  }
+}
+
 struct DevGuard {
   int prev = -1, dev = -1;
   explicit DevGuard(cudaStream_t s) {
@@ -2532,6 +2727,12 @@ int current_device() {
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) dev = 0;
   return dev;
 }
+
+// SM -> die table of the current device: 0 = not measured, 1 = g_sm_die valid, -1 = the
+// device did not split into two dies: die-affine items stay off.
+int g_die_state[64];
+int g_die_sms[64][2];
+bool sm_die_ready() { return g_die_state[current_device()] == 1; }
 
 // Opt-in dynamic shared memory of `func` on the current device (once per device and
 // kernel; the return code is checked).
@@ -2593,6 +2794,18 @@ size_t persist_bytes(size_t want) {
 
 // Bytes of the evict_last head (HB_HINT_MB, default 64); HB_PERSIST_WINDOW=0 turns the
 // persisting access-policy window off.
+// smallest register array that uses die-affine items (HB_DIE_MIN_MB, read per call: the
+// tests lower it to reach the path on small graphs)
+size_t die_min_bytes() {
+  const char *e = getenv("HB_DIE_MIN_MB");
+  return (size_t)(e ? atoll(e) : HB_L1NA_MIN_MB) << 20;
+}
+// persisting window over the head copy of the die-affine items (HB_DIE_WINDOW_MB; default:
+// the step's window size)
+size_t die_window_bytes(size_t win) {
+  const char *e = getenv("HB_DIE_WINDOW_MB");
+  return e ? (size_t)atoll(e) << 20 : win;
+}
 int64_t hint_bytes() {
   static int64_t b = [] {
     int64_t mb = 64;
@@ -2725,7 +2938,9 @@ int union_step_impl(int64_t lo, int64_t hi, const int64_t *offsets, const int32_
                     int64_t item_arcs, uint8_t *partial, unsigned long long *nch,
                     unsigned long long *merged, int64_t hot_rows, const uint32_t *active,
                     const Peers &peers, cudaStream_t s, RunArgs ra = RunArgs{nullptr, 0, 0},
-                    int64_t n_rows = 0, unsigned int *ticket = nullptr) {
+                    int64_t n_rows = 0, unsigned int *ticket = nullptr,
+                    uint8_t *die_head = nullptr, int64_t die_head_rows = 0,
+                    const int32_t *item_split = nullptr) {
   using Gm = Geo<LOGP>;
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof(tmap));
@@ -2743,10 +2958,17 @@ int union_step_impl(int64_t lo, int64_t hi, const int64_t *offsets, const int32_
     cudaCtxResetPersistingL2Cache();    // lines of last iteration's buffer stop persisting
     set_hot_window(s, cur, (size_t)hot_rows * Gm::P, win);
   }
-  const int64_t hot_lim = hot_rows > 0 ? std::min<int64_t>(hot_rows, hint_bytes() / Gm::P) : 0;
   constexpr bool kCanHint = LOGP <= HB_HINT_MAX_LOGP;
-  const bool hint = kCanHint && hot_lim > 0;
   const bool l1na = (size_t)n_rows * Gm::P >= ((size_t)HB_L1NA_MIN_MB << 20);
+  // die-affine heavy items: hinted rows (p <= 32) of a register array too large for L1,
+  // ticket-dealt (not in frontier mode), with the chunk map of this `cur` buffer
+  const bool die = kCanHint && (size_t)n_rows * Gm::P >= die_min_bytes() && die_head &&
+                   item_split && ticket && !active && n_items > 0 && hot_rows > 0 &&
+                   item_arcs <= kDieItemMax && sm_die_ready();
+  const int64_t die_rows = die ? std::min<int64_t>(hot_rows, die_head_rows) : 0;
+  const int64_t hot_lim = hot_rows > 0 ? std::min<int64_t>(hot_rows, hint_bytes() / Gm::P) : 0;
+  const bool hint = kCanHint && hot_lim > 0;
+  int pshift = 0;
   if (n_items > 0) {
     // ticket word 1 deals the heavy items (word 0 the light kernel's chunks), except in
     // frontier mode, whose skip-ahead probe walks the grid-stride order
@@ -2754,6 +2976,11 @@ int union_step_impl(int64_t lo, int64_t hi, const int64_t *offsets, const int32_
     const void *hfunc = !hint ? (const void *)k_heavy_partial<LOGP, false>
                         : (l1na ? (const void *)k_heavy_partial<LOGP, kCanHint, kCanHint>
                                 : (const void *)k_heavy_partial<LOGP, kCanHint>);
+    if constexpr (kCanHint) {
+      if (die && hint && die_rows > 0)
+        hfunc = (const void *)k_heavy_partial<LOGP, true, true, true>;
+    }
+    const bool die_on = kCanHint && hfunc == (const void *)k_heavy_partial<LOGP, kCanHint, kCanHint, kCanHint>;
     const unsigned hgrid = hticket ? grid_resident(hfunc, 0, n_items) : grid_for_warps(n_items);
     // items per draw: ~16 draws per resident warp, at most 8 items (config 5: 27.8 ms; 28.0 /
     // 28.2 ms at 32 / 128; 4 is 27.6 ms but the draws start to queue on config 5s; env
@@ -2763,7 +2990,17 @@ int union_step_impl(int64_t lo, int64_t hi, const int64_t *offsets, const int32_
     const int draw_items = (int)std::max<int64_t>(
         1, std::min<int64_t>(dmax, n_items / ((int64_t)hgrid * (kThreads / 32) * dpw)));
     if constexpr (kCanHint) {
-      if (hint && l1na)
+      if (die_on) {
+        pshift = 1;
+        // the head copy the passes gather from (fixed address: its die map is static)
+        if (cudaMemcpyAsync(die_head, cur, (size_t)die_rows * Gm::P, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+          return set_err("hb_union_step head copy", cudaGetLastError());
+        if (win > 0) set_hot_window(s, die_head, (size_t)die_rows * Gm::P, die_window_bytes(win));
+        k_heavy_partial<LOGP, true, true, true><<<hgrid, kThreads, 0, s>>>(
+            offsets, succ, cur, chg_prev, item_node, item_beg, n_items, item_arcs, dense,
+            partial, merged, active, die_rows, hticket, draw_items, item_split, die_head, die_rows);
+        if (win > 0) set_hot_window(s, cur, (size_t)hot_rows * Gm::P, win);
+      } else if (hint && l1na)
         k_heavy_partial<LOGP, true, true><<<hgrid, kThreads, 0, s>>>(
             offsets, succ, cur, chg_prev, item_node, item_beg, n_items, item_arcs, dense,
             partial, merged, active, hot_lim, hticket, draw_items);
@@ -2800,14 +3037,14 @@ int union_step_impl(int64_t lo, int64_t hi, const int64_t *offsets, const int32_
     if (n_mega > 0) {
       k_heavy_finish<LOGP, PUSH, LOGR><<<grid_for_warps(n_mega), kThreads, 0, s>>>(
           heavy_nodes, item_first, finish_order, 0, n_mega, 1, partial, cur, nxt, chg_prev,
-          chg_now, est, sum_dist, sum_recip, ec, tf, nch, active, peers, ra);
+          chg_now, est, sum_dist, sum_recip, ec, tf, nch, active, peers, ra, pshift);
       if (int e = check_launch("k_heavy_finish(mega)")) return e;
     }
     if (n_heavy > n_mega)
       k_heavy_finish<LOGP, PUSH, LOGR>
           <<<grid_for_warps((n_heavy - n_mega + Gm::NPW - 1) / Gm::NPW), kThreads, 0, s>>>(
               heavy_nodes, item_first, finish_order, n_mega, n_heavy, 0, partial, cur, nxt,
-              chg_prev, chg_now, est, sum_dist, sum_recip, ec, tf, nch, active, peers, ra);
+              chg_prev, chg_now, est, sum_dist, sum_recip, ec, tf, nch, active, peers, ra, pshift);
     if (int e = check_launch("k_heavy_finish")) return e;
   }
   if (win > 0) set_hot_window(s, nullptr, 0, 0);
@@ -2917,6 +3154,10 @@ int hb_union_step_v2(const hb_step_args *a) {
   }();
   uint64_t *ticket = tickets_on && a->struct_size >= offsetof(hb_step_args, ticket) + sizeof(uint64_t *)
                          ? a->ticket : nullptr;
+  const bool has_die = a->struct_size >= offsetof(hb_step_args, item_split) + sizeof(void *);
+  uint8_t *die_head = has_die && ticket && a->item_split && a->die_rows > 0 ? a->die_head : nullptr;
+  const int64_t die_head_rows = die_head ? a->die_rows : 0;
+  const int32_t *item_split = die_head ? a->item_split : nullptr;
   DevGuard dg_((cudaStream_t)a->stream);
   const int n_peers = a->n_peers, n_disc = a->n_disc;
   const int64_t n = a->n, lo = a->lo, hi = a->hi, t = a->t;
@@ -2951,7 +3192,7 @@ int hb_union_step_v2(const hb_step_args *a) {
     return set_err("hb_union_step memset nch", e);
   if (a->merged_out && (e = cudaMemsetAsync(a->merged_out, 0, sizeof(uint64_t), s)) != cudaSuccess)
     return set_err("hb_union_step memset merged", e);
-  if (ticket && (e = cudaMemsetAsync(ticket, 0, sizeof(uint64_t), s)) != cudaSuccess)
+  if (ticket && (e = cudaMemsetAsync(ticket, 0, sizeof(uint64_t) * (die_head ? 2 : 1), s)) != cudaSuccess)
     return set_err("hb_union_step memset ticket", e);
   if (a->clear_chg_now && n > 0) {
     if ((e = cudaMemsetAsync(a->chg_now, 0, sizeof(uint32_t) * (size_t)((n + 31) / 32), s)) !=
@@ -2977,7 +3218,7 @@ int hb_union_step_v2(const hb_step_args *a) {
                        a->heavy_nodes, a->item_first, a->n_heavy, a->finish_order, a->n_mega,
                        a->item_node, a->item_beg, a->n_items, a->item_arcs, a->partial, nch,
                        merged, a->hot_rows, a->active, peers, s, RunArgs{nullptr, 0, 0}, n,
-                       reinterpret_cast<unsigned int *>(ticket))));
+                       reinterpret_cast<unsigned int *>(ticket), die_head, die_head_rows, item_split)));
   }
   HB_DISPATCH(a->b, return (union_step_impl<LB, false>(
                      lo, hi, a->offsets, a->succ, a->cur, a->nxt, a->chg_prev, a->chg_now,
@@ -2985,7 +3226,7 @@ int hb_union_step_v2(const hb_step_args *a) {
                      a->heavy_nodes, a->item_first, a->n_heavy, a->finish_order, a->n_mega,
                      a->item_node, a->item_beg, a->n_items, a->item_arcs, a->partial, nch,
                      merged, a->hot_rows, a->active, peers, s, RunArgs{nullptr, 0, 0}, n,
-                       reinterpret_cast<unsigned int *>(ticket))));
+                       reinterpret_cast<unsigned int *>(ticket), die_head, die_head_rows, item_split)));
   return 0;
 }
 
@@ -3021,6 +3262,119 @@ int hb_union_step(int64_t n, int64_t lo, int64_t hi, const int64_t *offsets,
 }
 
 void hb_set_l2_persist(int enable) { g_l2_persist = enable != 0; }
+
+// SM -> die classification of the current device (once): latency vectors of kDieTest
+// chunks per SM, split by the sign of their correlation with the first SM's vector.
+static int classify_sms(uint8_t *base, int64_t bytes, int64_t chunks, cudaStream_t s) {
+  const int dev = current_device();
+  if (g_die_state[dev] != 0) return 0;
+  g_die_state[dev] = -1;
+  const int64_t stride = chunks / kDieTest;
+  if (stride < 3) return 0;                       // needs >= 768 KB to probe
+  int *claimed = nullptr;
+  uint32_t *lat = nullptr;
+  if (cudaMalloc(&claimed, 256 * sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&lat, 256 * kDieTest * sizeof(uint32_t)) != cudaSuccess) {
+    cudaFree(claimed);
+    return set_err("hb_die_map: scratch", cudaGetLastError());
+  }
+  std::vector<uint32_t> hl(256 * kDieTest);
+  std::vector<int> hc(256);
+  cudaMemsetAsync(claimed, 0, 256 * sizeof(int), s);
+  cudaMemsetAsync(lat, 0, 256 * kDieTest * sizeof(uint32_t), s);
+  k_sm_probe<<<num_sms() * 16, 32, 0, s>>>(base, bytes, stride, claimed, lat);
+  cudaMemcpyAsync(hl.data(), lat, hl.size() * 4, cudaMemcpyDeviceToHost, s);
+  cudaMemcpyAsync(hc.data(), claimed, hc.size() * 4, cudaMemcpyDeviceToHost, s);
+  const cudaError_t e = cudaStreamSynchronize(s);
+  cudaFree(claimed);
+  cudaFree(lat);
+  if (e != cudaSuccess) return set_err("hb_die_map: SM probe", e);
+  int ref = -1;
+  for (int i = 0; i < 256; i++) if (hc[i]) { ref = i; break; }
+  if (ref < 0) return 0;
+  int8_t die[256];
+  int cnt[2] = {0, 0};
+  double min_abs = 1.0;
+  for (int i = 0; i < 256; i++) {
+    die[i] = (int8_t)(i & 1);                     // SMs no CTA landed on: either queue
+    if (!hc[i]) continue;
+    double ma = 0, mb = 0, cov = 0, va = 0, vb = 0;
+    for (int k = 0; k < kDieTest; k++) { ma += hl[ref * kDieTest + k]; mb += hl[i * kDieTest + k]; }
+    ma /= kDieTest; mb /= kDieTest;
+    for (int k = 0; k < kDieTest; k++) {
+      const double a = hl[ref * kDieTest + k] - ma, b = hl[i * kDieTest + k] - mb;
+      cov += a * b; va += a * a; vb += b * b;
+    }
+    const double corr = cov / std::sqrt(va * vb + 1e-9);
+    die[i] = corr > 0 ? 0 : 1;
+    cnt[die[i]]++;
+    min_abs = std::min(min_abs, std::fabs(corr));
+  }
+  // two dies, each with at least a quarter of the SMs, cleanly separated
+  if (cnt[0] * 4 < cnt[0] + cnt[1] || cnt[1] * 4 < cnt[0] + cnt[1] || min_abs < 0.5) return 0;
+  if (cudaMemcpyToSymbol(g_sm_die, die, sizeof(die)) != cudaSuccess)
+    return set_err("hb_die_map: SM table", cudaGetLastError());
+  g_die_sms[dev][0] = cnt[0];
+  g_die_sms[dev][1] = cnt[1];
+  g_die_state[dev] = 1;
+  return 0;
+}
+
+int hb_die_map(void *base, int64_t bytes, uint32_t *bits_out, int64_t *stats, void *stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  DevGuard dg_(s);
+  if (stats) stats[0] = stats[1] = stats[2] = stats[3] = 0;
+  if (!base || bytes < 4096 || !bits_out || !stats) return set_err_msg("hb_die_map: bad arguments");
+  // opt-in (HB_DIE=1): on config 5 the two passes per item cost more instructions than the
+  // L2 hits they add save; without it the call reports "no split"
+  const char *en = getenv("HB_DIE");
+  if (!en || en[0] != '1') return 0;
+  const int64_t chunks = (int64_t)(((reinterpret_cast<uintptr_t>(base) & 2047u) + (uint64_t)bytes + 2047u) >> 11);
+  if (int e = classify_sms((uint8_t *)base, bytes, chunks, s)) return e;
+  const int dev = current_device();
+  if (g_die_state[dev] != 1) return 0;            // stats all zero: not available
+  uint32_t *lat2 = nullptr;
+  unsigned long long *scr = nullptr;              // [0] the two deal counters, [2..3] stats
+  if (cudaMalloc(&lat2, 2 * chunks * sizeof(uint32_t)) != cudaSuccess ||
+      cudaMalloc(&scr, 4 * sizeof(unsigned long long)) != cudaSuccess) {
+    cudaFree(lat2);
+    return set_err("hb_die_map: scratch", cudaGetLastError());
+  }
+  cudaMemsetAsync(scr, 0, 4 * sizeof(unsigned long long), s);
+  k_chunk_probe<<<num_sms() * 4, 32, 0, s>>>((uint8_t *)base, bytes, chunks,
+                                             reinterpret_cast<unsigned int *>(scr), lat2);
+  k_chunk_bits<<<(unsigned)(((chunks + 31) / 32 + 255) / 256), 256, 0, s>>>(lat2, chunks, bits_out, scr + 2);
+  unsigned long long h[2] = {0, 0};
+  cudaMemcpyAsync(h, scr + 2, sizeof(h), cudaMemcpyDeviceToHost, s);
+  const cudaError_t e = cudaStreamSynchronize(s);
+  cudaFree(lat2);
+  cudaFree(scr);
+  if (e != cudaSuccess) return set_err("hb_die_map: chunk probe", e);
+  stats[0] = g_die_sms[dev][0];
+  stats[1] = g_die_sms[dev][1];
+  stats[2] = (int64_t)h[0];
+  stats[3] = (int64_t)h[1];
+  return 0;
+}
+int hb_die_partition(int64_t n_items, const int32_t *item_node, const int64_t *item_beg,
+                     const int64_t *offsets, int32_t *succ, int64_t item_arcs, int b,
+                     const void *head, int64_t die_rows, const uint32_t *die_bits,
+                     int32_t *item_split, void *stream) {
+  cudaStream_t s = (cudaStream_t)stream;
+  DevGuard dg_(s);
+  if (n_items <= 0) return 0;
+  if (!item_node || !item_beg || !offsets || !succ || !head || !die_bits || !item_split ||
+      b < HB_MIN_B || b > HB_MAX_B || die_rows < 0 || item_arcs <= 0 || item_arcs > kDieItemMax)
+    return set_err_msg("hb_die_partition: bad arguments (item_arcs <= 512)");
+  k_die_partition<<<grid_for_warps(n_items), kThreads, 0, s>>>(
+      n_items, item_node, item_beg, offsets, succ, item_arcs, b,
+      (uint32_t)(reinterpret_cast<uintptr_t>(head) & 2047u), die_rows, die_bits, item_split);
+  return check_launch("k_die_partition");
+}
+int64_t hb_die_map_words(const void *base, int64_t bytes) {
+  const int64_t chunks = (int64_t)(((reinterpret_cast<uintptr_t>(base) & 2047u) + (uint64_t)bytes + 2047u) >> 11);
+  return (chunks + 31) / 32;
+}
 uint64_t hb_step_args_size(void) { return sizeof(hb_step_args); }
 uint64_t hb_step_args_min_size(void) { return offsetof(hb_step_args, peer_packed_stride); }
 
@@ -3488,6 +3842,19 @@ __device__ __forceinline__ int owner_rank(const RankBounds &rb, int64_t v) {
   while (r + 1 < rb.world && v >= rb.b[r + 1]) r++;
   return r;
 }
+// Sort window of the `window` order: HB_WINDOW_MULT chunk windows of the light kernel
+// (env override for sweeps).
+#ifndef HB_WINDOW_MULT
+#define HB_WINDOW_MULT 8
+#endif
+int64_t sort_window(int b) {
+  static const int mult = [] {
+    const char *e = getenv("HB_WINDOW_MULT");
+    const int m = e ? atoi(e) : HB_WINDOW_MULT;
+    return m > 0 ? m : 1;
+  }();
+  return hb_light_window(b) * mult;
+}
 // key per node: order 1 (degree) 0xFFFFFFFF - in-degree, so an ascending stable sort is by
 // descending in-degree; order 2 (window) the same in the low 32 bits under the global index
 // of the node's light-kernel chunk window (rank r, window w of its range) in the high 32
@@ -3641,7 +4008,7 @@ int hb_schedule_order(int64_t n, const int64_t *offsets, int order, int b, int w
   memset(&rb, 0, sizeof(rb));
   rb.world = world;
   for (int r = 0; r <= world; r++) rb.b[r] = bounds[r];
-  k_order_keys<<<grid_for_threads(n), kThreads, 0, s>>>(n, offsets, order, hb_light_window(b),
+  k_order_keys<<<grid_for_threads(n), kThreads, 0, s>>>(n, offsets, order, sort_window(b),
                                                         hb_light_npw(b), rb, k0, v0);
   if (int er = check_launch("k_order_keys")) return er;
   cub::DoubleBuffer<uint64_t> keys(k0, k1);

@@ -36,7 +36,7 @@ import torch
 from . import _lib
 from .centrality import BallObserver, CentralityAccumulator, fusable
 from .hll import CounterArray, CounterParams, estimator_constants, lc_table
-from .schedule import Schedule, build_schedule, pack_bits, unpack_bits
+from .schedule import Schedule, build_schedule, die_eligible, pack_bits, unpack_bits
 
 import os as _os
 
@@ -341,7 +341,7 @@ class _Device:
         self.lc = torch.from_numpy(lc_table(p)).to(dv)
         self.alpha_p2, self.lc_cut, _ = estimator_constants(p)
         self.counts = torch.zeros(2, dtype=torch.int64, device=dv)   # [changed, merged arcs]
-        self.ticket = torch.zeros(1, dtype=torch.int64, device=dv)   # light-kernel chunk tickets
+        self.ticket = torch.zeros(2, dtype=torch.int64, device=dv)   # chunk / item tickets
         self.merged_total = 0         # arcs whose source row was merged, all iterations
         self.prev_all = True          # chg_prev is all-ones (first iteration)
         self.full_pass = True         # zero in-degree nodes may still need their copy
@@ -378,7 +378,7 @@ class _Device:
         other.chg_now = torch.zeros_like(self.chg_now)
         other.est = torch.zeros(n, dtype=torch.float64, device=dv)
         other.counts = torch.zeros(2, dtype=torch.int64, device=dv)
-        other.ticket = torch.zeros(1, dtype=torch.int64, device=dv)
+        other.ticket = torch.zeros(2, dtype=torch.int64, device=dv)
         other.merged_total = 0
         other.prev_all = True
         other.full_pass = True
@@ -577,6 +577,7 @@ class _Device:
             self.slice_counts = torch.zeros((len(parts), 2), dtype=torch.int64,
                                             device=self.device)
         L = _lib.hb()
+        die = self.die_args() if active is None and n_peers == 0 else {}
         for k, (lo, hi, ev) in enumerate(parts):
             if ev is not None:
                 s.ready_slice(lo, hi, ev)
@@ -596,7 +597,7 @@ class _Device:
                 else None,
                 peer_chg=ctypes.cast(peer_chg, ctypes.c_void_p) if peer_chg is not None
                 else None, peer_packed_stride=pstride, ticket=self.ticket.data_ptr(),
-                stream=self.stream.cuda_stream, **_lib.schedule_args(s)))
+                stream=self.stream.cuda_stream, **die, **_lib.schedule_args(s)))
             self.launches += (hi > lo) + (s.n_items > 0) + (s.n_heavy > 0)
         if len(parts) > 1:
             s.relabel = None
@@ -626,6 +627,45 @@ class _Device:
         self.chg_prev, self.chg_now = self.chg_now, self.chg_prev
         self.prev_all = False
         self.full_pass = False
+
+    def die_args(self) -> dict:
+        """hb_step_args.die_head / die_rows / item_split (die-affine heavy items) when the
+        schedule is eligible (schedule.die_eligible), every id is on the device and the
+        device splits into two L2 dies.  First use per schedule: allocate the head buffer,
+        map its chunks (hb_die_map) and reorder the ids inside the items
+        (hb_die_partition); later runs on the same schedule reuse it."""
+        s = self.sched
+        if not (s.n_items > 0 and s.hot_rows > 0 and die_eligible(self.n, self.b, s.order)
+                and s.partial.shape[0] >= 2 * s.n_items) or s.pending:
+            return {}
+        if _os.environ.get("HB_DIE", "0") != "1":     # opt-in (DESIGN.md section 9)
+            return {}
+        if s.die is None:
+            L = _lib.hb()
+            mb = int(_os.environ.get("HB_DIE_HEAD_MB", "112"))
+            rows = min(s.hot_rows, (mb << 20) >> self.b)
+            nbytes = rows << self.b
+            s.die = False
+            if nbytes >= 4096 and s.item_arcs <= 512:
+                head = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+                bits = torch.zeros(int(L.hb_die_map_words(head.data_ptr(), nbytes)),
+                                   dtype=torch.int32, device=self.device)
+                stats = (ctypes.c_int64 * 4)()
+                st = self.stream.cuda_stream
+                _lib.check(L.hb_die_map(head.data_ptr(), nbytes, bits.data_ptr(), stats, st),
+                           "hb_die_map")
+                if stats[0] > 0:
+                    split = torch.empty(s.n_items, dtype=torch.int32, device=self.device)
+                    _lib.check(L.hb_die_partition(
+                        s.n_items, s.item_node.data_ptr(), s.item_beg.data_ptr(),
+                        s.offsets_ptr(), s.succ_buf.data_ptr(), s.item_arcs, self.b,
+                        head.data_ptr(), rows, bits.data_ptr(), split.data_ptr(), st),
+                        "hb_die_partition")
+                    s.die = (head, rows, split, tuple(stats))
+        if not s.die:
+            return {}
+        return dict(die_head=s.die[0].data_ptr(), die_rows=s.die[1],
+                    item_split=s.die[2].data_ptr())
 
 
 class _IdentityOrder:

@@ -28,6 +28,15 @@ import torch
 from . import _lib
 
 
+def die_eligible(n: int, b: int, order: str) -> bool:
+    """Can hb_union_step_v2 use die-affine heavy items on this schedule?  (16- / 32-register
+    rows of a register array >= 1 GB in degree order: include/hyperball_b200.h, die_bits.)"""
+    if os.environ.get("HB_DIE", "0") != "1":        # opt-in
+        return False
+    min_mb = int(os.environ.get("HB_DIE_MIN_MB", "1024"))
+    return order == "degree" and b <= 5 and (n << b) >= (min_mb << 20)
+
+
 @dataclass
 class Schedule:
     n: int
@@ -54,6 +63,8 @@ class Schedule:
     partial: torch.Tensor
     max_deg: int
     hot_rows: int = 0              # degree order: head of the rows kept persisting in L2
+    die: object = None             # die-affine items: None = not tried, False = off, else
+                                   # (head buffer, rows, item_split, hb_die_map stats)
     # Streamed upload (window / identity order): row slices [r0, r1) whose successor ids
     # are still in flight on the side stream (event) and, for the window order, not yet
     # relabelled (relabel = (old offsets, old ids, perm, rank)).  Iteration 1 consumes them
@@ -553,7 +564,9 @@ def build_rank_local(offsets, successors, b: int, device, order: str, world: int
     heavy, item_first, n_items, item_node, item_beg, finish_order, n_mega, n_nonzero = \
         heavy_items(off_loc, nloc, lo, light_max_deg, item_arcs, s_main)
     p = 1 << b
-    partial = torch.empty((max(n_items, 1), p), dtype=torch.uint8, device=device)
+    # die-affine heavy items (hb_step_args.die_bits) leave two partial rows per item
+    partial = torch.empty((max(n_items, 1) * (2 if die_eligible(n, b, order) else 1), p),
+                          dtype=torch.uint8, device=device)
     if order == "degree":
         n_heavy = int(heavy.numel())
         light_lo, light_hi = lo + n_heavy, hi
@@ -686,7 +699,9 @@ def build_schedule(offsets, successors, b: int, device, order: str = "auto", wor
     heavy, item_first, n_items, item_node, item_beg, finish_order, n_mega, n_nonzero = \
         heavy_items(off[lo:], hi - lo, lo, light_max_deg, item_arcs, s_main)
     p = 1 << b
-    partial = torch.empty((max(n_items, 1), p), dtype=torch.uint8, device=device)
+    # die-affine heavy items (hb_step_args.die_bits) leave two partial rows per item
+    partial = torch.empty((max(n_items, 1) * (2 if die_eligible(n, b, order) else 1), p),
+                          dtype=torch.uint8, device=device)
     if order == "degree":
         # this rank's slice is in descending degree: heavy first, zero in-degree last
         n_heavy = int(heavy.numel())
