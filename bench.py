@@ -303,6 +303,16 @@ def load_traffic(config: str):
         return None
 
 
+def dram_side(traffic, kernel_ms: float, peak: float) -> dict:
+    """The DRAM side of the roofline: the ncu-measured bytes of one dense step (traffic,
+    profiles/ncu_traffic.json) over the live kernel time -- what the HBM actually moved,
+    next to `achieved` (algorithmic bytes, which count source rows the L2 served)."""
+    if not traffic or not kernel_ms:
+        return {}
+    gbs = traffic / (kernel_ms * 1e-3) / 1e9
+    return {"dram_gbs": gbs, "dram_frac": gbs / peak}
+
+
 def dense_steps(g, cfgd, local: int, steps: int, warmup: int, schedule: str = "auto",
                 world: int = 1, rank: int = 0, exchange: str = "push", clocks: bool = False):
     """Device-resident dense iterations of config `cfgd` on graph `g`: `warmup` untimed,
@@ -571,10 +581,11 @@ def run_b200(args):
                     "workload": f"{name}: {cd.description}", "n": gq.n, "m": gq.m,
                     "log2m": cd.log2m, "dense_ms": r["ms_per_step"],
                     "kernel_ms": r["kernel_ms"], "value": r["value"], "unit": UNIT,
-                    "roofline": {"bound": "hbm", "achieved": r["achieved"], "peak": r["peak"],
-                                 "unit": "GB/s", "frac": r["frac"],
-                                 "algorithmic_bytes_per_launch": r["alg_bytes"],
-                                 "traffic": load_traffic(name)},
+                    "roofline": dict({"bound": "hbm", "achieved": r["achieved"], "peak": r["peak"],
+                                      "unit": "GB/s", "frac": r["frac"],
+                                      "algorithmic_bytes_per_launch": r["alg_bytes"],
+                                      "traffic": load_traffic(name)},
+                                     **dram_side(load_traffic(name), r["kernel_ms"], r["peak"])),
                     "schedule": r["schedule"], "steps": args.per_config_steps}
                 del gq, r
                 torch.cuda.empty_cache()
@@ -607,6 +618,7 @@ def run_b200(args):
             "roofline": {"bound": "hbm", "achieved": d["achieved"], "peak": d["peak"],
                          "unit": "GB/s", "frac": d["frac"], "traffic": load_traffic(args.config),
                          "algorithmic_bytes_per_launch": d["alg_bytes"],
+                         **dram_side(load_traffic(args.config), d["kernel_ms"], d["peak"]),
                          "kernel_ms": d["kernel_ms"], "peak_source": d["peak_src"],
                          "kernels": "hb_union_step (light%s)" % (
                              " + heavy items + finish" if d["items"] else "")},
