@@ -2899,6 +2899,10 @@ unsigned grid_resident(const void *func, size_t smem, int64_t work_warps) {
   return (unsigned)ctas;
 }
 
+#ifndef HB_OVERLAP_LIGHT_DEFAULT
+#define HB_OVERLAP_LIGHT_DEFAULT 0   // measured on config 5: 27.3 ms back to back; side by side
+                                     // 33.9 / 27.5 / 36.0 ms with 1 / 2 / 3 light CTAs per SM
+#endif
 #ifndef HB_TMA_L2PROMO
 #define HB_TMA_L2PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_256B
 #endif
@@ -2925,6 +2929,42 @@ int encode_row_map(CUtensorMap *tm, const uint8_t *base, int64_t rows, int p) {
                          CU_TENSOR_MAP_SWIZZLE_NONE, (CUtensorMapL2promotion)HB_TMA_L2PROMO,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? 0 : set_err_msg("cuTensorMapEncodeTiled failed");
+}
+
+// Side stream of the current device for the light kernel of an overlapped step (below):
+// created on first use, non-blocking; fork / join by two events, so the caller's stream
+// still orders the whole step.
+struct SideStream {
+  cudaStream_t st = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  int state = 0;   // 0 = not tried, 1 = ready, -1 = unavailable
+};
+SideStream *side_stream() {
+  static SideStream sd[kMaxDevices];
+  SideStream &x = sd[current_device()];
+  if (x.state == 0) {
+    x.state = -1;
+    if (cudaStreamCreateWithFlags(&x.st, cudaStreamNonBlocking) == cudaSuccess &&
+        cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming) == cudaSuccess &&
+        cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming) == cudaSuccess)
+      x.state = 1;
+    cudaGetLastError();
+  }
+  return x.state == 1 ? &x : nullptr;
+}
+// Overlapped step (p <= 32 rows of a register array >= 1 GB, heavy items present, ticket-
+// dealt): the heavy-item kernel is bound by the DRAM random-access rate of its cold rows,
+// the light kernel half by streams (own rows, estimates, sums, ids) -- run side by side
+// they share the SMs, HB_OVERLAP_LIGHT resident CTAs per SM for the light kernel, the rest
+// for the items.  Off by default (HB_OVERLAP_LIGHT=0): the two kernels turn out to be
+// bound by the same resource -- the misses of both are served at the same DRAM
+// random-access rate -- so side by side they take as long as back to back.
+int overlap_light_ctas() {
+  const char *e = getenv("HB_OVERLAP");
+  if (e && e[0] == '0') return 0;
+  const char *l = getenv("HB_OVERLAP_LIGHT");
+  const int v = l ? atoi(l) : HB_OVERLAP_LIGHT_DEFAULT;
+  return v > 0 ? v : 0;
 }
 
 template <int LOGP, bool PUSH, int LOGR = 0>
@@ -2969,6 +3009,21 @@ int union_step_impl(int64_t lo, int64_t hi, const int64_t *offsets, const int32_
   const int64_t hot_lim = hot_rows > 0 ? std::min<int64_t>(hot_rows, hint_bytes() / Gm::P) : 0;
   const bool hint = kCanHint && hot_lim > 0;
   int pshift = 0;
+  // overlapped step: the light kernel on the side stream, next to the heavy items
+  int lshare = 0;
+  SideStream *side = nullptr;
+  if constexpr (kCanHint && !PUSH && LOGR == 0) {
+    if (hint && l1na && ticket && !active && n_items > 0 && hi > lo && (lshare = overlap_light_ctas()) > 0)
+      side = side_stream();
+  }
+  if (!side) lshare = 0;
+  if (side) {
+    if (cudaEventRecord(side->fork, s) != cudaSuccess ||
+        cudaStreamWaitEvent(side->st, side->fork, 0) != cudaSuccess)
+      return set_err("hb_union_step overlap fork", cudaGetLastError());
+    if (win > 0) set_hot_window(side->st, cur, (size_t)hot_rows * Gm::P, win);
+  }
+  cudaStream_t sl = side ? side->st : s;     // the light kernel's stream
   if (n_items > 0) {
     // ticket word 1 deals the heavy items (word 0 the light kernel's chunks), except in
     // frontier mode, whose skip-ahead probe walks the grid-stride order
@@ -2981,7 +3036,12 @@ int union_step_impl(int64_t lo, int64_t hi, const int64_t *offsets, const int32_
         hfunc = (const void *)k_heavy_partial<LOGP, true, true, true>;
     }
     const bool die_on = kCanHint && hfunc == (const void *)k_heavy_partial<LOGP, kCanHint, kCanHint, kCanHint>;
-    const unsigned hgrid = hticket ? grid_resident(hfunc, 0, n_items) : grid_for_warps(n_items);
+    unsigned hgrid = hticket ? grid_resident(hfunc, 0, n_items) : grid_for_warps(n_items);
+    if (side) {
+      const int occ = resident_ctas(hfunc, 0);
+      if (occ > lshare) hgrid = std::min<unsigned>(hgrid, (unsigned)(num_sms() * (occ - lshare)));
+      else { lshare = 0; }
+    }
     // items per draw: ~16 draws per resident warp, at most 8 items (config 5: 27.8 ms; 28.0 /
     // 28.2 ms at 32 / 128; 4 is 27.6 ms but the draws start to queue on config 5s; env
     // overrides for sweeps)
@@ -3019,7 +3079,7 @@ int union_step_impl(int64_t lo, int64_t hi, const int64_t *offsets, const int32_
     const int64_t warps = (hi - lo + Gm::NPW - 1) / Gm::NPW + 1;   // capped at the resident set
     if constexpr (kCanHint) {
       if (hint && l1na)
-        k_light<LOGP, PUSH, LOGR, true, true><<<grid_resident((const void *)k_light<LOGP, PUSH, LOGR, true, true>, 0, warps), kThreads, 0, s>>>(
+        k_light<LOGP, PUSH, LOGR, true, true><<<(side && lshare > 0) ? std::min<unsigned>(grid_resident((const void *)k_light<LOGP, PUSH, LOGR, true, true>, 0, warps), (unsigned)(num_sms() * lshare)) : grid_resident((const void *)k_light<LOGP, PUSH, LOGR, true, true>, 0, warps), kThreads, 0, sl>>>(
             offsets, succ, cur, nxt, chg_prev, chg_now, est, sum_dist, sum_recip, ec, lo, hi,
             light_max_deg, dense, tf, nch, merged, active, peers, ra, hot_lim, ticket, tmap);
       else if (hint)
@@ -3032,6 +3092,12 @@ int union_step_impl(int64_t lo, int64_t hi, const int64_t *offsets, const int32_
           offsets, succ, cur, nxt, chg_prev, chg_now, est, sum_dist, sum_recip, ec, lo, hi,
           light_max_deg, dense, tf, nch, merged, active, peers, ra, hot_lim, ticket, tmap);
     if (int e = check_launch("k_light")) return e;
+  }
+  if (side) {
+    if (win > 0) set_hot_window(side->st, nullptr, 0, 0);
+    if (cudaEventRecord(side->join, side->st) != cudaSuccess ||
+        cudaStreamWaitEvent(s, side->join, 0) != cudaSuccess)
+      return set_err("hb_union_step overlap join", cudaGetLastError());
   }
   if (n_heavy > 0) {
     if (n_mega > 0) {
@@ -3093,7 +3159,18 @@ const char *hb_last_error(void) { return g_err; }
 int hb_min_log2m(void) { return HB_MIN_B; }
 int hb_max_log2m(void) { return HB_MAX_B; }
 int64_t hb_item_arcs(int b) { return item_arcs_for(b); }
-int64_t hb_light_max_deg(int b) { (void)b; return kLightMaxDeg; }
+int64_t hb_light_max_deg(int b) {
+  if (const char *e = getenv("HB_LIGHT_MAX_DEG")) {   // sweeps
+    const int64_t v = atoll(e);
+    if (v > 0) return v;
+  }
+  // 16- / 32-register rows: one lane per node (or two) keeps 8 row loads in flight by
+  // itself, and a heavy item costs ~400 warp instructions before its first row -- nodes of
+  // up to 128 arcs are cheaper in the light kernel (config 5 27.7 -> 27.1 ms, config 5s
+  // 1.50 -> 1.45 ms; 96-192 within 1%, 256-512 back to 27.7, 2048 29.4 ms); above, 64
+  // (config 2, p = 128: 0.39 ms at 64, 0.49 at 256)
+  return b <= 5 ? 2 * kLightMaxDeg : kLightMaxDeg;
+}
 int64_t hb_light_npw(int b) {
   switch (b) {
     case 4: return light_npw_t<4>();   case 5: return light_npw_t<5>();
