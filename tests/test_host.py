@@ -51,6 +51,22 @@ def test_library_metadata_calls():
     assert b"sm_100a" in L.hb_version()
     assert L.hb_min_log2m() == 4 and L.hb_max_log2m() >= 12
     assert L.hb_item_arcs(4) == 512 and L.hb_item_arcs(8) == 64
+    # light/heavy threshold: 128 arcs for 16- / 32-register rows, 64 above
+    assert L.hb_light_max_deg(4) == 128 and L.hb_light_max_deg(5) == 128
+    assert L.hb_light_max_deg(6) == 64 and L.hb_light_max_deg(8) == 64
+    assert L.hb_die_map_words(ctypes.c_void_p(4096 + 1000), 8192) == 1   # 5 chunks -> 1 word
+
+
+def test_die_affine_items_are_opt_in(monkeypatch):
+    from paper_1308_2144_b200.schedule import die_eligible
+    monkeypatch.delenv("HB_DIE", raising=False)
+    assert not die_eligible(1 << 28, 4, "degree")
+    monkeypatch.setenv("HB_DIE", "1")
+    assert die_eligible(1 << 28, 4, "degree")            # 4 GB of 16-byte rows
+    assert not die_eligible(1 << 24, 4, "degree")        # 268 MB: below the 1 GB threshold
+    assert not die_eligible(1 << 28, 4, "identity") and not die_eligible(1 << 28, 6, "degree")
+    monkeypatch.setenv("HB_DIE_MIN_MB", "0")
+    assert die_eligible(1 << 12, 5, "degree")
 
 
 def _abi_args(name, **at):
@@ -97,6 +113,9 @@ def test_c_abi_rejects_bad_arguments():
         "hb_relabel_csr_src_rows", a0=5, a1=3, a2=6)))
     assert "hb_sample_flagged_arcs" in err(L.hb_sample_flagged_arcs(*_abi_args(
         "hb_sample_flagged_arcs", a0=5, a3=8, a5=ctypes.c_void_p(8))))
+    assert "hb_die_map" in err(L.hb_die_map(*_abi_args("hb_die_map", a1=1 << 20)))
+    assert "hb_die_partition" in err(L.hb_die_partition(*_abi_args(
+        "hb_die_partition", a0=5, a5=512, a6=4)))
 
 
 def test_hash_and_register_pins(pins):
