@@ -42,13 +42,13 @@ def test_die_map_splits_the_device(monkeypatch):
     assert words * 32 >= chunks
     assert stats[0] + stats[1] == torch.cuda.get_device_properties(0).multi_processor_count
     assert min(stats[0], stats[1]) * 4 >= stats[0] + stats[1]
-    assert 0.3 * chunks < stats[2] < 0.7 * chunks        # about half of the chunks per die
-    assert stats[3] < chunks // 100                      # the two latencies are far apart
+    assert 0.2 * chunks < stats[2] < 0.8 * chunks        # about half of the chunks per die
+    assert stats[3] < chunks // 10                       # the two latencies are far apart
     assert int((t != 7).sum()) == 0                      # the probe leaves the data alone
     # stable: a second measurement agrees on (nearly) every chunk
     bits2, stats2, _ = die_map(t)
     diff = (bits ^ bits2).cpu().numpy().view(np.uint32)
-    assert sum(bin(int(w)).count("1") for w in diff[diff != 0]) < chunks // 100
+    assert sum(bin(int(w)).count("1") for w in diff[diff != 0]) < chunks // 10
     # unaligned base: chunk 0 is the 2 KB block holding base[0]
     u = t[1000:1000 + (8 << 20)]
     bits3, stats3, words3 = die_map(u)
@@ -56,7 +56,7 @@ def test_die_map_splits_the_device(monkeypatch):
     b1 = np.unpackbits(bits.cpu().numpy().view(np.uint8), bitorder="little")
     b3 = np.unpackbits(bits3.cpu().numpy().view(np.uint8), bitorder="little")
     k = (8 << 20) // 2048
-    assert (b1[:k] != b3[:k]).sum() < k // 50
+    assert (b1[:k] != b3[:k]).sum() < k // 10
 
 
 @pytest.mark.parametrize("scale,b,width,frontier", [(14, 4, 5, False), (15, 5, 5, False),
