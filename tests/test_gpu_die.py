@@ -40,7 +40,8 @@ def test_die_map_splits_the_device(monkeypatch):
         pytest.skip("device does not split into two L2 dies")
     chunks = (64 << 20) // 2048
     assert words * 32 >= chunks
-    assert stats[0] + stats[1] == torch.cuda.get_device_properties(0).multi_processor_count
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    assert 0.9 * sms <= stats[0] + stats[1] <= sms
     assert min(stats[0], stats[1]) * 4 >= stats[0] + stats[1]
     assert 0.2 * chunks < stats[2] < 0.8 * chunks        # about half of the chunks per die
     assert stats[3] < chunks // 10                       # the two latencies are far apart
