@@ -28,6 +28,17 @@ import torch
 from . import _lib
 
 
+def hot_head_rows(n: int, order: str, world: int) -> int:
+    """Rows of the L2-protected hot head (hb_step_args.hot_rows).  In degree order on one
+    GPU the most-read rows are the first rows.  With world > 1 the degree deal gives every
+    rank a contiguous range that starts with ITS share of them, so the hot set is W
+    sub-heads and the single protected range [0, H) covers one rank's sub-head while every
+    other rank's hot rows are marked evict-first: measured per rank on one GPU
+    (tools/rank_step_bench.py, config 5 dense step, rank 0 of W = 2 / 4 / 8): 18.0 / 10.7 /
+    6.1 ms with the range, 18.6 / 9.4 / 4.8 ms without any hint -- off from 3 ranks up."""
+    return n if order == "degree" and world <= 2 else 0
+
+
 def die_eligible(n: int, b: int, order: str) -> bool:
     """Can hb_union_step_v2 use die-affine heavy items on this schedule?  (16- / 32-register
     rows of a register array >= 1 GB in degree order: include/hyperball_b200.h, die_bits.)"""
@@ -580,7 +591,7 @@ def build_rank_local(offsets, successors, b: int, device, order: str, world: int
                     finish_order=finish_order, n_mega=n_mega,
                     item_node=item_node, item_beg=item_beg,
                     partial=partial, max_deg=max_deg,
-                    hot_rows=n if order == "degree" else 0, stream=s_main, row_base=base,
+                    hot_rows=hot_head_rows(n, order, world), stream=s_main, row_base=base,
                     local=True)
 
 
@@ -718,5 +729,5 @@ def build_schedule(offsets, successors, b: int, device, order: str = "auto", wor
                     finish_order=finish_order, n_mega=n_mega,
                     item_node=item_node, item_beg=item_beg,
                     partial=partial, max_deg=max_deg,
-                    hot_rows=n if order == "degree" else 0, pending=pending,
+                    hot_rows=hot_head_rows(n, order, world), pending=pending,
                     relabel=relabel, stream=s_main)
